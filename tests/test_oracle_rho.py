@@ -1,0 +1,110 @@
+"""Pins for Eq. (1) [P:69] (reference B, from exact integers) and the two-pass
+Pearson (reference A) [S:244-251, S:274-285, S:455]; and Phases 3/4
+[P:83; S:252-265]."""
+from decimal import Decimal, getcontext
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from synth import synth as S
+from tests.test_oracle_sums import h_matrix, rand_data
+
+
+def test_perfect_and_anti_correlation():
+    t, _ = rand_data(60, 1, 11)
+    H = h_matrix(O.HD_LAST, t)
+    h = 256 * 3 + 77
+    W = np.stack([H[:, h], -H[:, h], np.full(60, 5)], 1).astype(np.int8)  # [S:248-250]
+    r = O.attack_i8(O.HD_LAST, t, W)["rho"][h]
+    assert r[0] == 1.0 and r[1] == -1.0 and r[2] == 0.0
+    ra = O.rho_two_pass_i8(O.HD_LAST, t, W, hyps=[h])[0]
+    assert abs(ra[0] - 1) <= 1e-12 and abs(ra[1] + 1) <= 1e-12 and ra[2] == 0.0
+
+
+def test_numpy_corrcoef_tiny():
+    t, W = rand_data(40, 5, 12)
+    H = h_matrix(O.HD_LAST, t).astype(float)
+    r = O.attack_i8(O.HD_LAST, t, W)["rho"]
+    for h in (0, 500, 4095):
+        for j in range(5):
+            ref = np.corrcoef(H[:, h], W[:, j].astype(float))[0, 1]
+            assert abs(r[h, j] - ref) <= 1e-12
+
+
+def test_exact_rational_spot_cells():
+    """rho_B is within 1 ulp of the exact value num / sqrt(dw dh) (50 digits)."""
+    getcontext().prec = 50
+    t, W = rand_data(500, 4, 13)
+    a = O.attack_i8(O.HD_LAST, t, W)
+    n = 500
+    for h in (7, 1234, 3000):
+        for j in range(4):
+            num = n * int(a["sum_hw"][h, j]) - int(a["sum_h"][h]) * int(a["sum_w"][j])
+            dw = n * int(a["sum_w2"][j]) - int(a["sum_w"][j]) ** 2
+            dh = n * int(a["sum_h2"][h]) - int(a["sum_h"][h]) ** 2
+            exact = Decimal(num) / (Decimal(dw).sqrt() * Decimal(dh).sqrt())
+            got = a["rho"][h, j]
+            assert abs(Decimal(got) - exact) <= Decimal(np.spacing(abs(got))) * 2
+
+
+def test_two_pass_agreement_acceptance_1():
+    """SPEC acceptance 1: n=50, m=64, all 4096x64 cells within 1e-9."""
+    t, W = rand_data(50, 64, 14)
+    rb = O.attack_i8(O.HD_LAST, t, W)["rho"]
+    ra = O.rho_two_pass_i8(O.HD_LAST, t, W)
+    assert np.max(np.abs(ra - rb)) <= 1e-9
+    assert np.all(np.abs(rb) <= 1.0)
+
+
+def test_affine_invariance_exact():
+    """Integer offset: num and dw unchanged exactly -> bit-identical rho_B;
+    negation: exact sign flip; duplication: bit-identical [S:285]."""
+    t, W = rand_data(300, 12, 15)
+    W = np.clip(W, -100, 100).astype(np.int8)
+    r0 = O.attack_i8(O.HD_LAST, t, W)["rho"]
+    r1 = O.attack_i8(O.HD_LAST, t, (W.astype(np.int16) + 27).astype(np.int8))["rho"]
+    assert np.array_equal(r0, r1)
+    rn = O.attack_i8(O.HD_LAST, t, (-W.astype(np.int16)).astype(np.int8))["rho"]
+    assert np.array_equal(rn, -r0)
+    ru = O.attack_i8(O.HD_LAST, t, (W.astype(np.int16) + 128).astype(np.uint8))["rho"]
+    assert np.array_equal(ru, r0)                         # u8 = s8 + 128
+    rd = O.attack_i8(O.HD_LAST, np.concatenate([t, t]), np.concatenate([W, W]))["rho"]
+    assert np.array_equal(rd, r0)
+
+
+def test_eq1_overflow_guard():
+    with pytest.raises(OverflowError):
+        O.rho_eq1(2**40, 2**40, 2**40, 2**41, 2**40, 2**50)
+
+
+def test_phase3_phase4_constructed_surfaces():
+    rho = np.zeros((4096, 3))
+    for b in range(16):
+        rho[256 * b + b, 1] = -1.0                           # [S:263]
+    mx, am, pk = O.phase3(rho)
+    best, rank = O.phase4(mx)
+    assert best.tolist() == list(range(16))
+    assert all(am[256 * b + b] == 1 and pk[256 * b + b] == -1.0 for b in range(16))
+    best, rank = O.phase4(np.zeros(4096))                    # all equal -> 0x00 [S:264]
+    assert best.tolist() == [0] * 16 and rank[:256].tolist() == list(range(1, 257))
+    rho = np.full((4096, 4), 0.25)                           # ties -> lowest sample
+    mx, am, _ = O.phase3(rho, np.array([3, 5, 8, 9], np.int32))
+    assert (am == 3).all()
+
+
+def test_end_to_end_noiseless_and_noisy():
+    """[S:331, S:341, S:456-457]: noiseless -> rho = 1 exactly at the planted
+    sample for all 16 bytes; noisy C1 -> the true round-10 key, master key."""
+    for name in ("C1-0", "C1"):
+        w = S.CONFIGS[name]
+        t, W = S.dataset(w)
+        a = O.attack_i8(O.HD_LAST, t, W)
+        rk = O.expand_key(w.key)[10].astype(int)
+        assert a["best"].tolist() == rk.tolist()
+        assert O.invert_key_schedule(a["best"].tobytes()).tobytes() == w.key
+        hs = [256 * b + rk[b] for b in range(16)]
+        assert a["argmax"][hs].tolist() == w.leak_positions()
+        assert (a["rank"][hs] == 1).all()
+        if name == "C1-0":
+            assert np.all(np.abs(a["maxabs"][hs] - 1.0) <= 1e-12)
