@@ -1,0 +1,159 @@
+/*
+ * cpa.h -- C ABI of libcpa.so, the B200 (sm_100a) Correlation Power Analysis
+ * engine for AES-128 following Gamaarachchi, Ragel & Jayasinghe,
+ * "Accelerating Correlation Power Analysis Using GPUs" (arXiv:1412.7682).
+ * [P:n] = line n of the paper text, [S:n] = line n of SPEC.md.
+ *
+ * Problem statement [P:65-67]: N power traces of M sample points W[i][j] and
+ * the N matching ciphertexts (plaintexts for the first-round model) in; the
+ * correlation of every (key byte b, sub-key guess k, sample j) by Eq. (1)
+ * [P:69] and the round key (Phase 4, [P:85-87]) out.
+ *
+ * Hypothesis index h = 256*b + k (b = 0..15 key byte, k = 0..255 guess).
+ *
+ * Conventions for every function:
+ *   - Returns cpa_status; CPA_OK = 0.  No C++ exception crosses the ABI.
+ *   - Pointers named d_* are CUDA device pointers on the context's device,
+ *     h_* are host pointers.  The caller owns every buffer it passes; a
+ *     buffer passed to an asynchronous call must stay alive and unmodified
+ *     until the next synchronising call (cpa_finalize, cpa_sync, cpa_destroy).
+ *   - The library owns only its context, its lookup tables and its scratch.
+ *   - Argument errors are reported synchronously; CUDA launch/runtime errors
+ *     map to CPA_E_CUDA with detail in cpa_last_error().
+ *   - Not thread-safe per context; distinct contexts are independent.
+ */
+#ifndef CPA_H
+#define CPA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CPA_API __attribute__((visibility("default")))
+#else
+#define CPA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cpa_ctx cpa_ctx; /* opaque; one per GPU / rank */
+
+typedef enum {
+    CPA_OK = 0,
+    CPA_E_INVALID_ARG = 1,        /* bad size, null pointer, misalignment */
+    CPA_E_BAD_STATE = 2,          /* e.g. call on a destroyed context */
+    CPA_E_CUDA = 3,               /* CUDA error, see cpa_last_error() */
+    CPA_E_NO_MEMORY = 4,          /* device scratch allocation failed */
+    CPA_E_TOO_FEW_TRACES = 5,     /* N < 2 at finalize: Eq. (1) undefined [S:268] */
+    CPA_E_OVERFLOW = 6,           /* N beyond the exact-int64 bound (2^23 traces) */
+    CPA_E_UNSUPPORTED_DEVICE = 7  /* not a compute-capability 10.0 (sm_100a) GPU */
+} cpa_status;
+
+typedef enum {
+    CPA_S8 = 0,  /* signed 8-bit ADC samples (exact int path) */
+    CPA_U8 = 1,  /* unsigned 8-bit ADC samples (exact int path) */
+    CPA_F32 = 2  /* float32 samples (bf16 hi/lo tensor-core path, fp64 sums) */
+} cpa_dtype;
+
+/* Selection function H [P:67, P:75] (the paper never writes it out; see
+ * DESIGN.md "Readings"):                                                    */
+typedef enum {
+    CPA_HD_LAST = 0,  /* HW(InvS(c[b] ^ k) ^ c[SR(b)]), last round, ciphertexts [S:85] */
+    CPA_HW_LAST = 1,  /* HW(InvS(c[b] ^ k)), last round, ciphertexts */
+    CPA_HW_FIRST = 2  /* HW(S(p[b] ^ k)), first round, plaintexts [P:63] */
+} cpa_model;
+
+/* ---- packed accumulator ----------------------------------------------------
+ * The Phase 1/2 sums [P:75, P:79] live in ONE caller-owned device buffer of
+ * cpa_accum_words(M) 8-byte words, so that a multi-GPU run combines partial
+ * sums with a single all-reduce(SUM) of that buffer between the last
+ * cpa_accumulate and cpa_finalize (traces shard over GPUs, [P:230]).
+ * Word layout (offsets in words):
+ *   [0, 4096*M)            sum_i H_i W_ij   as [h][j]  (j fastest)
+ *   [4096*M, +M)           sum_i W_ij
+ *   [4097*M, +M)           sum_i W_ij^2
+ *   [4098*M, +4096)        sum_i H_i
+ *   [4098*M+4096, +4096)   sum_i H_i^2
+ *   [4098*M+8192]          N (trace count)
+ * Word type: int64 for CPA_S8/CPA_U8 (exact, order-independent); double for
+ * CPA_F32 (all words, including N and the H sums, which stay exact < 2^53).
+ */
+CPA_API size_t cpa_accum_words(int32_t M);
+CPA_API size_t cpa_accum_bytes(int32_t M);
+CPA_API size_t cpa_accum_offset(int32_t M, int field); /* field: 0 HW,1 W,2 W2,3 H,4 H2,5 N */
+
+/* Create a context for M samples per trace on CUDA device `device`.
+ * stream: cudaStream_t (NULL = legacy default) all work is ordered on.
+ * d_accum: caller-owned, cpa_accum_bytes(M) bytes, 256-byte aligned; it is
+ * zeroed (asynchronously) here.  1 <= M <= 1<<22.                          */
+CPA_API cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model,
+                    int device, void *stream, void *d_accum);
+
+/* Add N traces to the sums (Phases 1-2, [P:73-79]); asynchronous.
+ * d_traces: N rows of M samples, row stride ld ELEMENTS (ld >= M).  Fast path
+ *   (read in place by TMA): base 16-byte aligned and ld*sizeof(elem) a
+ *   multiple of 16; otherwise the rows are first copied (pitched D2D copy)
+ *   into the library's aligned staging buffers.
+ * d_texts: N x 16 bytes (ciphertexts; plaintexts for CPA_HW_FIRST), byte b =
+ *   AES state byte b (column-major FIPS-197 order [S:107]).
+ * N = 0 is a no-op.  Sums are exact (int path), so any chunking or ordering of
+ * the traces gives bit-identical results.                                    */
+CPA_API cpa_status cpa_accumulate(cpa_ctx *ctx, const void *d_traces, int64_t ld,
+                          const uint8_t *d_texts, int64_t N);
+
+/* Same, from HOST buffers: the library streams them through its own device
+ * staging buffers (H2D copies overlapped with compute).  Synchronous: returns
+ * after the last copy was consumed, so the host buffers may be reused.  Host
+ * buffers should be pinned (cudaHostAlloc / cudaHostRegister) for speed.     */
+CPA_API cpa_status cpa_accumulate_host(cpa_ctx *ctx, const void *h_traces, int64_t ld,
+                               const uint8_t *h_texts, int64_t N);
+
+typedef struct {
+    uint8_t round_key[16];   /* Phase 4: best sub-key per byte [P:87] */
+    uint8_t master_key[16];  /* key schedule inverted from round 10 [P:63]
+                                (= round_key for CPA_HW_FIRST) */
+    int32_t peak_sample[16]; /* sample j of max |rho| for the best sub-key */
+    double peak_rho[16];     /* signed rho at that sample */
+    int64_t n_traces;        /* N the result was computed from */
+} cpa_result;
+
+/* Phase 3 + 4 [P:81-87] from the (possibly all-reduced) accumulator; blocks
+ * until done.  rho is Eq. (1) [P:69] in fp64 from the exact integer sums,
+ * 0 where a variance term is 0 [S:293], clamped to [-1, 1] [S:246].
+ * Optional device outputs (NULL to skip):
+ *   d_rho     [4096][M] double   (h-major, j fastest)
+ *   d_maxabs  [4096]    double   max_j |rho| per hypothesis [S:292]
+ *   d_argmax  [4096]    int32    lowest j attaining it [S:298]
+ *   d_rank    [4096]    int32    rank of k within byte b (1 = best; ties to
+ *                                lower k [S:261, S:298])
+ * res (host, may be NULL) receives the recovered key.                        */
+CPA_API cpa_status cpa_finalize(cpa_ctx *ctx, double *d_rho, double *d_maxabs,
+                        int32_t *d_argmax, int32_t *d_rank, cpa_result *res);
+
+CPA_API cpa_status cpa_reset(cpa_ctx *ctx);    /* zero the accumulator (async) */
+CPA_API cpa_status cpa_sync(cpa_ctx *ctx);     /* wait for all queued work */
+CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum) */
+
+/* Tuning / test knobs.  CPA_OPT_KCHUNK: traces per split-K work unit of the
+ * cross-term kernel (multiple of 64, <= 2^20; 0 = automatic).               */
+enum { CPA_OPT_KCHUNK = 1 };
+CPA_API cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value);
+
+/* Kernel launches issued by this context since creation (for bench
+ * accounting).                                                              */
+CPA_API int64_t cpa_launch_count(const cpa_ctx *ctx);
+
+CPA_API const char *cpa_status_str(cpa_status s);
+CPA_API const char *cpa_last_error(void); /* thread-local detail of the last error */
+
+/* ---- host helpers (pure, no GPU) ---------------------------------------- */
+CPA_API void cpa_aes_expand_key(const uint8_t key[16], uint8_t round_keys[11][16]);
+/* master key whose expansion has `rk` as round key `round` (1..10) [P:63] */
+CPA_API void cpa_aes_invert_key_schedule(const uint8_t rk[16], int round, uint8_t key[16]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPA_H */

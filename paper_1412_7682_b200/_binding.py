@@ -1,0 +1,170 @@
+"""Thin ctypes binding of libcpa.so -- same names as include/cpa.h.
+
+Argument marshalling only: every step of the CPA hot path runs in the CUDA
+kernels behind the C ABI.  There is no CPU fallback: importing this module
+without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libcpa.so")
+
+CPA_OK = 0
+CPA_E_INVALID_ARG, CPA_E_BAD_STATE, CPA_E_CUDA, CPA_E_NO_MEMORY = 1, 2, 3, 4
+CPA_E_TOO_FEW_TRACES, CPA_E_OVERFLOW, CPA_E_UNSUPPORTED_DEVICE = 5, 6, 7
+CPA_S8, CPA_U8, CPA_F32 = 0, 1, 2
+CPA_HD_LAST, CPA_HW_LAST, CPA_HW_FIRST = 0, 1, 2
+CPA_OPT_KCHUNK = 1
+FIELD_HW, FIELD_W, FIELD_W2, FIELD_H, FIELD_H2, FIELD_N = range(6)
+
+# every symbol include/cpa.h declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = (
+    "cpa_accum_words", "cpa_accum_bytes", "cpa_accum_offset", "cpa_init", "cpa_accumulate",
+    "cpa_accumulate_host", "cpa_finalize", "cpa_reset", "cpa_sync", "cpa_destroy",
+    "cpa_set_option", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
+    "cpa_aes_expand_key", "cpa_aes_invert_key_schedule",
+)
+
+
+class CpaError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        detail = _lib.cpa_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {_lib.cpa_status_str(status).decode()} ({detail})")
+
+
+class cpa_result(C.Structure):
+    _fields_ = [("round_key", C.c_uint8 * 16), ("master_key", C.c_uint8 * 16),
+                ("peak_sample", C.c_int32 * 16), ("peak_rho", C.c_double * 16),
+                ("n_traces", C.c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(the CUDA path has no fallback)")
+    L = C.CDLL(LIB_PATH)
+    P, I64, I32, ST = C.c_void_p, C.c_int64, C.c_int32, C.c_int
+    sig = {
+        "cpa_accum_words": (C.c_size_t, [I32]),
+        "cpa_accum_bytes": (C.c_size_t, [I32]),
+        "cpa_accum_offset": (C.c_size_t, [I32, C.c_int]),
+        "cpa_init": (ST, [C.POINTER(P), I32, C.c_int, C.c_int, C.c_int, P, P]),
+        "cpa_accumulate": (ST, [P, P, I64, P, I64]),
+        "cpa_accumulate_host": (ST, [P, P, I64, P, I64]),
+        "cpa_finalize": (ST, [P, P, P, P, P, C.POINTER(cpa_result)]),
+        "cpa_reset": (ST, [P]),
+        "cpa_sync": (ST, [P]),
+        "cpa_destroy": (ST, [P]),
+        "cpa_set_option": (ST, [P, C.c_int, I64]),
+        "cpa_launch_count": (I64, [P]),
+        "cpa_status_str": (C.c_char_p, [C.c_int]),
+        "cpa_last_error": (C.c_char_p, []),
+        "cpa_aes_expand_key": (None, [P, P]),
+        "cpa_aes_invert_key_schedule": (None, [P, C.c_int, P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    return L
+
+
+_lib = _load()
+
+
+def _ptr(x):
+    """Raw address of a torch tensor / int / None for the C ABI."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):
+        return x.ctypes.data
+    raise TypeError(type(x))
+
+
+def _check(st: int, where: str):
+    if st != CPA_OK:
+        raise CpaError(st, where)
+
+
+# ---- same-name wrappers ------------------------------------------------------
+def cpa_accum_words(M: int) -> int:
+    return _lib.cpa_accum_words(M)
+
+
+def cpa_accum_bytes(M: int) -> int:
+    return _lib.cpa_accum_bytes(M)
+
+
+def cpa_accum_offset(M: int, field: int) -> int:
+    return _lib.cpa_accum_offset(M, field)
+
+
+def cpa_init(M: int, dtype: int, model: int, device: int, stream: int, d_accum) -> int:
+    h = C.c_void_p()
+    _check(_lib.cpa_init(C.byref(h), M, dtype, model, device, stream, _ptr(d_accum)), "cpa_init")
+    return h.value
+
+
+def cpa_accumulate(ctx, d_traces, ld: int, d_texts, N: int):
+    _check(_lib.cpa_accumulate(ctx, _ptr(d_traces), ld, _ptr(d_texts), N), "cpa_accumulate")
+
+
+def cpa_accumulate_host(ctx, h_traces, ld: int, h_texts, N: int):
+    _check(_lib.cpa_accumulate_host(ctx, _ptr(h_traces), ld, _ptr(h_texts), N), "cpa_accumulate_host")
+
+
+def cpa_finalize(ctx, d_rho=None, d_maxabs=None, d_argmax=None, d_rank=None) -> cpa_result:
+    res = cpa_result()
+    _check(_lib.cpa_finalize(ctx, _ptr(d_rho), _ptr(d_maxabs), _ptr(d_argmax), _ptr(d_rank),
+                             C.byref(res)), "cpa_finalize")
+    return res
+
+
+def cpa_reset(ctx):
+    _check(_lib.cpa_reset(ctx), "cpa_reset")
+
+
+def cpa_sync(ctx):
+    _check(_lib.cpa_sync(ctx), "cpa_sync")
+
+
+def cpa_destroy(ctx):
+    _check(_lib.cpa_destroy(ctx), "cpa_destroy")
+
+
+def cpa_set_option(ctx, option: int, value: int):
+    _check(_lib.cpa_set_option(ctx, option, value), "cpa_set_option")
+
+
+def cpa_launch_count(ctx) -> int:
+    return _lib.cpa_launch_count(ctx)
+
+
+def cpa_status_str(st: int) -> str:
+    return _lib.cpa_status_str(st).decode()
+
+
+def cpa_last_error() -> str:
+    return _lib.cpa_last_error().decode()
+
+
+def cpa_aes_expand_key(key: bytes) -> list[bytes]:
+    k = (C.c_uint8 * 16).from_buffer_copy(bytes(key))
+    rk = (C.c_uint8 * 176)()
+    _lib.cpa_aes_expand_key(k, rk)
+    raw = bytes(rk)
+    return [raw[16 * r:16 * r + 16] for r in range(11)]
+
+
+def cpa_aes_invert_key_schedule(rk: bytes, round_index: int = 10) -> bytes:
+    r = (C.c_uint8 * 16).from_buffer_copy(bytes(rk))
+    k = (C.c_uint8 * 16)()
+    _lib.cpa_aes_invert_key_schedule(r, round_index, k)
+    return bytes(k)

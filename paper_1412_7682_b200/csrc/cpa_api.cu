@@ -1,0 +1,426 @@
+// cpa_api.cu -- the C ABI of libcpa.so (declared and documented in
+// include/cpa.h): context, argument validation, TMA descriptor set-up and the
+// launch sequence of the hot path
+//   cpa_accumulate: a3 model sums -> a4 trace moments -> a5 cross term
+//   cpa_finalize:   a8 Eq. (1) + per-(b,k) max|rho| -> a9 per-byte ranking
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/cpa.h"
+#include "kernels.h"
+#include "tables.h"
+#include "xterm_f32.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+cpa_status fail(cpa_status s, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+cpa_status cuda_fail(cudaError_t e, const char *where)
+{
+    return fail(CPA_E_CUDA, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr, where)                        \
+    do {                                             \
+        cudaError_t e_ = (expr);                     \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+    } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+constexpr int64_t kMaxTraces = 1LL << 23;  // exact-int64 bound of Eq. (1), see DESIGN.md
+constexpr int32_t kMaxSamples = 1 << 22;
+constexpr int64_t kHostChunk = 1LL << 18;  // traces per staging buffer (cpa_accumulate_host)
+
+}  // namespace
+
+struct cpa_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    int32_t M = 0;
+    cpa_dtype dtype = CPA_S8;
+    cpa_model model = CPA_HD_LAST;
+    void *accum = nullptr;
+    uint8_t *d_vtab = nullptr;
+    double *d_sqrt_dw = nullptr;
+    double *d_maxabs = nullptr, *d_peak = nullptr, *d_best_rho = nullptr;
+    int32_t *d_argmax = nullptr, *d_rank = nullptr, *d_best = nullptr;
+    int64_t kchunk = 0;
+    int64_t launches = 0;
+    // cpa_accumulate_host staging
+    void *d_stage[2] = {nullptr, nullptr};
+    uint8_t *d_stage_tx[2] = {nullptr, nullptr};
+    int64_t stage_bytes = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+    cpa::XtermF32Scratch f32;  // float-path scratch
+};
+
+extern "C" {
+
+size_t cpa_accum_words(int32_t M) { return (size_t)4098 * (size_t)M + 8193; }
+size_t cpa_accum_bytes(int32_t M) { return cpa_accum_words(M) * 8; }
+size_t cpa_accum_offset(int32_t M, int field)
+{
+    const size_t m = (size_t)M;
+    switch (field) {
+    case 0: return 0;
+    case 1: return 4096 * m;
+    case 2: return 4097 * m;
+    case 3: return 4098 * m;
+    case 4: return 4098 * m + 4096;
+    case 5: return 4098 * m + 8192;
+    default: return (size_t)-1;
+    }
+}
+
+const char *cpa_status_str(cpa_status s)
+{
+    switch (s) {
+    case CPA_OK: return "CPA_OK";
+    case CPA_E_INVALID_ARG: return "CPA_E_INVALID_ARG";
+    case CPA_E_BAD_STATE: return "CPA_E_BAD_STATE";
+    case CPA_E_CUDA: return "CPA_E_CUDA";
+    case CPA_E_NO_MEMORY: return "CPA_E_NO_MEMORY";
+    case CPA_E_TOO_FEW_TRACES: return "CPA_E_TOO_FEW_TRACES";
+    case CPA_E_OVERFLOW: return "CPA_E_OVERFLOW";
+    case CPA_E_UNSUPPORTED_DEVICE: return "CPA_E_UNSUPPORTED_DEVICE";
+    }
+    return "CPA_E_UNKNOWN";
+}
+
+const char *cpa_last_error(void) { return g_err; }
+
+void cpa_aes_expand_key(const uint8_t key[16], uint8_t round_keys[11][16]) { cpa::aes_expand_key(key, round_keys); }
+void cpa_aes_invert_key_schedule(const uint8_t rk[16], int round, uint8_t key[16])
+{
+    cpa::aes_invert_key_schedule(rk, round, key);
+}
+
+int64_t cpa_launch_count(const cpa_ctx *ctx) { return ctx ? ctx->launches : -1; }
+
+cpa_status cpa_reset(cpa_ctx *ctx)
+{
+    if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
+    CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CUDA_TRY(cudaMemsetAsync(ctx->accum, 0, cpa_accum_bytes(ctx->M), ctx->stream), "reset accumulator");
+    return CPA_OK;
+}
+
+cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, int device, void *stream,
+                    void *d_accum)
+{
+    if (!out) return fail(CPA_E_INVALID_ARG, "out is null");
+    *out = nullptr;
+    if (M < 1 || M > kMaxSamples) return fail(CPA_E_INVALID_ARG, "M=%d outside [1, %d]", M, kMaxSamples);
+    if (dtype != CPA_S8 && dtype != CPA_U8 && dtype != CPA_F32) return fail(CPA_E_INVALID_ARG, "bad dtype %d", (int)dtype);
+    if (model != CPA_HD_LAST && model != CPA_HW_LAST && model != CPA_HW_FIRST)
+        return fail(CPA_E_INVALID_ARG, "bad model %d", (int)model);
+    if (!d_accum || ((uintptr_t)d_accum & 255)) return fail(CPA_E_INVALID_ARG, "d_accum null or not 256-byte aligned");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) return fail(CPA_E_INVALID_ARG, "device %d of %d", device, ndev);
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(CPA_E_UNSUPPORTED_DEVICE, "device %d is sm_%d%d; libcpa is built for sm_100a only", device,
+                    prop.major, prop.minor);
+    if (!get_encode()) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
+
+    cpa_ctx *c = new (std::nothrow) cpa_ctx();
+    if (!c) return fail(CPA_E_NO_MEMORY, "context allocation");
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    c->stream = (cudaStream_t)stream;
+    c->M = M;
+    c->dtype = dtype;
+    c->model = model;
+    c->accum = d_accum;
+
+    uint8_t vt[65536];
+    cpa::build_vtable((int)model, vt);
+    cudaError_t e = cudaMalloc(&c->d_vtab, 65536);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_sqrt_dw, sizeof(double) * M);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_maxabs, sizeof(double) * 4096);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_peak, sizeof(double) * 4096);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_best_rho, sizeof(double) * 16);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_argmax, sizeof(int32_t) * 4096);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_rank, sizeof(int32_t) * 4096);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_best, sizeof(int32_t) * 32);
+    if (e != cudaSuccess) {
+        cpa_destroy(c);
+        return fail(CPA_E_NO_MEMORY, "device scratch: %s", cudaGetErrorString(e));
+    }
+    e = cudaMemcpyAsync(c->d_vtab, vt, 65536, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_accum, 0, cpa_accum_bytes(M), c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+        cpa_destroy(c);
+        return cuda_fail(e, "cpa_init upload");
+    }
+    *out = c;
+    return CPA_OK;
+}
+
+cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
+{
+    if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
+    if (option == CPA_OPT_KCHUNK) {
+        if (value < 0 || value % 64 || value > (1 << 20))
+            return fail(CPA_E_INVALID_ARG, "KCHUNK=%lld must be a multiple of 64 in [0, 2^20]", (long long)value);
+        ctx->kchunk = value;
+        return CPA_OK;
+    }
+    return fail(CPA_E_INVALID_ARG, "unknown option %d", option);
+}
+
+static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, const uint8_t *d_tx, int64_t n)
+{
+    const int M = c->M;
+    int launches = 0;
+    if (c->dtype == CPA_F32) {
+        double *acc = (double *)c->accum;
+        CUDA_TRY(cpa::launch_modelsums_f64(d_tx, n, c->d_vtab, acc + cpa_accum_offset(M, 3),
+                                           acc + cpa_accum_offset(M, 4), acc + cpa_accum_offset(M, 5),
+                                           c->stream, &launches),
+                 "modelsums");
+        cudaError_t e = cpa::xterm_f32_accumulate(c->f32, (const float *)d_w, ld, d_tx, n, M, c->d_vtab,
+                                                  acc, c->num_sms, c->stream, &launches);
+        c->launches += launches;
+        if (e != cudaSuccess) return cuda_fail(e, "float-path cross term");
+        return CPA_OK;
+    }
+    int64_t *acc = (int64_t *)c->accum;
+    const bool sgn = c->dtype == CPA_S8;
+    CUDA_TRY(cpa::launch_modelsums(d_tx, n, c->d_vtab, acc + cpa_accum_offset(M, 3), acc + cpa_accum_offset(M, 4),
+                                   acc + cpa_accum_offset(M, 5), c->stream, &launches),
+             "modelsums");
+    CUDA_TRY(cpa::launch_moments_i8(d_w, ld, n, M, sgn, acc + cpa_accum_offset(M, 1), acc + cpa_accum_offset(M, 2),
+                                    c->stream, &launches),
+             "moments");
+    CUtensorMap tmap;
+    cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)n};
+    cuuint64_t strides[1] = {(cuuint64_t)ld};
+    cuuint32_t box[2] = {128, 64};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode()(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(d_w), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    const int64_t kc = c->kchunk ? c->kchunk : cpa::xterm_i8_auto_kchunk(M, n, c->num_sms);
+    CUDA_TRY(cpa::launch_xterm_i8(tmap, d_tx, c->d_vtab, acc, M, n, kc, sgn, c->num_sms, c->stream, &launches),
+             "xterm_i8");
+    c->launches += launches;
+    return CPA_OK;
+}
+
+static cpa_status check_accumulate_args(cpa_ctx *c, const void *w, int64_t ld, const uint8_t *tx, int64_t n,
+                                        bool device)
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    if (n < 0) return fail(CPA_E_INVALID_ARG, "N=%lld < 0", (long long)n);
+    if (n == 0) return CPA_OK;
+    if (!w || !tx) return fail(CPA_E_INVALID_ARG, "null traces or texts");
+    if (n > kMaxTraces) return fail(CPA_E_OVERFLOW, "N=%lld per call exceeds 2^23", (long long)n);
+    if (ld < c->M) return fail(CPA_E_INVALID_ARG, "ld=%lld < M=%d", (long long)ld, c->M);
+    const int64_t esz = c->dtype == CPA_F32 ? 4 : 1;
+    (void)device;
+    (void)esz;
+    return CPA_OK;
+}
+
+static cpa_status accumulate_staged(cpa_ctx *c, const void *src, int64_t ld, const uint8_t *tx, int64_t N);
+
+cpa_status cpa_accumulate(cpa_ctx *c, const void *d_traces, int64_t ld, const uint8_t *d_texts, int64_t N)
+{
+    cpa_status st = check_accumulate_args(c, d_traces, ld, d_texts, N, false);
+    if (st != CPA_OK || N == 0) return st;
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    const int64_t esz = c->dtype == CPA_F32 ? 4 : 1;
+    if (((uintptr_t)d_traces & 15) || ((ld * esz) & 15) || ((uintptr_t)d_texts & 15))
+        return accumulate_staged(c, d_traces, ld, d_texts, N);  // TMA needs 16-byte strides
+    return accumulate_device(c, d_traces, ld, d_texts, N);
+}
+
+// Stream (host or unaligned device) traces through the library's staging
+// buffers: a pitched copy into a 16-byte aligned layout, double-buffered so
+// the copy of chunk c+1 overlaps the kernels of chunk c.
+static cpa_status accumulate_staged(cpa_ctx *c, const void *src, int64_t ld, const uint8_t *tx, int64_t N)
+{
+    const int64_t esz = c->dtype == CPA_F32 ? 4 : 1;
+    const int64_t ldd = (c->M * esz + 15) / 16 * 16 / esz;  // packed device row stride
+    const int64_t chunk = N < kHostChunk ? N : kHostChunk;
+    const int64_t need = chunk * ldd * esz;
+    if (c->stage_bytes < need) {
+        CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+        for (int k = 0; k < 2; k++) {
+            cudaFree(c->d_stage[k]);
+            cudaFree(c->d_stage_tx[k]);
+            c->d_stage[k] = nullptr;
+            c->d_stage_tx[k] = nullptr;
+        }
+        c->stage_bytes = 0;
+        for (int k = 0; k < 2; k++) {
+            if (cudaMalloc(&c->d_stage[k], need) != cudaSuccess ||
+                cudaMalloc(&c->d_stage_tx[k], chunk * 16) != cudaSuccess)
+                return fail(CPA_E_NO_MEMORY, "staging buffers (%lld bytes)", (long long)need);
+        }
+        c->stage_bytes = need;
+        if (!c->copy_stream) {
+            CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "copy stream");
+            for (int k = 0; k < 2; k++) {
+                CUDA_TRY(cudaEventCreateWithFlags(&c->ev_copied[k], cudaEventDisableTiming), "event");
+                CUDA_TRY(cudaEventCreateWithFlags(&c->ev_used[k], cudaEventDisableTiming), "event");
+            }
+        }
+    }
+    // the copy stream must not overwrite a buffer earlier compute still reads
+    CUDA_TRY(cudaEventRecord(c->ev_used[0], c->stream), "event");
+    CUDA_TRY(cudaEventRecord(c->ev_used[1], c->stream), "event");
+    int k = 0;
+    for (int64_t i0 = 0; i0 < N; i0 += chunk, k ^= 1) {
+        const int64_t n = (N - i0) < chunk ? (N - i0) : chunk;
+        CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev_used[k], 0), "wait");
+        CUDA_TRY(cudaMemcpy2DAsync(c->d_stage[k], ldd * esz, (const uint8_t *)src + i0 * ld * esz, ld * esz,
+                                   c->M * esz, n, cudaMemcpyDefault, c->copy_stream),
+                 "copy traces");
+        CUDA_TRY(cudaMemcpyAsync(c->d_stage_tx[k], tx + i0 * 16, n * 16, cudaMemcpyDefault, c->copy_stream),
+                 "copy texts");
+        CUDA_TRY(cudaEventRecord(c->ev_copied[k], c->copy_stream), "event");
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_copied[k], 0), "wait");
+        cpa_status st = accumulate_device(c, c->d_stage[k], ldd, c->d_stage_tx[k], n);
+        if (st != CPA_OK) return st;
+        CUDA_TRY(cudaEventRecord(c->ev_used[k], c->stream), "event");
+    }
+    return CPA_OK;
+}
+
+cpa_status cpa_accumulate_host(cpa_ctx *c, const void *h_traces, int64_t ld, const uint8_t *h_texts, int64_t N)
+{
+    cpa_status st = check_accumulate_args(c, h_traces, ld, h_texts, N, false);
+    if (st != CPA_OK || N == 0) return st;
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    st = accumulate_staged(c, h_traces, ld, h_texts, N);
+    if (st != CPA_OK) return st;
+    CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+    return CPA_OK;
+}
+
+cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_argmax, int32_t *d_rank,
+                        cpa_result *res)
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    const int M = c->M;
+    int64_t n = 0;
+    if (c->dtype == CPA_F32) {
+        double dn = 0;
+        CUDA_TRY(cudaMemcpyAsync(&dn, (double *)c->accum + cpa_accum_offset(M, 5), 8, cudaMemcpyDeviceToHost, c->stream),
+                 "read N");
+        CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+        n = (int64_t)dn;
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(&n, (int64_t *)c->accum + cpa_accum_offset(M, 5), 8, cudaMemcpyDeviceToHost, c->stream),
+                 "read N");
+        CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+    }
+    if (n < 2) return fail(CPA_E_TOO_FEW_TRACES, "N=%lld < 2: Eq. (1) undefined", (long long)n);
+    if (c->dtype != CPA_F32 && n > kMaxTraces)
+        return fail(CPA_E_OVERFLOW, "N=%lld > 2^23: Eq. (1) intermediates may overflow int64", (long long)n);
+    cpa::FinalizeOut o;
+    o.rho = d_rho;
+    o.maxabs = d_maxabs ? d_maxabs : c->d_maxabs;
+    o.argmax = d_argmax ? d_argmax : c->d_argmax;
+    o.rank = d_rank ? d_rank : c->d_rank;
+    o.peak = c->d_peak;
+    o.best = c->d_best;
+    o.best_rho = c->d_best_rho;
+    int launches = 0;
+    if (c->dtype == CPA_F32)
+        CUDA_TRY(cpa::launch_finalize_f64((const double *)c->accum, M, c->d_sqrt_dw, o, c->stream, &launches), "finalize");
+    else
+        CUDA_TRY(cpa::launch_finalize_i8((const int64_t *)c->accum, M, c->d_sqrt_dw, o, c->stream, &launches), "finalize");
+    CUDA_TRY(cpa::launch_phase4(o, c->stream, &launches), "phase4");
+    c->launches += launches;
+    int32_t best[32];
+    double brho[16];
+    CUDA_TRY(cudaMemcpyAsync(best, c->d_best, sizeof best, cudaMemcpyDeviceToHost, c->stream), "D2H best");
+    CUDA_TRY(cudaMemcpyAsync(brho, c->d_best_rho, sizeof brho, cudaMemcpyDeviceToHost, c->stream), "D2H best rho");
+    CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+    if (res) {
+        for (int b = 0; b < 16; b++) {
+            res->round_key[b] = (uint8_t)best[b];
+            res->peak_sample[b] = best[16 + b];
+            res->peak_rho[b] = brho[b];
+        }
+        if (c->model == CPA_HW_FIRST)
+            std::memcpy(res->master_key, res->round_key, 16);
+        else
+            cpa::aes_invert_key_schedule(res->round_key, 10, res->master_key);
+        res->n_traces = n;
+    }
+    return CPA_OK;
+}
+
+cpa_status cpa_sync(cpa_ctx *c)
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+    return CPA_OK;
+}
+
+cpa_status cpa_destroy(cpa_ctx *c)
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    cudaFree(c->d_vtab);
+    cudaFree(c->d_sqrt_dw);
+    cudaFree(c->d_maxabs);
+    cudaFree(c->d_peak);
+    cudaFree(c->d_best_rho);
+    cudaFree(c->d_argmax);
+    cudaFree(c->d_rank);
+    cudaFree(c->d_best);
+    for (int k = 0; k < 2; k++) {
+        cudaFree(c->d_stage[k]);
+        cudaFree(c->d_stage_tx[k]);
+        if (c->ev_copied[k]) cudaEventDestroy(c->ev_copied[k]);
+        if (c->ev_used[k]) cudaEventDestroy(c->ev_used[k]);
+    }
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    cpa::xterm_f32_free(c->f32);
+    delete c;
+    return CPA_OK;
+}
+
+}  // extern "C"

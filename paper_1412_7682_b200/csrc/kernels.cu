@@ -1,0 +1,381 @@
+// kernels.cu -- the HBM/latency-bound steps of the path:
+//   a3 model sums      sum_i H_i, sum_i H_i^2 per (b, k)            [P:75]
+//   a4 trace moments   sum_i W_ij, sum_i W_ij^2 per sample j        [P:79]
+//   a8 finalize        Eq. (1) [P:69] in fp64 + max |rho| per (b,k) [P:83]
+//   a9 phase 4         per-byte ranking / best sub-key              [P:87]
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "kernels.h"
+
+namespace cpa {
+namespace {
+
+__device__ __forceinline__ int shiftrows_src(int b) { return (b & 3) + 4 * (((b >> 2) + (b & 3)) & 3); }
+
+// ---------------------------------------------------------------------------
+// a3: one block = 16 warps (warp = key byte b), lane owns keys lane + 32 q.
+// H = V[c_s][c_b ^ k]; per-thread int32 partials, one int64 atomic per (b,k).
+// ---------------------------------------------------------------------------
+constexpr int MS_THREADS = 512;
+constexpr int MS_CHUNK = 2048;  // traces per block (int32-exact: 64 * 2048)
+constexpr int MS_STAGE = 256;   // traces staged in smem at a time
+
+template <typename Acc>
+__global__ void __launch_bounds__(MS_THREADS)
+k_modelsums(const uint8_t *__restrict__ texts, int64_t n, const uint8_t *__restrict__ vtab,
+            Acc *sum_h, Acc *sum_h2, Acc *count)
+{
+    extern __shared__ uint8_t sm[];
+    uint8_t *vs = sm;              // 64 KB
+    uint8_t *ts = sm + 65536;      // MS_STAGE x 16
+    for (int i = threadIdx.x; i < 4096; i += MS_THREADS) ((uint4 *)vs)[i] = ((const uint4 *)vtab)[i];
+    const int b = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sb = shiftrows_src(b);
+    int32_t s1[8], s2[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) s1[q] = s2[q] = 0;
+    const int64_t i0 = (int64_t)blockIdx.x * MS_CHUNK;
+    const int64_t i1 = min(n, i0 + MS_CHUNK);
+    for (int64_t base = i0; base < i1; base += MS_STAGE) {
+        __syncthreads();
+        const int cnt = (int)min((int64_t)MS_STAGE, i1 - base);
+        for (int t = threadIdx.x; t < cnt; t += MS_THREADS)
+            ((uint4 *)ts)[t] = ((const uint4 *)texts)[base + t];
+        __syncthreads();
+        for (int t = 0; t < cnt; t++) {
+            const uint32_t cb = ts[t * 16 + b], cs = ts[t * 16 + sb];
+            const uint8_t *vrow = vs + cs * 256;
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const int32_t h = vrow[cb ^ (uint32_t)(lane + 32 * q)];
+                s1[q] += h;
+                s2[q] += h * h;
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        const int hidx = b * 256 + lane + 32 * q;
+        if constexpr (std::is_integral<Acc>::value) {
+            atomicAdd((unsigned long long *)&sum_h[hidx], (unsigned long long)(long long)s1[q]);
+            atomicAdd((unsigned long long *)&sum_h2[hidx], (unsigned long long)(long long)s2[q]);
+        } else {
+            atomicAdd(&sum_h[hidx], (Acc)s1[q]);
+            atomicAdd(&sum_h2[hidx], (Acc)s2[q]);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if constexpr (std::is_integral<Acc>::value)
+            atomicAdd((unsigned long long *)count, (unsigned long long)n);
+        else
+            atomicAdd(count, (Acc)n);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a4: thread = 16 consecutive samples (one 16-byte vector per trace row) over
+// MO_ROWS rows; int32/uint32 partials (exact: 16384*4096, 65025*4096 < 2^32).
+// ---------------------------------------------------------------------------
+constexpr int MO_THREADS = 256;
+constexpr int MO_ROWS = 4096;
+
+template <bool SIGNED>
+__device__ __forceinline__ int32_t byte_at(uint32_t w, int k)
+{
+    if (SIGNED) return (int32_t)(w << (24 - 8 * k)) >> 24;
+    return (int32_t)((w >> (8 * k)) & 0xFF);
+}
+
+template <bool SIGNED>
+__global__ void __launch_bounds__(MO_THREADS)
+k_moments_i8(const uint8_t *__restrict__ w, int64_t ld, int64_t n, int32_t M,
+             unsigned long long *sum_w, unsigned long long *sum_w2)
+{
+    const int groups = (M + 15) >> 4;
+    const int g = blockIdx.x * MO_THREADS + threadIdx.x;
+    if (g >= groups) return;
+    const int j0 = g * 16;
+    const int64_t r0 = (int64_t)blockIdx.y * MO_ROWS;
+    const int64_t r1 = min(n, r0 + MO_ROWS);
+    int32_t s1[16];
+    uint32_t s2[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) { s1[q] = 0; s2[q] = 0; }
+    const uint8_t *col = w + j0;
+    int64_t r = r0;
+    for (; r + 4 <= r1; r += 4) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = __ldg((const uint4 *)(col + (r + u) * ld));
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint32_t ws[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int q = 0; q < 16; q++) {
+                const int32_t x = byte_at<SIGNED>(ws[q >> 2], q & 3);
+                s1[q] += x;
+                s2[q] += (uint32_t)(x * x);
+            }
+        }
+    }
+    for (; r < r1; r++) {
+        const uint4 v = __ldg((const uint4 *)(col + r * ld));
+        const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+            const int32_t x = byte_at<SIGNED>(ws[q >> 2], q & 3);
+            s1[q] += x;
+            s2[q] += (uint32_t)(x * x);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+        if (j0 + q < M) {
+            atomicAdd(&sum_w[j0 + q], (unsigned long long)(long long)s1[q]);
+            atomicAdd(&sum_w2[j0 + q], (unsigned long long)s2[q]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a8: Eq. (1) with the fixed, FMA-free fp64 sequence of DESIGN.md:
+//   num = N*S_hw - S_h*S_w ; dw = N*S_w2 - S_w^2 ; dh = N*S_h2 - S_h^2 (int64)
+//   rho = (double)num / (sqrt((double)dw) * sqrt((double)dh)), 0 if dw or dh
+//   is 0, clamped to [-1, 1].  Host guarantees N <= 2^23 so all fit int64.
+// ---------------------------------------------------------------------------
+__global__ void k_sqrt_dw_i8(const int64_t *__restrict__ sw, const int64_t *__restrict__ sw2,
+                             const int64_t *__restrict__ count, int32_t M, double *out)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    const int64_t n = *count;
+    const int64_t dw = n * sw2[j] - sw[j] * sw[j];
+    out[j] = __dsqrt_rn(__ll2double_rn(dw));
+}
+
+struct Best {
+    double v;   // |rho|
+    double r;   // signed rho
+    int j;
+};
+__device__ __forceinline__ bool better(const Best &a, const Best &b)
+{
+    return a.v > b.v || (a.v == b.v && a.j < b.j);
+}
+__device__ __forceinline__ Best warp_best(Best x)
+{
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        Best y;
+        y.v = __shfl_xor_sync(0xffffffffu, x.v, off);
+        y.r = __shfl_xor_sync(0xffffffffu, x.r, off);
+        y.j = __shfl_xor_sync(0xffffffffu, x.j, off);
+        if (better(y, x)) x = y;
+    }
+    return x;
+}
+
+constexpr int FIN_THREADS = 256;
+
+__device__ __forceinline__ void block_best_store(Best best, int h, const FinalizeOut &o)
+{
+    __shared__ Best red[FIN_THREADS / 32];
+    best = warp_best(best);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        Best x = threadIdx.x < FIN_THREADS / 32 ? red[threadIdx.x] : Best{-1.0, 0.0, 0x7fffffff};
+        x = warp_best(x);
+        if (threadIdx.x == 0) {
+            o.maxabs[h] = x.v;
+            o.argmax[h] = x.j;
+            o.peak[h] = x.r;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(FIN_THREADS)
+k_finalize_i8(const int64_t *__restrict__ hw, const int64_t *__restrict__ sw,
+              const int64_t *__restrict__ sh, const int64_t *__restrict__ sh2,
+              const int64_t *__restrict__ count, const double *__restrict__ sqrt_dw, int32_t M,
+              FinalizeOut o)
+{
+    const int h = blockIdx.x;
+    const int64_t n = *count;
+    const int64_t s_h = sh[h];
+    const int64_t dh = n * sh2[h] - s_h * s_h;
+    const double den_h = __dsqrt_rn(__ll2double_rn(dh));
+    const int64_t *row = hw + (int64_t)h * M;
+    double *rrow = o.rho ? o.rho + (int64_t)h * M : nullptr;
+    Best best{-1.0, 0.0, 0x7fffffff};
+    for (int j = threadIdx.x; j < M; j += FIN_THREADS) {
+        const double den_w = sqrt_dw[j];
+        double r = 0.0;
+        if (den_w != 0.0 && den_h != 0.0) {
+            const int64_t num = n * row[j] - s_h * sw[j];
+            r = __ddiv_rn(__ll2double_rn(num), __dmul_rn(den_w, den_h));
+            r = fmin(1.0, fmax(-1.0, r));
+        }
+        if (rrow) rrow[j] = r;
+        const double a = fabs(r);
+        if (a > best.v) best = Best{a, r, j};
+    }
+    block_best_store(best, h, o);
+}
+
+// float path: all sums fp64 (same shape as the int accumulator)
+__global__ void k_sqrt_dw_f64(const double *__restrict__ sw, const double *__restrict__ sw2,
+                              const double *__restrict__ count, int32_t M, double *out)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    const double n = *count;
+    const double dw = __dsub_rn(__dmul_rn(n, sw2[j]), __dmul_rn(sw[j], sw[j]));
+    // degenerate column [S:293]: dw <= 1e-12 * N * S_w2 -> rho = 0 (marked by 0)
+    out[j] = (dw > __dmul_rn(1e-12, __dmul_rn(n, sw2[j]))) ? __dsqrt_rn(dw) : 0.0;
+}
+
+__global__ void __launch_bounds__(FIN_THREADS)
+k_finalize_f64(const double *__restrict__ hw, const double *__restrict__ sw,
+               const double *__restrict__ sh, const double *__restrict__ sh2,
+               const double *__restrict__ count, const double *__restrict__ sqrt_dw, int32_t M,
+               FinalizeOut o)
+{
+    const int h = blockIdx.x;
+    const double n = *count;
+    const double s_h = sh[h];
+    const double dh = __dsub_rn(__dmul_rn(n, sh2[h]), __dmul_rn(s_h, s_h));
+    const double den_h = dh > 0.0 ? __dsqrt_rn(dh) : 0.0;
+    const double *row = hw + (int64_t)h * M;
+    double *rrow = o.rho ? o.rho + (int64_t)h * M : nullptr;
+    Best best{-1.0, 0.0, 0x7fffffff};
+    for (int j = threadIdx.x; j < M; j += FIN_THREADS) {
+        const double den_w = sqrt_dw[j];
+        double r = 0.0;
+        if (den_w != 0.0 && den_h != 0.0) {
+            const double num = __dsub_rn(__dmul_rn(n, row[j]), __dmul_rn(s_h, sw[j]));
+            r = __ddiv_rn(num, __dmul_rn(den_w, den_h));
+            r = fmin(1.0, fmax(-1.0, r));
+        }
+        if (rrow) rrow[j] = r;
+        const double a = fabs(r);
+        if (a > best.v) best = Best{a, r, j};
+    }
+    block_best_store(best, h, o);
+}
+
+// ---------------------------------------------------------------------------
+// a9: per byte b (block), thread k: rank = 1 + #{k' better than k}
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_phase4(FinalizeOut o)
+{
+    __shared__ double m[256];
+    const int b = blockIdx.x, k = threadIdx.x;
+    m[k] = o.maxabs[b * 256 + k];
+    __syncthreads();
+    const double mk = m[k];
+    int r = 1;
+    for (int k2 = 0; k2 < 256; k2++) {
+        const double a = m[k2];
+        r += (a > mk || (a == mk && k2 < k)) ? 1 : 0;
+    }
+    o.rank[b * 256 + k] = r;
+    if (r == 1) {
+        o.best[b] = k;
+        o.best[16 + b] = o.argmax[b * 256 + k];
+        o.best_rho[b] = o.peak[b * 256 + k];
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_modelsums(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab, int64_t *d_sum_h,
+                             int64_t *d_sum_h2, int64_t *d_count, cudaStream_t s, int *launches)
+{
+    static bool attr = false;
+    const int smem = 65536 + MS_STAGE * 16;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_modelsums<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int blocks = (int)((n + MS_CHUNK - 1) / MS_CHUNK);
+    k_modelsums<int64_t><<<blocks, MS_THREADS, smem, s>>>(d_texts, n, d_vtab, d_sum_h, d_sum_h2, d_count);
+    if (launches) (*launches)++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_modelsums_f64(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab, double *d_sum_h,
+                                 double *d_sum_h2, double *d_count, cudaStream_t s, int *launches)
+{
+    static bool attr = false;
+    const int smem = 65536 + MS_STAGE * 16;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_modelsums<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int blocks = (int)((n + MS_CHUNK - 1) / MS_CHUNK);
+    k_modelsums<double><<<blocks, MS_THREADS, smem, s>>>(d_texts, n, d_vtab, d_sum_h, d_sum_h2, d_count);
+    if (launches) (*launches)++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M, bool w_signed,
+                              int64_t *d_sum_w, int64_t *d_sum_w2, cudaStream_t s, int *launches)
+{
+    const int groups = (M + 15) / 16;
+    dim3 grid((groups + MO_THREADS - 1) / MO_THREADS, (unsigned)((n + MO_ROWS - 1) / MO_ROWS));
+    if (w_signed)
+        k_moments_i8<true><<<grid, MO_THREADS, 0, s>>>((const uint8_t *)d_w, ld, n, M,
+                                                        (unsigned long long *)d_sum_w,
+                                                        (unsigned long long *)d_sum_w2);
+    else
+        k_moments_i8<false><<<grid, MO_THREADS, 0, s>>>((const uint8_t *)d_w, ld, n, M,
+                                                         (unsigned long long *)d_sum_w,
+                                                         (unsigned long long *)d_sum_w2);
+    if (launches) (*launches)++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_i8(const int64_t *d_accum, int32_t M, double *d_sqrt_dw, const FinalizeOut &o,
+                               cudaStream_t s, int *launches)
+{
+    const int64_t *hw = d_accum;
+    const int64_t *sw = d_accum + 4096LL * M;
+    const int64_t *sw2 = sw + M;
+    const int64_t *sh = sw2 + M;
+    const int64_t *sh2 = sh + 4096;
+    const int64_t *cnt = sh2 + 4096;
+    k_sqrt_dw_i8<<<(M + 255) / 256, 256, 0, s>>>(sw, sw2, cnt, M, d_sqrt_dw);
+    k_finalize_i8<<<4096, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o);
+    if (launches) (*launches) += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_f64(const double *d_accum, int32_t M, double *d_sqrt_dw, const FinalizeOut &o,
+                                cudaStream_t s, int *launches)
+{
+    const double *hw = d_accum;
+    const double *sw = d_accum + 4096LL * M;
+    const double *sw2 = sw + M;
+    const double *sh = sw2 + M;
+    const double *sh2 = sh + 4096;
+    const double *cnt = sh2 + 4096;
+    k_sqrt_dw_f64<<<(M + 255) / 256, 256, 0, s>>>(sw, sw2, cnt, M, d_sqrt_dw);
+    k_finalize_f64<<<4096, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o);
+    if (launches) (*launches) += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_phase4(const FinalizeOut &o, cudaStream_t s, int *launches)
+{
+    k_phase4<<<16, 256, 0, s>>>(o);
+    if (launches) (*launches)++;
+    return cudaGetLastError();
+}
+
+}  // namespace cpa

@@ -1,0 +1,45 @@
+// kernels.h -- internal launchers of libcpa (not part of the C ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace cpa {
+
+// a3: Phase 1 model sums [P:75]; also adds n to the trace count word.
+cudaError_t launch_modelsums(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab,
+                             int64_t *d_sum_h, int64_t *d_sum_h2, int64_t *d_count,
+                             cudaStream_t s, int *launches);
+cudaError_t launch_modelsums_f64(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab,
+                                 double *d_sum_h, double *d_sum_h2, double *d_count,
+                                 cudaStream_t s, int *launches);
+
+// a4: Phase 2 trace moments sum W, sum W^2 [P:79] (int8 traces, exact int64)
+cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M, bool w_signed,
+                              int64_t *d_sum_w, int64_t *d_sum_w2, cudaStream_t s, int *launches);
+
+// a5: cross term (tcgen05 kind::i8)
+int xterm_i8_smem_bytes();
+int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms);
+cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
+                            int64_t *d_hw, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
+                            int num_sms, cudaStream_t stream, int *launches);
+
+// a8/a9: Phase 3 + 4 [P:81-87]
+struct FinalizeOut {
+    double *rho;       // optional [4096][M]
+    double *maxabs;    // [4096]
+    int32_t *argmax;   // [4096]
+    double *peak;      // [4096] signed rho at argmax
+    int32_t *rank;     // [4096]
+    int32_t *best;     // [16] best k, [16] peak sample (packed: best[0..15], best[16..31])
+    double *best_rho;  // [16]
+};
+cudaError_t launch_finalize_i8(const int64_t *d_accum, int32_t M, double *d_sqrt_dw,
+                               const FinalizeOut &o, cudaStream_t s, int *launches);
+cudaError_t launch_finalize_f64(const double *d_accum, int32_t M, double *d_sqrt_dw,
+                                const FinalizeOut &o, cudaStream_t s, int *launches);
+cudaError_t launch_phase4(const FinalizeOut &o, cudaStream_t s, int *launches);
+
+}  // namespace cpa

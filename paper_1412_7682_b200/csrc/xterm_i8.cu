@@ -1,0 +1,329 @@
+// xterm_i8.cu -- the dominant Phase-2 term [P:79]:
+//     sum_hw[h][j] = sum_i H_i(h) * W[i][j]      (h = 256 b + k, 4096 rows)
+// as a 4096 x N . N x M contraction on the sm_100a tensor cores
+// (tcgen05.mma kind::i8, exact int32 accumulation in TMEM, spilled to int64).
+//
+// The paper computed this serially per (k, b, j) thread [P:121]; here:
+//   * A = H tile (128 sub-keys x 64 traces, u8, MN-major) is GENERATED in
+//     shared memory from the ciphertext bytes:  H[k] = V[c_s][c_b ^ k] with
+//     V[y][x] = HW(InvS[x] ^ y) (64 KB table in smem), so one 16-byte chunk of
+//     16 consecutive keys is a 16-byte chunk of row V[c_s], byte-permuted by
+//     (c_b & 15) -- one LDS.128 + 4 SEL + 4 PRMT + one STS.128 per chunk.
+//   * B = W tile (64 traces x 256 samples, s8/u8, MN-major = the caller's
+//     trace-major layout, no transpose) arrives by TMA with 128-byte swizzle.
+//   * D = 128 x 256 int32 in TMEM, double-buffered (512 columns) so the
+//     epilogue of one work unit overlaps the MMAs of the next.
+//   * Work unit = (32 hypothesis tiles) x (M/256 sample tiles) x (trace
+//     chunks); hypothesis tile fastest so co-resident CTAs share W in L2.
+//     Units spill with red.global.add.u64 -- integer adds are associative, so
+//     the int64 sums are bit-exact for any split / order.
+// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM owner,
+// w4-7 epilogue (TMEM lanes 32*(w%4)...), w8-11 hypothesis generators.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace cpa {
+namespace {
+
+constexpr int BM = 128;           // sub-keys per tile (MMA M)
+constexpr int BN = 256;           // samples per tile (MMA N)
+constexpr int BK = 64;            // traces per pipeline stage
+constexpr int MMA_K = 32;         // kind::i8 K per instruction
+constexpr int STAGES = 5;
+constexpr int A_BYTES = BK * BM;              // 8 KB
+constexpr int B_BYTES = BK * BN;              // 16 KB (two 128-sample TMA boxes)
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int V_BYTES = 65536;
+constexpr int EPI_WARPS = 4;
+constexpr int TB_BYTES = EPI_WARPS * 32 * 33 * 4;
+constexpr int SMEM_V = 0;
+constexpr int SMEM_STAGE = SMEM_V + V_BYTES;
+constexpr int SMEM_TB = SMEM_STAGE + STAGES * STAGE_BYTES;
+constexpr int SMEM_BAR = SMEM_TB + TB_BYTES;
+constexpr int NUM_BARS = 2 * STAGES + 4;
+constexpr int SMEM_TOTAL = SMEM_BAR + NUM_BARS * 8 + 16;
+constexpr int SMEM_ALLOC = SMEM_TOTAL + 1024;  // slack for 1024-byte alignment
+constexpr int THREADS = 384;
+constexpr uint32_t TMEM_COLS = 512;
+
+struct Params {
+    const uint8_t *texts;    // N x 16
+    const uint8_t *vtab;     // 256 x 256 (global copy of V)
+    unsigned long long *hw;  // sum_hw [4096][M]
+    int32_t M;
+    int32_t n_tiles;
+    int32_t kc_count;
+    int32_t units;
+    int64_t N;
+    int64_t kc_len;
+    uint32_t idesc;
+};
+
+__device__ __forceinline__ void unit_coords(const Params &p, int u, int &hyp_tile, int &n_tile,
+                                            int64_t &t0, int64_t &t1)
+{
+    hyp_tile = u & 31;
+    int r = u >> 5;
+    n_tile = r % p.n_tiles;
+    int kc = r / p.n_tiles;
+    t0 = (int64_t)kc * p.kc_len;
+    t1 = t0 + p.kc_len;
+    if (t1 > p.N) t1 = p.N;
+}
+
+__device__ __forceinline__ int shiftrows_src(int b) { return (b & 3) + 4 * (((b >> 2) + (b & 3)) & 3); }
+
+__global__ void __launch_bounds__(THREADS, 1)
+k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
+{
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const uint32_t sbase = smem_u32(smem);
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    auto full_bar = [&](int s) { return sbase + SMEM_BAR + 8 * s; };
+    auto empty_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (STAGES + s); };
+    auto tfull_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (2 * STAGES + a); };
+    auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (2 * STAGES + 2 + a); };
+    uint32_t *tmem_slot = (uint32_t *)(smem + SMEM_BAR + NUM_BARS * 8);
+
+    // ---- setup: V table to smem, barriers, TMEM ----
+    {
+        const uint4 *src = (const uint4 *)p.vtab;
+        uint4 *dst = (uint4 *)(smem + SMEM_V);
+        for (int i = threadIdx.x; i < V_BYTES / 16; i += THREADS) dst[i] = src[i];
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmap_w);
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(full_bar(s), 1 + 4);  // TMA expect_tx arrive + 4 generator warps
+            mbar_init(empty_bar(s), 1);     // tcgen05.commit
+        }
+        for (int a = 0; a < 2; a++) {
+            mbar_init(tfull_bar(a), 1);
+            mbar_init(tempty_bar(a), EPI_WARPS);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<TMEM_COLS>(smem_u32(tmem_slot));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ================= TMA producer (W tiles) =================
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                int ht, nt;
+                int64_t t0, t1;
+                unit_coords(p, u, ht, nt, t0, t1);
+                for (int64_t tb = t0; tb < t1; tb += BK, it++) {
+                    int s = it % STAGES;
+                    uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(empty_bar(s), ph ^ 1);
+                    uint32_t bdst = sbase + SMEM_STAGE + s * STAGE_BYTES + A_BYTES;
+                    mbar_arrive_expect_tx(full_bar(s), B_BYTES);
+                    tma_load_2d(bdst, &tmap_w, nt * BN, (int32_t)tb, full_bar(s));
+                    tma_load_2d(bdst + B_BYTES / 2, &tmap_w, nt * BN + 128, (int32_t)tb, full_bar(s));
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer (one thread) =================
+        if (lane == 0) {
+            uint32_t it = 0, t = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x, t++) {
+                int ht, nt;
+                int64_t t0, t1;
+                unit_coords(p, u, ht, nt, t0, t1);
+                const uint32_t acc = t & 1;
+                mbar_wait(tempty_bar(acc), ((t >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dtmem = tmem_base + acc * BN;
+                bool first = true;
+                for (int64_t tb = t0; tb < t1; tb += BK, it++) {
+                    int s = it % STAGES;
+                    uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(full_bar(s), ph);
+                    tc_fence_after();
+                    const uint32_t a_addr = sbase + SMEM_STAGE + s * STAGE_BYTES;
+                    const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / MMA_K; kk++) {
+                        // K step = 32 rows = 4 swizzle atoms of 8 rows x 128 B
+                        uint64_t ad = smem_desc_sw128(a_addr + kk * (MMA_K * 128), A_BYTES, 1024);
+                        uint64_t bd = smem_desc_sw128(b_addr + kk * (MMA_K * 128), B_BYTES / 2, 1024);
+                        mma_i8(dtmem, ad, bd, p.idesc, first ? 0u : 1u);
+                        first = false;
+                    }
+                    mma_commit(empty_bar(s));  // frees the smem stage when the MMAs finish
+                }
+                mma_commit(tfull_bar(acc));    // accumulator ready for the epilogue
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ================= epilogue: TMEM -> int64 global (red.add) =================
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        uint32_t *tb = (uint32_t *)(smem + SMEM_TB) + q * 32 * 33;
+        uint32_t t = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x, t++) {
+            int ht, nt;
+            int64_t t0, t1;
+            unit_coords(p, u, ht, nt, t0, t1);
+            const uint32_t acc = t & 1;
+            mbar_wait(tfull_bar(acc), (t >> 1) & 1);
+            tc_fence_after();
+            const int hrow0 = (ht >> 1) * 256 + (ht & 1) * BM + q * 32;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; c++) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int x = 0; x < 32; x++) tb[lane * 33 + x] = v[x];
+                __syncwarp();
+                const int j = nt * BN + c * 32 + lane;
+                if (j < p.M) {
+                    unsigned long long *dst = p.hw + (int64_t)hrow0 * p.M + j;
+#pragma unroll 4
+                    for (int r = 0; r < 32; r++) {
+                        long long val = (int32_t)tb[r * 33 + lane];
+                        atomicAdd(dst + (int64_t)r * p.M, (unsigned long long)val);
+                    }
+                }
+                __syncwarp();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_bar(acc));
+        }
+    } else if (warp >= 8) {
+        // ================= hypothesis generators (H tile, MN-major, swizzled) =================
+        const int g = warp - 8;
+        const int row = (g & 1) * 32 + lane;  // trace row within the stage
+        const int qh = g >> 1;                // which 4 of the 8 16-byte chunks of the row
+        const uint8_t *vs = smem + SMEM_V;
+        uint32_t it = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            int ht, nt;
+            int64_t t0, t1;
+            unit_coords(p, u, ht, nt, t0, t1);
+            const int b = ht >> 1;
+            const int s_idx = shiftrows_src(b);
+            const int chunk0 = (ht & 1) * 8;  // first global 16-key chunk of this tile
+            for (int64_t tb = t0; tb < t1; tb += BK, it++) {
+                int s = it % STAGES;
+                uint32_t ph = (it / STAGES) & 1;
+                const int64_t i = tb + row;
+                // per-trace parameters (loaded before the wait to hide latency)
+                uint32_t cb = 0, cs = 0;
+                const bool valid = i < t1;
+                if (valid) {
+                    const uint8_t *tx = p.texts + i * 16;
+                    cb = __ldg(tx + b);
+                    cs = __ldg(tx + s_idx);
+                }
+                const uint32_t hi = cb >> 4, lo = cb & 15, u4 = lo >> 2, v4 = lo & 3;
+                const uint32_t sel_e = (0x3210u ^ (v4 * 0x1111u)) ^ ((u4 & 1) ? 0x4444u : 0u);
+                const uint32_t sel_o = sel_e ^ 0x4444u;
+                const bool swap2 = (u4 & 2) != 0;
+                const uint8_t *vrow = vs + cs * 256;
+                mbar_wait(empty_bar(s), ph ^ 1);
+                uint8_t *arow = smem + SMEM_STAGE + s * STAGE_BYTES + row * 128;
+#pragma unroll
+                for (int qq = 0; qq < 4; qq++) {
+                    const int ql = qh * 4 + qq;  // chunk within the 128-key row
+                    uint4 outv = make_uint4(0, 0, 0, 0);
+                    if (valid) {
+                        const uint4 a = *(const uint4 *)(vrow + (((uint32_t)(chunk0 + ql) ^ hi) << 4));
+                        const uint32_t c0 = swap2 ? a.z : a.x, c1 = swap2 ? a.w : a.y;
+                        const uint32_t c2 = swap2 ? a.x : a.z, c3 = swap2 ? a.y : a.w;
+                        outv.x = __byte_perm(c0, c1, sel_e);
+                        outv.y = __byte_perm(c0, c1, sel_o);
+                        outv.z = __byte_perm(c2, c3, sel_e);
+                        outv.w = __byte_perm(c2, c3, sel_o);
+                    }
+                    *(uint4 *)(arow + ((ql ^ (row & 7)) << 4)) = outv;  // 128B swizzle
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(full_bar(s));
+            }
+        }
+    }
+
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<TMEM_COLS>(tmem_base);
+    }
+}
+
+}  // namespace
+
+int xterm_i8_smem_bytes() { return SMEM_ALLOC; }
+
+cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
+                            int64_t *d_hw, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
+                            int num_sms, cudaStream_t stream, int *launches)
+{
+    Params p;
+    p.texts = d_texts;
+    p.vtab = d_vtab;
+    p.hw = (unsigned long long *)d_hw;
+    p.M = M;
+    p.N = N;
+    p.n_tiles = (M + BN - 1) / BN;
+    p.kc_len = kc_len;
+    p.kc_count = (int32_t)((N + kc_len - 1) / kc_len);
+    p.units = 32 * p.n_tiles * p.kc_count;
+    p.idesc = idesc_i8(BM, BN, w_signed);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_xterm_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    int grid = p.units < num_sms ? p.units : num_sms;
+    k_xterm_i8<<<grid, THREADS, SMEM_ALLOC, stream>>>(tmap_w, p);
+    if (launches) (*launches)++;
+    return cudaGetLastError();
+}
+
+// The automatic split-K length: whole 64-trace stages, <= 2^20 traces (int32
+// TMEM accumulators stay exact: |H W| <= 8 * 255), and a unit count that fills
+// the SMs in as close to whole waves as possible.
+int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms)
+{
+    const int64_t tiles = 32LL * ((M + BN - 1) / BN);
+    const int64_t max_len = 1 << 20;
+    int64_t best_len = 0;
+    double best_eff = -1.0;
+    for (int64_t kc = 1; kc <= 256; kc++) {
+        int64_t len = (N + kc - 1) / kc;
+        len = (len + BK - 1) / BK * BK;
+        if (len > max_len) continue;
+        if (len < 4096 && kc > 1) break;  // keep units long enough to amortise the epilogue
+        int64_t kcount = (N + len - 1) / len;
+        int64_t units = tiles * kcount;
+        int64_t waves = (units + num_sms - 1) / num_sms;
+        double eff = (double)units / (double)(waves * num_sms);
+        if (eff > best_eff + 0.02) {  // prefer fewer chunks unless clearly better
+            best_eff = eff;
+            best_len = len;
+        }
+        if (eff > 0.97) break;
+    }
+    if (best_len == 0) best_len = (N + BK - 1) / BK * BK;
+    return best_len;
+}
+
+}  // namespace cpa

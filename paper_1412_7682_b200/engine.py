@@ -1,0 +1,112 @@
+"""Engine: a convenience wrapper over the C ABI for PyTorch callers.
+
+PyTorch supplies device memory, streams and process groups only; the CPA
+arithmetic runs in libcpa.so.  Multi-GPU (traces sharded over ranks [P:230]):
+every rank calls ``accumulate`` on its shard, then ``allreduce`` (one NCCL
+all-reduce(SUM) of the packed accumulator), then ``finalize``.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _binding as B
+
+_TORCH_DTYPE = {B.CPA_S8: torch.int8, B.CPA_U8: torch.uint8, B.CPA_F32: torch.float32}
+
+
+class Engine:
+    def __init__(self, M: int, dtype: int = B.CPA_S8, model: int = B.CPA_HD_LAST,
+                 device: int | torch.device = 0, stream: torch.cuda.Stream | None = None):
+        self.device = torch.device("cuda", device if isinstance(device, int) else device.index)
+        self.M, self.dtype, self.model = M, dtype, model
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        words = B.cpa_accum_words(M)
+        acc_t = torch.float64 if dtype == B.CPA_F32 else torch.int64
+        self.accum = torch.zeros(words, dtype=acc_t, device=self.device)
+        self.ctx = B.cpa_init(M, dtype, model, self.device.index, self.stream.cuda_stream, self.accum)
+
+    # ---- views into the packed accumulator (include/cpa.h layout) ----
+    def _field(self, f, n):
+        o = B.cpa_accum_offset(self.M, f)
+        return self.accum[o:o + n]
+
+    @property
+    def sum_hw(self):
+        return self._field(B.FIELD_HW, 4096 * self.M).view(4096, self.M)
+
+    @property
+    def sum_w(self):
+        return self._field(B.FIELD_W, self.M)
+
+    @property
+    def sum_w2(self):
+        return self._field(B.FIELD_W2, self.M)
+
+    @property
+    def sum_h(self):
+        return self._field(B.FIELD_H, 4096)
+
+    @property
+    def sum_h2(self):
+        return self._field(B.FIELD_H2, 4096)
+
+    @property
+    def n(self):
+        return self._field(B.FIELD_N, 1)
+
+    # ---- the path ----
+    def set_kchunk(self, k: int):
+        B.cpa_set_option(self.ctx, B.CPA_OPT_KCHUNK, k)
+
+    def accumulate(self, traces: torch.Tensor, texts: torch.Tensor):
+        assert traces.device == self.device and texts.device == self.device
+        assert traces.dtype == _TORCH_DTYPE[self.dtype] and texts.dtype == torch.uint8
+        assert traces.dim() == 2 and traces.shape[1] == self.M and traces.stride(1) == 1
+        assert texts.shape == (traces.shape[0], 16) and texts.is_contiguous()
+        B.cpa_accumulate(self.ctx, traces, traces.stride(0), texts, traces.shape[0])
+
+    def accumulate_host(self, traces: np.ndarray | torch.Tensor, texts: np.ndarray | torch.Tensor):
+        n = traces.shape[0]
+        ld = traces.strides[0] // traces.itemsize if isinstance(traces, np.ndarray) else traces.stride(0)
+        B.cpa_accumulate_host(self.ctx, traces, ld, texts, n)
+
+    def allreduce(self, group=None):
+        """Combine partial sums over ranks: one all-reduce(SUM) [a7].  Exact
+        for the int64 accumulator under any reduction order."""
+        import torch.distributed as dist
+        with torch.cuda.stream(self.stream):
+            dist.all_reduce(self.accum, op=dist.ReduceOp.SUM, group=group)
+
+    def finalize(self, want_rho: bool = False):
+        dev = self.device
+        rho = torch.empty((4096, self.M), dtype=torch.float64, device=dev) if want_rho else None
+        maxabs = torch.empty(4096, dtype=torch.float64, device=dev)
+        argmax = torch.empty(4096, dtype=torch.int32, device=dev)
+        rank = torch.empty(4096, dtype=torch.int32, device=dev)
+        res = B.cpa_finalize(self.ctx, rho, maxabs, argmax, rank)
+        return dict(rho=rho, maxabs=maxabs, argmax=argmax, rank=rank,
+                    round_key=bytes(res.round_key), master_key=bytes(res.master_key),
+                    peak_sample=list(res.peak_sample), peak_rho=list(res.peak_rho),
+                    n_traces=res.n_traces)
+
+    def reset(self):
+        B.cpa_reset(self.ctx)
+
+    def sync(self):
+        B.cpa_sync(self.ctx)
+
+    @property
+    def launches(self) -> int:
+        return B.cpa_launch_count(self.ctx)
+
+    def close(self):
+        if self.ctx:
+            B.cpa_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

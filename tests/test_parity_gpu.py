@@ -1,0 +1,211 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bar: int64 sums bit-exact; rho
+bit-exact to Eq. (1)-from-integers (reference B) and within 1e-9 relative
+(+1e-12 abs) of the two-pass reference A; max/argmax/ranks/key identical."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from synth import synth as S  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1412_7682_b200 as P
+    return P
+
+
+MODEL = {O.HD_LAST: 0, O.HW_LAST: 1, O.HW_FIRST: 2}
+
+
+def run_gpu(P, texts, W, model=0, kchunk=0, chunks=None, want_rho=True):
+    dtype = {np.int8: P.CPA_S8, np.uint8: P.CPA_U8}[W.dtype.type]
+    eng = P.Engine(W.shape[1], dtype, model, 0)
+    if kchunk:
+        eng.set_kchunk(kchunk)
+    bounds = chunks or [0, W.shape[0]]
+    # pad rows to a 16-byte multiple (TMA stride rule); ld > M exercises strides
+    ld = (W.shape[1] + 15) // 16 * 16
+    Wp = np.zeros((W.shape[0], ld), W.dtype)
+    Wp[:, :W.shape[1]] = W
+    dW = torch.from_numpy(Wp).cuda()
+    dT = torch.from_numpy(np.ascontiguousarray(texts)).cuda()
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        eng.accumulate(dW[a:b, :W.shape[1]], dT[a:b])
+    out = eng.finalize(want_rho=want_rho) if W.shape[0] >= 2 else None
+    sums = dict(sum_hw=eng.sum_hw.cpu().numpy(), sum_w=eng.sum_w.cpu().numpy(),
+                sum_w2=eng.sum_w2.cpu().numpy(), sum_h=eng.sum_h.cpu().numpy(),
+                sum_h2=eng.sum_h2.cpu().numpy(), n=int(eng.n.cpu().numpy()[0]))
+    eng.close()
+    return sums, out
+
+
+def assert_parity(sums, out, ref, rho_exact=True):
+    for k in ("sum_hw", "sum_w", "sum_w2", "sum_h", "sum_h2"):
+        assert np.array_equal(sums[k], ref[k]), k
+    assert sums["n"] == ref["n"]
+    if out is None:
+        return
+    rho = out["rho"].cpu().numpy()
+    if rho_exact:
+        assert np.array_equal(rho, ref["rho"])          # bit-exact vs reference B
+    assert np.array_equal(out["maxabs"].cpu().numpy(), ref["maxabs"])
+    assert np.array_equal(out["argmax"].cpu().numpy(), ref["argmax"])
+    assert np.array_equal(out["rank"].cpu().numpy(), ref["rank"])
+    assert out["round_key"] == ref["best"].tobytes()
+
+
+def test_c1_full_parity(P):
+    w = S.CONFIGS["C1"]
+    texts, W = S.dataset(w)
+    ref = O.attack_i8(O.HD_LAST, texts, W)
+    sums, out = run_gpu(P, texts, W)
+    assert_parity(sums, out, ref)
+    assert out["master_key"] == w.key
+    rk = O.expand_key(w.key)[10].astype(int)
+    assert out["peak_sample"] == w.leak_positions()
+    # reference A (two-pass) on the true-key rows and a spread of others
+    hyps = np.array([256 * b + rk[b] for b in range(16)] + list(range(0, 4096, 97)), np.int32)
+    ra = O.rho_two_pass_i8(O.HD_LAST, texts, W, hyps=hyps)
+    rg = out["rho"].cpu().numpy()[hyps]
+    assert np.all(np.abs(rg - ra) <= 1e-9 * np.abs(ra) + 1e-12)
+
+
+def test_c1_noiseless_rho_one(P):
+    w = S.CONFIGS["C1-0"]
+    texts, W = S.dataset(w)
+    _, out = run_gpu(P, texts, W)
+    rk = O.expand_key(w.key)[10].astype(int)
+    mx = out["maxabs"].cpu().numpy()
+    am = out["argmax"].cpu().numpy()
+    for b in range(16):
+        assert abs(mx[256 * b + rk[b]] - 1.0) <= 1e-12 and am[256 * b + rk[b]] == w.leak_positions()[b]
+    assert out["master_key"] == w.key
+
+
+@pytest.mark.parametrize("model", [O.HD_LAST, O.HW_LAST, O.HW_FIRST])
+@pytest.mark.parametrize("dtype", [np.int8, np.uint8])
+def test_models_dtypes_ragged(P, model, dtype):
+    rng = np.random.default_rng(100 + model)
+    n, m = 333, 300                     # ragged: 333 = 5*64+13 traces, 300 = 256+44 samples
+    texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    lo, hi = (-128, 128) if dtype == np.int8 else (0, 256)
+    W = rng.integers(lo, hi, (n, m)).astype(dtype)
+    ref = O.attack_i8(model, texts, W)
+    sums, out = run_gpu(P, texts, W, model=MODEL[model])
+    assert_parity(sums, out, ref)
+
+
+@pytest.mark.parametrize("n,m", [(2, 1), (3, 17), (64, 256), (65, 257), (130, 513), (1000, 16)])
+def test_edge_shapes(P, n, m):
+    rng = np.random.default_rng(n * 1000 + m)
+    texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    W = rng.integers(-128, 128, (n, m)).astype(np.int8)
+    ref = O.attack_i8(O.HD_LAST, texts, W)
+    sums, out = run_gpu(P, texts, W)
+    assert_parity(sums, out, ref)
+
+
+def test_degenerate_columns(P):
+    """Constant columns (dw = 0) give rho = 0 exactly [S:250, S:293]."""
+    rng = np.random.default_rng(5)
+    texts = rng.integers(0, 256, (200, 16), dtype=np.uint8)
+    W = rng.integers(-128, 128, (200, 40)).astype(np.int8)
+    W[:, 3] = 7
+    W[:, 39] = -128
+    ref = O.attack_i8(O.HD_LAST, texts, W)
+    sums, out = run_gpu(P, texts, W)
+    assert_parity(sums, out, ref)
+    rho = out["rho"].cpu().numpy()
+    assert not rho[:, 3].any() and not rho[:, 39].any()
+
+
+def test_split_k_chunks_and_permutation_bit_identical(P):
+    """Integer sums are order-independent: split-K units, several accumulate
+    calls and a trace permutation all give bit-identical results."""
+    rng = np.random.default_rng(9)
+    n, m = 9000, 700
+    texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    W = rng.integers(-128, 128, (n, m)).astype(np.int8)
+    base, out0 = run_gpu(P, texts, W)
+    for kw in (dict(kchunk=128), dict(kchunk=1024), dict(chunks=[0, 1, 700, 4097, 9000])):
+        s, o = run_gpu(P, texts, W, **kw)
+        for k in base:
+            assert np.array_equal(base[k], s[k]), (kw, k)
+        assert np.array_equal(out0["rho"].cpu().numpy(), o["rho"].cpu().numpy())
+    perm = rng.permutation(n)
+    s, o = run_gpu(P, texts[perm], W[perm])
+    assert np.array_equal(out0["rho"].cpu().numpy(), o["rho"].cpu().numpy())
+    # oracle on a column subset
+    cols = np.array([0, 1, 255, 256, 511, 699], np.int32)
+    ref_hw = O.cross_sums_i8(O.HD_LAST, texts, W, cols)
+    assert np.array_equal(base["sum_hw"][:, cols], ref_hw)
+
+
+def test_c2_subset_and_closed_form(P):
+    w = S.CONFIGS["C2"]
+    texts, W = S.dataset(w)
+    cols = np.array(sorted(set(w.leak_positions()) | {0, 1, 255, 256, 4095, 4999}), np.int32)
+    sums, out = run_gpu(P, texts, W)
+    assert np.array_equal(sums["sum_hw"][:, cols], O.cross_sums_i8(O.HD_LAST, texts, W, cols))
+    sw, sw2 = O.trace_sums_i8(W)
+    assert np.array_equal(sums["sum_w"], sw) and np.array_equal(sums["sum_w2"], sw2)
+    sh, sh2 = O.model_sums(O.HD_LAST, texts)
+    assert np.array_equal(sums["sum_h"], sh) and np.array_equal(sums["sum_h2"], sh2)
+    # closed form over ALL columns: sum_k sumHW[b,k,j] = 1024 sumW[j]
+    assert (sums["sum_hw"].reshape(16, 256, -1).sum(1) == 1024 * sums["sum_w"][None, :]).all()
+    rho_ref = O.rho_eq1_grid(w.n, sums["sum_hw"][:, cols], sh, sh2, sw[cols], sw2[cols])
+    assert np.array_equal(out["rho"].cpu().numpy()[:, cols], rho_ref)
+    assert out["master_key"] == w.key
+
+
+def test_unaligned_device_input_is_staged(P):
+    """ld*1 not a multiple of 16 (TMA rule): the library stages the rows."""
+    w = S.CONFIGS["C1"]
+    texts, W = S.dataset(w)                  # ld = 500
+    ref = O.attack_i8(O.HD_LAST, texts, W)
+    eng = P.Engine(w.m, P.CPA_S8, P.CPA_HD_LAST, 0)
+    eng.accumulate(torch.from_numpy(W).cuda(), torch.from_numpy(texts).cuda())
+    out = eng.finalize(want_rho=True)
+    assert np.array_equal(eng.sum_hw.cpu().numpy(), ref["sum_hw"])
+    assert np.array_equal(out["rho"].cpu().numpy(), ref["rho"])
+    eng.close()
+
+
+def test_host_buffer_path_matches_device(P):
+    w = S.CONFIGS["C2"].replace(n=3000)
+    texts, W = S.dataset(w)
+    s_dev, o_dev = run_gpu(P, texts, W)
+    eng = P.Engine(w.m, P.CPA_S8, P.CPA_HD_LAST, 0)
+    eng.accumulate_host(W, texts)
+    o = eng.finalize(want_rho=True)
+    assert np.array_equal(eng.sum_hw.cpu().numpy(), s_dev["sum_hw"])
+    assert np.array_equal(o["rho"].cpu().numpy(), o_dev["rho"].cpu().numpy())
+    eng.close()
+
+
+def test_errors(P):
+    eng = P.Engine(100, P.CPA_S8, P.CPA_HD_LAST, 0)
+    W = torch.zeros((10, 100), dtype=torch.int8, device="cuda")
+    T = torch.zeros((10, 16), dtype=torch.uint8, device="cuda")
+    with pytest.raises(P.CpaError, match="INVALID_ARG"):
+        P.cpa_accumulate(eng.ctx, W, 99, T, 10)           # ld < M
+    with pytest.raises(P.CpaError, match="TOO_FEW"):
+        eng.finalize()                                     # N = 0 < 2
+    eng.close()
+
+
+def test_synth_device_generator_matches_host(P):
+    for name in ("C1", "C3"):
+        w = S.CONFIGS[name].replace(n=300)
+        texts, lv = S.texts(w)
+        Wh = S.traces(w, lv)
+        d = torch.empty(Wh.shape, dtype={S.S8: torch.int8, S.F32: torch.float32}[w.dtype], device="cuda")
+        S.dev_traces(w, torch.from_numpy(lv).cuda(), 0, w.n, d, w.m)
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy(), Wh)
