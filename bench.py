@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""bench.py -- the BASELINE.json metric on B200: hypothesis x sample
+correlations per second at 1.5M traces (workload C4: 1.5M x 5000 int8
+traces, HD last-round model), plus time-to-key end to end.
+
+One step = the whole hot path over the workload: cpa_reset -> cpa_accumulate
+(a3 model sums, a4 trace moments, a5 tcgen05 cross term) -> [N>1: one NCCL
+all-reduce of the packed int64 accumulator (a7)] -> cpa_finalize (a8 Eq. (1)
+rho [4096][M] in fp64 + max/argmax, a9 ranking, key D2H).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Traces are sharded over ranks (strong scaling, fixed 1.5M total).  Inputs
+(7.5 GB) exceed L2 (126 MB), so no L2 flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAK_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+INT8_PER_BF16 = 4.5 / 2.25  # nominal dense int8 : bf16 ratio (B200_PROFILING.md)
+CPU_SAMPLE_TRACES = 131072
+CPU_SAMPLE_COLS = 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return dict(PEAK_FALLBACK), "fallback"
+
+
+# ---------------------------------------------------------------- clocks ----
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int, enabled: bool = True):
+        self.enabled = enabled
+        self.idx = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        if self.enabled:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                     "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            except OSError:
+                self.proc = None
+            time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.proc:
+            return None
+        rows = []
+        with open(self.f.name) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3] not in ("[N/A]",))}
+
+
+# ---------------------------------------------------------- cpu baseline ----
+def cpu_baseline(w, sample_traces=CPU_SAMPLE_TRACES, ncols=CPU_SAMPLE_COLS):
+    """The oracle as it stands (single-threaded C, oracle/oracle.c), timed on a
+    bounded sample of the same workload; rate scaled linearly to N = w.n."""
+    import numpy as np
+    from oracle import oracle as O
+    from synth import synth as S
+    n = min(sample_traces, w.n)
+    texts, lv = S.texts(w, 0, n)
+    cols = np.array(sorted(w.leak_positions()[:2] + [w.m // 5, (3 * w.m) // 5]), np.int32)[:ncols]
+    Ws = S.traces(w, lv, 0, cols)
+    t0 = time.perf_counter()
+    a = O.attack_i8(O.HD_LAST, texts, Ws, np.arange(len(cols), dtype=np.int32))
+    t = time.perf_counter() - t0
+    t_full = t * (w.n / n)
+    return {"value": 4096 * len(cols) / t_full, "unit": "correlations/s", "cores": 1, "kind": "oracle",
+            "sample": f"{len(cols)} sample columns x first {n} traces of {w.name}; time x{w.n / n:.2f} to N={w.n}",
+            "seconds": t, "key_bytes_ranked_first": int(sum(a["best"] == O.expand_key(w.key)[10]))}
+
+
+def run_reference(args, w):
+    """--impl reference: the oracle on the host cores, one bounded sample of the
+    workload per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import oracle as O
+    from synth import synth as S
+    n = min(65536, w.n)
+    texts, lv = S.texts(w, 0, n)
+    cols = np.array(sorted(w.leak_positions()[:2] + [w.m // 5, (3 * w.m) // 5]), np.int32)
+    Ws = S.traces(w, lv, 0, cols)
+    ts = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.attack_i8(O.HD_LAST, texts, Ws, np.arange(len(cols), dtype=np.int32))
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            ts.append(dt * (w.n / n))
+    t = sum(ts) / len(ts)
+    val = 4096 * len(cols) / t
+    sample = f"{len(cols)} sample columns x first {n} traces of {w.name}; time x{w.n / n:.2f} to N={w.n}"
+    line = {"metric": "hypothesis x sample correlations/s at 1.5M traces", "impl": "reference", "value": val,
+            "unit": "correlations/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic",
+            "config": {"workload": f"{w.name}: {w.n} traces x {w.m} samples int8, HD last-round model",
+                       "n_traces": w.n, "n_samples": w.m},
+            "cpu_baseline": {"value": val, "unit": "correlations/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": "correlations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours ----
+def main():
+    args = parse()
+    from synth import synth as S
+    w = S.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, w)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1412_7682_b200 as P
+
+    dev = torch.device("cuda", local)
+    i0 = w.n * rank // world
+    i1 = w.n * (rank + 1) // world
+    n_local = i1 - i0
+    # ---- inputs: texts + planted leakage on the host, traces generated on device
+    texts, lv = S.texts(w, i0, n_local)
+    ld = (w.m + 15) // 16 * 16
+    dW = torch.empty((n_local, ld), dtype=torch.int8, device=dev)
+    dT = torch.from_numpy(texts).to(dev)
+    S.dev_traces(w, torch.from_numpy(lv).to(dev), i0, n_local, dW, ld)
+    dWv = dW[:, :w.m]
+    torch.cuda.synchronize()
+
+    eng = P.Engine(w.m, P.CPA_S8, P.CPA_HD_LAST, local)
+    rho = torch.empty((4096, w.m), dtype=torch.float64, device=dev)
+    maxabs = torch.empty(4096, dtype=torch.float64, device=dev)
+    argmax = torch.empty(4096, dtype=torch.int32, device=dev)
+    rank_t = torch.empty(4096, dtype=torch.int32, device=dev)
+    stream = eng.stream
+
+    def step(host=None):
+        eng.reset()
+        if host is None:
+            eng.accumulate(dWv, dT)
+        else:
+            eng.accumulate_host(*host)
+        if world > 1:
+            eng.allreduce()
+        return P.cpa_finalize(eng.ctx, rho, maxabs, argmax, rank_t)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        res = step()
+    eng.set_timing(True)
+    eng.phase_times()  # clear
+    barrier()
+    launches0 = eng.launches
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local, not args.no_clocks) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = step()
+        ev1.record(stream)
+        barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    launches = eng.launches - launches0
+    phase_ms, phase_n = eng.phase_times()
+    eng.set_timing(False)
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = 4096 * w.m / (ms_step * 1e-3)
+    key_ok = bytes(res.master_key) == w.key
+
+    # ---- roofline of the dominant kernel (cross term, tensor-bound)
+    peaks, src = load_peaks()
+    xt_ms = phase_ms["xterm"] / max(1, phase_n["xterm"])
+    ops = 2.0 * 4096 * n_local * w.m
+    achieved = ops / (xt_ms * 1e-3) / 1e12
+    peak = peaks["bf16_tflops_sustained"] * INT8_PER_BF16
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "xterm_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        if tj.get("config") == w.name and tj.get("n_gpus", 1) == world:
+            traffic = tj.get("dram_bytes_per_launch")
+    roofline = {"kernel": "k_xterm_i8", "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_source": f"{src} bf16_tflops_sustained x {INT8_PER_BF16:g} (int8:bf16 nominal ratio)",
+                "frac_of_burst": achieved / (peaks["bf16_tflops"] * INT8_PER_BF16),
+                "algorithmic_ops_per_launch": ops, "ms_per_launch": xt_ms}
+    step_phase_ms = {k: v / args.steps for k, v in phase_ms.items()}
+    tot = sum(step_phase_ms.values()) or 1.0
+    # HBM-bound kernels: achieved GB/s on their algorithmic bytes
+    hbm = {"moments_GBps": (n_local * w.m) / (step_phase_ms["moments"] * 1e-3) / 1e9 if step_phase_ms["moments"] else None,
+           "finalize_GBps": (4096 * w.m * 16) / (step_phase_ms["finalize"] * 1e-3) / 1e9 if step_phase_ms["finalize"] else None,
+           "hbm_peak_GBps": peaks["hbm_gbs"]}
+
+    # ---- end to end through the public API: host (pinned) buffers -> key on host
+    e2e = None
+    if not args.no_e2e:
+        try:
+            hW = torch.empty((n_local, w.m), dtype=torch.int8, pin_memory=True)
+            hW.copy_(dWv)
+            hT = torch.from_numpy(texts).pin_memory()
+            step((hW, hT))  # warm the staging buffers
+            barrier()
+            ts = []
+            for _ in range(args.e2e_steps):
+                barrier()
+                t0 = time.perf_counter()
+                r2 = step((hW, hT))
+                barrier()
+                ts.append(time.perf_counter() - t0)
+            te = max(ts) if world == 1 else ts[-1]
+            if world > 1:
+                t = torch.tensor([statistics.mean(ts)], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                te = float(t.item())
+            else:
+                te = statistics.mean(ts)
+            e2e = {"value": 4096 * w.m / te, "unit": "correlations/s",
+                   "h2d_bytes_per_step": n_local * (w.m + 16), "d2h_bytes_per_step": 8 + 32 * 4 + 16 * 8,
+                   "ms_per_step": te * 1e3, "time_to_key_s": te, "key_recovered": bytes(r2.master_key) == w.key,
+                   "host_buffers": "pinned"}
+            del hW
+        except Exception as ex:  # noqa: BLE001
+            e2e = {"value": None, "unit": "correlations/s", "error": f"{type(ex).__name__}: {ex}"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(w)
+
+    if rank == 0:
+        line = {
+            "metric": "hypothesis x sample correlations/s at 1.5M traces", "value": value,
+            "unit": "correlations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "s8", "data": "synthetic",
+            "config": {"workload": f"{w.name}: {w.n} traces x {w.m} samples int8 (s8), HD last-round model, "
+                                   f"AES-128 key {w.key.hex()}",
+                       "n_traces": w.n, "n_samples": w.m, "hypotheses": 4096, "parallelism": f"trace-shard x{world}",
+                       "l2": "inputs 7.5 GB > 126 MB L2, no flush needed", "rho_written": True},
+            "key_recovered": key_ok, "gpu_launches": launches,
+            "phases_ms_per_step": step_phase_ms,
+            "phase_share": {k: v / tot for k, v in step_phase_ms.items()},
+            "roofline": roofline, "hbm": hbm, "e2e": e2e, "cpu_baseline": cpu,
+            "cell_trace_macs_per_s": 4096 * w.m * w.n / (ms_step * 1e-3),
+        }
+        if not args.no_clocks:
+            line["clocks"] = clk.summary()
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

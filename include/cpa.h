@@ -136,10 +136,21 @@ CPA_API cpa_status cpa_reset(cpa_ctx *ctx);    /* zero the accumulator (async) *
 CPA_API cpa_status cpa_sync(cpa_ctx *ctx);     /* wait for all queued work */
 CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum) */
 
-/* Tuning / test knobs.  CPA_OPT_KCHUNK: traces per split-K work unit of the
- * cross-term kernel (multiple of 64, <= 2^20; 0 = automatic).               */
-enum { CPA_OPT_KCHUNK = 1 };
+/* Tuning / test knobs.
+ *   CPA_OPT_KCHUNK: traces per split-K work unit of the cross-term kernel
+ *                   (multiple of 64, <= 2^20; 0 = automatic).
+ *   CPA_OPT_TIMING: nonzero = record CUDA events on the context's stream
+ *                   around every kernel launch (read with cpa_phase_times). */
+enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2 };
 CPA_API cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value);
+
+/* Per-phase device time (ms) and launch count since the last call, from the
+ * CPA_OPT_TIMING events; synchronises the stream.  Phases:
+ *   0 model sums (a3)  1 trace moments (a4)  2 cross term (a5/a6)
+ *   3 Eq. (1) finalize (a8)  4 phase-4 ranking (a9)                         */
+enum { CPA_NUM_PHASES = 5 };
+CPA_API cpa_status cpa_phase_times(cpa_ctx *ctx, double ms[CPA_NUM_PHASES],
+                                   int64_t launches[CPA_NUM_PHASES]);
 
 /* Kernel launches issued by this context since creation (for bench
  * accounting).                                                              */

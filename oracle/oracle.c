@@ -254,6 +254,37 @@ void or_cross_sums_i8(int model, const uint8_t *texts, const void *W, int w_sign
     }
 }
 
+void or_model_sums_hyps(int model, const uint8_t *texts, int64_t n, const int32_t *hyps,
+                        int nhyps, int64_t *sum_h, int64_t *sum_h2)
+{
+    for (int a = 0; a < nhyps; a++) {
+        int b = hyps[a] / 256, k = hyps[a] % 256;
+        int64_t s1 = 0, s2 = 0;
+        for (int64_t i = 0; i < n; i++) {
+            int64_t H = or_selection(model, texts + 16 * i, b, k);
+            s1 += H;
+            s2 += H * H;
+        }
+        sum_h[a] = s1;
+        sum_h2[a] = s2;
+    }
+}
+
+void or_cross_sums_hyps_i8(int model, const uint8_t *texts, const void *W, int w_signed,
+                           int64_t n, int64_t ld, const int32_t *cols, int ncols,
+                           const int32_t *hyps, int nhyps, int64_t *sum_hw)
+{
+    memset(sum_hw, 0, sizeof(int64_t) * (size_t)nhyps * (size_t)ncols);
+    for (int a = 0; a < nhyps; a++) {
+        int b = hyps[a] / 256, k = hyps[a] % 256;
+        int64_t *row = sum_hw + (size_t)a * ncols;
+        for (int64_t i = 0; i < n; i++) {
+            int64_t H = or_selection(model, texts + 16 * i, b, k);
+            for (int c = 0; c < ncols; c++) row[c] += H * wval(W, w_signed, ld, i, cols[c]);
+        }
+    }
+}
+
 /* ------------------------------------------------------------------------ */
 /* Eq. (1) [P:69] from the exact integer sums ("reference B"):                */
 /*   num = N*S_hw - S_h*S_w ; dw = N*S_w2 - S_w^2 ; dh = N*S_h2 - S_h^2       */

@@ -51,6 +51,14 @@ void or_cross_sums_i8(int model, const uint8_t *texts, const void *W,
                       int w_signed, int64_t n, int64_t ld,
                       const int32_t *cols, int ncols, int64_t *sum_hw);
 
+/* Same sums restricted to a list of hypotheses h (rows of sum_hw follow
+ * `hyps`): used to check full-size GPU runs on sampled outputs.             */
+void or_model_sums_hyps(int model, const uint8_t *texts, int64_t n, const int32_t *hyps,
+                        int nhyps, int64_t *sum_h, int64_t *sum_h2);
+void or_cross_sums_hyps_i8(int model, const uint8_t *texts, const void *W, int w_signed,
+                           int64_t n, int64_t ld, const int32_t *cols, int ncols,
+                           const int32_t *hyps, int nhyps, int64_t *sum_hw);
+
 /* ---- Eq. (1) from the exact integer sums (reference B) [P:69] ----------
  * Returns 0 on success, -1 if an intermediate does not fit int64.          */
 int or_rho_eq1(int64_t n, int64_t s_hw, int64_t s_h, int64_t s_h2,

@@ -54,6 +54,8 @@ def lib():
         L.or_rho_two_pass_f32.argtypes = [i32, P, P, i64, i64, P, i32, P, i32, P]
         L.or_sums_f32.argtypes = [i32, P, P, i64, i64, P, i32, P, P, P]
         L.or_rho_eq1_f64_grid.argtypes = [i64, P, P, P, P, P, i32, P]
+        L.or_model_sums_hyps.argtypes = [i32, P, i64, P, i32, P, P]
+        L.or_cross_sums_hyps_i8.argtypes = [i32, P, P, i32, i64, i64, P, i32, P, i32, P]
         L.or_phase3.argtypes = [P, i32, P, P, P, P]
         L.or_phase4.argtypes = [P, P, P]
         L.or_invert_key_schedule.argtypes = [P, C.c_int, P]
@@ -138,6 +140,24 @@ def cross_sums_i8(model: int, texts: np.ndarray, W: np.ndarray, cols=None):
     shw = np.zeros((4096, len(cols)), np.int64)
     lib().or_cross_sums_i8(model, _p(texts), _p(W), int(W.dtype == np.int8),
                            W.shape[0], W.shape[1], _p(cols), len(cols), _p(shw))
+    return shw
+
+
+def model_sums_hyps(model: int, texts: np.ndarray, hyps):
+    texts = np.ascontiguousarray(texts, np.uint8)
+    hyps = np.ascontiguousarray(hyps, np.int32)
+    sh = np.zeros(len(hyps), np.int64); sh2 = np.zeros(len(hyps), np.int64)
+    lib().or_model_sums_hyps(model, _p(texts), texts.shape[0], _p(hyps), len(hyps), _p(sh), _p(sh2))
+    return sh, sh2
+
+
+def cross_sums_hyps_i8(model: int, texts: np.ndarray, W: np.ndarray, hyps, cols=None):
+    W = np.ascontiguousarray(W); texts = np.ascontiguousarray(texts, np.uint8)
+    cols = _cols(W, cols)
+    hyps = np.ascontiguousarray(hyps, np.int32)
+    shw = np.zeros((len(hyps), len(cols)), np.int64)
+    lib().or_cross_sums_hyps_i8(model, _p(texts), _p(W), int(W.dtype == np.int8), W.shape[0], W.shape[1],
+                                _p(cols), len(cols), _p(hyps), len(hyps), _p(shw))
     return shw
 
 

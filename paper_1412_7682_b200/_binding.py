@@ -17,14 +17,16 @@ CPA_E_INVALID_ARG, CPA_E_BAD_STATE, CPA_E_CUDA, CPA_E_NO_MEMORY = 1, 2, 3, 4
 CPA_E_TOO_FEW_TRACES, CPA_E_OVERFLOW, CPA_E_UNSUPPORTED_DEVICE = 5, 6, 7
 CPA_S8, CPA_U8, CPA_F32 = 0, 1, 2
 CPA_HD_LAST, CPA_HW_LAST, CPA_HW_FIRST = 0, 1, 2
-CPA_OPT_KCHUNK = 1
+CPA_OPT_KCHUNK, CPA_OPT_TIMING = 1, 2
+CPA_NUM_PHASES = 5
+PHASE_NAMES = ("modelsums", "moments", "xterm", "finalize", "phase4")
 FIELD_HW, FIELD_W, FIELD_W2, FIELD_H, FIELD_H2, FIELD_N = range(6)
 
 # every symbol include/cpa.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = (
     "cpa_accum_words", "cpa_accum_bytes", "cpa_accum_offset", "cpa_init", "cpa_accumulate",
     "cpa_accumulate_host", "cpa_finalize", "cpa_reset", "cpa_sync", "cpa_destroy",
-    "cpa_set_option", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
+    "cpa_set_option", "cpa_phase_times", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
     "cpa_aes_expand_key", "cpa_aes_invert_key_schedule",
 )
 
@@ -60,6 +62,7 @@ def _load():
         "cpa_sync": (ST, [P]),
         "cpa_destroy": (ST, [P]),
         "cpa_set_option": (ST, [P, C.c_int, I64]),
+        "cpa_phase_times": (ST, [P, P, P]),
         "cpa_launch_count": (I64, [P]),
         "cpa_status_str": (C.c_char_p, [C.c_int]),
         "cpa_last_error": (C.c_char_p, []),
@@ -141,6 +144,14 @@ def cpa_destroy(ctx):
 
 def cpa_set_option(ctx, option: int, value: int):
     _check(_lib.cpa_set_option(ctx, option, value), "cpa_set_option")
+
+
+def cpa_phase_times(ctx):
+    """({phase: ms}, {phase: launches}) since the last call (CPA_OPT_TIMING)."""
+    ms = (C.c_double * CPA_NUM_PHASES)()
+    n = (C.c_int64 * CPA_NUM_PHASES)()
+    _check(_lib.cpa_phase_times(ctx, ms, n), "cpa_phase_times")
+    return dict(zip(PHASE_NAMES, list(ms))), dict(zip(PHASE_NAMES, list(n)))
 
 
 def cpa_launch_count(ctx) -> int:

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "../../include/cpa.h"
 #include "kernels.h"
@@ -81,6 +82,25 @@ struct cpa_ctx {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
     cpa::XtermF32Scratch f32;  // float-path scratch
+    // CPA_OPT_TIMING: CUDA events recorded on `stream` around every launch
+    bool timing = false;
+    struct Rec { int phase; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t ev() {
+        if (pool.empty()) { cudaEvent_t e; cudaEventCreate(&e); return e; }
+        cudaEvent_t e = pool.back(); pool.pop_back(); return e;
+    }
+    // time the launches `fn` issues on the stream as phase `ph`
+    template <typename F> cudaError_t timed(int ph, F &&fn) {
+        if (!timing) return fn();
+        Rec r{ph, ev(), ev()};
+        cudaEventRecord(r.a, stream);
+        cudaError_t e = fn();
+        cudaEventRecord(r.b, stream);
+        recs.push_back(r);
+        return e;
+    }
 };
 
 extern "C" {
@@ -193,6 +213,10 @@ cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, 
 cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
 {
     if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
+    if (option == CPA_OPT_TIMING) {
+        ctx->timing = value != 0;
+        return CPA_OK;
+    }
     if (option == CPA_OPT_KCHUNK) {
         if (value < 0 || value % 64 || value > (1 << 20))
             return fail(CPA_E_INVALID_ARG, "KCHUNK=%lld must be a multiple of 64 in [0, 2^20]", (long long)value);
@@ -208,23 +232,32 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     int launches = 0;
     if (c->dtype == CPA_F32) {
         double *acc = (double *)c->accum;
-        CUDA_TRY(cpa::launch_modelsums_f64(d_tx, n, c->d_vtab, acc + cpa_accum_offset(M, 3),
-                                           acc + cpa_accum_offset(M, 4), acc + cpa_accum_offset(M, 5),
-                                           c->stream, &launches),
+        CUDA_TRY(c->timed(0, [&] {
+                     return cpa::launch_modelsums_f64(d_tx, n, c->d_vtab, acc + cpa_accum_offset(M, 3),
+                                                      acc + cpa_accum_offset(M, 4), acc + cpa_accum_offset(M, 5),
+                                                      c->stream, &launches);
+                 }),
                  "modelsums");
-        cudaError_t e = cpa::xterm_f32_accumulate(c->f32, (const float *)d_w, ld, d_tx, n, M, c->d_vtab,
-                                                  acc, c->num_sms, c->stream, &launches);
+        cudaError_t e = c->timed(2, [&] {
+            return cpa::xterm_f32_accumulate(c->f32, (const float *)d_w, ld, d_tx, n, M, c->d_vtab, acc,
+                                             c->num_sms, c->stream, &launches);
+        });
         c->launches += launches;
         if (e != cudaSuccess) return cuda_fail(e, "float-path cross term");
         return CPA_OK;
     }
     int64_t *acc = (int64_t *)c->accum;
     const bool sgn = c->dtype == CPA_S8;
-    CUDA_TRY(cpa::launch_modelsums(d_tx, n, c->d_vtab, acc + cpa_accum_offset(M, 3), acc + cpa_accum_offset(M, 4),
-                                   acc + cpa_accum_offset(M, 5), c->stream, &launches),
+    CUDA_TRY(c->timed(0, [&] {
+                 return cpa::launch_modelsums(d_tx, n, c->d_vtab, acc + cpa_accum_offset(M, 3),
+                                              acc + cpa_accum_offset(M, 4), acc + cpa_accum_offset(M, 5), c->stream,
+                                              &launches);
+             }),
              "modelsums");
-    CUDA_TRY(cpa::launch_moments_i8(d_w, ld, n, M, sgn, acc + cpa_accum_offset(M, 1), acc + cpa_accum_offset(M, 2),
-                                    c->stream, &launches),
+    CUDA_TRY(c->timed(1, [&] {
+                 return cpa::launch_moments_i8(d_w, ld, n, M, sgn, acc + cpa_accum_offset(M, 1),
+                                               acc + cpa_accum_offset(M, 2), c->stream, &launches);
+             }),
              "moments");
     CUtensorMap tmap;
     cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)n};
@@ -236,7 +269,10 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     const int64_t kc = c->kchunk ? c->kchunk : cpa::xterm_i8_auto_kchunk(M, n, c->num_sms);
-    CUDA_TRY(cpa::launch_xterm_i8(tmap, d_tx, c->d_vtab, acc, M, n, kc, sgn, c->num_sms, c->stream, &launches),
+    CUDA_TRY(c->timed(2, [&] {
+                 return cpa::launch_xterm_i8(tmap, d_tx, c->d_vtab, acc, M, n, kc, sgn, c->num_sms, c->stream,
+                                             &launches);
+             }),
              "xterm_i8");
     c->launches += launches;
     return CPA_OK;
@@ -364,11 +400,15 @@ cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_
     o.best = c->d_best;
     o.best_rho = c->d_best_rho;
     int launches = 0;
-    if (c->dtype == CPA_F32)
-        CUDA_TRY(cpa::launch_finalize_f64((const double *)c->accum, M, c->d_sqrt_dw, o, c->stream, &launches), "finalize");
-    else
-        CUDA_TRY(cpa::launch_finalize_i8((const int64_t *)c->accum, M, c->d_sqrt_dw, o, c->stream, &launches), "finalize");
-    CUDA_TRY(cpa::launch_phase4(o, c->stream, &launches), "phase4");
+    CUDA_TRY(c->timed(3, [&] {
+                 return c->dtype == CPA_F32
+                            ? cpa::launch_finalize_f64((const double *)c->accum, M, c->d_sqrt_dw, o, c->stream,
+                                                       &launches)
+                            : cpa::launch_finalize_i8((const int64_t *)c->accum, M, c->d_sqrt_dw, o, c->stream,
+                                                      &launches);
+             }),
+             "finalize");
+    CUDA_TRY(c->timed(4, [&] { return cpa::launch_phase4(o, c->stream, &launches); }), "phase4");
     c->launches += launches;
     int32_t best[32];
     double brho[16];
@@ -387,6 +427,26 @@ cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_
             cpa::aes_invert_key_schedule(res->round_key, 10, res->master_key);
         res->n_traces = n;
     }
+    return CPA_OK;
+}
+
+cpa_status cpa_phase_times(cpa_ctx *c, double ms[CPA_NUM_PHASES], int64_t launches[CPA_NUM_PHASES])
+{
+    if (!c || !ms) return fail(CPA_E_INVALID_ARG, "null argument");
+    CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+    for (int p = 0; p < CPA_NUM_PHASES; p++) {
+        ms[p] = 0.0;
+        if (launches) launches[p] = 0;
+    }
+    for (auto &r : c->recs) {
+        float t = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b), "cudaEventElapsedTime");
+        ms[r.phase] += t;
+        if (launches) launches[r.phase]++;
+        c->pool.push_back(r.a);
+        c->pool.push_back(r.b);
+    }
+    c->recs.clear();
     return CPA_OK;
 }
 
@@ -419,6 +479,11 @@ cpa_status cpa_destroy(cpa_ctx *c)
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     cpa::xterm_f32_free(c->f32);
+    for (auto &r : c->recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : c->pool) cudaEventDestroy(e);
     delete c;
     return CPA_OK;
 }

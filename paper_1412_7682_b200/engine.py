@@ -59,6 +59,14 @@ class Engine:
     def set_kchunk(self, k: int):
         B.cpa_set_option(self.ctx, B.CPA_OPT_KCHUNK, k)
 
+    def set_timing(self, on: bool = True):
+        B.cpa_set_option(self.ctx, B.CPA_OPT_TIMING, int(on))
+
+    def phase_times(self):
+        """({phase: ms}, {phase: launches}) of the CUDA-event-timed launches
+        since the last call (needs set_timing(True))."""
+        return B.cpa_phase_times(self.ctx)
+
     def accumulate(self, traces: torch.Tensor, texts: torch.Tensor):
         assert traces.device == self.device and texts.device == self.device
         assert traces.dtype == _TORCH_DTYPE[self.dtype] and texts.dtype == torch.uint8

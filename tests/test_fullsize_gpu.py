@@ -1,0 +1,62 @@
+"""Full-size parity at BASELINE.json's configs[3] (C4: 1.5M traces x 5000
+samples int8), in the launch configuration bench.py times (one accumulate of
+all traces, automatic split-K), checked on sampled outputs the oracle computes
+one by one and on properties that hold at any size."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from synth import synth as S  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def test_c4_fullsize_sampled_parity():
+    import paper_1412_7682_b200 as P
+    w = S.CONFIGS["C4"]
+    texts, lv = S.texts(w)
+    ld = (w.m + 15) // 16 * 16
+    dW = torch.empty((w.n, ld), dtype=torch.int8, device="cuda")
+    S.dev_traces(w, torch.from_numpy(lv).cuda(), 0, w.n, dW, ld)
+    eng = P.Engine(w.m, P.CPA_S8, P.CPA_HD_LAST, 0)
+    eng.accumulate(dW[:, :w.m], torch.from_numpy(texts).cuda())
+    out = eng.finalize(want_rho=True)
+    rk = O.expand_key(w.key)[10].astype(int)
+
+    # properties over every output: closed forms of the selection function
+    hw = eng.sum_hw.view(16, 256, w.m)
+    sw = eng.sum_w
+    assert int(eng.n.item()) == w.n
+    assert torch.equal(hw.sum(1), 1024 * sw.view(1, -1).expand(16, -1))
+    assert torch.equal(eng.sum_h.view(16, 256).sum(1), torch.full((16,), 1024 * w.n, device="cuda", dtype=torch.int64))
+    assert torch.equal(eng.sum_h2.view(16, 256).sum(1), torch.full((16,), 4608 * w.n, device="cuda", dtype=torch.int64))
+
+    # sampled outputs against the oracle: 6 columns x 48 hypotheses, all traces
+    cols = np.array(sorted([0, w.leak_positions()[0], w.leak_positions()[7], 2047, 4097, w.m - 1]), np.int32)
+    rng = np.random.default_rng(0)
+    hyps = np.array(sorted(set([256 * b + rk[b] for b in range(16)]) | set(rng.integers(0, 4096, 32).tolist())),
+                    np.int32)
+    Wc = S.traces(w, lv, 0, cols)                     # host generator, same bytes
+    assert np.array_equal(Wc, dW[:, torch.from_numpy(cols).long().cuda()].cpu().numpy())
+    ref_sw, ref_sw2 = O.trace_sums_i8(Wc)
+    assert np.array_equal(eng.sum_w.cpu().numpy()[cols], ref_sw)
+    assert np.array_equal(eng.sum_w2.cpu().numpy()[cols], ref_sw2)
+    ref_sh, ref_sh2 = O.model_sums_hyps(O.HD_LAST, texts, hyps)
+    assert np.array_equal(eng.sum_h.cpu().numpy()[hyps], ref_sh)
+    assert np.array_equal(eng.sum_h2.cpu().numpy()[hyps], ref_sh2)
+    ref_hw = O.cross_sums_hyps_i8(O.HD_LAST, texts, Wc, hyps)
+    got_hw = eng.sum_hw.cpu().numpy()[hyps][:, cols]
+    assert np.array_equal(got_hw, ref_hw)
+    rho = out["rho"].cpu().numpy()
+    for a, h in enumerate(hyps):
+        for c, j in enumerate(cols):
+            r = O.rho_eq1(w.n, ref_hw[a, c], ref_sh[a], ref_sh2[a], ref_sw[c], ref_sw2[c])
+            assert rho[h, j] == r                      # bit-exact Eq. (1)
+    # end to end: the key, at the planted samples
+    assert out["master_key"] == w.key
+    assert out["peak_sample"] == w.leak_positions()
+    ranks = out["rank"].cpu().numpy()
+    assert all(ranks[256 * b + rk[b]] == 1 for b in range(16))
+    eng.close()

@@ -103,3 +103,14 @@ def test_chunk_and_permutation_invariance():
     assert np.array_equal(full, parts)
     perm = np.random.default_rng(0).permutation(120)
     assert np.array_equal(full, O.cross_sums_i8(O.HD_LAST, t[perm], W[perm]))
+
+
+def test_hypothesis_subset_sums_match_full():
+    t, W = rand_data(150, 12, 21)
+    hyps = np.array([0, 17, 256, 3333, 4095], np.int32)
+    cols = np.array([2, 5, 11], np.int32)
+    full = O.cross_sums_i8(O.HD_LAST, t, W)
+    assert np.array_equal(O.cross_sums_hyps_i8(O.HD_LAST, t, W, hyps, cols), full[hyps][:, cols])
+    sh, sh2 = O.model_sums(O.HD_LAST, t)
+    a, b = O.model_sums_hyps(O.HD_LAST, t, hyps)
+    assert np.array_equal(a, sh[hyps]) and np.array_equal(b, sh2[hyps])
