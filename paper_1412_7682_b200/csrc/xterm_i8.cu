@@ -39,16 +39,19 @@ constexpr int A_BYTES = BK * BM;              // 8 KB
 constexpr int B_BYTES = BK * BN;              // 16 KB (two 128-sample TMA boxes)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int V_BYTES = 65536;
+constexpr int TX_BYTES = BK * 16;             // ciphertext rows of one stage
 constexpr int EPI_WARPS = 4;
+constexpr int GEN_WARPS = 8;
 constexpr int TB_BYTES = EPI_WARPS * 32 * 33 * 4;
 constexpr int SMEM_V = 0;
 constexpr int SMEM_STAGE = SMEM_V + V_BYTES;
-constexpr int SMEM_TB = SMEM_STAGE + STAGES * STAGE_BYTES;
+constexpr int SMEM_TX = SMEM_STAGE + STAGES * STAGE_BYTES;
+constexpr int SMEM_TB = SMEM_TX + STAGES * TX_BYTES;
 constexpr int SMEM_BAR = SMEM_TB + TB_BYTES;
-constexpr int NUM_BARS = 2 * STAGES + 4;
+constexpr int NUM_BARS = 3 * STAGES + 4;
 constexpr int SMEM_TOTAL = SMEM_BAR + NUM_BARS * 8 + 16;
 constexpr int SMEM_ALLOC = SMEM_TOTAL + 1024;  // slack for 1024-byte alignment
-constexpr int THREADS = 384;
+constexpr int THREADS = 32 * (8 + GEN_WARPS);
 constexpr uint32_t TMEM_COLS = 512;
 
 struct Params {
@@ -91,6 +94,7 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
     auto empty_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (STAGES + s); };
     auto tfull_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (2 * STAGES + a); };
     auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (2 * STAGES + 2 + a); };
+    auto txfull_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (2 * STAGES + 4 + s); };
     uint32_t *tmem_slot = (uint32_t *)(smem + SMEM_BAR + NUM_BARS * 8);
 
     // ---- setup: V table to smem, barriers, TMEM ----
@@ -102,8 +106,9 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmap_w);
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(full_bar(s), 1 + 4);  // TMA expect_tx arrive + 4 generator warps
-            mbar_init(empty_bar(s), 1);     // tcgen05.commit
+            mbar_init(full_bar(s), 1 + GEN_WARPS);  // TMA expect_tx arrive + generator warps
+            mbar_init(empty_bar(s), 1);             // tcgen05.commit
+            mbar_init(txfull_bar(s), 1);            // ciphertext rows landed
         }
         for (int a = 0; a < 2; a++) {
             mbar_init(tfull_bar(a), 1);
@@ -130,6 +135,11 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
                     uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(empty_bar(s), ph ^ 1);
                     uint32_t bdst = sbase + SMEM_STAGE + s * STAGE_BYTES + A_BYTES;
+                    // ciphertext rows for the generators (separate barrier: they
+                    // must see them before they can produce the A tile)
+                    const int rows = (int)((t1 - tb) < BK ? (t1 - tb) : BK);
+                    mbar_arrive_expect_tx(txfull_bar(s), rows * 16);
+                    bulk_load(sbase + SMEM_TX + s * TX_BYTES, p.texts + tb * 16, rows * 16, txfull_bar(s));
                     mbar_arrive_expect_tx(full_bar(s), B_BYTES);
                     tma_load_2d(bdst, &tmap_w, nt * BN, (int32_t)tb, full_bar(s));
                     tma_load_2d(bdst + B_BYTES / 2, &tmap_w, nt * BN + 128, (int32_t)tb, full_bar(s));
@@ -207,9 +217,12 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
         }
     } else if (warp >= 8) {
         // ================= hypothesis generators (H tile, MN-major, swizzled) =================
+        // A quarter-warp (8 lanes) builds one 128-byte trace row: lane = 16-key
+        // chunk, so the V-row reads and the swizzled A-row writes are both
+        // bank-conflict free.  Warp g owns rows 8g..8g+7 of the stage.
         const int g = warp - 8;
-        const int row = (g & 1) * 32 + lane;  // trace row within the stage
-        const int qh = g >> 1;                // which 4 of the 8 16-byte chunks of the row
+        const int ql = lane & 7;           // chunk within the 128-key row
+        const int sub = lane >> 3;         // row within a group of 4
         const uint8_t *vs = smem + SMEM_V;
         uint32_t it = 0;
         for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
@@ -218,32 +231,26 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
             unit_coords(p, u, ht, nt, t0, t1);
             const int b = ht >> 1;
             const int s_idx = shiftrows_src(b);
-            const int chunk0 = (ht & 1) * 8;  // first global 16-key chunk of this tile
+            const uint32_t gchunk = (uint32_t)((ht & 1) * 8 + ql);  // global 16-key chunk
             for (int64_t tb = t0; tb < t1; tb += BK, it++) {
-                int s = it % STAGES;
-                uint32_t ph = (it / STAGES) & 1;
-                const int64_t i = tb + row;
-                // per-trace parameters (loaded before the wait to hide latency)
-                uint32_t cb = 0, cs = 0;
-                const bool valid = i < t1;
-                if (valid) {
-                    const uint8_t *tx = p.texts + i * 16;
-                    cb = __ldg(tx + b);
-                    cs = __ldg(tx + s_idx);
-                }
-                const uint32_t hi = cb >> 4, lo = cb & 15, u4 = lo >> 2, v4 = lo & 3;
-                const uint32_t sel_e = (0x3210u ^ (v4 * 0x1111u)) ^ ((u4 & 1) ? 0x4444u : 0u);
-                const uint32_t sel_o = sel_e ^ 0x4444u;
-                const bool swap2 = (u4 & 2) != 0;
-                const uint8_t *vrow = vs + cs * 256;
+                const int s = it % STAGES;
+                const uint32_t ph = (it / STAGES) & 1;
+                const int nrows = (int)((t1 - tb) < BK ? (t1 - tb) : BK);
                 mbar_wait(empty_bar(s), ph ^ 1);
-                uint8_t *arow = smem + SMEM_STAGE + s * STAGE_BYTES + row * 128;
+                mbar_wait(txfull_bar(s), ph);
+                const uint8_t *tx = smem + SMEM_TX + s * TX_BYTES;
+                uint8_t *abase = smem + SMEM_STAGE + s * STAGE_BYTES;
 #pragma unroll
-                for (int qq = 0; qq < 4; qq++) {
-                    const int ql = qh * 4 + qq;  // chunk within the 128-key row
+                for (int pass = 0; pass < 2; pass++) {
+                    const int row = 8 * g + 4 * pass + sub;
                     uint4 outv = make_uint4(0, 0, 0, 0);
-                    if (valid) {
-                        const uint4 a = *(const uint4 *)(vrow + (((uint32_t)(chunk0 + ql) ^ hi) << 4));
+                    if (row < nrows) {
+                        const uint32_t cb = tx[row * 16 + b], cs = tx[row * 16 + s_idx];
+                        const uint32_t hi = cb >> 4, lo = cb & 15, u4 = lo >> 2, v4 = lo & 3;
+                        const uint32_t sel_e = (0x3210u ^ (v4 * 0x1111u)) ^ ((u4 & 1) ? 0x4444u : 0u);
+                        const uint32_t sel_o = sel_e ^ 0x4444u;
+                        const bool swap2 = (u4 & 2) != 0;
+                        const uint4 a = *(const uint4 *)(vs + cs * 256 + ((gchunk ^ hi) << 4));
                         const uint32_t c0 = swap2 ? a.z : a.x, c1 = swap2 ? a.w : a.y;
                         const uint32_t c2 = swap2 ? a.x : a.z, c3 = swap2 ? a.y : a.w;
                         outv.x = __byte_perm(c0, c1, sel_e);
@@ -251,7 +258,7 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
                         outv.z = __byte_perm(c2, c3, sel_e);
                         outv.w = __byte_perm(c2, c3, sel_o);
                     }
-                    *(uint4 *)(arow + ((ql ^ (row & 7)) << 4)) = outv;  // 128B swizzle
+                    *(uint4 *)(abase + row * 128 + ((ql ^ (row & 7)) << 4)) = outv;  // 128B swizzle
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
