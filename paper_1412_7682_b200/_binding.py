@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libcpa.so")
+LIB_PATH = os.environ.get("CPA_LIB_PATH") or os.path.join(_PKG, "libcpa.so")  # override: debugging only
 
 CPA_OK = 0
 CPA_E_INVALID_ARG, CPA_E_BAD_STATE, CPA_E_CUDA, CPA_E_NO_MEMORY = 1, 2, 3, 4

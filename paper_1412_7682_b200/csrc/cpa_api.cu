@@ -73,6 +73,7 @@ struct cpa_ctx {
     double *d_sqrt_dw = nullptr;
     double *d_maxabs = nullptr, *d_peak = nullptr, *d_best_rho = nullptr;
     int32_t *d_argmax = nullptr, *d_rank = nullptr, *d_best = nullptr;
+    int *d_counter = nullptr;  // work-unit counter of the cross-term scheduler
     int64_t kchunk = 0;
     int64_t launches = 0;
     // cpa_accumulate_host staging
@@ -195,6 +196,7 @@ cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, 
     if (e == cudaSuccess) e = cudaMalloc(&c->d_argmax, sizeof(int32_t) * 4096);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_rank, sizeof(int32_t) * 4096);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_best, sizeof(int32_t) * 32);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_counter, 256);
     if (e != cudaSuccess) {
         cpa_destroy(c);
         return fail(CPA_E_NO_MEMORY, "device scratch: %s", cudaGetErrorString(e));
@@ -270,7 +272,8 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     if (r != CUDA_SUCCESS) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     const int64_t kc = c->kchunk ? c->kchunk : cpa::xterm_i8_auto_kchunk(M, n, c->num_sms);
     CUDA_TRY(c->timed(2, [&] {
-                 return cpa::launch_xterm_i8(tmap, d_tx, c->d_vtab, acc, M, n, kc, sgn, c->num_sms, c->stream,
+                 return cpa::launch_xterm_i8(tmap, d_tx, c->d_vtab, acc, c->d_counter, M, n, kc, sgn, c->num_sms,
+                                             c->stream,
                                              &launches);
              }),
              "xterm_i8");
@@ -471,6 +474,7 @@ cpa_status cpa_destroy(cpa_ctx *c)
     cudaFree(c->d_argmax);
     cudaFree(c->d_rank);
     cudaFree(c->d_best);
+    cudaFree(c->d_counter);
     for (int k = 0; k < 2; k++) {
         cudaFree(c->d_stage[k]);
         cudaFree(c->d_stage_tx[k]);

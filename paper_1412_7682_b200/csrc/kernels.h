@@ -23,7 +23,7 @@ cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M,
 int xterm_i8_smem_bytes();
 int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms);
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
-                            int64_t *d_hw, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
+                            int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
                             int num_sms, cudaStream_t stream, int *launches);
 
 // a8/a9: Phase 3 + 4 [P:81-87]

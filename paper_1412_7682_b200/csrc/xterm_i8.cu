@@ -10,15 +10,19 @@
 //     16 consecutive keys is a 16-byte chunk of row V[c_s], byte-permuted by
 //     (c_b & 15) -- one LDS.128 + 4 SEL + 4 PRMT + one STS.128 per chunk.
 //   * B = W tile (64 traces x 256 samples, s8/u8, MN-major = the caller's
-//     trace-major layout, no transpose) arrives by TMA with 128-byte swizzle.
+//     trace-major layout, no transpose) arrives by TMA with 128-byte swizzle;
+//     the stage's ciphertext rows arrive by a 1-D bulk copy.
 //   * D = 128 x 256 int32 in TMEM, double-buffered (512 columns) so the
 //     epilogue of one work unit overlaps the MMAs of the next.
-//   * Work unit = (32 hypothesis tiles) x (M/256 sample tiles) x (trace
-//     chunks); hypothesis tile fastest so co-resident CTAs share W in L2.
+//   * Work unit = (hypothesis tile, trace chunk, sample tile), hypothesis
+//     tile fastest, handed out IN ORDER by a global atomic counter: the ~148
+//     units in flight always cover a few W blocks, each read by up to 32 CTAs
+//     at the same time, so W streams from HBM about once (L2 reuse).
 //     Units spill with red.global.add.u64 -- integer adds are associative, so
-//     the int64 sums are bit-exact for any split / order.
-// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM owner,
-// w4-7 epilogue (TMEM lanes 32*(w%4)...), w8-11 hypothesis generators.
+//     the int64 sums are bit-exact for any split / order / schedule.
+// Warp roles (768 threads): w0 TMA producer + scheduler, w1 MMA issuer,
+// w2 TMEM owner, w4-7 epilogue (TMEM lanes 32*(w%4)...), w8-23 generators
+// (two groups of 8 warps on alternate pipeline stages).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -34,23 +38,34 @@ constexpr int BM = 128;           // sub-keys per tile (MMA M)
 constexpr int BN = 256;           // samples per tile (MMA N)
 constexpr int BK = 64;            // traces per pipeline stage
 constexpr int MMA_K = 32;         // kind::i8 K per instruction
-constexpr int STAGES = 5;
+constexpr int STAGES = 6;  // even: generator group g owns slots s with s % XT_GROUPS == g, so it
+                           // sees every phase of its slots in order (mbarrier parity waits
+                           // are 1-bit and would alias if a waiter could skip a phase)
+constexpr int SCHED_Q = 4;        // depth of the unit-id ring
 constexpr int A_BYTES = BK * BM;              // 8 KB
 constexpr int B_BYTES = BK * BN;              // 16 KB (two 128-sample TMA boxes)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int V_BYTES = 65536;
 constexpr int TX_BYTES = BK * 16;             // ciphertext rows of one stage
 constexpr int EPI_WARPS = 4;
-constexpr int GEN_WARPS = 8;
-constexpr int TB_BYTES = EPI_WARPS * 32 * 33 * 4;
+constexpr int GEN_GROUP = 8;                 // generator warps per stage
+#ifndef XT_GROUPS
+#define XT_GROUPS 2
+#endif
+constexpr int GEN_WARPS = XT_GROUPS * GEN_GROUP;  // groups take alternate stages
+static_assert(STAGES % XT_GROUPS == 0, "generator groups must own whole pipeline slots");
+constexpr int SCHED_CONSUMERS = 1 + EPI_WARPS + GEN_WARPS;  // MMA thread + warps
+constexpr int TB_LD = 9;                      // epilogue transpose row stride (words, odd)
+constexpr int TB_BYTES = EPI_WARPS * 32 * TB_LD * 4;
 constexpr int SMEM_V = 0;
 constexpr int SMEM_STAGE = SMEM_V + V_BYTES;
 constexpr int SMEM_TX = SMEM_STAGE + STAGES * STAGE_BYTES;
 constexpr int SMEM_TB = SMEM_TX + STAGES * TX_BYTES;
 constexpr int SMEM_BAR = SMEM_TB + TB_BYTES;
-constexpr int NUM_BARS = 3 * STAGES + 4;
-constexpr int SMEM_TOTAL = SMEM_BAR + NUM_BARS * 8 + 16;
-constexpr int SMEM_ALLOC = SMEM_TOTAL + 1024;  // slack for 1024-byte alignment
+constexpr int NUM_BARS = 3 * STAGES + 4 + 2 * SCHED_Q;
+constexpr int SMEM_SCHED = SMEM_BAR + NUM_BARS * 8;
+constexpr int SMEM_TOTAL = SMEM_SCHED + SCHED_Q * 4 + 16;
+constexpr int SMEM_ALLOC = SMEM_TOTAL;
 constexpr int THREADS = 32 * (8 + GEN_WARPS);
 constexpr uint32_t TMEM_COLS = 512;
 
@@ -58,6 +73,7 @@ struct Params {
     const uint8_t *texts;    // N x 16
     const uint8_t *vtab;     // 256 x 256 (global copy of V)
     unsigned long long *hw;  // sum_hw [4096][M]
+    int *unit_counter;       // zeroed before the launch
     int32_t M;
     int32_t n_tiles;
     int32_t kc_count;
@@ -71,9 +87,9 @@ __device__ __forceinline__ void unit_coords(const Params &p, int u, int &hyp_til
                                             int64_t &t0, int64_t &t1)
 {
     hyp_tile = u & 31;
-    int r = u >> 5;
-    n_tile = r % p.n_tiles;
-    int kc = r / p.n_tiles;
+    const int r = u >> 5;
+    const int kc = r % p.kc_count;
+    n_tile = r / p.kc_count;
     t0 = (int64_t)kc * p.kc_len;
     t1 = t0 + p.kc_len;
     if (t1 > p.N) t1 = p.N;
@@ -84,18 +100,31 @@ __device__ __forceinline__ int shiftrows_src(int b) { return (b & 3) + 4 * (((b 
 __global__ void __launch_bounds__(THREADS, 1)
 k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
 {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    extern __shared__ __align__(1024) uint8_t smem[];  // keeps shared provenance (LDS/STS)
     const uint32_t sbase = smem_u32(smem);
+    if (threadIdx.x == 0 && (sbase & 1023)) __trap();  // 128B-swizzle atoms need 1 KB alignment
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
     auto full_bar = [&](int s) { return sbase + SMEM_BAR + 8 * s; };
     auto empty_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (STAGES + s); };
-    auto tfull_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (2 * STAGES + a); };
-    auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (2 * STAGES + 2 + a); };
-    auto txfull_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (2 * STAGES + 4 + s); };
-    uint32_t *tmem_slot = (uint32_t *)(smem + SMEM_BAR + NUM_BARS * 8);
+    auto txfull_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (2 * STAGES + s); };
+    auto tfull_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (3 * STAGES + a); };
+    auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (3 * STAGES + 2 + a); };
+    auto sfull_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (3 * STAGES + 4 + q); };
+    auto sempty_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (3 * STAGES + 4 + SCHED_Q + q); };
+    volatile int *sched = (volatile int *)(smem + SMEM_SCHED);
+    uint32_t *tmem_slot = (uint32_t *)(smem + SMEM_SCHED + SCHED_Q * 4);
+
+    // consumers: the t-th unit this CTA works on (-1 = done)
+    auto next_unit = [&](uint32_t t) {
+        const int q = t % SCHED_Q;
+        mbar_wait(sfull_bar(q), (t / SCHED_Q) & 1);
+        const int u = sched[q];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sempty_bar(q));
+        return u;
+    };
 
     // ---- setup: V table to smem, barriers, TMEM ----
     {
@@ -106,13 +135,17 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmap_w);
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(full_bar(s), 1 + GEN_WARPS);  // TMA expect_tx arrive + generator warps
+            mbar_init(full_bar(s), 1 + GEN_GROUP);  // TMA expect_tx arrive + one generator group
             mbar_init(empty_bar(s), 1);             // tcgen05.commit
             mbar_init(txfull_bar(s), 1);            // ciphertext rows landed
         }
         for (int a = 0; a < 2; a++) {
             mbar_init(tfull_bar(a), 1);
             mbar_init(tempty_bar(a), EPI_WARPS);
+        }
+        for (int q = 0; q < SCHED_Q; q++) {
+            mbar_init(sfull_bar(q), 1);
+            mbar_init(sempty_bar(q), SCHED_CONSUMERS);
         }
         fence_mbar_init();
     }
@@ -123,18 +156,25 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ================= TMA producer (W tiles) =================
+        // ================= scheduler + TMA producer =================
         if (lane == 0) {
             uint32_t it = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            for (uint32_t t = 0;; t++) {
+                int u = atomicAdd(p.unit_counter, 1);
+                if (u >= p.units) u = -1;
+                const int q = t % SCHED_Q;
+                mbar_wait(sempty_bar(q), ((t / SCHED_Q) & 1) ^ 1);
+                sched[q] = u;
+                mbar_arrive(sfull_bar(q));  // release: the unit id is visible to waiters
+                if (u < 0) break;
                 int ht, nt;
                 int64_t t0, t1;
                 unit_coords(p, u, ht, nt, t0, t1);
                 for (int64_t tb = t0; tb < t1; tb += BK, it++) {
-                    int s = it % STAGES;
-                    uint32_t ph = (it / STAGES) & 1;
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(empty_bar(s), ph ^ 1);
-                    uint32_t bdst = sbase + SMEM_STAGE + s * STAGE_BYTES + A_BYTES;
+                    const uint32_t bdst = sbase + SMEM_STAGE + s * STAGE_BYTES + A_BYTES;
                     // ciphertext rows for the generators (separate barrier: they
                     // must see them before they can produce the A tile)
                     const int rows = (int)((t1 - tb) < BK ? (t1 - tb) : BK);
@@ -149,8 +189,13 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
     } else if (warp == 1) {
         // ================= MMA issuer (one thread) =================
         if (lane == 0) {
-            uint32_t it = 0, t = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x, t++) {
+            uint32_t it = 0;
+            for (uint32_t t = 0;; t++) {
+                const int q = t % SCHED_Q;
+                mbar_wait(sfull_bar(q), (t / SCHED_Q) & 1);
+                const int u = sched[q];
+                mbar_arrive(sempty_bar(q));
+                if (u < 0) break;
                 int ht, nt;
                 int64_t t0, t1;
                 unit_coords(p, u, ht, nt, t0, t1);
@@ -160,8 +205,8 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
                 const uint32_t dtmem = tmem_base + acc * BN;
                 bool first = true;
                 for (int64_t tb = t0; tb < t1; tb += BK, it++) {
-                    int s = it % STAGES;
-                    uint32_t ph = (it / STAGES) & 1;
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(full_bar(s), ph);
                     tc_fence_after();
                     const uint32_t a_addr = sbase + SMEM_STAGE + s * STAGE_BYTES;
@@ -169,8 +214,8 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
 #pragma unroll
                     for (int kk = 0; kk < BK / MMA_K; kk++) {
                         // K step = 32 rows = 4 swizzle atoms of 8 rows x 128 B
-                        uint64_t ad = smem_desc_sw128(a_addr + kk * (MMA_K * 128), A_BYTES, 1024);
-                        uint64_t bd = smem_desc_sw128(b_addr + kk * (MMA_K * 128), B_BYTES / 2, 1024);
+                        const uint64_t ad = smem_desc_sw128(a_addr + kk * (MMA_K * 128), A_BYTES, 1024);
+                        const uint64_t bd = smem_desc_sw128(b_addr + kk * (MMA_K * 128), B_BYTES / 2, 1024);
                         mma_i8(dtmem, ad, bd, p.idesc, first ? 0u : 1u);
                         first = false;
                     }
@@ -182,9 +227,10 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
     } else if (warp >= 4 && warp < 8) {
         // ================= epilogue: TMEM -> int64 global (red.add) =================
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        uint32_t *tb = (uint32_t *)(smem + SMEM_TB) + q * 32 * 33;
-        uint32_t t = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x, t++) {
+        uint32_t *tbuf = (uint32_t *)(smem + SMEM_TB) + q * 32 * TB_LD;
+        for (uint32_t t = 0;; t++) {
+            const int u = next_unit(t);
+            if (u < 0) break;
             int ht, nt;
             int64_t t0, t1;
             unit_coords(p, u, ht, nt, t0, t1);
@@ -192,21 +238,25 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
             mbar_wait(tfull_bar(acc), (t >> 1) & 1);
             tc_fence_after();
             const int hrow0 = (ht >> 1) * 256 + (ht & 1) * BM + q * 32;
+            // 8 columns at a time through a small transpose buffer: each warp-wide
+            // red.add then covers 4 rows x 8 consecutive samples = 8 full 32-byte
+            // sectors (sector-efficient without a full 32x32 transpose)
+            const int rsub = lane >> 3, csub = lane & 7;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; c++) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+            for (int c = 0; c < BN / 8; c++) {
+                uint32_t v[8];
+                tmem_ld_32x32b_x8(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 8, v);
                 tmem_ld_wait();
 #pragma unroll
-                for (int x = 0; x < 32; x++) tb[lane * 33 + x] = v[x];
+                for (int x = 0; x < 8; x++) tbuf[lane * TB_LD + x] = v[x];
                 __syncwarp();
-                const int j = nt * BN + c * 32 + lane;
+                const int j = nt * BN + c * 8 + csub;
                 if (j < p.M) {
-                    unsigned long long *dst = p.hw + (int64_t)hrow0 * p.M + j;
-#pragma unroll 4
-                    for (int r = 0; r < 32; r++) {
-                        long long val = (int32_t)tb[r * 33 + lane];
-                        atomicAdd(dst + (int64_t)r * p.M, (unsigned long long)val);
+                    unsigned long long *dst = p.hw + (int64_t)(hrow0 + rsub) * p.M + j;
+#pragma unroll
+                    for (int rr = 0; rr < 8; rr++) {
+                        const long long val = (int32_t)tbuf[(4 * rr + rsub) * TB_LD + csub];
+                        atomicAdd(dst + (int64_t)(4 * rr) * p.M, (unsigned long long)val);
                     }
                 }
                 __syncwarp();
@@ -220,12 +270,15 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
         // A quarter-warp (8 lanes) builds one 128-byte trace row: lane = 16-key
         // chunk, so the V-row reads and the swizzled A-row writes are both
         // bank-conflict free.  Warp g owns rows 8g..8g+7 of the stage.
-        const int g = warp - 8;
+        const int g = (warp - 8) % GEN_GROUP;
+        const uint32_t group = (warp - 8) / GEN_GROUP;  // takes stages with it % 2 == group
         const int ql = lane & 7;           // chunk within the 128-key row
         const int sub = lane >> 3;         // row within a group of 4
         const uint8_t *vs = smem + SMEM_V;
         uint32_t it = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        for (uint32_t t = 0;; t++) {
+            const int u = next_unit(t);
+            if (u < 0) break;
             int ht, nt;
             int64_t t0, t1;
             unit_coords(p, u, ht, nt, t0, t1);
@@ -233,10 +286,12 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
             const int s_idx = shiftrows_src(b);
             const uint32_t gchunk = (uint32_t)((ht & 1) * 8 + ql);  // global 16-key chunk
             for (int64_t tb = t0; tb < t1; tb += BK, it++) {
+                if ((int)(it % XT_GROUPS) != (int)group) continue;
                 const int s = it % STAGES;
                 const uint32_t ph = (it / STAGES) & 1;
                 const int nrows = (int)((t1 - tb) < BK ? (t1 - tb) : BK);
-                mbar_wait(empty_bar(s), ph ^ 1);
+                // the producer issues a stage's text copy only after the stage
+                // was freed, so txfull also implies "A slot empty"
                 mbar_wait(txfull_bar(s), ph);
                 const uint8_t *tx = smem + SMEM_TX + s * TX_BYTES;
                 uint8_t *abase = smem + SMEM_STAGE + s * STAGE_BYTES;
@@ -279,13 +334,14 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
 int xterm_i8_smem_bytes() { return SMEM_ALLOC; }
 
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
-                            int64_t *d_hw, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
+                            int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
                             int num_sms, cudaStream_t stream, int *launches)
 {
     Params p;
     p.texts = d_texts;
     p.vtab = d_vtab;
     p.hw = (unsigned long long *)d_hw;
+    p.unit_counter = d_counter;
     p.M = M;
     p.N = N;
     p.n_tiles = (M + BN - 1) / BN;
@@ -299,38 +355,28 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, c
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    int grid = p.units < num_sms ? p.units : num_sms;
+    cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(int), stream);
+    if (e != cudaSuccess) return e;
+    const int grid = p.units < num_sms ? p.units : num_sms;
     k_xterm_i8<<<grid, THREADS, SMEM_ALLOC, stream>>>(tmap_w, p);
     if (launches) (*launches)++;
     return cudaGetLastError();
 }
 
-// The automatic split-K length: whole 64-trace stages, <= 2^20 traces (int32
-// TMEM accumulators stay exact: |H W| <= 8 * 255), and a unit count that fills
-// the SMs in as close to whole waves as possible.
+// Automatic split-K length: whole 64-trace stages, <= 2^20 traces (int32
+// TMEM accumulators stay exact: |H W| <= 8 * 255), about 8 units per CTA so
+// the dynamic schedule balances, but >= 32K traces per unit so the epilogue
+// (256 KB of int64 red.add per unit) stays a small fraction of the MMA time.
 int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms)
 {
     const int64_t tiles = 32LL * ((M + BN - 1) / BN);
-    const int64_t max_len = 1 << 20;
-    int64_t best_len = 0;
-    double best_eff = -1.0;
-    for (int64_t kc = 1; kc <= 256; kc++) {
-        int64_t len = (N + kc - 1) / kc;
-        len = (len + BK - 1) / BK * BK;
-        if (len > max_len) continue;
-        if (len < 4096 && kc > 1) break;  // keep units long enough to amortise the epilogue
-        int64_t kcount = (N + len - 1) / len;
-        int64_t units = tiles * kcount;
-        int64_t waves = (units + num_sms - 1) / num_sms;
-        double eff = (double)units / (double)(waves * num_sms);
-        if (eff > best_eff + 0.02) {  // prefer fewer chunks unless clearly better
-            best_eff = eff;
-            best_len = len;
-        }
-        if (eff > 0.97) break;
-    }
-    if (best_len == 0) best_len = (N + BK - 1) / BK * BK;
-    return best_len;
+    int64_t kc = (8LL * num_sms + tiles - 1) / tiles;  // chunks so that units >= 8 per SM
+    int64_t len = (N + kc - 1) / kc;
+    if (len < 32768) len = 32768;
+    if (len > (1 << 20)) len = 1 << 20;
+    len = (len + BK - 1) / BK * BK;
+    if (len >= N) len = (N + BK - 1) / BK * BK;
+    return len;
 }
 
 }  // namespace cpa
