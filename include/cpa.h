@@ -138,7 +138,7 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
 
 /* Tuning / test knobs.
  *   CPA_OPT_KCHUNK: traces per split-K work unit of the cross-term kernel
- *                   (multiple of 64, <= 2^20; 0 = automatic).
+ *                   (multiple of 128, <= 2^20; 0 = automatic).
  *   CPA_OPT_TIMING: nonzero = record CUDA events on the context's stream
  *                   around every kernel launch (read with cpa_phase_times). */
 enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2 };

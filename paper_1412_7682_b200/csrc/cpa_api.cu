@@ -220,8 +220,8 @@ cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
         return CPA_OK;
     }
     if (option == CPA_OPT_KCHUNK) {
-        if (value < 0 || value % 64 || value > (1 << 20))
-            return fail(CPA_E_INVALID_ARG, "KCHUNK=%lld must be a multiple of 64 in [0, 2^20]", (long long)value);
+        if (value < 0 || value % 128 || value > (1 << 20))
+            return fail(CPA_E_INVALID_ARG, "KCHUNK=%lld must be a multiple of 128 in [0, 2^20]", (long long)value);
         ctx->kchunk = value;
         return CPA_OK;
     }
@@ -264,7 +264,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     CUtensorMap tmap;
     cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)n};
     cuuint64_t strides[1] = {(cuuint64_t)ld};
-    cuuint32_t box[2] = {128, 64};
+    cuuint32_t box[2] = {128, 128};  // 128 samples (128-byte swizzle span) x 128 traces
     cuuint32_t estr[2] = {1, 1};
     CUresult r = get_encode()(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(d_w), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -4,12 +4,12 @@
 // (tcgen05.mma kind::i8, exact int32 accumulation in TMEM, spilled to int64).
 //
 // The paper computed this serially per (k, b, j) thread [P:121]; here:
-//   * A = H tile (128 sub-keys x 64 traces, u8, MN-major) is GENERATED in
+//   * A = H tile (128 sub-keys x 128 traces, u8, MN-major) is GENERATED in
 //     shared memory from the ciphertext bytes:  H[k] = V[c_s][c_b ^ k] with
 //     V[y][x] = HW(InvS[x] ^ y) (64 KB table in smem), so one 16-byte chunk of
 //     16 consecutive keys is a 16-byte chunk of row V[c_s], byte-permuted by
 //     (c_b & 15) -- one LDS.128 + 4 SEL + 4 PRMT + one STS.128 per chunk.
-//   * B = W tile (64 traces x 256 samples, s8/u8, MN-major = the caller's
+//   * B = W tile (128 traces x 256 samples, s8/u8, MN-major = the caller's
 //     trace-major layout, no transpose) arrives by TMA with 128-byte swizzle;
 //     the stage's ciphertext rows arrive by a 1-D bulk copy.
 //   * D = 128 x 256 int32 in TMEM, double-buffered (512 columns) so the
@@ -20,9 +20,9 @@
 //     at the same time, so W streams from HBM about once (L2 reuse).
 //     Units spill with red.global.add.u64 -- integer adds are associative, so
 //     the int64 sums are bit-exact for any split / order / schedule.
-// Warp roles (768 threads): w0 TMA producer + scheduler, w1 MMA issuer,
-// w2 TMEM owner, w4-7 epilogue (TMEM lanes 32*(w%4)...), w8-23 generators
-// (two groups of 8 warps on alternate pipeline stages).
+// Warp roles (768 threads): w0 scheduler + W TMA producer, w1 MMA issuer,
+// w2 TMEM owner, w3 ciphertext producer (12-slot ring, runs ahead),
+// w4-7 epilogue (TMEM lanes 32*(w%4)...), w8-23 H generators.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -36,33 +36,30 @@ namespace {
 
 constexpr int BM = 128;           // sub-keys per tile (MMA M)
 constexpr int BN = 256;           // samples per tile (MMA N)
-constexpr int BK = 64;            // traces per pipeline stage
+constexpr int BK = 128;           // traces per pipeline stage (4 MMAs per commit: tcgen05.commit
+                                  // costs ~45 clk of tensor-pipe time, measured in tools/mma_bench)
 constexpr int MMA_K = 32;         // kind::i8 K per instruction
-constexpr int STAGES = 6;  // even: generator group g owns slots s with s % XT_GROUPS == g, so it
-                           // sees every phase of its slots in order (mbarrier parity waits
-                           // are 1-bit and would alias if a waiter could skip a phase)
+constexpr int STAGES = 3;
+constexpr int TX_STAGES = 2 * STAGES;  // ciphertext ring, prefetched further ahead
 constexpr int SCHED_Q = 4;        // depth of the unit-id ring
 constexpr int A_BYTES = BK * BM;              // 8 KB
-constexpr int B_BYTES = BK * BN;              // 16 KB (two 128-sample TMA boxes)
+constexpr int B_BYTES = BK * BN;              // 32 KB (two 128-sample x 128-trace TMA boxes)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int V_BYTES = 65536;
 constexpr int TX_BYTES = BK * 16;             // ciphertext rows of one stage
 constexpr int EPI_WARPS = 4;
-constexpr int GEN_GROUP = 8;                 // generator warps per stage
-#ifndef XT_GROUPS
-#define XT_GROUPS 2
-#endif
-constexpr int GEN_WARPS = XT_GROUPS * GEN_GROUP;  // groups take alternate stages
-static_assert(STAGES % XT_GROUPS == 0, "generator groups must own whole pipeline slots");
-constexpr int SCHED_CONSUMERS = 1 + EPI_WARPS + GEN_WARPS;  // MMA thread + warps
+constexpr int GEN_WARPS = 16;                 // all generator warps work on every stage,
+                                              // so each waits every phase of every slot in
+                                              // order (mbarrier parity waits are 1-bit)
+constexpr int SCHED_CONSUMERS = 2 + EPI_WARPS + GEN_WARPS;  // MMA + text producer + warps
 constexpr int TB_LD = 9;                      // epilogue transpose row stride (words, odd)
 constexpr int TB_BYTES = EPI_WARPS * 32 * TB_LD * 4;
 constexpr int SMEM_V = 0;
 constexpr int SMEM_STAGE = SMEM_V + V_BYTES;
 constexpr int SMEM_TX = SMEM_STAGE + STAGES * STAGE_BYTES;
-constexpr int SMEM_TB = SMEM_TX + STAGES * TX_BYTES;
+constexpr int SMEM_TB = SMEM_TX + TX_STAGES * TX_BYTES;
 constexpr int SMEM_BAR = SMEM_TB + TB_BYTES;
-constexpr int NUM_BARS = 3 * STAGES + 4 + 2 * SCHED_Q;
+constexpr int NUM_BARS = 2 * STAGES + 2 * TX_STAGES + 4 + 2 * SCHED_Q;
 constexpr int SMEM_SCHED = SMEM_BAR + NUM_BARS * 8;
 constexpr int SMEM_TOTAL = SMEM_SCHED + SCHED_Q * 4 + 16;
 constexpr int SMEM_ALLOC = SMEM_TOTAL;
@@ -108,11 +105,13 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
 
     auto full_bar = [&](int s) { return sbase + SMEM_BAR + 8 * s; };
     auto empty_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (STAGES + s); };
-    auto txfull_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (2 * STAGES + s); };
-    auto tfull_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (3 * STAGES + a); };
-    auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (3 * STAGES + 2 + a); };
-    auto sfull_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (3 * STAGES + 4 + q); };
-    auto sempty_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (3 * STAGES + 4 + SCHED_Q + q); };
+    constexpr int BAR_T = 2 * STAGES + 2 * TX_STAGES, BAR_S = BAR_T + 4;
+    auto txfull_bar = [&](int x) { return sbase + SMEM_BAR + 8 * (2 * STAGES + x); };
+    auto txempty_bar = [&](int x) { return sbase + SMEM_BAR + 8 * (2 * STAGES + TX_STAGES + x); };
+    auto tfull_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + a); };
+    auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + 2 + a); };
+    auto sfull_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + q); };
+    auto sempty_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + SCHED_Q + q); };
     volatile int *sched = (volatile int *)(smem + SMEM_SCHED);
     uint32_t *tmem_slot = (uint32_t *)(smem + SMEM_SCHED + SCHED_Q * 4);
 
@@ -135,9 +134,12 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmap_w);
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(full_bar(s), 1 + GEN_GROUP);  // TMA expect_tx arrive + one generator group
+            mbar_init(full_bar(s), 1 + GEN_WARPS);  // TMA expect_tx arrive + generator warps
             mbar_init(empty_bar(s), 1);             // tcgen05.commit
-            mbar_init(txfull_bar(s), 1);            // ciphertext rows landed
+        }
+        for (int x = 0; x < TX_STAGES; x++) {
+            mbar_init(txfull_bar(x), 1);            // ciphertext rows landed
+            mbar_init(txempty_bar(x), GEN_WARPS);   // rows consumed by the generators
         }
         for (int a = 0; a < 2; a++) {
             mbar_init(tfull_bar(a), 1);
@@ -175,14 +177,33 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
                     const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(empty_bar(s), ph ^ 1);
                     const uint32_t bdst = sbase + SMEM_STAGE + s * STAGE_BYTES + A_BYTES;
-                    // ciphertext rows for the generators (separate barrier: they
-                    // must see them before they can produce the A tile)
-                    const int rows = (int)((t1 - tb) < BK ? (t1 - tb) : BK);
-                    mbar_arrive_expect_tx(txfull_bar(s), rows * 16);
-                    bulk_load(sbase + SMEM_TX + s * TX_BYTES, p.texts + tb * 16, rows * 16, txfull_bar(s));
                     mbar_arrive_expect_tx(full_bar(s), B_BYTES);
                     tma_load_2d(bdst, &tmap_w, nt * BN, (int32_t)tb, full_bar(s));
                     tma_load_2d(bdst + B_BYTES / 2, &tmap_w, nt * BN + 128, (int32_t)tb, full_bar(s));
+                }
+            }
+        }
+    } else if (warp == 3) {
+        // ================= ciphertext producer (feeds the generators) =================
+        // Own ring, TX_STAGES deep: the rows are in smem before the stage's A
+        // slot frees, so H generation overlaps the W fetch instead of following it.
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (uint32_t t = 0;; t++) {
+                const int q = t % SCHED_Q;
+                mbar_wait(sfull_bar(q), (t / SCHED_Q) & 1);
+                const int u = sched[q];
+                mbar_arrive(sempty_bar(q));
+                if (u < 0) break;
+                int ht, nt;
+                int64_t t0, t1;
+                unit_coords(p, u, ht, nt, t0, t1);
+                for (int64_t tb = t0; tb < t1; tb += BK, it++) {
+                    const int x = it % TX_STAGES;
+                    mbar_wait(txempty_bar(x), ((it / TX_STAGES) & 1) ^ 1);
+                    const int rows = (int)((t1 - tb) < BK ? (t1 - tb) : BK);
+                    mbar_arrive_expect_tx(txfull_bar(x), rows * 16);
+                    bulk_load(sbase + SMEM_TX + x * TX_BYTES, p.texts + tb * 16, rows * 16, txfull_bar(x));
                 }
             }
         }
@@ -269,9 +290,8 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
         // ================= hypothesis generators (H tile, MN-major, swizzled) =================
         // A quarter-warp (8 lanes) builds one 128-byte trace row: lane = 16-key
         // chunk, so the V-row reads and the swizzled A-row writes are both
-        // bank-conflict free.  Warp g owns rows 8g..8g+7 of the stage.
-        const int g = (warp - 8) % GEN_GROUP;
-        const uint32_t group = (warp - 8) / GEN_GROUP;  // takes stages with it % 2 == group
+        // bank-conflict free.  Warp g owns rows 8g..8g+7 of the 128-row stage.
+        const int g = warp - 8;
         const int ql = lane & 7;           // chunk within the 128-key row
         const int sub = lane >> 3;         // row within a group of 4
         const uint8_t *vs = smem + SMEM_V;
@@ -286,14 +306,13 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
             const int s_idx = shiftrows_src(b);
             const uint32_t gchunk = (uint32_t)((ht & 1) * 8 + ql);  // global 16-key chunk
             for (int64_t tb = t0; tb < t1; tb += BK, it++) {
-                if ((int)(it % XT_GROUPS) != (int)group) continue;
                 const int s = it % STAGES;
                 const uint32_t ph = (it / STAGES) & 1;
+                const int x = it % TX_STAGES;
                 const int nrows = (int)((t1 - tb) < BK ? (t1 - tb) : BK);
-                // the producer issues a stage's text copy only after the stage
-                // was freed, so txfull also implies "A slot empty"
-                mbar_wait(txfull_bar(s), ph);
-                const uint8_t *tx = smem + SMEM_TX + s * TX_BYTES;
+                mbar_wait(txfull_bar(x), (it / TX_STAGES) & 1);
+                mbar_wait(empty_bar(s), ph ^ 1);  // A slot free
+                const uint8_t *tx = smem + SMEM_TX + x * TX_BYTES;
                 uint8_t *abase = smem + SMEM_STAGE + s * STAGE_BYTES;
 #pragma unroll
                 for (int pass = 0; pass < 2; pass++) {
@@ -317,7 +336,10 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(full_bar(s));
+                if (lane == 0) {
+                    mbar_arrive(full_bar(s));
+                    mbar_arrive(txempty_bar(x));
+                }
             }
         }
     }
@@ -376,6 +398,7 @@ int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms)
     if (len > (1 << 20)) len = 1 << 20;
     len = (len + BK - 1) / BK * BK;
     if (len >= N) len = (N + BK - 1) / BK * BK;
+    if (len > (1 << 20)) len = 1 << 20;
     return len;
 }
 
