@@ -3,26 +3,33 @@
 // as a 4096 x N . N x M contraction on the sm_100a tensor cores
 // (tcgen05.mma kind::i8, exact int32 accumulation in TMEM, spilled to int64).
 //
-// The paper computed this serially per (k, b, j) thread [P:121]; here:
-//   * A = H tile (128 sub-keys x 128 traces, u8, MN-major) is GENERATED in
+// The paper computed this serially per (k, b, j) thread [P:121]; here a CTA
+// PAIR (cluster of 2, tcgen05 cta_group::2) owns one key byte b (M = 256
+// sub-keys, 128 per CTA) x 512 samples (two N = 256 accumulators = all 512
+// TMEM columns of each CTA):
+//   * A = H (128 sub-keys x 128 traces per CTA, u8, MN-major) is GENERATED in
 //     shared memory from the ciphertext bytes:  H[k] = V[c_s][c_b ^ k] with
-//     V[y][x] = HW(InvS[x] ^ y) (64 KB table in smem), so one 16-byte chunk of
-//     16 consecutive keys is a 16-byte chunk of row V[c_s], byte-permuted by
-//     (c_b & 15) -- one LDS.128 + 4 SEL + 4 PRMT + one STS.128 per chunk.
-//   * B = W tile (128 traces x 256 samples, s8/u8, MN-major = the caller's
-//     trace-major layout, no transpose) arrives by TMA with 128-byte swizzle;
-//     the stage's ciphertext rows arrive by a 1-D bulk copy.
-//   * D = 128 x 256 int32 in TMEM, double-buffered (512 columns) so the
-//     epilogue of one work unit overlaps the MMAs of the next.
-//   * Work unit = (hypothesis tile, trace chunk, sample tile), hypothesis
-//     tile fastest, handed out IN ORDER by a global atomic counter: the ~148
-//     units in flight always cover a few W blocks, each read by up to 32 CTAs
-//     at the same time, so W streams from HBM about once (L2 reuse).
-//     Units spill with red.global.add.u64 -- integer adds are associative, so
+//     V[y][x] = HW(InvS[x] ^ y) (64 KB table in smem): one 16-byte chunk of 16
+//     consecutive keys = one 16-byte chunk of row V[c_s], byte-permuted by
+//     (c_b & 15) -- LDS.128 + 4 SEL + 4 PRMT + STS.128.
+//   * B = W (128 traces x 512 samples, s8/u8, MN-major = the caller's
+//     trace-major layout, no transpose): each CTA TMA-loads HALF of each N=256
+//     tile (128 samples), so the pair reads W once for 256 keys.
+//   * 8 MMAs (2 N-tiles x 4 K-steps of 32 traces) per 128-trace stage and per
+//     tcgen05.commit (a commit costs ~45 clk of tensor-pipe time,
+//     tools/mma_bench), 3 stages.
+//   * Per stage and SM: TMA 32 KB + tensor-core operand reads 64 KB + H
+//     generation 32 KB of shared-memory traffic for 1024 clk of MMA -- the
+//     shared-memory data pipe (128 B/clk/SM) was the bound of the 1-CTA
+//     version (960 wavefronts per 512 clk).
+//   * Work unit = (byte, trace chunk, 512-sample tile), byte fastest, handed
+//     out IN ORDER by a global atomic counter (leader CTA) so the units in
+//     flight share a few W blocks in L2 (W streams from HBM about once).
+//     Units spill with red.global.add.u64: integer adds are associative, so
 //     the int64 sums are bit-exact for any split / order / schedule.
-// Warp roles (768 threads): w0 scheduler + W TMA producer, w1 MMA issuer,
-// w2 TMEM owner, w3 ciphertext producer (12-slot ring, runs ahead),
-// w4-7 epilogue (TMEM lanes 32*(w%4)...), w8-23 H generators.
+// Warp roles (768 threads per CTA): w0 scheduler (leader) + W TMA producer,
+// w1 MMA issuer (leader), w2 TMEM owner, w3 ciphertext producer, w4-7
+// epilogue (TMEM lanes 32*(w%4)...), w8-23 H generators.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -34,24 +41,26 @@
 namespace cpa {
 namespace {
 
-constexpr int BM = 128;           // sub-keys per tile (MMA M)
-constexpr int BN = 256;           // samples per tile (MMA N)
-constexpr int BK = 128;           // traces per pipeline stage (4 MMAs per commit: tcgen05.commit
-                                  // costs ~45 clk of tensor-pipe time, measured in tools/mma_bench)
+constexpr int BMC = 128;          // sub-keys per CTA (pair MMA M = 256)
+constexpr int BN = 256;           // samples per accumulator (MMA N)
+constexpr int NT = 2;             // accumulators per CTA (512 TMEM columns)
+constexpr int BNP = BN * NT;      // samples per work unit
+constexpr int BK = 128;           // traces per pipeline stage
 constexpr int MMA_K = 32;         // kind::i8 K per instruction
 constexpr int STAGES = 3;
-constexpr int TX_STAGES = 2 * STAGES;  // ciphertext ring, prefetched further ahead
+constexpr int TX_STAGES = 6;      // ciphertext ring, prefetched ahead of the stages
 constexpr int SCHED_Q = 4;        // depth of the unit-id ring
-constexpr int A_BYTES = BK * BM;              // 8 KB
-constexpr int B_BYTES = BK * BN;              // 32 KB (two 128-sample x 128-trace TMA boxes)
+constexpr int A_BYTES = BK * BMC;             // 16 KB
+constexpr int BH_BYTES = BK * (BN / 2);       // 16 KB: this CTA's half of one N tile
+constexpr int B_BYTES = NT * BH_BYTES;        // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int V_BYTES = 65536;
 constexpr int TX_BYTES = BK * 16;             // ciphertext rows of one stage
 constexpr int EPI_WARPS = 4;
-constexpr int GEN_WARPS = 16;                 // all generator warps work on every stage,
-                                              // so each waits every phase of every slot in
-                                              // order (mbarrier parity waits are 1-bit)
-constexpr int SCHED_CONSUMERS = 2 + EPI_WARPS + GEN_WARPS;  // MMA + text producer + warps
+constexpr int GEN_WARPS = 16;                 // every generator warp works on every stage, so
+                                              // each waits every phase of every slot in order
+                                              // (mbarrier parity waits are 1-bit)
+constexpr int CONSUMERS_PER_CTA = 2 + EPI_WARPS + GEN_WARPS;  // (MMA | W producer) + text producer + warps
 constexpr int TB_LD = 9;                      // epilogue transpose row stride (words, odd)
 constexpr int TB_BYTES = EPI_WARPS * 32 * TB_LD * 4;
 constexpr int SMEM_V = 0;
@@ -59,12 +68,13 @@ constexpr int SMEM_STAGE = SMEM_V + V_BYTES;
 constexpr int SMEM_TX = SMEM_STAGE + STAGES * STAGE_BYTES;
 constexpr int SMEM_TB = SMEM_TX + TX_STAGES * TX_BYTES;
 constexpr int SMEM_BAR = SMEM_TB + TB_BYTES;
-constexpr int NUM_BARS = 2 * STAGES + 2 * TX_STAGES + 4 + 2 * SCHED_Q;
+constexpr int NUM_BARS = 2 * STAGES + 2 * TX_STAGES + 2 + 2 * SCHED_Q;
 constexpr int SMEM_SCHED = SMEM_BAR + NUM_BARS * 8;
 constexpr int SMEM_TOTAL = SMEM_SCHED + SCHED_Q * 4 + 16;
 constexpr int SMEM_ALLOC = SMEM_TOTAL;
 constexpr int THREADS = 32 * (8 + GEN_WARPS);
 constexpr uint32_t TMEM_COLS = 512;
+static_assert(BNP == TMEM_COLS, "two N=256 int32 accumulators fill TMEM");
 
 struct Params {
     const uint8_t *texts;    // N x 16
@@ -72,7 +82,7 @@ struct Params {
     unsigned long long *hw;  // sum_hw [4096][M]
     int *unit_counter;       // zeroed before the launch
     int32_t M;
-    int32_t n_tiles;
+    int32_t n_tiles;         // 512-sample tiles
     int32_t kc_count;
     int32_t units;
     int64_t N;
@@ -80,11 +90,10 @@ struct Params {
     uint32_t idesc;
 };
 
-__device__ __forceinline__ void unit_coords(const Params &p, int u, int &hyp_tile, int &n_tile,
-                                            int64_t &t0, int64_t &t1)
+__device__ __forceinline__ void unit_coords(const Params &p, int u, int &b, int &n_tile, int64_t &t0, int64_t &t1)
 {
-    hyp_tile = u & 31;
-    const int r = u >> 5;
+    b = u & 15;
+    const int r = u >> 4;
     const int kc = r % p.kc_count;
     n_tile = r / p.kc_count;
     t0 = (int64_t)kc * p.kc_len;
@@ -94,7 +103,7 @@ __device__ __forceinline__ void unit_coords(const Params &p, int u, int &hyp_til
 
 __device__ __forceinline__ int shiftrows_src(int b) { return (b & 3) + 4 * (((b >> 2) + (b & 3)) & 3); }
 
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
 {
     extern __shared__ __align__(1024) uint8_t smem[];  // keeps shared provenance (LDS/STS)
@@ -102,30 +111,34 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
     if (threadIdx.x == 0 && (sbase & 1023)) __trap();  // 128B-swizzle atoms need 1 KB alignment
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the pair's MMAs)
+    const bool leader = rank == 0;
 
-    auto full_bar = [&](int s) { return sbase + SMEM_BAR + 8 * s; };
-    auto empty_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (STAGES + s); };
-    constexpr int BAR_T = 2 * STAGES + 2 * TX_STAGES, BAR_S = BAR_T + 4;
+    auto full_bar = [&](int s) { return sbase + SMEM_BAR + 8 * s; };                 // leader's is used
+    auto empty_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (STAGES + s); };     // both CTAs
     auto txfull_bar = [&](int x) { return sbase + SMEM_BAR + 8 * (2 * STAGES + x); };
     auto txempty_bar = [&](int x) { return sbase + SMEM_BAR + 8 * (2 * STAGES + TX_STAGES + x); };
-    auto tfull_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + a); };
-    auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + 2 + a); };
-    auto sfull_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + q); };
-    auto sempty_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + SCHED_Q + q); };
+    constexpr int BAR_T = 2 * STAGES + 2 * TX_STAGES, BAR_S = BAR_T + 2;
+    const uint32_t tfull_bar = sbase + SMEM_BAR + 8 * BAR_T;        // both CTAs (multicast commit)
+    const uint32_t tempty_bar = sbase + SMEM_BAR + 8 * (BAR_T + 1);  // leader's is used
+    auto sfull_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + q); };        // both CTAs
+    auto sempty_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + SCHED_Q + q); };  // leader's
     volatile int *sched = (volatile int *)(smem + SMEM_SCHED);
     uint32_t *tmem_slot = (uint32_t *)(smem + SMEM_SCHED + SCHED_Q * 4);
+    auto to_leader = [&](uint32_t a) { return mapa_shared(a, 0); };
 
-    // consumers: the t-th unit this CTA works on (-1 = done)
-    auto next_unit = [&](uint32_t t) {
+    // consumers: the t-th unit of this pair (-1 = done).  Called either by a
+    // whole warp (one arrival per warp) or by a single thread (solo = true).
+    auto next_unit = [&](uint32_t t, bool solo) {
         const int q = t % SCHED_Q;
-        mbar_wait(sfull_bar(q), (t / SCHED_Q) & 1);
+        mbar_wait_cluster(sfull_bar(q), (t / SCHED_Q) & 1);
         const int u = sched[q];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(sempty_bar(q));
+        if (!solo) __syncwarp();
+        if (solo || lane == 0) mbar_arrive_cluster(to_leader(sempty_bar(q)));
         return u;
     };
 
-    // ---- setup: V table to smem, barriers, TMEM ----
+    // ---- setup: V table to smem, barriers, TMEM (pair allocation) ----
     {
         const uint4 *src = (const uint4 *)p.vtab;
         uint4 *dst = (uint4 *)(smem + SMEM_V);
@@ -134,70 +147,74 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmap_w);
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(full_bar(s), 1 + GEN_WARPS);  // TMA expect_tx arrive + generator warps
-            mbar_init(empty_bar(s), 1);             // tcgen05.commit
+            mbar_init(full_bar(s), 2 + 2 * GEN_WARPS);  // 2 producer arrivals (+tx) + both CTAs' generators
+            mbar_init(empty_bar(s), 1);                 // multicast tcgen05.commit
         }
         for (int x = 0; x < TX_STAGES; x++) {
             mbar_init(txfull_bar(x), 1);            // ciphertext rows landed
             mbar_init(txempty_bar(x), GEN_WARPS);   // rows consumed by the generators
         }
-        for (int a = 0; a < 2; a++) {
-            mbar_init(tfull_bar(a), 1);
-            mbar_init(tempty_bar(a), EPI_WARPS);
-        }
+        mbar_init(tfull_bar, 1);
+        mbar_init(tempty_bar, 2 * EPI_WARPS);       // both CTAs' epilogues
         for (int q = 0; q < SCHED_Q; q++) {
             mbar_init(sfull_bar(q), 1);
-            mbar_init(sempty_bar(q), SCHED_CONSUMERS);
+            mbar_init(sempty_bar(q), 2 * CONSUMERS_PER_CTA);
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc<TMEM_COLS>(smem_u32(tmem_slot));
+    if (warp == 2) tmem_alloc_pair<TMEM_COLS>(smem_u32(tmem_slot));
     tc_fence_before();
     __syncthreads();
+    cluster_sync_all();  // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ================= scheduler + TMA producer =================
+        // ================= scheduler (leader) + W TMA producer (both) =================
         if (lane == 0) {
+            const uint32_t peer_sched = mapa_shared(smem_u32((const void *)sched), 1);
             uint32_t it = 0;
             for (uint32_t t = 0;; t++) {
-                int u = atomicAdd(p.unit_counter, 1);
-                if (u >= p.units) u = -1;
-                const int q = t % SCHED_Q;
-                mbar_wait(sempty_bar(q), ((t / SCHED_Q) & 1) ^ 1);
-                sched[q] = u;
-                mbar_arrive(sfull_bar(q));  // release: the unit id is visible to waiters
+                int u;
+                if (leader) {
+                    u = atomicAdd(p.unit_counter, 1);
+                    if (u >= p.units) u = -1;
+                    const int q = t % SCHED_Q;
+                    mbar_wait(sempty_bar(q), ((t / SCHED_Q) & 1) ^ 1);
+                    sched[q] = u;
+                    st_cluster_u32(peer_sched + 4 * q, (uint32_t)u);
+                    mbar_arrive(sfull_bar(q));                       // release: ids visible to waiters
+                    mbar_arrive_cluster(mapa_shared(sfull_bar(q), 1));
+                } else {
+                    u = next_unit(t, true);
+                }
                 if (u < 0) break;
-                int ht, nt;
+                int b, nt;
                 int64_t t0, t1;
-                unit_coords(p, u, ht, nt, t0, t1);
+                unit_coords(p, u, b, nt, t0, t1);
+                const int x0 = nt * BNP + (int)rank * (BN / 2);  // this CTA's half of N tile 0
                 for (int64_t tb = t0; tb < t1; tb += BK, it++) {
                     const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
-                    mbar_wait(empty_bar(s), ph ^ 1);
+                    mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
+                    const uint32_t lbar = to_leader(full_bar(s));
+                    if (leader) mbar_arrive_expect_tx(full_bar(s), 2 * B_BYTES);  // both CTAs' bytes
+                    else mbar_arrive_cluster(lbar);
                     const uint32_t bdst = sbase + SMEM_STAGE + s * STAGE_BYTES + A_BYTES;
-                    mbar_arrive_expect_tx(full_bar(s), B_BYTES);
-                    tma_load_2d(bdst, &tmap_w, nt * BN, (int32_t)tb, full_bar(s));
-                    tma_load_2d(bdst + B_BYTES / 2, &tmap_w, nt * BN + 128, (int32_t)tb, full_bar(s));
+                    tma_load_2d_pair(bdst, &tmap_w, x0, (int32_t)tb, lbar);
+                    tma_load_2d_pair(bdst + BH_BYTES, &tmap_w, x0 + BN, (int32_t)tb, lbar);
                 }
             }
         }
     } else if (warp == 3) {
-        // ================= ciphertext producer (feeds the generators) =================
-        // Own ring, TX_STAGES deep: the rows are in smem before the stage's A
-        // slot frees, so H generation overlaps the W fetch instead of following it.
+        // ================= ciphertext producer (feeds this CTA's generators) =================
         if (lane == 0) {
             uint32_t it = 0;
             for (uint32_t t = 0;; t++) {
-                const int q = t % SCHED_Q;
-                mbar_wait(sfull_bar(q), (t / SCHED_Q) & 1);
-                const int u = sched[q];
-                mbar_arrive(sempty_bar(q));
+                const int u = next_unit(t, true);
                 if (u < 0) break;
-                int ht, nt;
+                int b, nt;
                 int64_t t0, t1;
-                unit_coords(p, u, ht, nt, t0, t1);
+                unit_coords(p, u, b, nt, t0, t1);
                 for (int64_t tb = t0; tb < t1; tb += BK, it++) {
                     const int x = it % TX_STAGES;
                     mbar_wait(txempty_bar(x), ((it / TX_STAGES) & 1) ^ 1);
@@ -208,27 +225,23 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
             }
         }
     } else if (warp == 1) {
-        // ================= MMA issuer (one thread) =================
-        if (lane == 0) {
+        // ================= MMA issuer (one thread of the leader) =================
+        // (the peer's w1 stays out of the unit ring: per CTA the ring has
+        //  CONSUMERS_PER_CTA readers -- MMA here, the W producer in the peer)
+        if (lane == 0 && leader) {
             uint32_t it = 0;
             for (uint32_t t = 0;; t++) {
-                const int q = t % SCHED_Q;
-                mbar_wait(sfull_bar(q), (t / SCHED_Q) & 1);
-                const int u = sched[q];
-                mbar_arrive(sempty_bar(q));
+                const int u = next_unit(t, true);
                 if (u < 0) break;
-                int ht, nt;
+                int b, nt;
                 int64_t t0, t1;
-                unit_coords(p, u, ht, nt, t0, t1);
-                const uint32_t acc = t & 1;
-                mbar_wait(tempty_bar(acc), ((t >> 1) & 1) ^ 1);
+                unit_coords(p, u, b, nt, t0, t1);
+                mbar_wait_cluster(tempty_bar, (t & 1) ^ 1);  // both epilogues drained TMEM
                 tc_fence_after();
-                const uint32_t dtmem = tmem_base + acc * BN;
                 bool first = true;
                 for (int64_t tb = t0; tb < t1; tb += BK, it++) {
                     const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
-                    mbar_wait(full_bar(s), ph);
+                    mbar_wait_cluster(full_bar(s), (it / STAGES) & 1);
                     tc_fence_after();
                     const uint32_t a_addr = sbase + SMEM_STAGE + s * STAGE_BYTES;
                     const uint32_t b_addr = a_addr + A_BYTES;
@@ -236,42 +249,43 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
                     for (int kk = 0; kk < BK / MMA_K; kk++) {
                         // K step = 32 rows = 4 swizzle atoms of 8 rows x 128 B
                         const uint64_t ad = smem_desc_sw128(a_addr + kk * (MMA_K * 128), A_BYTES, 1024);
-                        const uint64_t bd = smem_desc_sw128(b_addr + kk * (MMA_K * 128), B_BYTES / 2, 1024);
-                        mma_i8(dtmem, ad, bd, p.idesc, first ? 0u : 1u);
+#pragma unroll
+                        for (int n = 0; n < NT; n++) {
+                            const uint64_t bd = smem_desc_sw128(b_addr + n * BH_BYTES + kk * (MMA_K * 128), BH_BYTES, 1024);
+                            mma_i8_pair(tmem_base + n * BN, ad, bd, p.idesc, first ? 0u : 1u);
+                        }
                         first = false;
                     }
-                    mma_commit(empty_bar(s));  // frees the smem stage when the MMAs finish
+                    mma_commit_pair(empty_bar(s), 0x3);  // frees the stage in both CTAs when done
                 }
-                mma_commit(tfull_bar(acc));    // accumulator ready for the epilogue
+                mma_commit_pair(tfull_bar, 0x3);         // accumulators ready for both epilogues
             }
         }
     } else if (warp >= 4 && warp < 8) {
         // ================= epilogue: TMEM -> int64 global (red.add) =================
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         uint32_t *tbuf = (uint32_t *)(smem + SMEM_TB) + q * 32 * TB_LD;
+        const int rsub = lane >> 3, csub = lane & 7;
         for (uint32_t t = 0;; t++) {
-            const int u = next_unit(t);
+            const int u = next_unit(t, false);
             if (u < 0) break;
-            int ht, nt;
+            int b, nt;
             int64_t t0, t1;
-            unit_coords(p, u, ht, nt, t0, t1);
-            const uint32_t acc = t & 1;
-            mbar_wait(tfull_bar(acc), (t >> 1) & 1);
+            unit_coords(p, u, b, nt, t0, t1);
+            mbar_wait_cluster(tfull_bar, t & 1);
             tc_fence_after();
-            const int hrow0 = (ht >> 1) * 256 + (ht & 1) * BM + q * 32;
+            const int hrow0 = b * 256 + (int)rank * BMC + q * 32;
             // 8 columns at a time through a small transpose buffer: each warp-wide
-            // red.add then covers 4 rows x 8 consecutive samples = 8 full 32-byte
-            // sectors (sector-efficient without a full 32x32 transpose)
-            const int rsub = lane >> 3, csub = lane & 7;
+            // red.add covers 4 rows x 8 consecutive samples = 8 full 32-byte sectors
 #pragma unroll 1
-            for (int c = 0; c < BN / 8; c++) {
+            for (int c = 0; c < BNP / 8; c++) {
                 uint32_t v[8];
-                tmem_ld_32x32b_x8(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 8, v);
+                tmem_ld_32x32b_x8(tmem_base + ((uint32_t)(q * 32) << 16) + c * 8, v);
                 tmem_ld_wait();
 #pragma unroll
                 for (int x = 0; x < 8; x++) tbuf[lane * TB_LD + x] = v[x];
                 __syncwarp();
-                const int j = nt * BN + c * 8 + csub;
+                const int j = nt * BNP + c * 8 + csub;  // accumulator column c*8+csub = sample
                 if (j < p.M) {
                     unsigned long long *dst = p.hw + (int64_t)(hrow0 + rsub) * p.M + j;
 #pragma unroll
@@ -284,7 +298,7 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(tempty_bar(acc));
+            if (lane == 0) mbar_arrive_cluster(to_leader(tempty_bar));
         }
     } else if (warp >= 8) {
         // ================= hypothesis generators (H tile, MN-major, swizzled) =================
@@ -297,14 +311,13 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
         const uint8_t *vs = smem + SMEM_V;
         uint32_t it = 0;
         for (uint32_t t = 0;; t++) {
-            const int u = next_unit(t);
+            const int u = next_unit(t, false);
             if (u < 0) break;
-            int ht, nt;
+            int b, nt;
             int64_t t0, t1;
-            unit_coords(p, u, ht, nt, t0, t1);
-            const int b = ht >> 1;
+            unit_coords(p, u, b, nt, t0, t1);
             const int s_idx = shiftrows_src(b);
-            const uint32_t gchunk = (uint32_t)((ht & 1) * 8 + ql);  // global 16-key chunk
+            const uint32_t gchunk = rank * 8 + ql;  // global 16-key chunk (keys 128*rank ...)
             for (int64_t tb = t0; tb < t1; tb += BK, it++) {
                 const int s = it % STAGES;
                 const uint32_t ph = (it / STAGES) & 1;
@@ -337,23 +350,55 @@ k_xterm_i8(const __grid_constant__ CUtensorMap tmap_w, const Params p)
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive(full_bar(s));
+                    if (leader) mbar_arrive(full_bar(s));
+                    else mbar_arrive_cluster(to_leader(full_bar(s)));
                     mbar_arrive(txempty_bar(x));
                 }
             }
         }
     }
 
+    tc_fence_before();
     __syncthreads();
+    cluster_sync_all();  // the peer's MMAs / remote arrivals are done with our smem and TMEM
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<TMEM_COLS>(tmem_base);
+        tmem_dealloc_pair<TMEM_COLS>(tmem_base);
     }
 }
 
 }  // namespace
 
 int xterm_i8_smem_bytes() { return SMEM_ALLOC; }
+
+// Automatic split-K length: whole 128-trace stages, <= 2^20 traces (int32
+// TMEM accumulators stay exact: |H W| <= 8 * 255), chosen to balance the work
+// units over the CTA pairs while keeping each unit long enough that its
+// epilogue (which stalls the pair's MMAs: TMEM is not double-buffered) is a
+// small fraction (model: ~25k clk per epilogue, 1024 clk per stage).
+int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms)
+{
+    const int64_t tiles = 16LL * ((M + BNP - 1) / BNP);
+    const int64_t pairs = num_sms / 2;
+    int64_t best_len = 0;
+    double best = -1.0;
+    for (int64_t kc = 1; kc <= 64; kc++) {
+        int64_t len = (N + kc - 1) / kc;
+        len = (len + BK - 1) / BK * BK;
+        if (len > (1 << 20)) continue;
+        const int64_t kcount = (N + len - 1) / len;
+        const int64_t units = tiles * kcount;
+        const int64_t waves = (units + pairs - 1) / pairs;
+        const double stage_clk = (double)((len + BK - 1) / BK) * 1024.0;
+        const double eff = (double)units / (double)(waves * pairs) * stage_clk / (stage_clk + 25000.0);
+        if (eff > best + 1e-3) {
+            best = eff;
+            best_len = len;
+        }
+    }
+    if (best_len == 0) best_len = 1 << 20;
+    return best_len;
+}
 
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
                             int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
@@ -366,11 +411,11 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, c
     p.unit_counter = d_counter;
     p.M = M;
     p.N = N;
-    p.n_tiles = (M + BN - 1) / BN;
+    p.n_tiles = (M + BNP - 1) / BNP;
     p.kc_len = kc_len;
     p.kc_count = (int32_t)((N + kc_len - 1) / kc_len);
-    p.units = 32 * p.n_tiles * p.kc_count;
-    p.idesc = idesc_i8(BM, BN, w_signed);
+    p.units = 16 * p.n_tiles * p.kc_count;
+    p.idesc = idesc_i8(2 * BMC, BN, w_signed);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_xterm_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
@@ -379,27 +424,10 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, c
     }
     cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(int), stream);
     if (e != cudaSuccess) return e;
-    const int grid = p.units < num_sms ? p.units : num_sms;
-    k_xterm_i8<<<grid, THREADS, SMEM_ALLOC, stream>>>(tmap_w, p);
+    const int pairs = (p.units < num_sms / 2 ? p.units : num_sms / 2);
+    k_xterm_i8<<<2 * pairs, THREADS, SMEM_ALLOC, stream>>>(tmap_w, p);
     if (launches) (*launches)++;
     return cudaGetLastError();
-}
-
-// Automatic split-K length: whole 64-trace stages, <= 2^20 traces (int32
-// TMEM accumulators stay exact: |H W| <= 8 * 255), about 8 units per CTA so
-// the dynamic schedule balances, but >= 32K traces per unit so the epilogue
-// (256 KB of int64 red.add per unit) stays a small fraction of the MMA time.
-int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms)
-{
-    const int64_t tiles = 32LL * ((M + BN - 1) / BN);
-    int64_t kc = (8LL * num_sms + tiles - 1) / tiles;  // chunks so that units >= 8 per SM
-    int64_t len = (N + kc - 1) / kc;
-    if (len < 32768) len = 32768;
-    if (len > (1 << 20)) len = 1 << 20;
-    len = (len + BK - 1) / BK * BK;
-    if (len >= N) len = (N + BK - 1) / BK * BK;
-    if (len > (1 << 20)) len = 1 << 20;
-    return len;
 }
 
 }  // namespace cpa
