@@ -181,9 +181,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1412_7682_b200 as P
 
+    from paper_1412_7682_b200.multigpu import shard_range
     dev = torch.device("cuda", local)
-    i0 = w.n * rank // world
-    i1 = w.n * (rank + 1) // world
+    i0, i1 = shard_range(w.n, rank, world)
     n_local = i1 - i0
     # ---- inputs: texts + planted leakage on the host, traces generated on device
     texts, lv = S.texts(w, i0, n_local)

@@ -82,9 +82,9 @@ class Engine:
     def allreduce(self, group=None):
         """Combine partial sums over ranks: one all-reduce(SUM) [a7].  Exact
         for the int64 accumulator under any reduction order."""
-        import torch.distributed as dist
+        from .multigpu import allreduce_accumulator
         with torch.cuda.stream(self.stream):
-            dist.all_reduce(self.accum, op=dist.ReduceOp.SUM, group=group)
+            allreduce_accumulator(self.accum, group)
 
     def finalize(self, want_rho: bool = False):
         dev = self.device
