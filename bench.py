@@ -107,6 +107,19 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- cpu baseline ----
+def oracle_attack(O, texts, Ws):
+    """The oracle's Phases 1-4 on the sampled columns (int or float traces)."""
+    import numpy as np
+    if Ws.dtype == np.float32:
+        sh, sh2 = O.model_sums(O.HD_LAST, texts)
+        shw, sw, sw2 = O.sums_f32(O.HD_LAST, texts, Ws)
+        rho = O.rho_eq1_f64_grid(Ws.shape[0], shw, sh, sh2, sw, sw2)
+        mx, am, pk = O.phase3(rho)
+        best, rank = O.phase4(mx)
+        return {"best": best}
+    return O.attack_i8(O.HD_LAST, texts, Ws, np.arange(Ws.shape[1], dtype=np.int32))
+
+
 def cpu_baseline(w, sample_traces=CPU_SAMPLE_TRACES, ncols=CPU_SAMPLE_COLS):
     """The oracle as it stands (single-threaded C, oracle/oracle.c), timed on a
     bounded sample of the same workload; rate scaled linearly to N = w.n."""
@@ -118,7 +131,7 @@ def cpu_baseline(w, sample_traces=CPU_SAMPLE_TRACES, ncols=CPU_SAMPLE_COLS):
     cols = np.array(sorted(w.leak_positions()[:2] + [w.m // 5, (3 * w.m) // 5]), np.int32)[:ncols]
     Ws = S.traces(w, lv, 0, cols)
     t0 = time.perf_counter()
-    a = O.attack_i8(O.HD_LAST, texts, Ws, np.arange(len(cols), dtype=np.int32))
+    a = oracle_attack(O, texts, Ws)
     t = time.perf_counter() - t0
     t_full = t * (w.n / n)
     return {"value": 4096 * len(cols) / t_full, "unit": "correlations/s", "cores": 1, "kind": "oracle",
@@ -142,7 +155,7 @@ def run_reference(args, w):
     ts = []
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        O.attack_i8(O.HD_LAST, texts, Ws, np.arange(len(cols), dtype=np.int32))
+        oracle_attack(O, texts, Ws)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             ts.append(dt * (w.n / n))
@@ -186,15 +199,17 @@ def main():
     i0, i1 = shard_range(w.n, rank, world)
     n_local = i1 - i0
     # ---- inputs: texts + planted leakage on the host, traces generated on device
+    is_f32 = w.dtype == S.F32
+    tdt = torch.float32 if is_f32 else torch.int8
     texts, lv = S.texts(w, i0, n_local)
-    ld = (w.m + 15) // 16 * 16
-    dW = torch.empty((n_local, ld), dtype=torch.int8, device=dev)
+    ld = (w.m + 3) // 4 * 4 if is_f32 else (w.m + 15) // 16 * 16  # 16-byte rows for TMA
+    dW = torch.empty((n_local, ld), dtype=tdt, device=dev)
     dT = torch.from_numpy(texts).to(dev)
     S.dev_traces(w, torch.from_numpy(lv).to(dev), i0, n_local, dW, ld)
     dWv = dW[:, :w.m]
     torch.cuda.synchronize()
 
-    eng = P.Engine(w.m, P.CPA_S8, P.CPA_HD_LAST, local)
+    eng = P.Engine(w.m, P.CPA_F32 if is_f32 else P.CPA_S8, P.CPA_HD_LAST, local)
     rho = torch.empty((4096, w.m), dtype=torch.float64, device=dev)
     maxabs = torch.empty(4096, dtype=torch.float64, device=dev)
     argmax = torch.empty(4096, dtype=torch.int32, device=dev)
@@ -245,9 +260,10 @@ def main():
     # ---- roofline of the dominant kernel (cross term, tensor-bound)
     peaks, src = load_peaks()
     xt_ms = phase_ms["xterm"] / max(1, phase_n["xterm"])
-    ops = 2.0 * 4096 * n_local * w.m
+    ops = 2.0 * 4096 * n_local * w.m   # algorithmic: one multiply-add per (h, i, j)
     achieved = ops / (xt_ms * 1e-3) / 1e12
-    peak = peaks["bf16_tflops_sustained"] * INT8_PER_BF16
+    ratio = 1.0 if is_f32 else INT8_PER_BF16
+    peak = peaks["bf16_tflops_sustained"] * ratio
     traffic = None
     tp = os.path.join(ROOT, "profiles", "xterm_traffic.json")
     if os.path.exists(tp):
@@ -255,11 +271,15 @@ def main():
             tj = json.load(f)
         if tj.get("config") == w.name and tj.get("n_gpus", 1) == world:
             traffic = tj.get("dram_bytes_per_launch")
-    roofline = {"kernel": "k_xterm_i8", "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "peak_source": f"{src} bf16_tflops_sustained x {INT8_PER_BF16:g} (int8:bf16 nominal ratio)",
-                "frac_of_burst": achieved / (peaks["bf16_tflops"] * INT8_PER_BF16),
+    roofline = {"kernel": "k_xterm<F32>" if is_f32 else "k_xterm<I8>", "bound": "tensor", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": (f"{src} bf16_tflops_sustained" if is_f32 else
+                                f"{src} bf16_tflops_sustained x {INT8_PER_BF16:g} (int8:bf16 nominal ratio)"),
+                "frac_of_burst": achieved / (peaks["bf16_tflops"] * ratio),
                 "algorithmic_ops_per_launch": ops, "ms_per_launch": xt_ms}
+    if is_f32:
+        roofline["executed_ops_per_launch"] = 2 * ops  # bf16 hi + lo MMAs
+        roofline["executed_frac"] = 2 * achieved / peak
     step_phase_ms = {k: v / args.steps for k, v in phase_ms.items()}
     tot = sum(step_phase_ms.values()) or 1.0
     # HBM-bound kernels: achieved GB/s on their algorithmic bytes
@@ -271,7 +291,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         try:
-            hW = torch.empty((n_local, w.m), dtype=torch.int8, pin_memory=True)
+            hW = torch.empty((n_local, w.m), dtype=tdt, pin_memory=True)
             hW.copy_(dWv)
             hT = torch.from_numpy(texts).pin_memory()
             step((hW, hT))  # warm the staging buffers
@@ -291,7 +311,8 @@ def main():
             else:
                 te = statistics.mean(ts)
             e2e = {"value": 4096 * w.m / te, "unit": "correlations/s",
-                   "h2d_bytes_per_step": n_local * (w.m + 16), "d2h_bytes_per_step": 8 + 32 * 4 + 16 * 8,
+                   "h2d_bytes_per_step": n_local * (w.m * hW.element_size() + 16),
+                   "d2h_bytes_per_step": 8 + 32 * 4 + 16 * 8,
                    "ms_per_step": te * 1e3, "time_to_key_s": te, "key_recovered": bytes(r2.master_key) == w.key,
                    "host_buffers": "pinned"}
             del hW
@@ -307,11 +328,14 @@ def main():
             "metric": "hypothesis x sample correlations/s at 1.5M traces", "value": value,
             "unit": "correlations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "s8", "data": "synthetic",
-            "config": {"workload": f"{w.name}: {w.n} traces x {w.m} samples int8 (s8), HD last-round model, "
+            "dtype": "bf16x2 (f32 traces, fp32 accum, fp64 sums)" if is_f32 else "s8",
+            "data": "synthetic",
+            "config": {"workload": f"{w.name}: {w.n} traces x {w.m} samples "
+                                   f"{'float32' if is_f32 else 'int8 (s8)'}, HD last-round model, "
                                    f"AES-128 key {w.key.hex()}",
                        "n_traces": w.n, "n_samples": w.m, "hypotheses": 4096, "parallelism": f"trace-shard x{world}",
-                       "l2": "inputs 7.5 GB > 126 MB L2, no flush needed", "rho_written": True},
+                       "l2": f"inputs {n_local * w.m * dW.element_size() / 1e9:.1f} GB > 126 MB L2, no flush needed",
+                       "rho_written": True},
             "key_recovered": key_ok, "gpu_launches": launches,
             "phases_ms_per_step": step_phase_ms,
             "phase_share": {k: v / tot for k, v in step_phase_ms.items()},

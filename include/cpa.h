@@ -48,7 +48,9 @@ typedef enum {
     CPA_E_NO_MEMORY = 4,          /* device scratch allocation failed */
     CPA_E_TOO_FEW_TRACES = 5,     /* N < 2 at finalize: Eq. (1) undefined [S:268] */
     CPA_E_OVERFLOW = 6,           /* N beyond the exact-int64 bound (2^23 traces) */
-    CPA_E_UNSUPPORTED_DEVICE = 7  /* not a compute-capability 10.0 (sm_100a) GPU */
+    CPA_E_UNSUPPORTED_DEVICE = 7, /* not a compute-capability 10.0 (sm_100a) GPU */
+    CPA_E_NONFINITE = 8           /* CPA_F32: a trace sample was NaN/Inf [S:140, S:176];
+                                     sticky, reported by cpa_finalize */
 } cpa_status;
 
 typedef enum {
@@ -132,7 +134,16 @@ typedef struct {
 CPA_API cpa_status cpa_finalize(cpa_ctx *ctx, double *d_rho, double *d_maxabs,
                         int32_t *d_argmax, int32_t *d_rank, cpa_result *res);
 
-CPA_API cpa_status cpa_reset(cpa_ctx *ctx);    /* zero the accumulator (async) */
+/* CPA_F32 only: per-sample offsets o_j (device pointer, M floats; NULL = 0)
+ * subtracted from every sample before the bf16 hi/lo split.  rho is invariant
+ * to per-sample offsets [S:285]; centring keeps the split and the fp32 tensor-
+ * core accumulation accurate.  Default: the first trace of the first
+ * cpa_accumulate call.  Multi-GPU: every rank must use the same offsets (the
+ * accumulated sums are of the offset samples).                               */
+CPA_API cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets);
+
+CPA_API cpa_status cpa_reset(cpa_ctx *ctx);    /* zero the accumulator and the
+                                                  non-finite flag (async) */
 CPA_API cpa_status cpa_sync(cpa_ctx *ctx);     /* wait for all queued work */
 CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum) */
 

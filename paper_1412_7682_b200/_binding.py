@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("CPA_LIB_PATH") or os.path.join(_PKG, "libcpa.so")  # 
 
 CPA_OK = 0
 CPA_E_INVALID_ARG, CPA_E_BAD_STATE, CPA_E_CUDA, CPA_E_NO_MEMORY = 1, 2, 3, 4
-CPA_E_TOO_FEW_TRACES, CPA_E_OVERFLOW, CPA_E_UNSUPPORTED_DEVICE = 5, 6, 7
+CPA_E_TOO_FEW_TRACES, CPA_E_OVERFLOW, CPA_E_UNSUPPORTED_DEVICE, CPA_E_NONFINITE = 5, 6, 7, 8
 CPA_S8, CPA_U8, CPA_F32 = 0, 1, 2
 CPA_HD_LAST, CPA_HW_LAST, CPA_HW_FIRST = 0, 1, 2
 CPA_OPT_KCHUNK, CPA_OPT_TIMING = 1, 2
@@ -26,7 +26,7 @@ FIELD_HW, FIELD_W, FIELD_W2, FIELD_H, FIELD_H2, FIELD_N = range(6)
 ABI_SYMBOLS = (
     "cpa_accum_words", "cpa_accum_bytes", "cpa_accum_offset", "cpa_init", "cpa_accumulate",
     "cpa_accumulate_host", "cpa_finalize", "cpa_reset", "cpa_sync", "cpa_destroy",
-    "cpa_set_option", "cpa_phase_times", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
+    "cpa_set_offsets", "cpa_set_option", "cpa_phase_times", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
     "cpa_aes_expand_key", "cpa_aes_invert_key_schedule",
 )
 
@@ -61,6 +61,7 @@ def _load():
         "cpa_reset": (ST, [P]),
         "cpa_sync": (ST, [P]),
         "cpa_destroy": (ST, [P]),
+        "cpa_set_offsets": (ST, [P, P]),
         "cpa_set_option": (ST, [P, C.c_int, I64]),
         "cpa_phase_times": (ST, [P, P, P]),
         "cpa_launch_count": (I64, [P]),
@@ -140,6 +141,10 @@ def cpa_sync(ctx):
 
 def cpa_destroy(ctx):
     _check(_lib.cpa_destroy(ctx), "cpa_destroy")
+
+
+def cpa_set_offsets(ctx, d_offsets):
+    _check(_lib.cpa_set_offsets(ctx, _ptr(d_offsets)), "cpa_set_offsets")
 
 
 def cpa_set_option(ctx, option: int, value: int):

@@ -9,8 +9,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcpa.so")
-SOURCES = ["cpa_api.cu", "kernels.cu", "xterm_i8.cu", "xterm_f32.cu", "aes_host.cpp"]
-HEADERS = ["ptx.cuh", "kernels.h", "tables.h", "xterm_f32.h"]
+SOURCES = ["cpa_api.cu", "kernels.cu", "xterm.cu", "aes_host.cpp"]
+HEADERS = ["ptx.cuh", "kernels.h", "tables.h"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-shared"]
 

@@ -16,7 +16,6 @@
 #include "../../include/cpa.h"
 #include "kernels.h"
 #include "tables.h"
-#include "xterm_f32.h"
 
 namespace {
 
@@ -82,7 +81,12 @@ struct cpa_ctx {
     int64_t stage_bytes = 0;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
-    cpa::XtermF32Scratch f32;  // float-path scratch
+    // float path (a6): per-sample offsets, bf16 hi/lo planes, non-finite flag
+    float *d_offset = nullptr;
+    bool offset_set = false;
+    uint16_t *d_hi = nullptr, *d_lo = nullptr;
+    int64_t plane_rows = 0;
+    int *d_nonfinite = nullptr;
     // CPA_OPT_TIMING: CUDA events recorded on `stream` around every launch
     bool timing = false;
     struct Rec { int phase; cudaEvent_t a, b; };
@@ -133,6 +137,7 @@ const char *cpa_status_str(cpa_status s)
     case CPA_E_TOO_FEW_TRACES: return "CPA_E_TOO_FEW_TRACES";
     case CPA_E_OVERFLOW: return "CPA_E_OVERFLOW";
     case CPA_E_UNSUPPORTED_DEVICE: return "CPA_E_UNSUPPORTED_DEVICE";
+    case CPA_E_NONFINITE: return "CPA_E_NONFINITE";
     }
     return "CPA_E_UNKNOWN";
 }
@@ -152,6 +157,7 @@ cpa_status cpa_reset(cpa_ctx *ctx)
     if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
     CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
     CUDA_TRY(cudaMemsetAsync(ctx->accum, 0, cpa_accum_bytes(ctx->M), ctx->stream), "reset accumulator");
+    CUDA_TRY(cudaMemsetAsync(ctx->d_nonfinite, 0, sizeof(int), ctx->stream), "reset flag");
     return CPA_OK;
 }
 
@@ -197,18 +203,35 @@ cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, 
     if (e == cudaSuccess) e = cudaMalloc(&c->d_rank, sizeof(int32_t) * 4096);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_best, sizeof(int32_t) * 32);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_counter, 256);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_nonfinite, 256);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_offset, sizeof(float) * M);
     if (e != cudaSuccess) {
         cpa_destroy(c);
         return fail(CPA_E_NO_MEMORY, "device scratch: %s", cudaGetErrorString(e));
     }
     e = cudaMemcpyAsync(c->d_vtab, vt, 65536, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_accum, 0, cpa_accum_bytes(M), c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->d_nonfinite, 0, sizeof(int), c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
         cpa_destroy(c);
         return cuda_fail(e, "cpa_init upload");
     }
     *out = c;
+    return CPA_OK;
+}
+
+cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets)
+{
+    if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
+    if (ctx->dtype != CPA_F32) return fail(CPA_E_INVALID_ARG, "offsets apply to CPA_F32 contexts only");
+    CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (d_offsets)
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_offset, d_offsets, sizeof(float) * ctx->M, cudaMemcpyDeviceToDevice, ctx->stream),
+                 "offsets");
+    else
+        CUDA_TRY(cudaMemsetAsync(ctx->d_offset, 0, sizeof(float) * ctx->M, ctx->stream), "offsets");
+    ctx->offset_set = true;
     return CPA_OK;
 }
 
@@ -240,12 +263,57 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                                       c->stream, &launches);
                  }),
                  "modelsums");
-        cudaError_t e = c->timed(2, [&] {
-            return cpa::xterm_f32_accumulate(c->f32, (const float *)d_w, ld, d_tx, n, M, c->d_vtab, acc,
-                                             c->num_sms, c->stream, &launches);
-        });
+        // per-sample offsets (centring keeps the bf16 hi/lo split and the fp32
+        // accumulation accurate; rho is invariant to them [S:285]): unless the
+        // caller set them, take the first trace of the first accumulate call
+        if (!c->offset_set) {
+            CUDA_TRY(cudaMemcpyAsync(c->d_offset, d_w, sizeof(float) * M, cudaMemcpyDeviceToDevice, c->stream),
+                     "offsets");
+            c->offset_set = true;
+        }
+        const int64_t ldh = (M + 7) / 8 * 8;
+        const int64_t max_rows = (1LL << 30) / (ldh * 2);  // <= 1 GiB per bf16 plane
+        const int64_t chunk = n < max_rows ? n : max_rows;
+        if (c->plane_rows < chunk) {
+            CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+            cudaFree(c->d_hi);
+            cudaFree(c->d_lo);
+            c->d_hi = c->d_lo = nullptr;
+            c->plane_rows = 0;
+            if (cudaMalloc(&c->d_hi, chunk * ldh * 2) != cudaSuccess || cudaMalloc(&c->d_lo, chunk * ldh * 2) != cudaSuccess)
+                return fail(CPA_E_NO_MEMORY, "bf16 planes (%lld rows)", (long long)chunk);
+            c->plane_rows = chunk;
+        }
+        for (int64_t i0 = 0; i0 < n; i0 += chunk) {
+            const int64_t m = (n - i0) < chunk ? (n - i0) : chunk;
+            const float *w = (const float *)d_w + i0 * ld;
+            CUDA_TRY(c->timed(1, [&] {
+                         return cpa::launch_split_f32(w, ld, m, M, c->d_offset, c->d_hi, c->d_lo, ldh,
+                                                      acc + cpa_accum_offset(M, 1), acc + cpa_accum_offset(M, 2),
+                                                      c->d_nonfinite, c->stream, &launches);
+                     }),
+                     "split_f32");
+            CUtensorMap mh, ml;
+            cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)m};
+            cuuint64_t strides[1] = {(cuuint64_t)(ldh * 2)};
+            cuuint32_t box[2] = {64, 64};  // 64 bf16 = the 128-byte swizzle span, x 64 traces
+            cuuint32_t estr[2] = {1, 1};
+            for (int k = 0; k < 2; k++) {
+                CUresult r = get_encode()(k ? &ml : &mh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, k ? c->d_lo : c->d_hi,
+                                          dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (r != CUDA_SUCCESS) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled (bf16) failed (%d)", (int)r);
+            }
+            const int64_t kc = c->kchunk ? (c->kchunk < 4096 ? c->kchunk : 4096)
+                                         : cpa::xterm_f32_auto_kchunk(M, m, c->num_sms);
+            CUDA_TRY(c->timed(2, [&] {
+                         return cpa::launch_xterm_bf16x2(mh, ml, d_tx + i0 * 16, c->d_vtab, acc, c->d_counter, M, m,
+                                                         kc, c->num_sms, c->stream, &launches);
+                     }),
+                     "xterm_bf16x2");
+        }
         c->launches += launches;
-        if (e != cudaSuccess) return cuda_fail(e, "float-path cross term");
         return CPA_OK;
     }
     int64_t *acc = (int64_t *)c->accum;
@@ -392,6 +460,11 @@ cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_
         CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
     }
     if (n < 2) return fail(CPA_E_TOO_FEW_TRACES, "N=%lld < 2: Eq. (1) undefined", (long long)n);
+    if (c->dtype == CPA_F32) {
+        int bad = 0;
+        CUDA_TRY(cudaMemcpy(&bad, c->d_nonfinite, sizeof(int), cudaMemcpyDeviceToHost), "read flag");
+        if (bad) return fail(CPA_E_NONFINITE, "a float trace sample was NaN or Inf");
+    }
     if (c->dtype != CPA_F32 && n > kMaxTraces)
         return fail(CPA_E_OVERFLOW, "N=%lld > 2^23: Eq. (1) intermediates may overflow int64", (long long)n);
     cpa::FinalizeOut o;
@@ -482,7 +555,10 @@ cpa_status cpa_destroy(cpa_ctx *c)
         if (c->ev_used[k]) cudaEventDestroy(c->ev_used[k]);
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
-    cpa::xterm_f32_free(c->f32);
+    cudaFree(c->d_offset);
+    cudaFree(c->d_hi);
+    cudaFree(c->d_lo);
+    cudaFree(c->d_nonfinite);
     for (auto &r : c->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);

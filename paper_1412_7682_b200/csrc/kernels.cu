@@ -3,6 +3,7 @@
 //   a4 trace moments   sum_i W_ij, sum_i W_ij^2 per sample j        [P:79]
 //   a8 finalize        Eq. (1) [P:69] in fp64 + max |rho| per (b,k) [P:83]
 //   a9 phase 4         per-byte ranking / best sub-key              [P:87]
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -378,4 +379,89 @@ cudaError_t launch_phase4(const FinalizeOut &o, cudaStream_t s, int *launches)
     return cudaGetLastError();
 }
 
+}  // namespace cpa
+
+// ---------------------------------------------------------------------------
+// a6 pre-pass: float traces -> centred bf16 hi/lo planes + fp64 moments.
+// Thread = 4 consecutive samples (one float4 per row) over SP_ROWS rows.
+// ---------------------------------------------------------------------------
+namespace cpa {
+namespace {
+constexpr int SP_THREADS = 256;
+constexpr int SP_ROWS = 512;
+
+__device__ __forceinline__ uint16_t bf16_bits(float x)
+{
+    __nv_bfloat16 h = __float2bfloat16_rn(x);
+    return *reinterpret_cast<uint16_t *>(&h);
+}
+__device__ __forceinline__ float bf16_val(uint16_t b)
+{
+    return __uint_as_float((uint32_t)b << 16);
+}
+
+__global__ void __launch_bounds__(SP_THREADS)
+k_split_f32(const float *__restrict__ w, int64_t ld, int64_t n, int32_t M, const float *__restrict__ offset,
+            uint16_t *__restrict__ hi, uint16_t *__restrict__ lo, int64_t ldh, double *sum_w, double *sum_w2,
+            int *nonfinite)
+{
+    const int g = blockIdx.x * SP_THREADS + threadIdx.x;
+    const int j0 = g * 4;
+    if (j0 >= M) return;
+    const int cnt = min(4, M - j0);
+    float o[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) o[q] = (q < cnt && offset) ? offset[j0 + q] : 0.0f;
+    double s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+    bool bad = false;
+    const int64_t r0 = (int64_t)blockIdx.y * SP_ROWS;
+    const int64_t r1 = min(n, r0 + SP_ROWS);
+    for (int64_t r = r0; r < r1; r++) {
+        float x[4];
+        if (cnt == 4) {
+            const float4 v = __ldg((const float4 *)(w + r * ld + j0));
+            x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; q++) x[q] = q < cnt ? w[r * ld + j0 + q] : 0.0f;
+        }
+        uint16_t h[4], l[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            bad |= !isfinite(x[q]);
+            const float c = __fsub_rn(x[q], o[q]);
+            h[q] = bf16_bits(c);
+            l[q] = bf16_bits(__fsub_rn(c, bf16_val(h[q])));
+            s1[q] += (double)c;
+            s2[q] += (double)c * (double)c;
+        }
+        uint16_t *hp = hi + r * ldh + j0, *lp = lo + r * ldh + j0;
+        if (cnt == 4) {
+            *(uint2 *)hp = make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
+            *(uint2 *)lp = make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
+        } else {
+            for (int q = 0; q < cnt; q++) {
+                hp[q] = h[q];
+                lp[q] = l[q];
+            }
+        }
+    }
+    for (int q = 0; q < cnt; q++) {
+        atomicAdd(&sum_w[j0 + q], s1[q]);
+        atomicAdd(&sum_w2[j0 + q], s2[q]);
+    }
+    if (bad) atomicOr(nonfinite, 1);
+}
+}  // namespace
+
+cudaError_t launch_split_f32(const float *d_w, int64_t ld, int64_t n, int32_t M, const float *d_offset,
+                             uint16_t *d_hi, uint16_t *d_lo, int64_t ldh, double *d_sum_w, double *d_sum_w2,
+                             int *d_nonfinite, cudaStream_t s, int *launches)
+{
+    const int groups = (M + 3) / 4;
+    dim3 grid((groups + SP_THREADS - 1) / SP_THREADS, (unsigned)((n + SP_ROWS - 1) / SP_ROWS));
+    k_split_f32<<<grid, SP_THREADS, 0, s>>>(d_w, ld, n, M, d_offset, d_hi, d_lo, ldh, d_sum_w, d_sum_w2, d_nonfinite);
+    if (launches) (*launches)++;
+    return cudaGetLastError();
+}
 }  // namespace cpa

@@ -19,12 +19,24 @@ cudaError_t launch_modelsums_f64(const uint8_t *d_texts, int64_t n, const uint8_
 cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M, bool w_signed,
                               int64_t *d_sum_w, int64_t *d_sum_w2, cudaStream_t s, int *launches);
 
-// a5: cross term (tcgen05 kind::i8)
-int xterm_i8_smem_bytes();
+// a5: cross term (tcgen05 kind::i8, CTA pairs)
+int xterm_smem_bytes();
 int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms);
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
                             int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
                             int num_sms, cudaStream_t stream, int *launches);
+
+// a6: float traces.  Split pre-pass: w' = w - offset[j] (fp32), hi = bf16(w'),
+// lo = bf16(w' - hi) into [n][ldh] bf16 planes; fp64 sum w', sum w'^2; sets
+// *nonfinite on NaN/Inf [S:140].  Cross term: kind::f16 on hi and lo, fp32 TMEM
+// accumulation per <= 4096-trace unit, fp64 atomic spill.
+cudaError_t launch_split_f32(const float *d_w, int64_t ld, int64_t n, int32_t M, const float *d_offset,
+                             uint16_t *d_hi, uint16_t *d_lo, int64_t ldh, double *d_sum_w, double *d_sum_w2,
+                             int *d_nonfinite, cudaStream_t s, int *launches);
+int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms);
+cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
+                                const uint8_t *d_vtab, double *d_hw, int *d_counter, int32_t M, int64_t N,
+                                int64_t kc_len, int num_sms, cudaStream_t stream, int *launches);
 
 // a8/a9: Phase 3 + 4 [P:81-87]
 struct FinalizeOut {

@@ -256,3 +256,17 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar, uint16_t mask)
         : "memory");
 }
 }  // namespace cpa
+
+namespace cpa {
+// D[tmem of both CTAs] (+)= A . B, kind::f16 (bf16 inputs, fp32 accumulate), CTA pair
+__device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+}  // namespace cpa

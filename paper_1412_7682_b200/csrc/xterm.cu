@@ -1,0 +1,526 @@
+// xterm.cu -- the dominant Phase-2 term [P:79]:
+//     sum_hw[h][j] = sum_i H_i(h) * W[i][j]      (h = 256 b + k, 4096 rows)
+// as a 4096 x N . N x M contraction on the sm_100a tensor cores.  One kernel
+// template, two instantiations:
+//   I8  (a5): W int8 (s8/u8), tcgen05.mma kind::i8, exact int32 accumulation in
+//        TMEM, spilled to int64 with red.add (bit-exact for any schedule);
+//   F32 (a6): W float32 pre-split into bf16 hi + lo planes (k_split_f32), two
+//        kind::f16 MMAs per K step (H.hi + H.lo), fp32 TMEM accumulation over
+//        <= 4096 traces per work unit, spilled to fp64 with atomicAdd [P:201-217].
+//
+// The paper computed this serially per (k, b, j) thread [P:121]; here a CTA
+// PAIR (cluster of 2, tcgen05 cta_group::2) owns one key byte b (M = 256
+// sub-keys, 128 per CTA) and 512 (I8) / 256 (F32) samples:
+//   * A = H (128 sub-keys x BK traces per CTA, MN-major, 128B swizzle) is
+//     GENERATED in shared memory from the ciphertext bytes: H[k] = V[c_s][c_b^k]
+//     with V[y][x] = HW(InvS[x] ^ y) (64 KB table in smem): one 16-byte chunk
+//     of 16 consecutive keys = one 16-byte chunk of row V[c_s], byte-permuted by
+//     (c_b & 15) -- LDS.128 + 4 SEL + 4 PRMT (+ 8 PRMT + 8 HSUB2.BF16 to widen to
+//     bf16 for F32) + STS.128.
+//   * B = W (MN-major = the caller's trace-major layout, no transpose): each CTA
+//     TMA-loads HALF of each N=256 tile, so the pair reads W once per 256 keys.
+//   * 8 MMAs per pipeline stage and per tcgen05.commit (a commit costs ~45 clk of
+//     tensor-pipe time, tools/mma_bench), 3 stages of 48 KB.
+//   * Per stage and SM: TMA 32 KB + tensor-core operand reads 64 KB + generation
+//     32 KB of shared-memory traffic for 1024 clk of MMA.
+//   * Work unit = (byte, trace chunk, N tile), byte fastest, handed out IN ORDER
+//     by a global atomic counter (leader CTA) so the units in flight share a
+//     few W blocks in L2 (W streams from HBM about once).
+// Warp roles (768 threads per CTA): w0 scheduler (leader) + W TMA producer,
+// w1 MMA issuer (leader), w2 TMEM owner, w3 ciphertext producer, w4-7
+// epilogue (TMEM lanes 32*(w%4)...), w8-23 H generators.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace cpa {
+namespace {
+
+template <bool F32>
+struct Cfg {
+    static constexpr int ESZ = F32 ? 2 : 1;         // bytes per operand element
+    static constexpr int KMMA = F32 ? 16 : 32;      // K per MMA instruction
+    static constexpr int NB = F32 ? 2 : 1;          // B operands (hi, lo)
+    static constexpr int NT = F32 ? 1 : 2;          // N=256 accumulators per unit
+    static constexpr int NBUF = F32 ? 2 : 1;        // TMEM accumulator buffers
+    static constexpr int BK = F32 ? 64 : 128;       // traces per pipeline stage
+    static constexpr int BOX_X = 128 / ESZ;         // samples per TMA box (128-byte swizzle span)
+    static constexpr int BH_BYTES = BK * 128 * ESZ; // one CTA's half (128 samples) of one N tile, one operand
+    static constexpr int A_BYTES = BK * 128 * ESZ;  // 128 keys x BK traces
+    static constexpr int A_ATOM = BK * 128;         // bytes between 128-byte MN groups (A and B)
+};
+
+constexpr int BMC = 128;          // sub-keys per CTA (pair MMA M = 256)
+constexpr int BN = 256;           // samples per accumulator (MMA N)
+constexpr int STAGES = 3;
+constexpr int TX_STAGES = 6;      // ciphertext ring, prefetched ahead of the stages
+constexpr int SCHED_Q = 4;        // depth of the unit-id ring
+constexpr int STAGE_BYTES = 49152;
+constexpr int V_BYTES = 65536;
+constexpr int TX_BYTES = 128 * 16;            // ciphertext rows of one stage (max BK)
+constexpr int EPI_WARPS = 4;
+constexpr int GEN_WARPS = 16;                 // every generator warp works on every stage, so
+                                              // each waits every phase of every slot in order
+                                              // (mbarrier parity waits are 1-bit)
+constexpr int CONSUMERS_PER_CTA = 2 + EPI_WARPS + GEN_WARPS;  // (MMA | W producer) + text producer + warps
+constexpr int TB_LD = 9;                      // epilogue transpose row stride (words, odd)
+constexpr int TB_BYTES = EPI_WARPS * 32 * TB_LD * 4;
+constexpr int SMEM_V = 0;
+constexpr int SMEM_STAGE = SMEM_V + V_BYTES;
+constexpr int SMEM_TX = SMEM_STAGE + STAGES * STAGE_BYTES;
+constexpr int SMEM_TB = SMEM_TX + TX_STAGES * TX_BYTES;
+constexpr int SMEM_BAR = SMEM_TB + TB_BYTES;
+constexpr int NUM_BARS = 2 * STAGES + 2 * TX_STAGES + 4 + 2 * SCHED_Q;
+constexpr int SMEM_SCHED = SMEM_BAR + NUM_BARS * 8;
+constexpr int SMEM_TOTAL = SMEM_SCHED + SCHED_Q * 4 + 16;
+constexpr int SMEM_ALLOC = SMEM_TOTAL;
+constexpr int THREADS = 32 * (8 + GEN_WARPS);
+constexpr uint32_t TMEM_COLS = 512;
+static_assert(Cfg<false>::A_BYTES + Cfg<false>::NT * Cfg<false>::NB * Cfg<false>::BH_BYTES == STAGE_BYTES, "");
+static_assert(Cfg<true>::A_BYTES + Cfg<true>::NT * Cfg<true>::NB * Cfg<true>::BH_BYTES == STAGE_BYTES, "");
+static_assert(Cfg<false>::NT * Cfg<false>::NBUF * BN == TMEM_COLS, "");
+static_assert(Cfg<true>::NT * Cfg<true>::NBUF * BN == TMEM_COLS, "");
+
+struct Params {
+    const uint8_t *texts;    // N x 16
+    const uint8_t *vtab;     // 256 x 256 (global copy of V)
+    void *hw;                // sum_hw [4096][M]: int64 (I8) or double (F32)
+    int *unit_counter;       // zeroed before the launch
+    int32_t M;
+    int32_t n_tiles;         // tiles of NT*256 samples
+    int32_t kc_count;
+    int32_t units;
+    int64_t N;
+    int64_t kc_len;
+    uint32_t idesc;
+};
+
+template <bool F32>
+__device__ __forceinline__ void unit_coords(const Params &p, int u, int &b, int &n_tile, int64_t &t0, int64_t &t1)
+{
+    b = u & 15;
+    const int r = u >> 4;
+    const int kc = r % p.kc_count;
+    n_tile = r / p.kc_count;
+    t0 = (int64_t)kc * p.kc_len;
+    t1 = t0 + p.kc_len;
+    if (t1 > p.N) t1 = p.N;
+}
+
+__device__ __forceinline__ int shiftrows_src(int b) { return (b & 3) + 4 * (((b >> 2) + (b & 3)) & 3); }
+
+// bf16(x) for two bytes x0 (byte sel0) and x1 of w, x in 0..255: the bf16 bit
+// pattern of 128 + x is 0x4300 | x (exact: spacing 1 in [128, 256)); subtract
+// 128 in packed bf16 arithmetic (exact).
+__device__ __forceinline__ uint32_t bf16x2_of_bytes(uint32_t w, uint32_t sel)
+{
+    const uint32_t biased = __byte_perm(w, 0x43434343u, sel);
+    __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162 *>(&biased);
+    const __nv_bfloat162 off = __floats2bfloat162_rn(128.0f, 128.0f);
+    v = __hsub2(v, off);
+    return *reinterpret_cast<const uint32_t *>(&v);
+}
+
+template <bool F32>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUtensorMap tmap_b1, const Params p)
+{
+    using C = Cfg<F32>;
+    extern __shared__ __align__(1024) uint8_t smem[];  // keeps shared provenance (LDS/STS)
+    const uint32_t sbase = smem_u32(smem);
+    if (threadIdx.x == 0 && (sbase & 1023)) __trap();  // 128B-swizzle atoms need 1 KB alignment
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the pair's MMAs)
+    const bool leader = rank == 0;
+
+    auto full_bar = [&](int s) { return sbase + SMEM_BAR + 8 * s; };                 // leader's is used
+    auto empty_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (STAGES + s); };     // both CTAs
+    auto txfull_bar = [&](int x) { return sbase + SMEM_BAR + 8 * (2 * STAGES + x); };
+    auto txempty_bar = [&](int x) { return sbase + SMEM_BAR + 8 * (2 * STAGES + TX_STAGES + x); };
+    constexpr int BAR_T = 2 * STAGES + 2 * TX_STAGES, BAR_S = BAR_T + 4;
+    auto tfull_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + a); };      // both (multicast)
+    auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + 2 + a); }; // leader's
+    auto sfull_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + q); };        // both CTAs
+    auto sempty_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + SCHED_Q + q); };  // leader's
+    volatile int *sched = (volatile int *)(smem + SMEM_SCHED);
+    uint32_t *tmem_slot = (uint32_t *)(smem + SMEM_SCHED + SCHED_Q * 4);
+    auto to_leader = [&](uint32_t a) { return mapa_shared(a, 0); };
+
+    // consumers: the t-th unit of this pair (-1 = done).  Called either by a
+    // whole warp (one arrival per warp) or by a single thread (solo = true).
+    auto next_unit = [&](uint32_t t, bool solo) {
+        const int q = t % SCHED_Q;
+        mbar_wait_cluster(sfull_bar(q), (t / SCHED_Q) & 1);
+        const int u = sched[q];
+        if (!solo) __syncwarp();
+        if (solo || lane == 0) mbar_arrive_cluster(to_leader(sempty_bar(q)));
+        return u;
+    };
+
+    // ---- setup: V table to smem, barriers, TMEM (pair allocation) ----
+    {
+        const uint4 *src = (const uint4 *)p.vtab;
+        uint4 *dst = (uint4 *)(smem + SMEM_V);
+        for (int i = threadIdx.x; i < V_BYTES / 16; i += THREADS) dst[i] = src[i];
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmap_b0);
+        if (F32) tma_prefetch(&tmap_b1);
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(full_bar(s), 2 + 2 * GEN_WARPS);  // 2 producer arrivals (+tx) + both CTAs' generators
+            mbar_init(empty_bar(s), 1);                 // multicast tcgen05.commit
+        }
+        for (int x = 0; x < TX_STAGES; x++) {
+            mbar_init(txfull_bar(x), 1);            // ciphertext rows landed
+            mbar_init(txempty_bar(x), GEN_WARPS);   // rows consumed by the generators
+        }
+        for (int a = 0; a < 2; a++) {
+            mbar_init(tfull_bar(a), 1);
+            mbar_init(tempty_bar(a), 2 * EPI_WARPS);  // both CTAs' epilogues
+        }
+        for (int q = 0; q < SCHED_Q; q++) {
+            mbar_init(sfull_bar(q), 1);
+            mbar_init(sempty_bar(q), 2 * CONSUMERS_PER_CTA);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc_pair<TMEM_COLS>(smem_u32(tmem_slot));
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // peer barriers initialised before any remote arrive
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ================= scheduler (leader) + W TMA producer (both) =================
+        if (lane == 0) {
+            const uint32_t peer_sched = mapa_shared(smem_u32((const void *)sched), 1);
+            uint32_t it = 0;
+            for (uint32_t t = 0;; t++) {
+                int u;
+                if (leader) {
+                    u = atomicAdd(p.unit_counter, 1);
+                    if (u >= p.units) u = -1;
+                    const int q = t % SCHED_Q;
+                    mbar_wait(sempty_bar(q), ((t / SCHED_Q) & 1) ^ 1);
+                    sched[q] = u;
+                    st_cluster_u32(peer_sched + 4 * q, (uint32_t)u);
+                    mbar_arrive(sfull_bar(q));                       // release: ids visible to waiters
+                    mbar_arrive_cluster(mapa_shared(sfull_bar(q), 1));
+                } else {
+                    u = next_unit(t, true);
+                }
+                if (u < 0) break;
+                int b, nt;
+                int64_t t0, t1;
+                unit_coords<F32>(p, u, b, nt, t0, t1);
+                const int x0 = nt * (C::NT * BN) + (int)rank * (BN / 2);  // this CTA's half of N tile 0
+                for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
+                    const int s = it % STAGES;
+                    mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
+                    const uint32_t lbar = to_leader(full_bar(s));
+                    if (leader) mbar_arrive_expect_tx(full_bar(s), 2 * (STAGE_BYTES - C::A_BYTES));  // both CTAs
+                    else mbar_arrive_cluster(lbar);
+                    uint32_t bdst = sbase + SMEM_STAGE + s * STAGE_BYTES + C::A_BYTES;
+#pragma unroll
+                    for (int n = 0; n < C::NT; n++)
+#pragma unroll
+                        for (int op = 0; op < C::NB; op++)
+#pragma unroll
+                            for (int at = 0; at < C::ESZ; at++) {  // 128-byte MN atoms of this half
+                                tma_load_2d_pair(bdst, op == 0 ? &tmap_b0 : &tmap_b1, x0 + n * BN + at * C::BOX_X,
+                                                 (int32_t)tb, lbar);
+                                bdst += C::A_ATOM;
+                            }
+                }
+            }
+        }
+    } else if (warp == 3) {
+        // ================= ciphertext producer (feeds this CTA's generators) =================
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (uint32_t t = 0;; t++) {
+                const int u = next_unit(t, true);
+                if (u < 0) break;
+                int b, nt;
+                int64_t t0, t1;
+                unit_coords<F32>(p, u, b, nt, t0, t1);
+                for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
+                    const int x = it % TX_STAGES;
+                    mbar_wait(txempty_bar(x), ((it / TX_STAGES) & 1) ^ 1);
+                    const int rows = (int)((t1 - tb) < C::BK ? (t1 - tb) : C::BK);
+                    mbar_arrive_expect_tx(txfull_bar(x), rows * 16);
+                    bulk_load(sbase + SMEM_TX + x * TX_BYTES, p.texts + tb * 16, rows * 16, txfull_bar(x));
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer (one thread of the leader) =================
+        // (the peer's w1 stays out of the unit ring: per CTA the ring has
+        //  CONSUMERS_PER_CTA readers -- MMA here, the W producer in the peer)
+        if (lane == 0 && leader) {
+            uint32_t it = 0;
+            for (uint32_t t = 0;; t++) {
+                const int u = next_unit(t, true);
+                if (u < 0) break;
+                int b, nt;
+                int64_t t0, t1;
+                unit_coords<F32>(p, u, b, nt, t0, t1);
+                const uint32_t acc = t % C::NBUF;
+                mbar_wait_cluster(tempty_bar(acc), ((t / C::NBUF) & 1) ^ 1);  // both epilogues drained it
+                tc_fence_after();
+                const uint32_t dbase = tmem_base + acc * (C::NT * BN);
+                bool first = true;
+                for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
+                    const int s = it % STAGES;
+                    mbar_wait_cluster(full_bar(s), (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t a_addr = sbase + SMEM_STAGE + s * STAGE_BYTES;
+                    const uint32_t b_addr = a_addr + C::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < C::BK / C::KMMA; kk++) {
+                        // K step = KMMA rows of 128 bytes in every MN atom
+                        const uint64_t ad = smem_desc_sw128(a_addr + kk * (C::KMMA * 128), C::A_ATOM, 1024);
+#pragma unroll
+                        for (int n = 0; n < C::NT; n++)
+#pragma unroll
+                            for (int op = 0; op < C::NB; op++) {
+                                const uint32_t bo = b_addr + (n * C::NB + op) * C::BH_BYTES + kk * (C::KMMA * 128);
+                                const uint64_t bd = smem_desc_sw128(bo, C::A_ATOM, 1024);
+                                if (F32) mma_bf16_pair(dbase + n * BN, ad, bd, p.idesc, (first && op == 0) ? 0u : 1u);
+                                else mma_i8_pair(dbase + n * BN, ad, bd, p.idesc, first ? 0u : 1u);
+                            }
+                        first = false;
+                    }
+                    mma_commit_pair(empty_bar(s), 0x3);  // frees the stage in both CTAs when done
+                }
+                mma_commit_pair(tfull_bar(acc), 0x3);    // accumulators ready for both epilogues
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ================= epilogue: TMEM -> int64 / fp64 global (atomic add) =================
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        uint32_t *tbuf = (uint32_t *)(smem + SMEM_TB) + q * 32 * TB_LD;
+        const int rsub = lane >> 3, csub = lane & 7;
+        for (uint32_t t = 0;; t++) {
+            const int u = next_unit(t, false);
+            if (u < 0) break;
+            int b, nt;
+            int64_t t0, t1;
+            unit_coords<F32>(p, u, b, nt, t0, t1);
+            const uint32_t acc = t % C::NBUF;
+            mbar_wait_cluster(tfull_bar(acc), (t / C::NBUF) & 1);
+            tc_fence_after();
+            const int hrow0 = b * 256 + (int)rank * BMC + q * 32;
+            // 8 columns at a time through a small transpose buffer: each warp-wide
+            // atomic covers 4 rows x 8 consecutive samples = 8 full 32-byte sectors
+#pragma unroll 1
+            for (int c = 0; c < C::NT * BN / 8; c++) {
+                uint32_t v[8];
+                tmem_ld_32x32b_x8(tmem_base + ((uint32_t)(q * 32) << 16) + acc * (C::NT * BN) + c * 8, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int x = 0; x < 8; x++) tbuf[lane * TB_LD + x] = v[x];
+                __syncwarp();
+                const int j = nt * (C::NT * BN) + c * 8 + csub;  // accumulator column = sample
+                if (j < p.M) {
+                    const int64_t off = (int64_t)(hrow0 + rsub) * p.M + j;
+#pragma unroll
+                    for (int rr = 0; rr < 8; rr++) {
+                        const uint32_t bits = tbuf[(4 * rr + rsub) * TB_LD + csub];
+                        if (F32) {
+                            atomicAdd((double *)p.hw + off + (int64_t)(4 * rr) * p.M, (double)__uint_as_float(bits));
+                        } else {
+                            atomicAdd((unsigned long long *)p.hw + off + (int64_t)(4 * rr) * p.M,
+                                      (unsigned long long)(long long)(int32_t)bits);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(to_leader(tempty_bar(acc)));
+        }
+    } else if (warp >= 8) {
+        // ================= hypothesis generators (H tile, MN-major, swizzled) =================
+        // A quarter-warp (8 lanes) builds one trace row: lane = 16-key chunk, so
+        // the V-row reads and the swizzled A-row writes are both bank-conflict
+        // free.  Warp g owns rows g*(BK/16) ... of the stage.
+        const int g = warp - 8;
+        const int ql = lane & 7;           // chunk within the 128-key row
+        const int sub = lane >> 3;         // row within a group of 4
+        const uint8_t *vs = smem + SMEM_V;
+        constexpr int PASSES = C::BK / (4 * GEN_WARPS);
+        uint32_t it = 0;
+        for (uint32_t t = 0;; t++) {
+            const int u = next_unit(t, false);
+            if (u < 0) break;
+            int b, nt;
+            int64_t t0, t1;
+            unit_coords<F32>(p, u, b, nt, t0, t1);
+            const int s_idx = shiftrows_src(b);
+            const uint32_t gchunk = rank * 8 + ql;  // global 16-key chunk (keys 128*rank ...)
+            for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
+                const int s = it % STAGES;
+                const uint32_t ph = (it / STAGES) & 1;
+                const int x = it % TX_STAGES;
+                const int nrows = (int)((t1 - tb) < C::BK ? (t1 - tb) : C::BK);
+                mbar_wait(txfull_bar(x), (it / TX_STAGES) & 1);
+                mbar_wait(empty_bar(s), ph ^ 1);  // A slot free
+                const uint8_t *tx = smem + SMEM_TX + x * TX_BYTES;
+                uint8_t *abase = smem + SMEM_STAGE + s * STAGE_BYTES;
+#pragma unroll
+                for (int pass = 0; pass < PASSES; pass++) {
+                    const int row = (PASSES * 4) * g + 4 * pass + sub;
+                    uint4 outv = make_uint4(0, 0, 0, 0);
+                    if (row < nrows) {
+                        const uint32_t cb = tx[row * 16 + b], cs = tx[row * 16 + s_idx];
+                        const uint32_t hi = cb >> 4, lo = cb & 15, u4 = lo >> 2, v4 = lo & 3;
+                        const uint32_t sel_e = (0x3210u ^ (v4 * 0x1111u)) ^ ((u4 & 1) ? 0x4444u : 0u);
+                        const uint32_t sel_o = sel_e ^ 0x4444u;
+                        const bool swap2 = (u4 & 2) != 0;
+                        const uint4 a = *(const uint4 *)(vs + cs * 256 + ((gchunk ^ hi) << 4));
+                        const uint32_t c0 = swap2 ? a.z : a.x, c1 = swap2 ? a.w : a.y;
+                        const uint32_t c2 = swap2 ? a.x : a.z, c3 = swap2 ? a.y : a.w;
+                        outv.x = __byte_perm(c0, c1, sel_e);
+                        outv.y = __byte_perm(c0, c1, sel_o);
+                        outv.z = __byte_perm(c2, c3, sel_e);
+                        outv.w = __byte_perm(c2, c3, sel_o);
+                    }
+                    if (!F32) {
+                        *(uint4 *)(abase + row * 128 + ((ql ^ (row & 7)) << 4)) = outv;  // 128B swizzle
+                    } else {
+                        // 16 keys -> 32 bytes of bf16: keys 16ql.. live in MN atom ql/4,
+                        // 16-byte chunks 2(ql%4) and 2(ql%4)+1 of the row (swizzled)
+                        const uint4 lo4 = make_uint4(bf16x2_of_bytes(outv.x, 0x7170), bf16x2_of_bytes(outv.x, 0x7372),
+                                                     bf16x2_of_bytes(outv.y, 0x7170), bf16x2_of_bytes(outv.y, 0x7372));
+                        const uint4 hi4 = make_uint4(bf16x2_of_bytes(outv.z, 0x7170), bf16x2_of_bytes(outv.z, 0x7372),
+                                                     bf16x2_of_bytes(outv.w, 0x7170), bf16x2_of_bytes(outv.w, 0x7372));
+                        uint8_t *rowp = abase + (ql >> 2) * C::A_ATOM + row * 128;
+                        const int c0i = 2 * (ql & 3);
+                        *(uint4 *)(rowp + (((c0i) ^ (row & 7)) << 4)) = lo4;
+                        *(uint4 *)(rowp + (((c0i + 1) ^ (row & 7)) << 4)) = hi4;
+                    }
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    if (leader) mbar_arrive(full_bar(s));
+                    else mbar_arrive_cluster(to_leader(full_bar(s)));
+                    mbar_arrive(txempty_bar(x));
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // the peer's MMAs / remote arrivals are done with our smem and TMEM
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+    }
+}
+
+template <bool F32>
+cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *d_texts, const uint8_t *d_vtab,
+                   void *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, uint32_t idesc, int num_sms,
+                   cudaStream_t stream, int *launches)
+{
+    using Cf = Cfg<F32>;
+    Params p;
+    p.texts = d_texts;
+    p.vtab = d_vtab;
+    p.hw = d_hw;
+    p.unit_counter = d_counter;
+    p.M = M;
+    p.N = N;
+    p.n_tiles = (M + Cf::NT * BN - 1) / (Cf::NT * BN);
+    p.kc_len = kc_len;
+    p.kc_count = (int32_t)((N + kc_len - 1) / kc_len);
+    p.units = 16 * p.n_tiles * p.kc_count;
+    p.idesc = idesc;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_xterm<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(int), stream);
+    if (e != cudaSuccess) return e;
+    const int pairs = (p.units < num_sms / 2 ? p.units : num_sms / 2);
+    k_xterm<F32><<<2 * pairs, THREADS, SMEM_ALLOC, stream>>>(m0, m1, p);
+    if (launches) (*launches)++;
+    return cudaGetLastError();
+}
+
+// Split-K length: whole stages, chosen to balance the units over the CTA pairs
+// while keeping each unit long enough that its epilogue is a small fraction
+// (model: ~25k clk per epilogue, 1024 clk per stage; with a double-buffered
+// accumulator (F32) the epilogue overlaps the next unit).  max_len bounds the
+// int32 exactness (I8: |H W| <= 8 * 255 -> 2^20 traces) or the fp32 rounding
+// (F32: 4096 traces).
+int64_t auto_kchunk(int32_t M, int64_t N, int num_sms, int nt, int bk, int64_t max_len, bool overlapped)
+{
+    const int64_t tiles = 16LL * ((M + nt * BN - 1) / (nt * BN));
+    const int64_t pairs = num_sms / 2;
+    int64_t best_len = 0;
+    double best = -1.0;
+    for (int64_t kc = 1; kc <= 4096; kc++) {
+        int64_t len = (N + kc - 1) / kc;
+        len = (len + bk - 1) / bk * bk;
+        if (len > max_len) continue;
+        const int64_t kcount = (N + len - 1) / len;
+        const int64_t units = tiles * kcount;
+        const int64_t waves = (units + pairs - 1) / pairs;
+        const double stage_clk = (double)((len + bk - 1) / bk) * 1024.0;
+        const double epi = overlapped ? 0.0 : 25000.0;
+        const double eff = (double)units / (double)(waves * pairs) * stage_clk / (stage_clk + epi);
+        if (eff > best + 1e-3) {
+            best = eff;
+            best_len = len;
+        }
+        if (len <= bk) break;
+    }
+    if (best_len == 0) best_len = max_len;
+    return best_len;
+}
+
+}  // namespace
+
+int xterm_smem_bytes() { return SMEM_ALLOC; }
+
+int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms)
+{
+    return auto_kchunk(M, N, num_sms, Cfg<false>::NT, Cfg<false>::BK, 1 << 20, false);
+}
+
+int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms)
+{
+    return auto_kchunk(M, N, num_sms, Cfg<true>::NT, Cfg<true>::BK, 4096, true);
+}
+
+cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
+                            int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
+                            int num_sms, cudaStream_t stream, int *launches)
+{
+    return launch<false>(tmap_w, tmap_w, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
+                         idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches);
+}
+
+cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
+                                const uint8_t *d_vtab, double *d_hw, int *d_counter, int32_t M, int64_t N,
+                                int64_t kc_len, int num_sms, cudaStream_t stream, int *launches)
+{
+    return launch<true>(tmap_hi, tmap_lo, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len, idesc_bf16(2 * BMC, BN),
+                        num_sms, stream, launches);
+}
+
+}  // namespace cpa

@@ -1,0 +1,90 @@
+"""GPU parity of the float-trace variant (a6, [P:201-217]): bf16 hi/lo tensor-core
+path vs the fp64 oracle.  Bar (north_star): |rho_gpu - rho_oracle| <= 1e-4 on
+every cell [S:461], identical recovered key."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from synth import synth as S  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def P():
+    assert torch.cuda.is_available()
+    import paper_1412_7682_b200 as P
+    return P
+
+
+def gpu_rho(P, texts, W, offsets="default"):
+    eng = P.Engine(W.shape[1], P.CPA_F32, P.CPA_HD_LAST, 0)
+    if offsets is None:
+        P.cpa_set_offsets(eng.ctx, None)
+    eng.accumulate(torch.from_numpy(np.ascontiguousarray(W)).cuda(), torch.from_numpy(texts).cuda())
+    out = eng.finalize(want_rho=True)
+    n = float(eng.n.item())
+    eng.close()
+    return out, n
+
+
+@pytest.mark.parametrize("n,m", [(2000, 300), (65, 257), (130, 17)])
+def test_float_parity_all_cells(P, n, m):
+    w = S.CONFIGS["C3"].replace(n=n, m=m, a=0.02)
+    texts, W = S.dataset(w)
+    out, cnt = gpu_rho(P, texts, W)
+    assert cnt == n
+    shw, sw, sw2 = O.sums_f32(O.HD_LAST, texts, W)
+    sh, sh2 = O.model_sums(O.HD_LAST, texts)
+    ref = O.rho_eq1_f64_grid(n, shw, sh, sh2, sw, sw2)
+    rho = out["rho"].cpu().numpy()
+    assert np.max(np.abs(rho - ref)) <= TOL
+    rk = O.expand_key(w.key)[10].astype(int)
+    hyps = np.array([256 * b + rk[b] for b in range(16)], np.int32)
+    ra = O.rho_two_pass_f32(O.HD_LAST, texts, W, hyps=hyps)
+    assert np.max(np.abs(rho[hyps] - ra)) <= TOL
+    if n >= 2000:
+        assert out["master_key"] == w.key
+
+
+def test_float_offsets_invariance(P):
+    w = S.CONFIGS["C3"].replace(n=1500, m=200, a=0.02)
+    texts, W = S.dataset(w)
+    a, _ = gpu_rho(P, texts, W)
+    b, _ = gpu_rho(P, texts, W, offsets=None)
+    assert np.max(np.abs(a["rho"].cpu().numpy() - b["rho"].cpu().numpy())) <= TOL
+
+
+def test_float_nonfinite_is_reported(P):
+    w = S.CONFIGS["C3"].replace(n=100, m=64)
+    texts, W = S.dataset(w)
+    W[37, 5] = np.nan
+    eng = P.Engine(w.m, P.CPA_F32, P.CPA_HD_LAST, 0)
+    eng.accumulate(torch.from_numpy(W).cuda(), torch.from_numpy(texts).cuda())
+    with pytest.raises(P.CpaError, match="NONFINITE"):
+        eng.finalize()
+    eng.close()
+
+
+def test_c3_fullsize_sampled(P):
+    """BASELINE configs[2]: 100,000 x 5000 float32, device-generated."""
+    w = S.CONFIGS["C3"]
+    texts, lv = S.texts(w)
+    dW = torch.empty((w.n, w.m), dtype=torch.float32, device="cuda")
+    S.dev_traces(w, torch.from_numpy(lv).cuda(), 0, w.n, dW, w.m)
+    eng = P.Engine(w.m, P.CPA_F32, P.CPA_HD_LAST, 0)
+    eng.accumulate(dW, torch.from_numpy(texts).cuda())
+    out = eng.finalize(want_rho=True)
+    cols = np.array(sorted(set(w.leak_positions()[:4]) | {0, 2500, w.m - 1}), np.int32)
+    Wc = S.traces(w, lv, 0, cols)
+    shw, sw, sw2 = O.sums_f32(O.HD_LAST, texts, Wc)
+    sh, sh2 = O.model_sums(O.HD_LAST, texts)
+    ref = O.rho_eq1_f64_grid(w.n, shw, sh, sh2, sw, sw2)
+    rho = out["rho"].cpu().numpy()[:, cols]
+    assert np.max(np.abs(rho - ref)) <= TOL
+    assert out["master_key"] == w.key
+    assert out["peak_sample"] == w.leak_positions()
+    eng.close()

@@ -108,3 +108,25 @@ def test_end_to_end_noiseless_and_noisy():
         assert (a["rank"][hs] == 1).all()
         if name == "C1-0":
             assert np.all(np.abs(a["maxabs"][hs] - 1.0) <= 1e-12)
+
+
+def test_float_oracle_pins():
+    """Float-trace oracle [S:297]: fp64 sums equal an independent numpy fp64
+    contraction; on integer-valued float traces the float and int oracles agree;
+    Eq. (1) in fp64 agrees with the two-pass reference."""
+    rng = np.random.default_rng(21)
+    t = rng.integers(0, 256, (300, 16), dtype=np.uint8)
+    Wf = (rng.normal(1.0, 0.05, (300, 20))).astype(np.float32)
+    H = h_matrix(O.HD_LAST, t).astype(np.float64)
+    shw, sw, sw2 = O.sums_f32(O.HD_LAST, t, Wf)
+    assert np.allclose(shw, H.T @ Wf.astype(np.float64), rtol=1e-14, atol=0)
+    assert np.allclose(sw, Wf.astype(np.float64).sum(0), rtol=1e-14)
+    assert np.allclose(sw2, (Wf.astype(np.float64) ** 2).sum(0), rtol=1e-14)
+    sh, sh2 = O.model_sums(O.HD_LAST, t)
+    rb = O.rho_eq1_f64_grid(300, shw, sh, sh2, sw, sw2)
+    ra = O.rho_two_pass_f32(O.HD_LAST, t, Wf)
+    assert np.max(np.abs(ra - rb)) <= 1e-9
+    Wi = rng.integers(-100, 100, (300, 20)).astype(np.int8)
+    ri = O.rho_two_pass_i8(O.HD_LAST, t, Wi)
+    rf = O.rho_two_pass_f32(O.HD_LAST, t, Wi.astype(np.float32))
+    assert np.array_equal(ri, rf)
