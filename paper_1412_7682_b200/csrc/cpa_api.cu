@@ -87,6 +87,7 @@ struct cpa_ctx {
     uint16_t *d_hi = nullptr, *d_lo = nullptr;
     int64_t plane_rows = 0;
     int *d_nonfinite = nullptr;
+    uint32_t *d_hist = nullptr;  // a3 byte-pair histogram scratch (16 x 65536)
     // CPA_OPT_TIMING: CUDA events recorded on `stream` around every launch
     bool timing = false;
     struct Rec { int phase; cudaEvent_t a, b; };
@@ -204,6 +205,7 @@ cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, 
     if (e == cudaSuccess) e = cudaMalloc(&c->d_best, sizeof(int32_t) * 32);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_counter, 256);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_nonfinite, 256);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_hist, sizeof(uint32_t) * 16 * 65536);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_offset, sizeof(float) * M);
     if (e != cudaSuccess) {
         cpa_destroy(c);
@@ -258,7 +260,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     if (c->dtype == CPA_F32) {
         double *acc = (double *)c->accum;
         CUDA_TRY(c->timed(0, [&] {
-                     return cpa::launch_modelsums_f64(d_tx, n, c->d_vtab, acc + cpa_accum_offset(M, 3),
+                     return cpa::launch_modelsums_f64(d_tx, n, c->d_vtab, c->d_hist, acc + cpa_accum_offset(M, 3),
                                                       acc + cpa_accum_offset(M, 4), acc + cpa_accum_offset(M, 5),
                                                       c->stream, &launches);
                  }),
@@ -319,7 +321,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     int64_t *acc = (int64_t *)c->accum;
     const bool sgn = c->dtype == CPA_S8;
     CUDA_TRY(c->timed(0, [&] {
-                 return cpa::launch_modelsums(d_tx, n, c->d_vtab, acc + cpa_accum_offset(M, 3),
+                 return cpa::launch_modelsums(d_tx, n, c->d_vtab, c->d_hist, acc + cpa_accum_offset(M, 3),
                                               acc + cpa_accum_offset(M, 4), acc + cpa_accum_offset(M, 5), c->stream,
                                               &launches);
              }),
@@ -559,6 +561,7 @@ cpa_status cpa_destroy(cpa_ctx *c)
     cudaFree(c->d_hi);
     cudaFree(c->d_lo);
     cudaFree(c->d_nonfinite);
+    cudaFree(c->d_hist);
     for (auto &r : c->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);

@@ -291,38 +291,106 @@ __global__ void __launch_bounds__(256) k_phase4(FinalizeOut o)
     }
 }
 
-}  // namespace
+// ---------------------------------------------------------------------------
+// a3 for large N: H(b,k) depends on a trace only through the byte pair
+// (c_b, c_s) = (c[b], c[SR(b)]), so
+//   sum_i H = sum_{x,y} cnt_b[x][y] * V[y][x ^ k],  sum_i H^2 likewise with V^2,
+// with cnt_b the (exact, integer) histogram of the pairs: 16 N atomics plus a
+// fixed 16 x 256 x 65536 contraction instead of 4096 N table lookups.
+// ---------------------------------------------------------------------------
+__global__ void k_texthist(const uint8_t *__restrict__ texts, int64_t n, uint32_t *hist)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 t4 = __ldg((const uint4 *)texts + i);
+        const uint32_t w[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+        for (int b = 0; b < 16; b++) {
+            const int sb = shiftrows_src(b);
+            const uint32_t cb = (w[b >> 2] >> (8 * (b & 3))) & 0xFF;
+            const uint32_t cs = (w[sb >> 2] >> (8 * (sb & 3))) & 0xFF;
+            atomicAdd(&hist[(b << 16) | (cb << 8) | cs], 1u);
+        }
+    }
+}
 
-cudaError_t launch_modelsums(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab, int64_t *d_sum_h,
-                             int64_t *d_sum_h2, int64_t *d_count, cudaStream_t s, int *launches)
+constexpr int HC_X = 8;  // histogram rows (x = c_b) per block
+template <typename Acc>
+__global__ void __launch_bounds__(256)
+k_hist_contract(const uint32_t *__restrict__ hist, const uint8_t *__restrict__ vtab, Acc *sum_h, Acc *sum_h2,
+                Acc *count, int64_t n)
+{
+    extern __shared__ uint8_t sm[];
+    uint8_t *vs = sm;                                // 64 KB: V[y][z]
+    uint32_t *hs = (uint32_t *)(sm + 65536);         // HC_X x 256 counts
+    const int b = blockIdx.y, x0 = blockIdx.x * HC_X, k = threadIdx.x;
+    for (int i = threadIdx.x; i < 4096; i += 256) ((uint4 *)vs)[i] = ((const uint4 *)vtab)[i];
+    for (int i = threadIdx.x; i < HC_X * 256; i += 256) hs[i] = hist[(b << 16) | (x0 << 8) | i];
+    __syncthreads();
+    uint32_t a1 = 0, a2 = 0;  // exact: <= 8 N and 64 N for N <= 2^23
+    for (int xx = 0; xx < HC_X; xx++) {
+        const uint32_t z = (uint32_t)(x0 + xx) ^ (uint32_t)k;
+        const uint32_t *hr = hs + xx * 256;
+#pragma unroll 4
+        for (int y = 0; y < 256; y++) {
+            const uint32_t c = hr[y];
+            const uint32_t v = vs[y * 256 + z];
+            a1 += c * v;
+            a2 += c * v * v;
+        }
+    }
+    const int h = b * 256 + k;
+    if constexpr (std::is_integral<Acc>::value) {
+        atomicAdd((unsigned long long *)&sum_h[h], (unsigned long long)a1);
+        atomicAdd((unsigned long long *)&sum_h2[h], (unsigned long long)a2);
+        if (blockIdx.x == 0 && blockIdx.y == 0 && k == 0) atomicAdd((unsigned long long *)count, (unsigned long long)n);
+    } else {
+        atomicAdd(&sum_h[h], (Acc)a1);
+        atomicAdd(&sum_h2[h], (Acc)a2);
+        if (blockIdx.x == 0 && blockIdx.y == 0 && k == 0) atomicAdd(count, (Acc)n);
+    }
+}
+
+template <typename Acc>
+cudaError_t modelsums(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab, uint32_t *d_hist, Acc *d_sum_h,
+                      Acc *d_sum_h2, Acc *d_count, cudaStream_t s, int *launches)
 {
     static bool attr = false;
-    const int smem = 65536 + MS_STAGE * 16;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_modelsums<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(k_modelsums<Acc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             65536 + MS_STAGE * 16);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_hist_contract<Acc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     65536 + HC_X * 256 * 4);
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    if (d_hist && n >= kHistMinTraces) {
+        cudaError_t e = cudaMemsetAsync(d_hist, 0, sizeof(uint32_t) * 16 * 65536, s);
+        if (e != cudaSuccess) return e;
+        k_texthist<<<1184, 256, 0, s>>>(d_texts, n, d_hist);
+        k_hist_contract<Acc><<<dim3(256 / HC_X, 16), 256, 65536 + HC_X * 256 * 4, s>>>(d_hist, d_vtab, d_sum_h,
+                                                                                       d_sum_h2, d_count, n);
+        if (launches) (*launches) += 2;
+        return cudaGetLastError();
+    }
     const int blocks = (int)((n + MS_CHUNK - 1) / MS_CHUNK);
-    k_modelsums<int64_t><<<blocks, MS_THREADS, smem, s>>>(d_texts, n, d_vtab, d_sum_h, d_sum_h2, d_count);
+    k_modelsums<Acc><<<blocks, MS_THREADS, 65536 + MS_STAGE * 16, s>>>(d_texts, n, d_vtab, d_sum_h, d_sum_h2, d_count);
     if (launches) (*launches)++;
     return cudaGetLastError();
 }
 
-cudaError_t launch_modelsums_f64(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab, double *d_sum_h,
-                                 double *d_sum_h2, double *d_count, cudaStream_t s, int *launches)
+}  // namespace
+
+cudaError_t launch_modelsums(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab, uint32_t *d_hist,
+                             int64_t *d_sum_h, int64_t *d_sum_h2, int64_t *d_count, cudaStream_t s, int *launches)
 {
-    static bool attr = false;
-    const int smem = 65536 + MS_STAGE * 16;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_modelsums<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    const int blocks = (int)((n + MS_CHUNK - 1) / MS_CHUNK);
-    k_modelsums<double><<<blocks, MS_THREADS, smem, s>>>(d_texts, n, d_vtab, d_sum_h, d_sum_h2, d_count);
-    if (launches) (*launches)++;
-    return cudaGetLastError();
+    return modelsums<int64_t>(d_texts, n, d_vtab, d_hist, d_sum_h, d_sum_h2, d_count, s, launches);
+}
+
+cudaError_t launch_modelsums_f64(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab, uint32_t *d_hist,
+                                 double *d_sum_h, double *d_sum_h2, double *d_count, cudaStream_t s, int *launches)
+{
+    return modelsums<double>(d_texts, n, d_vtab, d_hist, d_sum_h, d_sum_h2, d_count, s, launches);
 }
 
 cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M, bool w_signed,

@@ -7,11 +7,14 @@
 
 namespace cpa {
 
-// a3: Phase 1 model sums [P:75]; also adds n to the trace count word.
-cudaError_t launch_modelsums(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab,
+// a3: Phase 1 model sums [P:75]; also adds n to the trace count word.  With a
+// 16 x 65536 uint32 scratch (d_hist) and n >= kHistMinTraces the byte-pair
+// histogram path is used (exact integer counts, then a fixed contraction).
+constexpr int64_t kHistMinTraces = 65536;
+cudaError_t launch_modelsums(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab, uint32_t *d_hist,
                              int64_t *d_sum_h, int64_t *d_sum_h2, int64_t *d_count,
                              cudaStream_t s, int *launches);
-cudaError_t launch_modelsums_f64(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab,
+cudaError_t launch_modelsums_f64(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab, uint32_t *d_hist,
                                  double *d_sum_h, double *d_sum_h2, double *d_count,
                                  cudaStream_t s, int *launches);
 

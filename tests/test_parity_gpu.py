@@ -209,3 +209,20 @@ def test_synth_device_generator_matches_host(P):
         S.dev_traces(w, torch.from_numpy(lv).cuda(), 0, w.n, d, w.m)
         torch.cuda.synchronize()
         assert np.array_equal(d.cpu().numpy(), Wh)
+
+
+@pytest.mark.parametrize("model", [O.HD_LAST, O.HW_LAST, O.HW_FIRST])
+def test_model_sums_histogram_path(P, model):
+    """N >= 65536 in one call takes the byte-pair histogram path for a3; it must
+    equal the oracle and the direct path (chunks < 65536) bit for bit."""
+    rng = np.random.default_rng(31 + model)
+    n, m = 70001, 32
+    texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    W = rng.integers(-128, 128, (n, m)).astype(np.int8)
+    one, _ = run_gpu(P, texts, W, model=MODEL[model], want_rho=False)
+    chunked, _ = run_gpu(P, texts, W, model=MODEL[model], chunks=[0, 30000, 60000, n], want_rho=False)
+    sh, sh2 = O.model_sums(model, texts)
+    for s in (one, chunked):
+        assert np.array_equal(s["sum_h"], sh) and np.array_equal(s["sum_h2"], sh2)
+        assert s["n"] == n
+    assert np.array_equal(one["sum_hw"], chunked["sum_hw"])
