@@ -77,66 +77,98 @@ k_modelsums(const uint8_t *__restrict__ texts, int64_t n, const uint8_t *__restr
 }
 
 // ---------------------------------------------------------------------------
-// a4: thread = 16 consecutive samples (one 16-byte vector per trace row) over
-// MO_ROWS rows; int32/uint32 partials (exact: 16384*4096, 65025*4096 < 2^32).
+// a4: HBM-bound single pass.  Work item = (16-sample column group, `rows`-row
+// chunk), flattened so no thread idles on the ragged column edge.  Samples are
+// biased to u = w + 128 (s8) so sum u accumulates in packed 16-bit lanes (two
+// bytes per IADD, flushed every 256 rows) and sum u^2 in uint32 (exact:
+// 65025 * rows < 2^32 for rows <= 2^16); sum w = sum u - 128 n, sum w^2 = sum u^2 - 256 sum u
+// + 16384 n, all in exact integers.
 // ---------------------------------------------------------------------------
 constexpr int MO_THREADS = 256;
-constexpr int MO_ROWS = 4096;
+constexpr int MO_MAX_ROWS = 1 << 16;  // uint32 exactness of sum u^2
+constexpr int MO_UNROLL = 8;
 
-template <bool SIGNED>
-__device__ __forceinline__ int32_t byte_at(uint32_t w, int k)
+__device__ __forceinline__ uint4 ld_stream16(const void *p)
 {
-    if (SIGNED) return (int32_t)(w << (24 - 8 * k)) >> 24;
-    return (int32_t)((w >> (8 * k)) & 0xFF);
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
 }
 
 template <bool SIGNED>
 __global__ void __launch_bounds__(MO_THREADS)
-k_moments_i8(const uint8_t *__restrict__ w, int64_t ld, int64_t n, int32_t M,
+k_moments_i8(const uint8_t *__restrict__ w, int64_t ld, int64_t n, int32_t M, int64_t items, int64_t rows,
              unsigned long long *sum_w, unsigned long long *sum_w2)
 {
     const int groups = (M + 15) >> 4;
-    const int g = blockIdx.x * MO_THREADS + threadIdx.x;
-    if (g >= groups) return;
+    const int64_t item = (int64_t)blockIdx.x * MO_THREADS + threadIdx.x;
+    if (item >= items) return;
+    const int g = (int)(item % groups);
+    const int64_t r0 = (item / groups) * rows;
+    const int64_t r1 = min(n, r0 + rows);
     const int j0 = g * 16;
-    const int64_t r0 = (int64_t)blockIdx.y * MO_ROWS;
-    const int64_t r1 = min(n, r0 + MO_ROWS);
-    int32_t s1[16];
-    uint32_t s2[16];
+    uint32_t p1[8];   // packed 16-bit partial sums of u, lanes = (byte 0,2) / (1,3) of each word
+    uint32_t s1[16];  // flushed sums of u
+    uint32_t s2[16];  // sums of u^2
 #pragma unroll
-    for (int q = 0; q < 16; q++) { s1[q] = 0; s2[q] = 0; }
+    for (int q = 0; q < 16; q++) s1[q] = s2[q] = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) p1[q] = 0;
     const uint8_t *col = w + j0;
+    const uint32_t bias = SIGNED ? 0x80808080u : 0u;
     int64_t r = r0;
-    for (; r + 4 <= r1; r += 4) {
-        uint4 v[4];
+    int since_flush = 0;
+    auto consume = [&](uint4 v) {
+        const uint32_t ws[4] = {v.x ^ bias, v.y ^ bias, v.z ^ bias, v.w ^ bias};
 #pragma unroll
-        for (int u = 0; u < 4; u++) v[u] = __ldg((const uint4 *)(col + (r + u) * ld));
+        for (int k = 0; k < 4; k++) {
+            p1[2 * k] += ws[k] & 0x00FF00FFu;
+            p1[2 * k + 1] += (ws[k] >> 8) & 0x00FF00FFu;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const uint32_t ws[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-            for (int q = 0; q < 16; q++) {
-                const int32_t x = byte_at<SIGNED>(ws[q >> 2], q & 3);
-                s1[q] += x;
-                s2[q] += (uint32_t)(x * x);
+            for (int e = 0; e < 4; e++) {
+                const uint32_t u = (ws[k] >> (8 * e)) & 0xFF;
+                s2[4 * k + e] += u * u;
             }
         }
-    }
-    for (; r < r1; r++) {
-        const uint4 v = __ldg((const uint4 *)(col + r * ld));
-        const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+    };
+    auto flush = [&]() {
 #pragma unroll
-        for (int q = 0; q < 16; q++) {
-            const int32_t x = byte_at<SIGNED>(ws[q >> 2], q & 3);
-            s1[q] += x;
-            s2[q] += (uint32_t)(x * x);
+        for (int k = 0; k < 4; k++) {
+            s1[4 * k + 0] += p1[2 * k] & 0xFFFF;
+            s1[4 * k + 2] += p1[2 * k] >> 16;
+            s1[4 * k + 1] += p1[2 * k + 1] & 0xFFFF;
+            s1[4 * k + 3] += p1[2 * k + 1] >> 16;
+            p1[2 * k] = p1[2 * k + 1] = 0;
+        }
+    };
+    for (; r + MO_UNROLL <= r1; r += MO_UNROLL) {
+        uint4 v[MO_UNROLL];
+#pragma unroll
+        for (int u = 0; u < MO_UNROLL; u++) v[u] = ld_stream16(col + (r + u) * ld);
+#pragma unroll
+        for (int u = 0; u < MO_UNROLL; u++) consume(v[u]);
+        since_flush += MO_UNROLL;
+        if (since_flush >= 256) {  // 16-bit lanes hold <= 257 * 255
+            flush();
+            since_flush = 0;
         }
     }
+    flush();
+    for (; r < r1; r++) consume(ld_stream16(col + r * ld));  // < MO_UNROLL rows
+    flush();
+    const int64_t nrows = r1 - r0;
 #pragma unroll
     for (int q = 0; q < 16; q++) {
         if (j0 + q < M) {
-            atomicAdd(&sum_w[j0 + q], (unsigned long long)(long long)s1[q]);
-            atomicAdd(&sum_w2[j0 + q], (unsigned long long)s2[q]);
+            long long sw = (long long)s1[q], sw2 = (long long)s2[q];
+            if (SIGNED) {
+                sw2 = sw2 - 256LL * sw + 16384LL * nrows;  // sum (u-128)^2
+                sw = sw - 128LL * nrows;                   // sum (u-128)
+            }
+            atomicAdd(&sum_w[j0 + q], (unsigned long long)sw);
+            atomicAdd(&sum_w2[j0 + q], (unsigned long long)sw2);
         }
     }
 }
@@ -396,14 +428,31 @@ cudaError_t launch_modelsums_f64(const uint8_t *d_texts, int64_t n, const uint8_
 cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M, bool w_signed,
                               int64_t *d_sum_w, int64_t *d_sum_w2, cudaStream_t s, int *launches)
 {
-    const int groups = (M + 15) / 16;
-    dim3 grid((groups + MO_THREADS - 1) / MO_THREADS, (unsigned)((n + MO_ROWS - 1) / MO_ROWS));
+    // one resident wave: rows per item so that (groups x chunks) fills the
+    // GPU's resident threads exactly once (no wave-quantisation tail)
+    static int resident = 0;
+    if (!resident) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_moments_i8<true>, MO_THREADS, 0);
+        resident = sms * (per_sm > 0 ? per_sm : 1) * MO_THREADS;
+    }
+    const int64_t groups = (M + 15) / 16;
+    int64_t chunks = resident / groups;
+    if (chunks < 1) chunks = 1;
+    int64_t rows = (n + chunks - 1) / chunks;
+    rows = (rows + MO_UNROLL - 1) / MO_UNROLL * MO_UNROLL;
+    if (rows < 64) rows = 64;
+    if (rows > MO_MAX_ROWS) rows = MO_MAX_ROWS;
+    const int64_t items = groups * ((n + rows - 1) / rows);
+    const unsigned grid = (unsigned)((items + MO_THREADS - 1) / MO_THREADS);
     if (w_signed)
-        k_moments_i8<true><<<grid, MO_THREADS, 0, s>>>((const uint8_t *)d_w, ld, n, M,
+        k_moments_i8<true><<<grid, MO_THREADS, 0, s>>>((const uint8_t *)d_w, ld, n, M, items, rows,
                                                         (unsigned long long *)d_sum_w,
                                                         (unsigned long long *)d_sum_w2);
     else
-        k_moments_i8<false><<<grid, MO_THREADS, 0, s>>>((const uint8_t *)d_w, ld, n, M,
+        k_moments_i8<false><<<grid, MO_THREADS, 0, s>>>((const uint8_t *)d_w, ld, n, M, items, rows,
                                                          (unsigned long long *)d_sum_w,
                                                          (unsigned long long *)d_sum_w2);
     if (launches) (*launches)++;
