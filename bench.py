@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="serialise the a4 moments pass with the cross term")
     return ap.parse_args()
 
 
@@ -210,6 +212,8 @@ def main():
     torch.cuda.synchronize()
 
     eng = P.Engine(w.m, P.CPA_F32 if is_f32 else P.CPA_S8, P.CPA_HD_LAST, local)
+    if args.no_overlap:
+        eng.set_overlap(False)
     rho = torch.empty((4096, w.m), dtype=torch.float64, device=dev)
     maxabs = torch.empty(4096, dtype=torch.float64, device=dev)
     argmax = torch.empty(4096, dtype=torch.int32, device=dev)

@@ -151,8 +151,11 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *   CPA_OPT_KCHUNK: traces per split-K work unit of the cross-term kernel
  *                   (multiple of 128, <= 2^20; 0 = automatic).
  *   CPA_OPT_TIMING: nonzero = record CUDA events on the context's stream
- *                   around every kernel launch (read with cpa_phase_times). */
-enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2 };
+ *                   around every kernel launch (read with cpa_phase_times).
+ *   CPA_OPT_OVERLAP: nonzero (default) = run the trace-moment pass (a4) on a
+ *                   low-priority side stream concurrently with the cross term;
+ *                   0 = serialise everything on the context's stream.       */
+enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2, CPA_OPT_OVERLAP = 3 };
 CPA_API cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value);
 
 /* Per-phase device time (ms) and launch count since the last call, from the

@@ -98,15 +98,20 @@ struct cpa_ctx {
         cudaEvent_t e = pool.back(); pool.pop_back(); return e;
     }
     // time the launches `fn` issues on the stream as phase `ph`
-    template <typename F> cudaError_t timed(int ph, F &&fn) {
+    template <typename F> cudaError_t timed(int ph, F &&fn) { return timed_on(ph, stream, fn); }
+    template <typename F> cudaError_t timed_on(int ph, cudaStream_t st, F &&fn) {
         if (!timing) return fn();
         Rec r{ph, ev(), ev()};
-        cudaEventRecord(r.a, stream);
+        cudaEventRecord(r.a, st);
         cudaError_t e = fn();
-        cudaEventRecord(r.b, stream);
+        cudaEventRecord(r.b, st);
         recs.push_back(r);
         return e;
     }
+    // a4 on a low-priority side stream, overlapped with the cross term
+    bool overlap = true;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 extern "C" {
@@ -206,6 +211,13 @@ cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, 
     if (e == cudaSuccess) e = cudaMalloc(&c->d_counter, 256);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_nonfinite, 256);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_hist, sizeof(uint32_t) * 16 * 65536);
+    if (e == cudaSuccess) {
+        int lo = 0, hi = 0;  // numerically greatest = lowest priority
+        e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+    }
     if (e == cudaSuccess) e = cudaMalloc(&c->d_offset, sizeof(float) * M);
     if (e != cudaSuccess) {
         cpa_destroy(c);
@@ -240,6 +252,10 @@ cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets)
 cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
 {
     if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
+    if (option == CPA_OPT_OVERLAP) {
+        ctx->overlap = value != 0;
+        return CPA_OK;
+    }
     if (option == CPA_OPT_TIMING) {
         ctx->timing = value != 0;
         return CPA_OK;
@@ -326,11 +342,21 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                               &launches);
              }),
              "modelsums");
-    CUDA_TRY(c->timed(1, [&] {
-                 return cpa::launch_moments_i8(d_w, ld, n, M, sgn, acc + cpa_accum_offset(M, 1),
-                                               acc + cpa_accum_offset(M, 2), c->stream, &launches);
-             }),
-             "moments");
+    // a4 (HBM-bound) runs on a low-priority side stream concurrently with the
+    // tensor-bound cross term: its blocks fill the registers/threads the
+    // cross-term CTAs leave free on each SM
+    const bool ovl = c->overlap && c->side;
+    if (ovl) {
+        CUDA_TRY(cudaEventRecord(c->ev_fork, c->stream), "fork");
+        CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_fork, 0), "fork");
+    }
+    auto moments = [&] {
+        return c->timed_on(1, ovl ? c->side : c->stream, [&] {
+            return cpa::launch_moments_i8(d_w, ld, n, M, sgn, acc + cpa_accum_offset(M, 1),
+                                          acc + cpa_accum_offset(M, 2), ovl ? c->side : c->stream, &launches);
+        });
+    };
+    if (!ovl) CUDA_TRY(moments(), "moments");
     CUtensorMap tmap;
     cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)n};
     cuuint64_t strides[1] = {(cuuint64_t)ld};
@@ -347,6 +373,11 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                              &launches);
              }),
              "xterm_i8");
+    if (ovl) {
+        CUDA_TRY(moments(), "moments");
+        CUDA_TRY(cudaEventRecord(c->ev_join, c->side), "join");
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "join");
+    }
     c->launches += launches;
     return CPA_OK;
 }
@@ -557,6 +588,12 @@ cpa_status cpa_destroy(cpa_ctx *c)
         if (c->ev_used[k]) cudaEventDestroy(c->ev_used[k]);
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->side) {
+        cudaStreamSynchronize(c->side);
+        cudaStreamDestroy(c->side);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     cudaFree(c->d_offset);
     cudaFree(c->d_hi);
     cudaFree(c->d_lo);

@@ -62,6 +62,9 @@ class Engine:
     def set_timing(self, on: bool = True):
         B.cpa_set_option(self.ctx, B.CPA_OPT_TIMING, int(on))
 
+    def set_overlap(self, on: bool = True):
+        B.cpa_set_option(self.ctx, B.CPA_OPT_OVERLAP, int(on))
+
     def phase_times(self):
         """({phase: ms}, {phase: launches}) of the CUDA-event-timed launches
         since the last call (needs set_timing(True))."""

@@ -23,11 +23,13 @@ def P():
 MODEL = {O.HD_LAST: 0, O.HW_LAST: 1, O.HW_FIRST: 2}
 
 
-def run_gpu(P, texts, W, model=0, kchunk=0, chunks=None, want_rho=True):
+def run_gpu(P, texts, W, model=0, kchunk=0, chunks=None, want_rho=True, overlap=True):
     dtype = {np.int8: P.CPA_S8, np.uint8: P.CPA_U8}[W.dtype.type]
     eng = P.Engine(W.shape[1], dtype, model, 0)
     if kchunk:
         eng.set_kchunk(kchunk)
+    if not overlap:
+        eng.set_overlap(False)
     bounds = chunks or [0, W.shape[0]]
     # pad rows to a 16-byte multiple (TMA stride rule); ld > M exercises strides
     ld = (W.shape[1] + 15) // 16 * 16
@@ -133,7 +135,8 @@ def test_split_k_chunks_and_permutation_bit_identical(P):
     texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
     W = rng.integers(-128, 128, (n, m)).astype(np.int8)
     base, out0 = run_gpu(P, texts, W)
-    for kw in (dict(kchunk=128), dict(kchunk=1024), dict(chunks=[0, 1, 700, 4097, 9000])):
+    for kw in (dict(kchunk=128), dict(kchunk=1024), dict(chunks=[0, 1, 700, 4097, 9000]),
+               dict(overlap=False), dict(overlap=False, chunks=[0, 5000, 9000])):
         s, o = run_gpu(P, texts, W, **kw)
         for k in base:
             assert np.array_equal(base[k], s[k]), (kw, k)
