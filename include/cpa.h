@@ -106,7 +106,8 @@ CPA_API cpa_status cpa_accumulate(cpa_ctx *ctx, const void *d_traces, int64_t ld
                           const uint8_t *d_texts, int64_t N);
 
 /* Same, from HOST buffers: the library streams them through its own device
- * staging buffers (H2D copies overlapped with compute).  Synchronous: returns
+ * staging buffers (H2D copies overlapped with compute; contiguous rows, ld == M,
+ * travel as one linear copy per chunk, which is what reaches full PCIe rate).  Synchronous: returns
  * after the last copy was consumed, so the host buffers may be reused.  Host
  * buffers should be pinned (cudaHostAlloc / cudaHostRegister) for speed.     */
 CPA_API cpa_status cpa_accumulate_host(cpa_ctx *ctx, const void *h_traces, int64_t ld,
@@ -154,8 +155,11 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *                   around every kernel launch (read with cpa_phase_times).
  *   CPA_OPT_OVERLAP: nonzero (default) = run the trace-moment pass (a4) on a
  *                   low-priority side stream concurrently with the cross term;
- *                   0 = serialise everything on the context's stream.       */
-enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2, CPA_OPT_OVERLAP = 3 };
+ *                   0 = serialise everything on the context's stream.
+ *   CPA_OPT_STAGE_BYTES: bytes of trace rows per staging chunk of
+ *                   cpa_accumulate_host / unaligned cpa_accumulate
+ *                   (0 = default 256 MiB; at least one row per chunk).      */
+enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2, CPA_OPT_OVERLAP = 3, CPA_OPT_STAGE_BYTES = 4 };
 CPA_API cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value);
 
 /* Per-phase device time (ms) and launch count since the last call, from the

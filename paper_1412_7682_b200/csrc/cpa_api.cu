@@ -56,7 +56,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
 
 constexpr int64_t kMaxTraces = 1LL << 23;  // exact-int64 bound of Eq. (1), see DESIGN.md
 constexpr int32_t kMaxSamples = 1 << 22;
-constexpr int64_t kHostChunk = 1LL << 18;  // traces per staging buffer (cpa_accumulate_host)
+constexpr int64_t kStageBytes = 256LL << 20;  // bytes per staging chunk (cpa_accumulate_host / unaligned input)
 
 }  // namespace
 
@@ -78,7 +78,10 @@ struct cpa_ctx {
     // cpa_accumulate_host staging
     void *d_stage[2] = {nullptr, nullptr};
     uint8_t *d_stage_tx[2] = {nullptr, nullptr};
-    int64_t stage_bytes = 0;
+    int64_t stage_bytes = 0, stage_rows = 0;
+    void *d_pack = nullptr;  // 16-byte-pitch rows repacked from a linear staging copy
+    int64_t pack_bytes = 0;
+    int64_t stage_chunk_bytes = kStageBytes;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
     // float path (a6): per-sample offsets, bf16 hi/lo planes, non-finite flag
@@ -252,6 +255,11 @@ cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets)
 cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
 {
     if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
+    if (option == CPA_OPT_STAGE_BYTES) {
+        if (value < 0) return fail(CPA_E_INVALID_ARG, "STAGE_BYTES=%lld < 0", (long long)value);
+        ctx->stage_chunk_bytes = value ? value : kStageBytes;
+        return CPA_OK;
+    }
     if (option == CPA_OPT_OVERLAP) {
         ctx->overlap = value != 0;
         return CPA_OK;
@@ -411,15 +419,23 @@ cpa_status cpa_accumulate(cpa_ctx *c, const void *d_traces, int64_t ld, const ui
 }
 
 // Stream (host or unaligned device) traces through the library's staging
-// buffers: a pitched copy into a 16-byte aligned layout, double-buffered so
-// the copy of chunk c+1 overlaps the kernels of chunk c.
+// buffers, double-buffered so the copy of chunk c+1 overlaps the kernels of
+// chunk c (a1).  Contiguous rows (ld == M) go as ONE linear copy per chunk --
+// the H2D DMA runs at full PCIe rate only for linear copies -- and, when a row
+// is not a 16-byte multiple, a device repack kernel then lays them out at a
+// 16-byte pitch for TMA.  Strided rows fall back to a pitched 2D copy.
 static cpa_status accumulate_staged(cpa_ctx *c, const void *src, int64_t ld, const uint8_t *tx, int64_t N)
 {
     const int64_t esz = c->dtype == CPA_F32 ? 4 : 1;
-    const int64_t ldd = (c->M * esz + 15) / 16 * 16 / esz;  // packed device row stride
-    const int64_t chunk = N < kHostChunk ? N : kHostChunk;
-    const int64_t need = chunk * ldd * esz;
-    if (c->stage_bytes < need) {
+    const int64_t rb = c->M * esz;              // bytes per trace row
+    const int64_t pitch = (rb + 15) / 16 * 16;  // device row pitch
+    const bool linear = ld * esz == rb;
+    const bool repack = linear && rb != pitch;
+    int64_t chunk = c->stage_chunk_bytes / pitch;
+    if (chunk < 1) chunk = 1;
+    if (chunk > N) chunk = N;
+    const int64_t need = chunk * pitch + 64;  // + slack for the repack kernel's word reads
+    if (c->stage_bytes < need || c->stage_rows < chunk || (repack && c->pack_bytes < chunk * pitch)) {
         CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
         for (int k = 0; k < 2; k++) {
             cudaFree(c->d_stage[k]);
@@ -427,13 +443,19 @@ static cpa_status accumulate_staged(cpa_ctx *c, const void *src, int64_t ld, con
             c->d_stage[k] = nullptr;
             c->d_stage_tx[k] = nullptr;
         }
-        c->stage_bytes = 0;
+        cudaFree(c->d_pack);
+        c->d_pack = nullptr;
+        c->stage_bytes = c->stage_rows = c->pack_bytes = 0;
         for (int k = 0; k < 2; k++) {
             if (cudaMalloc(&c->d_stage[k], need) != cudaSuccess ||
                 cudaMalloc(&c->d_stage_tx[k], chunk * 16) != cudaSuccess)
                 return fail(CPA_E_NO_MEMORY, "staging buffers (%lld bytes)", (long long)need);
         }
+        if (repack && cudaMalloc(&c->d_pack, chunk * pitch) != cudaSuccess)
+            return fail(CPA_E_NO_MEMORY, "repack buffer (%lld bytes)", (long long)(chunk * pitch));
         c->stage_bytes = need;
+        c->stage_rows = chunk;
+        c->pack_bytes = repack ? chunk * pitch : 0;
         if (!c->copy_stream) {
             CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "copy stream");
             for (int k = 0; k < 2; k++) {
@@ -448,15 +470,27 @@ static cpa_status accumulate_staged(cpa_ctx *c, const void *src, int64_t ld, con
     int k = 0;
     for (int64_t i0 = 0; i0 < N; i0 += chunk, k ^= 1) {
         const int64_t n = (N - i0) < chunk ? (N - i0) : chunk;
+        const uint8_t *s = (const uint8_t *)src + i0 * ld * esz;
         CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev_used[k], 0), "wait");
-        CUDA_TRY(cudaMemcpy2DAsync(c->d_stage[k], ldd * esz, (const uint8_t *)src + i0 * ld * esz, ld * esz,
-                                   c->M * esz, n, cudaMemcpyDefault, c->copy_stream),
-                 "copy traces");
+        if (linear)
+            CUDA_TRY(cudaMemcpyAsync(c->d_stage[k], s, n * rb, cudaMemcpyDefault, c->copy_stream), "copy traces");
+        else
+            CUDA_TRY(cudaMemcpy2DAsync(c->d_stage[k], pitch, s, ld * esz, rb, n, cudaMemcpyDefault, c->copy_stream),
+                     "copy traces");
         CUDA_TRY(cudaMemcpyAsync(c->d_stage_tx[k], tx + i0 * 16, n * 16, cudaMemcpyDefault, c->copy_stream),
                  "copy texts");
         CUDA_TRY(cudaEventRecord(c->ev_copied[k], c->copy_stream), "event");
         CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_copied[k], 0), "wait");
-        cpa_status st = accumulate_device(c, c->d_stage[k], ldd, c->d_stage_tx[k], n);
+        const void *w = c->d_stage[k];
+        if (repack) {
+            int launches = 0;
+            CUDA_TRY(cpa::launch_repack((const uint8_t *)c->d_stage[k], rb, (uint8_t *)c->d_pack, pitch, n,
+                                        c->stream, &launches),
+                     "repack");
+            c->launches += launches;
+            w = c->d_pack;
+        }
+        cpa_status st = accumulate_device(c, w, pitch / esz, c->d_stage_tx[k], n);
         if (st != CPA_OK) return st;
         CUDA_TRY(cudaEventRecord(c->ev_used[k], c->stream), "event");
     }
@@ -587,6 +621,7 @@ cpa_status cpa_destroy(cpa_ctx *c)
         if (c->ev_copied[k]) cudaEventDestroy(c->ev_copied[k]);
         if (c->ev_used[k]) cudaEventDestroy(c->ev_used[k]);
     }
+    cudaFree(c->d_pack);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->side) {
         cudaStreamSynchronize(c->side);

@@ -571,6 +571,47 @@ k_split_f32(const float *__restrict__ w, int64_t ld, int64_t n, int32_t M, const
 }
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Staging repack: n packed rows of rb bytes (as copied 1D from the host) ->
+// rows of pitch `pitch` bytes (a multiple of 16, as TMA requires).  Thread =
+// one 16-byte output chunk, built from five aligned 32-bit source words and
+// funnel shifts.  The source buffer carries >= 20 bytes of readable slack.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int RP_THREADS = 256;
+__global__ void __launch_bounds__(RP_THREADS)
+k_repack(const uint8_t *__restrict__ src, int64_t rb, uint8_t *__restrict__ dst, int64_t pitch, int64_t n)
+{
+    const int64_t q = (int64_t)blockIdx.x * RP_THREADS + threadIdx.x;
+    if (q * 16 >= rb) return;
+    for (int64_t r = blockIdx.y; r < n; r += gridDim.y) {
+        const int64_t s = r * rb + q * 16;
+        const uint32_t *a = (const uint32_t *)(src + (s & ~(int64_t)3));
+        const uint32_t sh = (uint32_t)(s & 3) * 8;
+        uint32_t w[5];
+#pragma unroll
+        for (int i = 0; i < 5; i++) w[i] = __ldg(a + i);
+        uint4 o;
+        o.x = __funnelshift_r(w[0], w[1], sh);
+        o.y = __funnelshift_r(w[1], w[2], sh);
+        o.z = __funnelshift_r(w[2], w[3], sh);
+        o.w = __funnelshift_r(w[3], w[4], sh);
+        *(uint4 *)(dst + r * pitch + q * 16) = o;
+    }
+}
+}  // namespace
+
+cudaError_t launch_repack(const uint8_t *d_src, int64_t rb, uint8_t *d_dst, int64_t pitch, int64_t n,
+                          cudaStream_t s, int *launches)
+{
+    if (n <= 0) return cudaSuccess;
+    const int64_t nq = (rb + 15) / 16;
+    dim3 grid((unsigned)((nq + RP_THREADS - 1) / RP_THREADS), (unsigned)(n < 4096 ? n : 4096));
+    k_repack<<<grid, RP_THREADS, 0, s>>>(d_src, rb, d_dst, pitch, n);
+    if (launches) (*launches)++;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_split_f32(const float *d_w, int64_t ld, int64_t n, int32_t M, const float *d_offset,
                              uint16_t *d_hi, uint16_t *d_lo, int64_t ldh, double *d_sum_w, double *d_sum_w2,
                              int *d_nonfinite, cudaStream_t s, int *launches)

@@ -41,6 +41,11 @@ cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &t
                                 const uint8_t *d_vtab, double *d_hw, int *d_counter, int32_t M, int64_t N,
                                 int64_t kc_len, int num_sms, cudaStream_t stream, int *launches);
 
+// a1 staging: n rows of rb contiguous bytes -> rows of `pitch` bytes (multiple
+// of 16).  d_src needs >= 20 bytes of readable slack past n*rb.
+cudaError_t launch_repack(const uint8_t *d_src, int64_t rb, uint8_t *d_dst, int64_t pitch, int64_t n,
+                          cudaStream_t s, int *launches);
+
 // a8/a9: Phase 3 + 4 [P:81-87]
 struct FinalizeOut {
     double *rho;       // optional [4096][M]

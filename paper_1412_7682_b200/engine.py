@@ -62,6 +62,9 @@ class Engine:
     def set_timing(self, on: bool = True):
         B.cpa_set_option(self.ctx, B.CPA_OPT_TIMING, int(on))
 
+    def set_stage_bytes(self, nbytes: int):
+        B.cpa_set_option(self.ctx, B.CPA_OPT_STAGE_BYTES, nbytes)
+
     def set_overlap(self, on: bool = True):
         B.cpa_set_option(self.ctx, B.CPA_OPT_OVERLAP, int(on))
 

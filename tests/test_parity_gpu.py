@@ -192,6 +192,36 @@ def test_host_buffer_path_matches_device(P):
     eng.close()
 
 
+@pytest.mark.parametrize("m,ld,stage", [(300, 300, 0), (300, 300, 300 * 97), (301, 301, 320 * 50),
+                                        (320, 320, 320 * 64), (300, 333, 320 * 41), (5000, 5000, 5008 * 700)])
+def test_staging_chunks_linear_repack_and_pitched(P, m, ld, stage):
+    """a1 staging: linear copy + repack (row not a 16-byte multiple), linear
+    copy in place (row a 16-byte multiple) and the pitched 2D copy (ld > M),
+    over many double-buffered chunks, all bit-exact with the oracle."""
+    rng = np.random.default_rng(m + ld)
+    n = 2311
+    texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    base = rng.integers(-128, 128, (n, ld)).astype(np.int8)
+    W = base[:, :m]
+    cols = np.array([0, 1, m // 2, m - 1], np.int32)
+    ref_hw = O.cross_sums_i8(O.HD_LAST, texts, np.ascontiguousarray(W), cols)
+    for src in ("host", "device"):
+        eng = P.Engine(m, P.CPA_S8, P.CPA_HD_LAST, 0)
+        eng.set_stage_bytes(stage)
+        if src == "host":
+            eng.accumulate_host(W, texts)
+        else:  # an odd byte offset forces the staged path for device input too
+            raw = torch.from_numpy(np.concatenate([np.zeros(1, np.int8), base.reshape(-1)])).cuda()
+            dW = raw[1:].view(n, ld)[:, :m]
+            eng.accumulate(dW, torch.from_numpy(texts).cuda())
+        eng.sync()
+        assert np.array_equal(eng.sum_hw.cpu().numpy()[:, cols], ref_hw), src
+        assert np.array_equal(eng.sum_w.cpu().numpy(), W.astype(np.int64).sum(0)), src
+        assert np.array_equal(eng.sum_w2.cpu().numpy(), (W.astype(np.int64) ** 2).sum(0)), src
+        assert int(eng.n.cpu().numpy()[0]) == n
+        eng.close()
+
+
 def test_errors(P):
     eng = P.Engine(100, P.CPA_S8, P.CPA_HD_LAST, 0)
     W = torch.zeros((10, 100), dtype=torch.int8, device="cuda")
