@@ -27,8 +27,9 @@
 //     by a global atomic counter (leader CTA) so the units in flight share a
 //     few W blocks in L2 (W streams from HBM about once).
 // Warp roles (768 threads per CTA): w0 scheduler (leader) + W TMA producer,
-// w1 MMA issuer (leader), w2 TMEM owner, w3 ciphertext producer, w4-7
-// epilogue (TMEM lanes 32*(w%4)...), w8-23 H generators.
+// w1 MMA issuer (leader) / A-ready forwarder (peer), w2 TMEM owner, w3
+// ciphertext producer, w4-7 epilogue (TMEM lanes 32*(w%4)...), w8-23 H
+// generators.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -67,7 +68,9 @@ constexpr int EPI_WARPS = 4;
 constexpr int GEN_WARPS = 16;                 // every generator warp works on every stage, so
                                               // each waits every phase of every slot in order
                                               // (mbarrier parity waits are 1-bit)
-constexpr int CONSUMERS_PER_CTA = 2 + EPI_WARPS + GEN_WARPS;  // (MMA | W producer) + text producer + warps
+// readers of the unit-id ring: leader = MMA + text producer + epilogue + generators,
+// peer = W producer + A-ready forwarder + text producer + epilogue + generators
+constexpr int RING_CONSUMERS = (2 + EPI_WARPS + GEN_WARPS) + (3 + EPI_WARPS + GEN_WARPS);
 constexpr int TB_LD = 9;                      // epilogue transpose row stride (words, odd)
 constexpr int TB_BYTES = EPI_WARPS * 32 * TB_LD * 4;
 constexpr int SMEM_V = 0;
@@ -75,7 +78,7 @@ constexpr int SMEM_STAGE = SMEM_V + V_BYTES;
 constexpr int SMEM_TX = SMEM_STAGE + STAGES * STAGE_BYTES;
 constexpr int SMEM_TB = SMEM_TX + TX_STAGES * TX_BYTES;
 constexpr int SMEM_BAR = SMEM_TB + TB_BYTES;
-constexpr int NUM_BARS = 2 * STAGES + 2 * TX_STAGES + 4 + 2 * SCHED_Q;
+constexpr int NUM_BARS = 2 * STAGES + 2 * TX_STAGES + 4 + 2 * SCHED_Q + STAGES;
 constexpr int SMEM_SCHED = SMEM_BAR + NUM_BARS * 8;
 constexpr int SMEM_TOTAL = SMEM_SCHED + SCHED_Q * 4 + 16;
 constexpr int SMEM_ALLOC = SMEM_TOTAL;
@@ -148,6 +151,8 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
     auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + 2 + a); }; // leader's
     auto sfull_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + q); };        // both CTAs
     auto sempty_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + SCHED_Q + q); };  // leader's
+    // peer only: its generators finished stage s (forwarded to the leader's full_bar by one thread)
+    auto gdone_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (BAR_S + 2 * SCHED_Q + s); };
     volatile int *sched = (volatile int *)(smem + SMEM_SCHED);
     uint32_t *tmem_slot = (uint32_t *)(smem + SMEM_SCHED + SCHED_Q * 4);
     auto to_leader = [&](uint32_t a) { return mapa_shared(a, 0); };
@@ -173,8 +178,11 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
         tma_prefetch(&tmap_b0);
         if (F32) tma_prefetch(&tmap_b1);
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(full_bar(s), 2 + 2 * GEN_WARPS);  // 2 producer arrivals (+tx) + both CTAs' generators
-            mbar_init(empty_bar(s), 1);                 // multicast tcgen05.commit
+            // leader's W producer (arrive + tx of both CTAs) + leader's generator warps
+            // + the peer's forwarder (one arrival for all of the peer's generators)
+            mbar_init(full_bar(s), 2 + GEN_WARPS);
+            mbar_init(empty_bar(s), 1);       // multicast tcgen05.commit
+            mbar_init(gdone_bar(s), GEN_WARPS);
         }
         for (int x = 0; x < TX_STAGES; x++) {
             mbar_init(txfull_bar(x), 1);            // ciphertext rows landed
@@ -186,7 +194,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
         }
         for (int q = 0; q < SCHED_Q; q++) {
             mbar_init(sfull_bar(q), 1);
-            mbar_init(sempty_bar(q), 2 * CONSUMERS_PER_CTA);
+            mbar_init(sempty_bar(q), RING_CONSUMERS);
         }
         fence_mbar_init();
     }
@@ -224,9 +232,11 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
                     const int s = it % STAGES;
                     mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
+                    // the leader's arrival carries the tx bytes of BOTH CTAs' loads; the
+                    // peer's loads only complete tx on it (they cannot land in an earlier
+                    // phase: the peer waited for this slot's commit, which follows it)
                     const uint32_t lbar = to_leader(full_bar(s));
-                    if (leader) mbar_arrive_expect_tx(full_bar(s), 2 * (STAGE_BYTES - C::A_BYTES));  // both CTAs
-                    else mbar_arrive_cluster(lbar);
+                    if (leader) mbar_arrive_expect_tx(full_bar(s), 2 * (STAGE_BYTES - C::A_BYTES));
                     uint32_t bdst = sbase + SMEM_STAGE + s * STAGE_BYTES + C::A_BYTES;
 #pragma unroll
                     for (int n = 0; n < C::NT; n++)
@@ -261,11 +271,13 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             }
         }
     } else if (warp == 1) {
-        // ================= MMA issuer (one thread of the leader) =================
-        // (the peer's w1 stays out of the unit ring: per CTA the ring has
-        //  CONSUMERS_PER_CTA readers -- MMA here, the W producer in the peer)
         if (lane == 0 && leader) {
-            uint32_t it = 0;
+            // ================= MMA issuer (one thread of the leader) =================
+            // Lean issue loop: descriptors are precomputed and advanced by adding
+            // 16-byte units to their start-address field; the full barrier is waited
+            // on at CTA scope (tools/pair_bench: 65% -> 100% of the pair MMA rate).
+            const uint64_t desc0 = smem_desc_sw128(sbase + SMEM_STAGE, C::A_ATOM, 1024);
+            uint32_t s = 0, ph = 0;
             for (uint32_t t = 0;; t++) {
                 const int u = next_unit(t, true);
                 if (u < 0) break;
@@ -276,31 +288,51 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 mbar_wait_cluster(tempty_bar(acc), ((t / C::NBUF) & 1) ^ 1);  // both epilogues drained it
                 tc_fence_after();
                 const uint32_t dbase = tmem_base + acc * (C::NT * BN);
-                bool first = true;
-                for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
-                    const int s = it % STAGES;
-                    mbar_wait_cluster(full_bar(s), (it / STAGES) & 1);
+                uint32_t accum = 0;
+                for (int64_t tb = t0; tb < t1; tb += C::BK) {
+                    mbar_wait(full_bar(s), ph);
                     tc_fence_after();
-                    const uint32_t a_addr = sbase + SMEM_STAGE + s * STAGE_BYTES;
-                    const uint32_t b_addr = a_addr + C::A_BYTES;
+                    const uint64_t ad = desc0 + (uint64_t)((s * STAGE_BYTES) >> 4);
 #pragma unroll
                     for (int kk = 0; kk < C::BK / C::KMMA; kk++) {
                         // K step = KMMA rows of 128 bytes in every MN atom
-                        const uint64_t ad = smem_desc_sw128(a_addr + kk * (C::KMMA * 128), C::A_ATOM, 1024);
+                        const uint64_t adk = ad + (uint64_t)((kk * C::KMMA * 128) >> 4);
 #pragma unroll
                         for (int n = 0; n < C::NT; n++)
 #pragma unroll
                             for (int op = 0; op < C::NB; op++) {
-                                const uint32_t bo = b_addr + (n * C::NB + op) * C::BH_BYTES + kk * (C::KMMA * 128);
-                                const uint64_t bd = smem_desc_sw128(bo, C::A_ATOM, 1024);
-                                if (F32) mma_bf16_pair(dbase + n * BN, ad, bd, p.idesc, (first && op == 0) ? 0u : 1u);
-                                else mma_i8_pair(dbase + n * BN, ad, bd, p.idesc, first ? 0u : 1u);
+                                const uint64_t bd = adk + (uint64_t)((C::A_BYTES + (n * C::NB + op) * C::BH_BYTES) >> 4);
+                                if (F32) mma_bf16_pair(dbase + n * BN, adk, bd, p.idesc, op == 0 ? accum : 1u);
+                                else mma_i8_pair(dbase + n * BN, adk, bd, p.idesc, accum);
                             }
-                        first = false;
+                        accum = 1;
                     }
                     mma_commit_pair(empty_bar(s), 0x3);  // frees the stage in both CTAs when done
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1;
+                    }
                 }
                 mma_commit_pair(tfull_bar(acc), 0x3);    // accumulators ready for both epilogues
+            }
+        } else if (lane == 0) {
+            // ====== peer: forward "A tile generated" to the leader's full barrier ======
+            // one cluster-scope release per stage instead of one per generator warp
+            uint32_t s = 0, ph = 0;
+            for (uint32_t t = 0;; t++) {
+                const int u = next_unit(t, true);
+                if (u < 0) break;
+                int b, nt;
+                int64_t t0, t1;
+                unit_coords<F32>(p, u, b, nt, t0, t1);
+                for (int64_t tb = t0; tb < t1; tb += C::BK) {
+                    mbar_wait(gdone_bar(s), ph);
+                    mbar_arrive_cluster(to_leader(full_bar(s)));
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
             }
         }
     } else if (warp >= 4 && warp < 8) {
@@ -315,7 +347,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             int64_t t0, t1;
             unit_coords<F32>(p, u, b, nt, t0, t1);
             const uint32_t acc = t % C::NBUF;
-            mbar_wait_cluster(tfull_bar(acc), (t / C::NBUF) & 1);
+            mbar_wait(tfull_bar(acc), (t / C::NBUF) & 1);  // multicast commit: CTA-scope wait
             tc_fence_after();
             const int hrow0 = b * 256 + (int)rank * BMC + q * 32;
             // 8 columns at a time through a small transpose buffer: each warp-wide
@@ -412,8 +444,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    if (leader) mbar_arrive(full_bar(s));
-                    else mbar_arrive_cluster(to_leader(full_bar(s)));
+                    mbar_arrive(leader ? full_bar(s) : gdone_bar(s));
                     mbar_arrive(txempty_bar(x));
                 }
             }
