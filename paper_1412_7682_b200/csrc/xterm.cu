@@ -39,6 +39,16 @@
 #include "kernels.h"
 #include "ptx.cuh"
 
+// XT_EXP (profiling builds only, tools/xt_exp.sh; results are NOT valid):
+//   bit 0: W loads re-read the first 8192 traces (L2-resident W)
+//   bit 1: generators skip the H generation (barrier traffic only)
+//   bit 2: the epilogue skips its global atomics (TMEM reads only)
+//   bit 3: the MMA issuer does not wait for the stage data (pure issue rate)
+//   bit 4: no W loads (the leader's producer arrives without tx bytes)
+#ifndef XT_EXP
+#define XT_EXP 0
+#endif
+
 namespace cpa {
 namespace {
 
@@ -47,8 +57,10 @@ struct Cfg {
     static constexpr int ESZ = F32 ? 2 : 1;         // bytes per operand element
     static constexpr int KMMA = F32 ? 16 : 32;      // K per MMA instruction
     static constexpr int NB = F32 ? 2 : 1;          // B operands (hi, lo)
-    static constexpr int NT = F32 ? 1 : 2;          // N=256 accumulators per unit
+    static constexpr int KB = F32 ? 1 : 2;          // key bytes per unit (A tiles sharing one W tile)
+    static constexpr int NT = 1;                    // N=256 sample tiles per unit
     static constexpr int NBUF = F32 ? 2 : 1;        // TMEM accumulator buffers
+    static constexpr int NACC = KB * NT;            // N=256 accumulators per unit
     static constexpr int BK = F32 ? 64 : 128;       // traces per pipeline stage
     static constexpr int BOX_X = 128 / ESZ;         // samples per TMA box (128-byte swizzle span)
     static constexpr int BH_BYTES = BK * 128 * ESZ; // one CTA's half (128 samples) of one N tile, one operand
@@ -84,10 +96,12 @@ constexpr int SMEM_TOTAL = SMEM_SCHED + SCHED_Q * 4 + 16;
 constexpr int SMEM_ALLOC = SMEM_TOTAL;
 constexpr int THREADS = 32 * (8 + GEN_WARPS);
 constexpr uint32_t TMEM_COLS = 512;
-static_assert(Cfg<false>::A_BYTES + Cfg<false>::NT * Cfg<false>::NB * Cfg<false>::BH_BYTES == STAGE_BYTES, "");
-static_assert(Cfg<true>::A_BYTES + Cfg<true>::NT * Cfg<true>::NB * Cfg<true>::BH_BYTES == STAGE_BYTES, "");
-static_assert(Cfg<false>::NT * Cfg<false>::NBUF * BN == TMEM_COLS, "");
-static_assert(Cfg<true>::NT * Cfg<true>::NBUF * BN == TMEM_COLS, "");
+template <bool F32>
+__host__ __device__ constexpr int b_offset() { return Cfg<F32>::KB * Cfg<F32>::A_BYTES; }  // W tiles follow the A tiles
+static_assert(b_offset<false>() + Cfg<false>::NT * Cfg<false>::NB * Cfg<false>::BH_BYTES == STAGE_BYTES, "");
+static_assert(b_offset<true>() + Cfg<true>::NT * Cfg<true>::NB * Cfg<true>::BH_BYTES == STAGE_BYTES, "");
+static_assert(Cfg<false>::NACC * Cfg<false>::NBUF * BN == TMEM_COLS, "");
+static_assert(Cfg<true>::NACC * Cfg<true>::NBUF * BN == TMEM_COLS, "");
 
 struct Params {
     const uint8_t *texts;    // N x 16
@@ -96,6 +110,7 @@ struct Params {
     int *unit_counter;       // zeroed before the launch
     int32_t M;
     int32_t n_tiles;         // tiles of NT*256 samples
+    int32_t groups;          // key-byte groups (16 / KB)
     int32_t kc_count;
     int32_t units;
     int64_t N;
@@ -106,8 +121,9 @@ struct Params {
 template <bool F32>
 __device__ __forceinline__ void unit_coords(const Params &p, int u, int &b, int &n_tile, int64_t &t0, int64_t &t1)
 {
-    b = u & 15;
-    const int r = u >> 4;
+    // b = first key byte of the unit's group (bytes b .. b+KB-1)
+    b = (u % p.groups) * Cfg<F32>::KB;
+    const int r = u / p.groups;
     const int kc = r % p.kc_count;
     n_tile = r / p.kc_count;
     t0 = (int64_t)kc * p.kc_len;
@@ -236,8 +252,12 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     // peer's loads only complete tx on it (they cannot land in an earlier
                     // phase: the peer waited for this slot's commit, which follows it)
                     const uint32_t lbar = to_leader(full_bar(s));
-                    if (leader) mbar_arrive_expect_tx(full_bar(s), 2 * (STAGE_BYTES - C::A_BYTES));
-                    uint32_t bdst = sbase + SMEM_STAGE + s * STAGE_BYTES + C::A_BYTES;
+                    if (XT_EXP & 16) {
+                        if (leader) mbar_arrive(full_bar(s));
+                        continue;
+                    }
+                    if (leader) mbar_arrive_expect_tx(full_bar(s), 2 * (STAGE_BYTES - b_offset<F32>()));
+                    uint32_t bdst = sbase + SMEM_STAGE + s * STAGE_BYTES + b_offset<F32>();
 #pragma unroll
                     for (int n = 0; n < C::NT; n++)
 #pragma unroll
@@ -245,7 +265,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
 #pragma unroll
                             for (int at = 0; at < C::ESZ; at++) {  // 128-byte MN atoms of this half
                                 tma_load_2d_pair(bdst, op == 0 ? &tmap_b0 : &tmap_b1, x0 + n * BN + at * C::BOX_X,
-                                                 (int32_t)tb, lbar);
+                                                 (XT_EXP & 1) ? (int32_t)(tb & 8191) : (int32_t)tb, lbar);
                                 bdst += C::A_ATOM;
                             }
                 }
@@ -287,10 +307,10 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 const uint32_t acc = t % C::NBUF;
                 mbar_wait_cluster(tempty_bar(acc), ((t / C::NBUF) & 1) ^ 1);  // both epilogues drained it
                 tc_fence_after();
-                const uint32_t dbase = tmem_base + acc * (C::NT * BN);
+                const uint32_t dbase = tmem_base + acc * (C::NACC * BN);
                 uint32_t accum = 0;
                 for (int64_t tb = t0; tb < t1; tb += C::BK) {
-                    mbar_wait(full_bar(s), ph);
+                    if (!(XT_EXP & 8)) mbar_wait(full_bar(s), ph);
                     tc_fence_after();
                     const uint64_t ad = desc0 + (uint64_t)((s * STAGE_BYTES) >> 4);
 #pragma unroll
@@ -300,11 +320,16 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
 #pragma unroll
                         for (int n = 0; n < C::NT; n++)
 #pragma unroll
-                            for (int op = 0; op < C::NB; op++) {
-                                const uint64_t bd = adk + (uint64_t)((C::A_BYTES + (n * C::NB + op) * C::BH_BYTES) >> 4);
-                                if (F32) mma_bf16_pair(dbase + n * BN, adk, bd, p.idesc, op == 0 ? accum : 1u);
-                                else mma_i8_pair(dbase + n * BN, adk, bd, p.idesc, accum);
-                            }
+                            for (int kb = 0; kb < C::KB; kb++)
+#pragma unroll
+                                for (int op = 0; op < C::NB; op++) {
+                                    const uint64_t a = adk + (uint64_t)((kb * C::A_BYTES) >> 4);
+                                    const uint64_t bd =
+                                        adk + (uint64_t)((b_offset<F32>() + (n * C::NB + op) * C::BH_BYTES) >> 4);
+                                    const uint32_t d = dbase + (kb * C::NT + n) * BN;
+                                    if (F32) mma_bf16_pair(d, a, bd, p.idesc, op == 0 ? accum : 1u);
+                                    else mma_i8_pair(d, a, bd, p.idesc, accum);
+                                }
                         accum = 1;
                     }
                     mma_commit_pair(empty_bar(s), 0x3);  // frees the stage in both CTAs when done
@@ -349,19 +374,21 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             const uint32_t acc = t % C::NBUF;
             mbar_wait(tfull_bar(acc), (t / C::NBUF) & 1);  // multicast commit: CTA-scope wait
             tc_fence_after();
-            const int hrow0 = b * 256 + (int)rank * BMC + q * 32;
+            constexpr int CPB = C::NT * BN / 8;  // 8-column groups per key byte
             // 8 columns at a time through a small transpose buffer: each warp-wide
             // atomic covers 4 rows x 8 consecutive samples = 8 full 32-byte sectors
 #pragma unroll 1
-            for (int c = 0; c < C::NT * BN / 8; c++) {
+            for (int c = 0; c < C::NACC * BN / 8; c++) {
+                const int kb = c / CPB, cc = c % CPB;
+                const int hrow0 = (b + kb) * 256 + (int)rank * BMC + q * 32;
                 uint32_t v[8];
-                tmem_ld_32x32b_x8(tmem_base + ((uint32_t)(q * 32) << 16) + acc * (C::NT * BN) + c * 8, v);
+                tmem_ld_32x32b_x8(tmem_base + ((uint32_t)(q * 32) << 16) + acc * (C::NACC * BN) + c * 8, v);
                 tmem_ld_wait();
 #pragma unroll
                 for (int x = 0; x < 8; x++) tbuf[lane * TB_LD + x] = v[x];
                 __syncwarp();
-                const int j = nt * (C::NT * BN) + c * 8 + csub;  // accumulator column = sample
-                if (j < p.M) {
+                const int j = nt * (C::NT * BN) + cc * 8 + csub;  // accumulator column = sample
+                if (!(XT_EXP & 4) && j < p.M) {
                     const int64_t off = (int64_t)(hrow0 + rsub) * p.M + j;
 #pragma unroll
                     for (int rr = 0; rr < 8; rr++) {
@@ -397,7 +424,6 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             int b, nt;
             int64_t t0, t1;
             unit_coords<F32>(p, u, b, nt, t0, t1);
-            const int s_idx = shiftrows_src(b);
             const uint32_t gchunk = rank * 8 + ql;  // global 16-key chunk (keys 128*rank ...)
             for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
                 const int s = it % STAGES;
@@ -407,13 +433,15 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 mbar_wait(txfull_bar(x), (it / TX_STAGES) & 1);
                 mbar_wait(empty_bar(s), ph ^ 1);  // A slot free
                 const uint8_t *tx = smem + SMEM_TX + x * TX_BYTES;
-                uint8_t *abase = smem + SMEM_STAGE + s * STAGE_BYTES;
 #pragma unroll
-                for (int pass = 0; pass < PASSES; pass++) {
+                for (int kb = 0; kb < C::KB; kb++)  // the unit's key bytes b, b+1, ...
+#pragma unroll
+                for (int pass = 0; pass < ((XT_EXP & 2) ? 0 : PASSES); pass++) {
+                    uint8_t *abase = smem + SMEM_STAGE + s * STAGE_BYTES + kb * C::A_BYTES;
                     const int row = (PASSES * 4) * g + 4 * pass + sub;
                     uint4 outv = make_uint4(0, 0, 0, 0);
                     if (row < nrows) {
-                        const uint32_t cb = tx[row * 16 + b], cs = tx[row * 16 + s_idx];
+                        const uint32_t cb = tx[row * 16 + b + kb], cs = tx[row * 16 + shiftrows_src(b + kb)];
                         const uint32_t hi = cb >> 4, lo = cb & 15, u4 = lo >> 2, v4 = lo & 3;
                         const uint32_t sel_e = (0x3210u ^ (v4 * 0x1111u)) ^ ((u4 & 1) ? 0x4444u : 0u);
                         const uint32_t sel_o = sel_e ^ 0x4444u;
@@ -474,9 +502,10 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *
     p.M = M;
     p.N = N;
     p.n_tiles = (M + Cf::NT * BN - 1) / (Cf::NT * BN);
+    p.groups = 16 / Cf::KB;
     p.kc_len = kc_len;
     p.kc_count = (int32_t)((N + kc_len - 1) / kc_len);
-    p.units = 16 * p.n_tiles * p.kc_count;
+    p.units = p.groups * p.n_tiles * p.kc_count;
     p.idesc = idesc;
     static bool attr_set = false;
     if (!attr_set) {
@@ -498,9 +527,9 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *
 // accumulator (F32) the epilogue overlaps the next unit).  max_len bounds the
 // int32 exactness (I8: |H W| <= 8 * 255 -> 2^20 traces) or the fp32 rounding
 // (F32: 4096 traces).
-int64_t auto_kchunk(int32_t M, int64_t N, int num_sms, int nt, int bk, int64_t max_len, bool overlapped)
+int64_t auto_kchunk(int32_t M, int64_t N, int num_sms, int kb, int nt, int bk, int64_t max_len, bool overlapped)
 {
-    const int64_t tiles = 16LL * ((M + nt * BN - 1) / (nt * BN));
+    const int64_t tiles = (16LL / kb) * ((M + nt * BN - 1) / (nt * BN));
     const int64_t pairs = num_sms / 2;
     int64_t best_len = 0;
     double best = -1.0;
@@ -530,12 +559,12 @@ int xterm_smem_bytes() { return SMEM_ALLOC; }
 
 int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms)
 {
-    return auto_kchunk(M, N, num_sms, Cfg<false>::NT, Cfg<false>::BK, 1 << 20, false);
+    return auto_kchunk(M, N, num_sms, Cfg<false>::KB, Cfg<false>::NT, Cfg<false>::BK, 1 << 20, false);
 }
 
 int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms)
 {
-    return auto_kchunk(M, N, num_sms, Cfg<true>::NT, Cfg<true>::BK, 4096, true);
+    return auto_kchunk(M, N, num_sms, Cfg<true>::KB, Cfg<true>::NT, Cfg<true>::BK, 4096, true);
 }
 
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,

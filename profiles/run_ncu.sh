@@ -11,7 +11,8 @@ timeout -s KILL 300 ncu --metrics gpu__time_duration.sum --clock-control none --
     --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-clocks \
     > gpurun_out/launches_${TAG}.log 2>&1
 # full capture of each kernel of the step (second step = warm)
-for k in k_xterm_i8 k_moments_i8 k_modelsums k_finalize_i8; do
+KERNELS=${KERNELS:-"k_xterm k_moments_i8 k_texthist k_hist_contract k_repack k_finalize_i8"}
+for k in $KERNELS; do
   timeout -s KILL 300 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
       -o gpurun_out/${k}_${TAG} -f $B > gpurun_out/${k}_${TAG}.log 2>&1
 done
