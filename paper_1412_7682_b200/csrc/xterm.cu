@@ -27,7 +27,7 @@
 //     by a global atomic counter (leader CTA) so the units in flight share a
 //     few W blocks in L2 (W streams from HBM about once).
 // Warp roles (768 threads per CTA): w0 scheduler (leader) + W TMA producer,
-// w1 MMA issuer (leader) / A-ready forwarder (peer), w2 TMEM owner, w3
+// w1 MMA issuer (leader), w2 TMEM owner, w3
 // ciphertext producer, w4-7 epilogue (TMEM lanes 32*(w%4)...), w8-23 H
 // generators.
 #include <cuda.h>
@@ -71,6 +71,7 @@ struct Cfg {
 constexpr int BMC = 128;          // sub-keys per CTA (pair MMA M = 256)
 constexpr int BN = 256;           // samples per accumulator (MMA N)
 constexpr int STAGES = 3;
+constexpr int PREFETCH_STAGES = 8;  // W boxes are prefetched into L2 this many stages ahead
 constexpr int TX_STAGES = 6;      // ciphertext ring, prefetched ahead of the stages
 constexpr int SCHED_Q = 4;        // depth of the unit-id ring
 constexpr int STAGE_BYTES = 49152;
@@ -81,8 +82,8 @@ constexpr int GEN_WARPS = 16;                 // every generator warp works on e
                                               // each waits every phase of every slot in order
                                               // (mbarrier parity waits are 1-bit)
 // readers of the unit-id ring: leader = MMA + text producer + epilogue + generators,
-// peer = W producer + A-ready forwarder + text producer + epilogue + generators
-constexpr int RING_CONSUMERS = (2 + EPI_WARPS + GEN_WARPS) + (3 + EPI_WARPS + GEN_WARPS);
+// peer = W producer + text producer + epilogue + generators
+constexpr int RING_CONSUMERS = 2 * (2 + EPI_WARPS + GEN_WARPS);
 constexpr int TB_LD = 9;                      // epilogue transpose row stride (words, odd)
 constexpr int TB_BYTES = EPI_WARPS * 32 * TB_LD * 4;
 constexpr int SMEM_V = 0;
@@ -90,7 +91,7 @@ constexpr int SMEM_STAGE = SMEM_V + V_BYTES;
 constexpr int SMEM_TX = SMEM_STAGE + STAGES * STAGE_BYTES;
 constexpr int SMEM_TB = SMEM_TX + TX_STAGES * TX_BYTES;
 constexpr int SMEM_BAR = SMEM_TB + TB_BYTES;
-constexpr int NUM_BARS = 2 * STAGES + 2 * TX_STAGES + 4 + 2 * SCHED_Q + STAGES;
+constexpr int NUM_BARS = 2 * STAGES + 2 * TX_STAGES + 4 + 2 * SCHED_Q;
 constexpr int SMEM_SCHED = SMEM_BAR + NUM_BARS * 8;
 constexpr int SMEM_TOTAL = SMEM_SCHED + SCHED_Q * 4 + 16;
 constexpr int SMEM_ALLOC = SMEM_TOTAL;
@@ -167,8 +168,6 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
     auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + 2 + a); }; // leader's
     auto sfull_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + q); };        // both CTAs
     auto sempty_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + SCHED_Q + q); };  // leader's
-    // peer only: its generators finished stage s (forwarded to the leader's full_bar by one thread)
-    auto gdone_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (BAR_S + 2 * SCHED_Q + s); };
     volatile int *sched = (volatile int *)(smem + SMEM_SCHED);
     uint32_t *tmem_slot = (uint32_t *)(smem + SMEM_SCHED + SCHED_Q * 4);
     auto to_leader = [&](uint32_t a) { return mapa_shared(a, 0); };
@@ -194,11 +193,9 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
         tma_prefetch(&tmap_b0);
         if (F32) tma_prefetch(&tmap_b1);
         for (int s = 0; s < STAGES; s++) {
-            // leader's W producer (arrive + tx of both CTAs) + leader's generator warps
-            // + the peer's forwarder (one arrival for all of the peer's generators)
-            mbar_init(full_bar(s), 2 + GEN_WARPS);
+            // leader's W producer (arrive + tx of both CTAs) + both CTAs' generator warps
+            mbar_init(full_bar(s), 1 + 2 * GEN_WARPS);
             mbar_init(empty_bar(s), 1);       // multicast tcgen05.commit
-            mbar_init(gdone_bar(s), GEN_WARPS);
         }
         for (int x = 0; x < TX_STAGES; x++) {
             mbar_init(txfull_bar(x), 1);            // ciphertext rows landed
@@ -267,6 +264,12 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                                 tma_load_2d_pair(bdst, op == 0 ? &tmap_b0 : &tmap_b1, x0 + n * BN + at * C::BOX_X,
                                                  (XT_EXP & 1) ? (int32_t)(tb & 8191) : (int32_t)tb, lbar);
                                 bdst += C::A_ATOM;
+                                // the load latency (L2 miss -> HBM) exceeds the ring's
+                                // slack: pull the box PREFETCH_STAGES ahead into L2
+                                const int64_t tp = tb + PREFETCH_STAGES * C::BK;
+                                if (tp < t1)
+                                    tma_prefetch_2d(op == 0 ? &tmap_b0 : &tmap_b1, x0 + n * BN + at * C::BOX_X,
+                                                    (int32_t)tp);
                             }
                 }
             }
@@ -339,25 +342,6 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     }
                 }
                 mma_commit_pair(tfull_bar(acc), 0x3);    // accumulators ready for both epilogues
-            }
-        } else if (lane == 0) {
-            // ====== peer: forward "A tile generated" to the leader's full barrier ======
-            // one cluster-scope release per stage instead of one per generator warp
-            uint32_t s = 0, ph = 0;
-            for (uint32_t t = 0;; t++) {
-                const int u = next_unit(t, true);
-                if (u < 0) break;
-                int b, nt;
-                int64_t t0, t1;
-                unit_coords<F32>(p, u, b, nt, t0, t1);
-                for (int64_t tb = t0; tb < t1; tb += C::BK) {
-                    mbar_wait(gdone_bar(s), ph);
-                    mbar_arrive_cluster(to_leader(full_bar(s)));
-                    if (++s == STAGES) {
-                        s = 0;
-                        ph ^= 1;
-                    }
-                }
             }
         }
     } else if (warp >= 4 && warp < 8) {
@@ -472,7 +456,8 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive(leader ? full_bar(s) : gdone_bar(s));
+                    if (leader) mbar_arrive(full_bar(s));
+                    else mbar_arrive_remote(to_leader(full_bar(s)));
                     mbar_arrive(txempty_bar(x));
                 }
             }
