@@ -393,14 +393,22 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
         }
     } else if (warp >= 8) {
         // ================= hypothesis generators (H tile, MN-major, swizzled) =================
-        // A quarter-warp (8 lanes) builds one trace row: lane = 16-key chunk, so
-        // the V-row reads and the swizzled A-row writes are both bank-conflict
-        // free.  Warp g owns rows g*(BK/16) ... of the stage.
+        // A quarter-warp (8 lanes) builds one trace row of one key byte: lane =
+        // 16-key chunk, so the V-row reads and the swizzled A-row writes are both
+        // bank-conflict free.  Warp g owns rows g*ROWS .. g*ROWS+ROWS-1 of every
+        // stage.  Per (row, key byte) the XOR permutation of V[c_s] by c_b is
+        // reduced once (lanes 0..ROWS*KB-1) to a descriptor {V address with the
+        // 8-byte-half swap folded in, PRMT selector} and broadcast with a shuffle,
+        // so one 16-key chunk costs SHFL + LOP + 2 LDS.64 + 4 PRMT + STS.128.
+        // Rows past the end of the data get (valid) stale-text hypotheses: their
+        // W rows are TMA zero fill, so they add nothing.
         const int g = warp - 8;
         const int ql = lane & 7;           // chunk within the 128-key row
         const int sub = lane >> 3;         // row within a group of 4
         const uint8_t *vs = smem + SMEM_V;
-        constexpr int PASSES = C::BK / (4 * GEN_WARPS);
+        constexpr int ROWS = C::BK / GEN_WARPS;
+        constexpr int PASSES = ROWS / 4;
+        static_assert(ROWS * C::KB <= 32 && ROWS % 4 == 0, "descriptor lanes");
         uint32_t it = 0;
         for (uint32_t t = 0;; t++) {
             const int u = next_unit(t, false);
@@ -408,36 +416,40 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             int b, nt;
             int64_t t0, t1;
             unit_coords<F32>(p, u, b, nt, t0, t1);
-            const uint32_t gchunk = rank * 8 + ql;  // global 16-key chunk (keys 128*rank ...)
+            // this lane's descriptor slot: row ROWS*g + lane%ROWS, key byte b + lane/ROWS
+            const int drow = ROWS * g + lane % ROWS, dkb = lane / ROWS;
+            const int dsrc = shiftrows_src(b + dkb);
             for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
                 const int s = it % STAGES;
                 const uint32_t ph = (it / STAGES) & 1;
                 const int x = it % TX_STAGES;
-                const int nrows = (int)((t1 - tb) < C::BK ? (t1 - tb) : C::BK);
                 mbar_wait(txfull_bar(x), (it / TX_STAGES) & 1);
-                mbar_wait(empty_bar(s), ph ^ 1);  // A slot free
                 const uint8_t *tx = smem + SMEM_TX + x * TX_BYTES;
+                uint32_t desc = 0;
+                if (lane < ROWS * C::KB) {
+                    const uint32_t cb = tx[drow * 16 + b + dkb], cs = tx[drow * 16 + dsrc];
+                    const uint32_t hi = cb >> 4, lo = cb & 15, u4 = lo >> 2, v4 = lo & 3;
+                    const uint32_t sel_e = (0x3210u ^ (v4 * 0x1111u)) ^ ((u4 & 1) ? 0x4444u : 0u);
+                    desc = (cs * 256 + (((rank * 8) ^ hi) << 4) + ((u4 & 2) ? 8u : 0u)) | (sel_e << 16);
+                }
+                mbar_wait(empty_bar(s), ph ^ 1);  // A slot free
 #pragma unroll
                 for (int kb = 0; kb < C::KB; kb++)  // the unit's key bytes b, b+1, ...
 #pragma unroll
                 for (int pass = 0; pass < ((XT_EXP & 2) ? 0 : PASSES); pass++) {
                     uint8_t *abase = smem + SMEM_STAGE + s * STAGE_BYTES + kb * C::A_BYTES;
-                    const int row = (PASSES * 4) * g + 4 * pass + sub;
-                    uint4 outv = make_uint4(0, 0, 0, 0);
-                    if (row < nrows) {
-                        const uint32_t cb = tx[row * 16 + b + kb], cs = tx[row * 16 + shiftrows_src(b + kb)];
-                        const uint32_t hi = cb >> 4, lo = cb & 15, u4 = lo >> 2, v4 = lo & 3;
-                        const uint32_t sel_e = (0x3210u ^ (v4 * 0x1111u)) ^ ((u4 & 1) ? 0x4444u : 0u);
-                        const uint32_t sel_o = sel_e ^ 0x4444u;
-                        const bool swap2 = (u4 & 2) != 0;
-                        const uint4 a = *(const uint4 *)(vs + cs * 256 + ((gchunk ^ hi) << 4));
-                        const uint32_t c0 = swap2 ? a.z : a.x, c1 = swap2 ? a.w : a.y;
-                        const uint32_t c2 = swap2 ? a.x : a.z, c3 = swap2 ? a.y : a.w;
-                        outv.x = __byte_perm(c0, c1, sel_e);
-                        outv.y = __byte_perm(c0, c1, sel_o);
-                        outv.z = __byte_perm(c2, c3, sel_e);
-                        outv.w = __byte_perm(c2, c3, sel_o);
-                    }
+                    const int rl = 4 * pass + sub;
+                    const int row = ROWS * g + rl;
+                    const uint32_t d = __shfl_sync(0xffffffffu, desc, kb * ROWS + rl);
+                    const uint32_t a0 = (d & 0xffffu) ^ ((uint32_t)ql << 4);
+                    const uint2 h0 = *(const uint2 *)(vs + a0);
+                    const uint2 h1 = *(const uint2 *)(vs + (a0 ^ 8u));
+                    const uint32_t sel_e = d >> 16, sel_o = sel_e ^ 0x4444u;
+                    uint4 outv;
+                    outv.x = __byte_perm(h0.x, h0.y, sel_e);
+                    outv.y = __byte_perm(h0.x, h0.y, sel_o);
+                    outv.z = __byte_perm(h1.x, h1.y, sel_e);
+                    outv.w = __byte_perm(h1.x, h1.y, sel_o);
                     if (!F32) {
                         *(uint4 *)(abase + row * 128 + ((ql ^ (row & 7)) << 4)) = outv;  // 128B swizzle
                     } else {
