@@ -43,10 +43,21 @@
 //   bit 0: W loads re-read the first 8192 traces (L2-resident W)
 //   bit 1: generators skip the H generation (barrier traffic only)
 //   bit 2: the epilogue skips its global atomics (TMEM reads only)
-//   bit 3: the MMA issuer does not wait for the stage data (pure issue rate)
 //   bit 4: no W loads (the leader's producer arrives without tx bytes)
 #ifndef XT_EXP
 #define XT_EXP 0
+#endif
+#ifndef XT_A_STAGES_I8
+#define XT_A_STAGES_I8 3
+#endif
+#ifndef XT_B_STAGES_I8
+#define XT_B_STAGES_I8 3
+#endif
+#ifndef XT_A_STAGES_F32
+#define XT_A_STAGES_F32 3
+#endif
+#ifndef XT_B_STAGES_F32
+#define XT_B_STAGES_F32 3
 #endif
 
 namespace cpa {
@@ -66,15 +77,18 @@ struct Cfg {
     static constexpr int BH_BYTES = BK * 128 * ESZ; // one CTA's half (128 samples) of one N tile, one operand
     static constexpr int A_BYTES = BK * 128 * ESZ;  // 128 keys x BK traces
     static constexpr int A_ATOM = BK * 128;         // bytes between 128-byte MN groups (A and B)
+    static constexpr int A_STAGE = KB * A_BYTES;    // generated H tiles of one stage
+    static constexpr int B_STAGE = NT * NB * BH_BYTES;  // TMA-loaded W tiles of one stage
+    // separate rings: W (TMA, long latency) runs deeper than H (generated on chip)
+    static constexpr int A_STAGES = F32 ? XT_A_STAGES_F32 : XT_A_STAGES_I8;
+    static constexpr int B_STAGES = F32 ? XT_B_STAGES_F32 : XT_B_STAGES_I8;
 };
 
 constexpr int BMC = 128;          // sub-keys per CTA (pair MMA M = 256)
 constexpr int BN = 256;           // samples per accumulator (MMA N)
-constexpr int STAGES = 3;
 constexpr int PREFETCH_STAGES = 8;  // W boxes are prefetched into L2 this many stages ahead
 constexpr int TX_STAGES = 6;      // ciphertext ring, prefetched ahead of the stages
 constexpr int SCHED_Q = 4;        // depth of the unit-id ring
-constexpr int STAGE_BYTES = 49152;
 constexpr int V_BYTES = 65536;
 constexpr int TX_BYTES = 128 * 16;            // ciphertext rows of one stage (max BK)
 constexpr int EPI_WARPS = 4;
@@ -86,21 +100,26 @@ constexpr int GEN_WARPS = 16;                 // every generator warp works on e
 constexpr int RING_CONSUMERS = 2 * (2 + EPI_WARPS + GEN_WARPS);
 constexpr int TB_LD = 9;                      // epilogue transpose row stride (words, odd)
 constexpr int TB_BYTES = EPI_WARPS * 32 * TB_LD * 4;
+constexpr int MAX_RING = 8;                   // barrier slots reserved per ring
 constexpr int SMEM_V = 0;
-constexpr int SMEM_STAGE = SMEM_V + V_BYTES;
-constexpr int SMEM_TX = SMEM_STAGE + STAGES * STAGE_BYTES;
+constexpr int SMEM_A = SMEM_V + V_BYTES;      // A ring, then the B ring (per-config sizes)
+constexpr int RINGS_BYTES = 147456;           // A_STAGES*A_STAGE + B_STAGES*B_STAGE <= this
+constexpr int SMEM_TX = SMEM_A + RINGS_BYTES;
 constexpr int SMEM_TB = SMEM_TX + TX_STAGES * TX_BYTES;
 constexpr int SMEM_BAR = SMEM_TB + TB_BYTES;
-constexpr int NUM_BARS = 2 * STAGES + 2 * TX_STAGES + 4 + 2 * SCHED_Q;
+constexpr int NUM_BARS = 4 * MAX_RING + 2 * TX_STAGES + 4 + 2 * SCHED_Q;
 constexpr int SMEM_SCHED = SMEM_BAR + NUM_BARS * 8;
 constexpr int SMEM_TOTAL = SMEM_SCHED + SCHED_Q * 4 + 16;
 constexpr int SMEM_ALLOC = SMEM_TOTAL;
 constexpr int THREADS = 32 * (8 + GEN_WARPS);
 constexpr uint32_t TMEM_COLS = 512;
 template <bool F32>
-__host__ __device__ constexpr int b_offset() { return Cfg<F32>::KB * Cfg<F32>::A_BYTES; }  // W tiles follow the A tiles
-static_assert(b_offset<false>() + Cfg<false>::NT * Cfg<false>::NB * Cfg<false>::BH_BYTES == STAGE_BYTES, "");
-static_assert(b_offset<true>() + Cfg<true>::NT * Cfg<true>::NB * Cfg<true>::BH_BYTES == STAGE_BYTES, "");
+__host__ __device__ constexpr int smem_b() { return SMEM_A + Cfg<F32>::A_STAGES * Cfg<F32>::A_STAGE; }
+static_assert(Cfg<false>::A_STAGES * Cfg<false>::A_STAGE + Cfg<false>::B_STAGES * Cfg<false>::B_STAGE <= RINGS_BYTES, "");
+static_assert(Cfg<true>::A_STAGES * Cfg<true>::A_STAGE + Cfg<true>::B_STAGES * Cfg<true>::B_STAGE <= RINGS_BYTES, "");
+static_assert(Cfg<false>::A_STAGES <= MAX_RING && Cfg<false>::B_STAGES <= MAX_RING, "");
+static_assert(Cfg<true>::A_STAGES <= MAX_RING && Cfg<true>::B_STAGES <= MAX_RING, "");
+static_assert(SMEM_ALLOC <= 232448, "shared memory");
 static_assert(Cfg<false>::NACC * Cfg<false>::NBUF * BN == TMEM_COLS, "");
 static_assert(Cfg<true>::NACC * Cfg<true>::NBUF * BN == TMEM_COLS, "");
 
@@ -159,11 +178,14 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
     const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the pair's MMAs)
     const bool leader = rank == 0;
 
-    auto full_bar = [&](int s) { return sbase + SMEM_BAR + 8 * s; };                 // leader's is used
-    auto empty_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (STAGES + s); };     // both CTAs
-    auto txfull_bar = [&](int x) { return sbase + SMEM_BAR + 8 * (2 * STAGES + x); };
-    auto txempty_bar = [&](int x) { return sbase + SMEM_BAR + 8 * (2 * STAGES + TX_STAGES + x); };
-    constexpr int BAR_T = 2 * STAGES + 2 * TX_STAGES, BAR_S = BAR_T + 4;
+    constexpr int AS = C::A_STAGES, BS = C::B_STAGES;
+    auto afull_bar = [&](int s) { return sbase + SMEM_BAR + 8 * s; };                  // leader's is used
+    auto aempty_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (MAX_RING + s); };    // both CTAs
+    auto bfull_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (2 * MAX_RING + s); }; // leader's is used
+    auto bempty_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (3 * MAX_RING + s); };// both CTAs
+    auto txfull_bar = [&](int x) { return sbase + SMEM_BAR + 8 * (4 * MAX_RING + x); };
+    auto txempty_bar = [&](int x) { return sbase + SMEM_BAR + 8 * (4 * MAX_RING + TX_STAGES + x); };
+    constexpr int BAR_T = 4 * MAX_RING + 2 * TX_STAGES, BAR_S = BAR_T + 4;
     auto tfull_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + a); };      // both (multicast)
     auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + 2 + a); }; // leader's
     auto sfull_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + q); };        // both CTAs
@@ -192,10 +214,13 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmap_b0);
         if (F32) tma_prefetch(&tmap_b1);
-        for (int s = 0; s < STAGES; s++) {
-            // leader's W producer (arrive + tx of both CTAs) + both CTAs' generator warps
-            mbar_init(full_bar(s), 1 + 2 * GEN_WARPS);
-            mbar_init(empty_bar(s), 1);       // multicast tcgen05.commit
+        for (int s = 0; s < AS; s++) {
+            mbar_init(afull_bar(s), 2 * GEN_WARPS);  // both CTAs' generator warps
+            mbar_init(aempty_bar(s), 1);             // multicast tcgen05.commit
+        }
+        for (int s = 0; s < BS; s++) {
+            mbar_init(bfull_bar(s), 1);   // leader's W producer: arrive + tx of both CTAs' loads
+            mbar_init(bempty_bar(s), 1);  // multicast tcgen05.commit
         }
         for (int x = 0; x < TX_STAGES; x++) {
             mbar_init(txfull_bar(x), 1);            // ciphertext rows landed
@@ -243,18 +268,18 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 unit_coords<F32>(p, u, b, nt, t0, t1);
                 const int x0 = nt * (C::NT * BN) + (int)rank * (BN / 2);  // this CTA's half of N tile 0
                 for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
-                    const int s = it % STAGES;
-                    mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
+                    const int s = it % BS;
+                    mbar_wait(bempty_bar(s), ((it / BS) & 1) ^ 1);
                     // the leader's arrival carries the tx bytes of BOTH CTAs' loads; the
                     // peer's loads only complete tx on it (they cannot land in an earlier
                     // phase: the peer waited for this slot's commit, which follows it)
-                    const uint32_t lbar = to_leader(full_bar(s));
+                    const uint32_t lbar = to_leader(bfull_bar(s));
                     if (XT_EXP & 16) {
-                        if (leader) mbar_arrive(full_bar(s));
+                        if (leader) mbar_arrive(bfull_bar(s));
                         continue;
                     }
-                    if (leader) mbar_arrive_expect_tx(full_bar(s), 2 * (STAGE_BYTES - b_offset<F32>()));
-                    uint32_t bdst = sbase + SMEM_STAGE + s * STAGE_BYTES + b_offset<F32>();
+                    if (leader) mbar_arrive_expect_tx(bfull_bar(s), 2 * C::B_STAGE);
+                    uint32_t bdst = sbase + smem_b<F32>() + s * C::B_STAGE;
 #pragma unroll
                     for (int n = 0; n < C::NT; n++)
 #pragma unroll
@@ -299,8 +324,9 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             // Lean issue loop: descriptors are precomputed and advanced by adding
             // 16-byte units to their start-address field; the full barrier is waited
             // on at CTA scope (tools/pair_bench: 65% -> 100% of the pair MMA rate).
-            const uint64_t desc0 = smem_desc_sw128(sbase + SMEM_STAGE, C::A_ATOM, 1024);
-            uint32_t s = 0, ph = 0;
+            const uint64_t adesc0 = smem_desc_sw128(sbase + SMEM_A, C::A_ATOM, 1024);
+            const uint64_t bdesc0 = smem_desc_sw128(sbase + smem_b<F32>(), C::A_ATOM, 1024);
+            uint32_t sa = 0, pa = 0, sb = 0, pb = 0;
             for (uint32_t t = 0;; t++) {
                 const int u = next_unit(t, true);
                 if (u < 0) break;
@@ -313,13 +339,16 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 const uint32_t dbase = tmem_base + acc * (C::NACC * BN);
                 uint32_t accum = 0;
                 for (int64_t tb = t0; tb < t1; tb += C::BK) {
-                    if (!(XT_EXP & 8)) mbar_wait(full_bar(s), ph);
+                    mbar_wait(bfull_bar(sb), pb);
+                    mbar_wait(afull_bar(sa), pa);
                     tc_fence_after();
-                    const uint64_t ad = desc0 + (uint64_t)((s * STAGE_BYTES) >> 4);
+                    const uint64_t ad = adesc0 + (uint64_t)((sa * C::A_STAGE) >> 4);
+                    const uint64_t bdd = bdesc0 + (uint64_t)((sb * C::B_STAGE) >> 4);
 #pragma unroll
                     for (int kk = 0; kk < C::BK / C::KMMA; kk++) {
                         // K step = KMMA rows of 128 bytes in every MN atom
                         const uint64_t adk = ad + (uint64_t)((kk * C::KMMA * 128) >> 4);
+                        const uint64_t bdk = bdd + (uint64_t)((kk * C::KMMA * 128) >> 4);
 #pragma unroll
                         for (int n = 0; n < C::NT; n++)
 #pragma unroll
@@ -327,18 +356,22 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
 #pragma unroll
                                 for (int op = 0; op < C::NB; op++) {
                                     const uint64_t a = adk + (uint64_t)((kb * C::A_BYTES) >> 4);
-                                    const uint64_t bd =
-                                        adk + (uint64_t)((b_offset<F32>() + (n * C::NB + op) * C::BH_BYTES) >> 4);
+                                    const uint64_t bd = bdk + (uint64_t)(((n * C::NB + op) * C::BH_BYTES) >> 4);
                                     const uint32_t d = dbase + (kb * C::NT + n) * BN;
                                     if (F32) mma_bf16_pair(d, a, bd, p.idesc, op == 0 ? accum : 1u);
                                     else mma_i8_pair(d, a, bd, p.idesc, accum);
                                 }
                         accum = 1;
                     }
-                    mma_commit_pair(empty_bar(s), 0x3);  // frees the stage in both CTAs when done
-                    if (++s == STAGES) {
-                        s = 0;
-                        ph ^= 1;
+                    mma_commit_pair(aempty_bar(sa), 0x3);  // frees the slots in both CTAs when done
+                    mma_commit_pair(bempty_bar(sb), 0x3);
+                    if (++sa == AS) {
+                        sa = 0;
+                        pa ^= 1;
+                    }
+                    if (++sb == BS) {
+                        sb = 0;
+                        pb ^= 1;
                     }
                 }
                 mma_commit_pair(tfull_bar(acc), 0x3);    // accumulators ready for both epilogues
@@ -420,8 +453,8 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             const int drow = ROWS * g + lane % ROWS, dkb = lane / ROWS;
             const int dsrc = shiftrows_src(b + dkb);
             for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
-                const int s = it % STAGES;
-                const uint32_t ph = (it / STAGES) & 1;
+                const int s = it % AS;
+                const uint32_t ph = (it / AS) & 1;
                 const int x = it % TX_STAGES;
                 mbar_wait(txfull_bar(x), (it / TX_STAGES) & 1);
                 const uint8_t *tx = smem + SMEM_TX + x * TX_BYTES;
@@ -432,12 +465,12 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     const uint32_t sel_e = (0x3210u ^ (v4 * 0x1111u)) ^ ((u4 & 1) ? 0x4444u : 0u);
                     desc = (cs * 256 + (((rank * 8) ^ hi) << 4) + ((u4 & 2) ? 8u : 0u)) | (sel_e << 16);
                 }
-                mbar_wait(empty_bar(s), ph ^ 1);  // A slot free
+                mbar_wait(aempty_bar(s), ph ^ 1);  // A slot free
 #pragma unroll
                 for (int kb = 0; kb < C::KB; kb++)  // the unit's key bytes b, b+1, ...
 #pragma unroll
                 for (int pass = 0; pass < ((XT_EXP & 2) ? 0 : PASSES); pass++) {
-                    uint8_t *abase = smem + SMEM_STAGE + s * STAGE_BYTES + kb * C::A_BYTES;
+                    uint8_t *abase = smem + SMEM_A + s * C::A_STAGE + kb * C::A_BYTES;
                     const int rl = 4 * pass + sub;
                     const int row = ROWS * g + rl;
                     const uint32_t d = __shfl_sync(0xffffffffu, desc, kb * ROWS + rl);
@@ -468,8 +501,8 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    if (leader) mbar_arrive(full_bar(s));
-                    else mbar_arrive_remote(to_leader(full_bar(s)));
+                    if (leader) mbar_arrive(afull_bar(s));
+                    else mbar_arrive_remote(to_leader(afull_bar(s)));
                     mbar_arrive(txempty_bar(x));
                 }
             }

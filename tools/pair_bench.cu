@@ -54,8 +54,7 @@ k_pair(int stages_total, int nt, int n_mma, int kk_per_stage, int mode, uint32_t
                 // precomputed descriptors: one 64-bit add per MMA (start address in 16-byte units)
                 const uint64_t a0 = smem_desc_sw128(sb, 16384, 1024) + (uint64_t)((s * STAGE_BYTES) >> 4);
                 const uint64_t b0 = a0 + (16384 >> 4);
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
+                for (int k = 0; k < kk_per_stage; k++) {
                     mma_i8_pair(tm, a0 + k * 256, b0 + k * 256, idesc, 1);
                     mma_i8_pair(tm + 256, a0 + k * 256, b0 + 1024 + k * 256, idesc, 1);
                 }
@@ -107,7 +106,7 @@ int main()
     // never wait; 2: no commits until the end
     // 3: no commits, one stage buffer; 4: no commits, two stage buffers
     // 5: precomputed descriptors, no commits; 6: precomputed + commit/wait ring (CTA-scope wait)
-    V vs[] = {{2, 256, 4, 2}, {2, 256, 4, 5}, {2, 256, 4, 6}, {2, 256, 4, 0}, {2, 256, 4, 5}, {2, 256, 4, 6}};
+    V vs[] = {{2, 256, 4, 6}, {2, 256, 2, 6}, {2, 256, 1, 6}, {2, 256, 4, 6}, {2, 256, 2, 6}};
     const int stages_total = 20000;
     for (auto &v : vs) {
         const uint32_t idesc = idesc_i8(256, v.n, true);
