@@ -51,13 +51,13 @@
 #define XT_A_STAGES_I8 3
 #endif
 #ifndef XT_B_STAGES_I8
-#define XT_B_STAGES_I8 3
+#define XT_B_STAGES_I8 5
 #endif
 #ifndef XT_A_STAGES_F32
 #define XT_A_STAGES_F32 3
 #endif
 #ifndef XT_B_STAGES_F32
-#define XT_B_STAGES_F32 3
+#define XT_B_STAGES_F32 4
 #endif
 
 namespace cpa {
@@ -89,7 +89,9 @@ constexpr int BN = 256;           // samples per accumulator (MMA N)
 constexpr int PREFETCH_STAGES = 8;  // W boxes are prefetched into L2 this many stages ahead
 constexpr int TX_STAGES = 6;      // ciphertext ring, prefetched ahead of the stages
 constexpr int SCHED_Q = 4;        // depth of the unit-id ring
-constexpr int V_BYTES = 65536;
+// V[y][x] = HW(InvS[x] ^ y) is 0..8: stored as nibbles, V[y][2i] | V[y][2i+1] << 4
+// (32 KB; the freed 32 KB deepens the W ring)
+constexpr int V_BYTES = 32768;
 constexpr int TX_BYTES = 128 * 16;            // ciphertext rows of one stage (max BK)
 constexpr int EPI_WARPS = 4;
 constexpr int GEN_WARPS = 16;                 // every generator warp works on every stage, so
@@ -103,7 +105,7 @@ constexpr int TB_BYTES = EPI_WARPS * 32 * TB_LD * 4;
 constexpr int MAX_RING = 8;                   // barrier slots reserved per ring
 constexpr int SMEM_V = 0;
 constexpr int SMEM_A = SMEM_V + V_BYTES;      // A ring, then the B ring (per-config sizes)
-constexpr int RINGS_BYTES = 147456;           // A_STAGES*A_STAGE + B_STAGES*B_STAGE <= this
+constexpr int RINGS_BYTES = 180224;           // A_STAGES*A_STAGE + B_STAGES*B_STAGE <= this
 constexpr int SMEM_TX = SMEM_A + RINGS_BYTES;
 constexpr int SMEM_TB = SMEM_TX + TX_STAGES * TX_BYTES;
 constexpr int SMEM_BAR = SMEM_TB + TB_BYTES;
@@ -207,9 +209,17 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
 
     // ---- setup: V table to smem, barriers, TMEM (pair allocation) ----
     {
+        // pack the 64 KB byte table into nibbles: 16 bytes in -> 8 bytes out
         const uint4 *src = (const uint4 *)p.vtab;
-        uint4 *dst = (uint4 *)(smem + SMEM_V);
-        for (int i = threadIdx.x; i < V_BYTES / 16; i += THREADS) dst[i] = src[i];
+        uint2 *dst = (uint2 *)(smem + SMEM_V);
+        for (int i = threadIdx.x; i < V_BYTES / 8; i += THREADS) {
+            const uint4 v = src[i];
+            auto pack = [](uint32_t a, uint32_t b) {  // 8 bytes (values < 16) -> 8 nibbles
+                const uint32_t e = __byte_perm(a, b, 0x6420), o = __byte_perm(a, b, 0x7531);
+                return e | (o << 4);
+            };
+            dst[i] = make_uint2(pack(v.x, v.y), pack(v.z, v.w));
+        }
     }
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmap_b0);
@@ -427,12 +437,13 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
     } else if (warp >= 8) {
         // ================= hypothesis generators (H tile, MN-major, swizzled) =================
         // A quarter-warp (8 lanes) builds one trace row of one key byte: lane =
-        // 16-key chunk, so the V-row reads and the swizzled A-row writes are both
-        // bank-conflict free.  Warp g owns rows g*ROWS .. g*ROWS+ROWS-1 of every
-        // stage.  Per (row, key byte) the XOR permutation of V[c_s] by c_b is
-        // reduced once (lanes 0..ROWS*KB-1) to a descriptor {V address with the
-        // 8-byte-half swap folded in, PRMT selector} and broadcast with a shuffle,
-        // so one 16-key chunk costs SHFL + LOP + 2 LDS.64 + 4 PRMT + STS.128.
+        // 16-key chunk.  Warp g owns rows g*ROWS .. g*ROWS+ROWS-1 of every stage.
+        // Keys 16c .. 16c+15 need V[c_s][(16c + j) ^ c_b], j = 0..15: the 16
+        // nibbles of packed chunk c ^ (c_b >> 4) in the order j ^ (c_b & 15).
+        // Per (row, key byte) this is reduced once (lanes 0..ROWS*KB-1) to a
+        // descriptor {chunk address with the 8-nibble-half swap (c_b & 8) folded
+        // in, PRMT selector for c_b & 7} and broadcast with a shuffle; one chunk
+        // costs SHFL + LOP + 2 LDS.32 + 6 (nibble split) + 4 PRMT + STS.128.
         // Rows past the end of the data get (valid) stale-text hypotheses: their
         // W rows are TMA zero fill, so they add nothing.
         const int g = warp - 8;
@@ -461,9 +472,17 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 uint32_t desc = 0;
                 if (lane < ROWS * C::KB) {
                     const uint32_t cb = tx[drow * 16 + b + dkb], cs = tx[drow * 16 + dsrc];
-                    const uint32_t hi = cb >> 4, lo = cb & 15, u4 = lo >> 2, v4 = lo & 3;
-                    const uint32_t sel_e = (0x3210u ^ (v4 * 0x1111u)) ^ ((u4 & 1) ? 0x4444u : 0u);
-                    desc = (cs * 256 + (((rank * 8) ^ hi) << 4) + ((u4 & 2) ? 8u : 0u)) | (sel_e << 16);
+                    const uint32_t hi = cb >> 4, lo = cb & 15;
+                    // output byte jj of an even word takes nibble m = jj ^ (lo & 7) of its
+                    // 8-nibble group: even m from the low-nibble word (PRMT 0-3), odd from
+                    // the high-nibble word (PRMT 4-7), byte m >> 1
+                    uint32_t sel_e = 0;
+#pragma unroll
+                    for (int jj = 0; jj < 4; jj++) {
+                        const uint32_t m = (uint32_t)jj ^ (lo & 7);
+                        sel_e |= (((m & 1) << 2) | (m >> 1)) << (4 * jj);
+                    }
+                    desc = (cs * 128 + (((rank * 8) ^ hi) << 3) + ((lo & 8) ? 4u : 0u)) | (sel_e << 16);
                 }
                 mbar_wait(aempty_bar(s), ph ^ 1);  // A slot free
 #pragma unroll
@@ -474,15 +493,17 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     const int rl = 4 * pass + sub;
                     const int row = ROWS * g + rl;
                     const uint32_t d = __shfl_sync(0xffffffffu, desc, kb * ROWS + rl);
-                    const uint32_t a0 = (d & 0xffffu) ^ ((uint32_t)ql << 4);
-                    const uint2 h0 = *(const uint2 *)(vs + a0);
-                    const uint2 h1 = *(const uint2 *)(vs + (a0 ^ 8u));
-                    const uint32_t sel_e = d >> 16, sel_o = sel_e ^ 0x4444u;
+                    const uint32_t a0 = (d & 0xffffu) ^ ((uint32_t)ql << 3);
+                    const uint32_t wa = *(const uint32_t *)(vs + a0);         // nibbles j ^ lo, j < 8
+                    const uint32_t wb = *(const uint32_t *)(vs + (a0 ^ 4u));  // j >= 8
+                    const uint32_t la = wa & 0x0F0F0F0Fu, ha = (wa >> 4) & 0x0F0F0F0Fu;
+                    const uint32_t lb = wb & 0x0F0F0F0Fu, hb = (wb >> 4) & 0x0F0F0F0Fu;
+                    const uint32_t sel_e = d >> 16, sel_o = sel_e ^ 0x2222u;
                     uint4 outv;
-                    outv.x = __byte_perm(h0.x, h0.y, sel_e);
-                    outv.y = __byte_perm(h0.x, h0.y, sel_o);
-                    outv.z = __byte_perm(h1.x, h1.y, sel_e);
-                    outv.w = __byte_perm(h1.x, h1.y, sel_o);
+                    outv.x = __byte_perm(la, ha, sel_e);
+                    outv.y = __byte_perm(la, ha, sel_o);
+                    outv.z = __byte_perm(lb, hb, sel_e);
+                    outv.w = __byte_perm(lb, hb, sel_o);
                     if (!F32) {
                         *(uint4 *)(abase + row * 128 + ((ql ^ (row & 7)) << 4)) = outv;  // 128B swizzle
                     } else {
