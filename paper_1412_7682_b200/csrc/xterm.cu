@@ -86,7 +86,10 @@ struct Cfg {
 
 constexpr int BMC = 128;          // sub-keys per CTA (pair MMA M = 256)
 constexpr int BN = 256;           // samples per accumulator (MMA N)
-constexpr int PREFETCH_STAGES = 8;  // W boxes are prefetched into L2 this many stages ahead
+#ifndef XT_PREFETCH
+#define XT_PREFETCH 0
+#endif
+constexpr int PREFETCH_STAGES = XT_PREFETCH;  // >0: W boxes prefetched into L2 this many stages ahead
 constexpr int TX_STAGES = 6;      // ciphertext ring, prefetched ahead of the stages
 constexpr int SCHED_Q = 4;        // depth of the unit-id ring
 // V[y][x] = HW(InvS[x] ^ y) is 0..8: stored as nibbles, V[y][2i] | V[y][2i+1] << 4
@@ -302,7 +305,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                                 // the load latency (L2 miss -> HBM) exceeds the ring's
                                 // slack: pull the box PREFETCH_STAGES ahead into L2
                                 const int64_t tp = tb + PREFETCH_STAGES * C::BK;
-                                if (tp < t1)
+                                if (PREFETCH_STAGES > 0 && tp < t1)
                                     tma_prefetch_2d(op == 0 ? &tmap_b0 : &tmap_b1, x0 + n * BN + at * C::BOX_X,
                                                     (int32_t)tp);
                             }

@@ -13,7 +13,7 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-KERNELS = ["k_xterm_i8", "k_moments_i8", "k_modelsums", "k_finalize_i8"]
+KERNELS = ["k_xterm", "k_moments_i8", "k_texthist", "k_hist_contract", "k_finalize_i8"]
 METRICS = {
     "duration_ms": ("gpu__time_duration.sum", 1e-3),  # reported in us by default -> ms below
     "dram_read_bytes": ("dram__bytes_read.sum", None),
@@ -114,12 +114,12 @@ def main():
                      f"{g('l2_pct_peak', 1, '{:.1f}')} | {g('registers', 1, '{:.0f}')} |")
     with open(os.path.join(ROOT, "profiles", f"ncu_{tag}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    x = res["kernels"].get("k_xterm_i8")
+    x = res["kernels"].get("k_xterm")
     if x and "dram_read_bytes" in x:
         with open(os.path.join(ROOT, "profiles", "xterm_traffic.json"), "w") as f:
             json.dump({"config": "C4", "n_gpus": 1, "tag": tag,
                        "dram_bytes_per_launch": x["dram_read_bytes"] + x.get("dram_write_bytes", 0.0),
-                       "source": f"ncu --set full capture gpurun_out/k_xterm_i8_{tag}.ncu-rep"}, f, indent=1)
+                       "source": f"ncu --set full capture gpurun_out/k_xterm_{tag}.ncu-rep (profiles/ncu_{tag}.md)"}, f, indent=1)
     print("\n".join(lines))
 
 
