@@ -86,6 +86,9 @@ struct Cfg {
 
 constexpr int BMC = 128;          // sub-keys per CTA (pair MMA M = 256)
 constexpr int BN = 256;           // samples per accumulator (MMA N)
+#ifndef XT_VLDS64
+#define XT_VLDS64 1
+#endif
 #ifndef XT_PREFETCH
 #define XT_PREFETCH 0
 #endif
@@ -496,9 +499,19 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     const int rl = 4 * pass + sub;
                     const int row = ROWS * g + rl;
                     const uint32_t d = __shfl_sync(0xffffffffu, desc, kb * ROWS + rl);
+#if XT_VLDS64
+                    // one LDS.64 per chunk (a quarter-warp reads one 64-byte half row):
+                    // fewer bank conflicts between the quarter-warps than 2 x LDS.32
+                    const uint32_t a0 = (d & 0xfff8u) ^ ((uint32_t)ql << 3);
+                    const uint2 w2 = *(const uint2 *)(vs + a0);
+                    const bool sw = (d & 4u) != 0;
+                    const uint32_t wa = sw ? w2.y : w2.x;  // nibbles j ^ lo, j < 8
+                    const uint32_t wb = sw ? w2.x : w2.y;  // j >= 8
+#else
                     const uint32_t a0 = (d & 0xffffu) ^ ((uint32_t)ql << 3);
                     const uint32_t wa = *(const uint32_t *)(vs + a0);         // nibbles j ^ lo, j < 8
                     const uint32_t wb = *(const uint32_t *)(vs + (a0 ^ 4u));  // j >= 8
+#endif
                     const uint32_t la = wa & 0x0F0F0F0Fu, ha = (wa >> 4) & 0x0F0F0F0Fu;
                     const uint32_t lb = wb & 0x0F0F0F0Fu, hb = (wb >> 4) & 0x0F0F0F0Fu;
                     const uint32_t sel_e = d >> 16, sel_o = sel_e ^ 0x2222u;
