@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-overlap", action="store_true",
                     help="serialise the a4 moments pass with the cross term")
+    ap.add_argument("--chunk", type=int, default=0,
+                    help="stream the traces in chunks of this many, finalizing after every round "
+                         "(key-rank curve); default for C5: 65536")
     return ap.parse_args()
 
 
@@ -198,6 +201,8 @@ def main():
 
     from paper_1412_7682_b200.multigpu import shard_range
     dev = torch.device("cuda", local)
+    if args.chunk or w.name == "C5":
+        return run_stream(args, w, dev, world, rank, local)
     i0, i1 = shard_range(w.n, rank, world)
     n_local = i1 - i0
     # ---- inputs: texts + planted leakage on the host, traces generated on device
@@ -361,6 +366,114 @@ def main():
                     / (xt_ms * 1e-3) / 1e12 / ceil
         print(json.dumps(line), flush=True)
     eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_stream(args, w, dev, world, rank, local):
+    """Streamed workload (BASELINE config C5): global 64K-trace chunks, chunk
+    j*G + r on rank r, and after every round a checkpoint finalize from the
+    (all-reduced) sums so far -> the known-key rank curve.  One step = every
+    chunk + every checkpoint (the last one writes rho)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from synth import synth as S
+    import paper_1412_7682_b200 as P
+    from paper_1412_7682_b200.stream import Curve, StreamingAttack, chunk_rounds
+
+    chunk = args.chunk or 65536
+    rounds = chunk_rounds(w.n, chunk, world)
+    mine = [(i0, i1) for rnd in rounds for r, i0, i1 in rnd if r == rank]
+    n_local = sum(i1 - i0 for i0, i1 in mine)
+    ld = (w.m + 15) // 16 * 16
+    dW = torch.empty((max(n_local, 1), ld), dtype=torch.int8, device=dev)
+    dT = torch.empty((max(n_local, 1), 16), dtype=torch.uint8, device=dev)
+    off = 0
+    for i0, i1 in mine:   # traces generated on the device, chunk by chunk
+        t, lv = S.texts(w, i0, i1 - i0)
+        dT[off:off + i1 - i0].copy_(torch.from_numpy(t))
+        S.dev_traces(w, torch.from_numpy(lv).to(dev), i0, i1 - i0, dW[off:off + i1 - i0], ld)
+        off += i1 - i0
+    torch.cuda.synchronize()
+    rk10 = P.cpa_aes_expand_key(w.key)[10]   # the known round key (library host helper)
+    key_idx = torch.tensor([256 * b + rk10[b] for b in range(16)], device=dev)
+    st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, local)
+    stream = st.eng.stream
+
+    def step(curve=None):
+        st.reset()
+        o = 0
+        for j, rnd in enumerate(rounds):
+            for r, i0, i1 in rnd:
+                if r == rank:
+                    st.add(dW[o:o + i1 - i0, :w.m], dT[o:o + i1 - i0])
+                    o += i1 - i0
+            out = st.checkpoint(want_rho=(j == len(rounds) - 1))
+            ranks = out["rank"][key_idx].tolist()
+            if curve is not None:
+                curve.add(rnd[-1][2], ranks)
+        return out
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    st.eng.set_timing(True)
+    st.eng.phase_times()
+    barrier()
+    launches0 = st.launches
+    curve = Curve()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local, not args.no_clocks) as clk:
+        ev0.record(stream)
+        for s_ in range(args.steps):
+            out = step(curve if s_ == args.steps - 1 else None)
+        ev1.record(stream)
+        barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    launches = st.launches - launches0
+    phase_ms, phase_n = st.eng.phase_times()
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    peaks, src = load_peaks()
+    xt_ms = phase_ms["xterm"] / max(1, phase_n["xterm"])
+    ops = 2.0 * 4096 * n_local * w.m / max(1, phase_n["xterm"] // args.steps)  # per launch (one per chunk)
+    achieved = ops / (xt_ms * 1e-3) / 1e12
+    peak = peaks["bf16_tflops"] * INT8_PER_BF16
+    if rank == 0:
+        line = {
+            "metric": "hypothesis x sample correlations/s at 1.5M traces", "value": 4096 * w.m / (ms_step * 1e-3),
+            "unit": "correlations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "s8", "data": "synthetic",
+            "config": {"workload": f"{w.name}: {w.n} traces x {w.m} samples int8, streamed in {chunk}-trace chunks, "
+                                   f"checkpoint finalize after every round of {world}, HD last-round model",
+                       "n_traces": w.n, "n_samples": w.m, "chunk": chunk, "checkpoints": len(rounds),
+                       "parallelism": f"trace-chunk round-robin x{world}",
+                       "l2": f"inputs {w.n * w.m / 1e9:.0f} GB > 126 MB L2, no flush needed"},
+            "key_recovered": bytes(out["master_key"]) == w.key,
+            "traces_to_key": curve.traces_to_key(),
+            "rank_curve": {"columns": ["traces", "worst_rank", "bytes_at_rank_1"], "points": curve.summary()},
+            "gpu_launches": launches,
+            "phases_ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
+            "roofline": {"kernel": "k_xterm<I8>", "bound": "tensor", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "peak_source": f"{src} bf16_tflops (burst) x {INT8_PER_BF16:g}",
+                         "ms_per_launch": xt_ms, "algorithmic_ops_per_launch": ops},
+            "e2e": None, "cpu_baseline": None,
+        }
+        if not args.no_clocks:
+            line["clocks"] = clk.summary()
+        print(json.dumps(line), flush=True)
+    st.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -9,4 +9,7 @@ def __getattr__(name):
     if name == "Engine":  # torch import deferred until needed
         from .engine import Engine
         return Engine
+    if name == "StreamingAttack":
+        from .stream import StreamingAttack
+        return StreamingAttack
     raise AttributeError(name)

@@ -57,3 +57,11 @@ def allreduce_accumulator(acc, group=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
     return acc
+
+
+def combined_copy(acc, scratch, group=None):
+    """Checkpoint of a running multi-rank accumulation: copy this rank's partial
+    sums into `scratch` and all-reduce the copy, leaving `acc` (the running
+    partials) untouched so later chunks are not double counted."""
+    scratch.copy_(acc)
+    return allreduce_accumulator(scratch, group)

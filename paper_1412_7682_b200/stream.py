@@ -1,0 +1,112 @@
+"""Streamed accumulation with checkpoints -> the key-rank-vs-trace-count curve.
+
+BASELINE config C5 ("1.5M traces x 20,000 samples streamed in 64K-trace chunks
+with key-rank-vs-trace-count curve") and SURVEY §8a row a9 ("known-key rank for
+curves"): traces arrive in chunks; after each round of chunks the attack is
+finalized from the sums so far (Phases 3-4 [P:81-87] on a prefix of the traces)
+and the rank of the known key byte among the 256 guesses is recorded per byte.
+The traces-to-key point is the first checkpoint from which every byte ranks 1.
+
+Multi-GPU [P:230]: global chunk c covers traces [c*chunk, (c+1)*chunk); round j
+gives chunk j*G + r to rank r.  Each rank keeps its own partial sums; a
+checkpoint copies them into a scratch accumulator, all-reduces the copy (one
+NCCL all-reduce, exact for the int path) and finalizes from it, so the running
+partials are never double counted.
+
+Only index bookkeeping and orchestration live here; every sum, rho and rank is
+computed by libcpa through the C ABI."""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+
+def chunk_rounds(n_total: int, chunk: int, world: int = 1) -> list[list[tuple[int, int, int]]]:
+    """Rounds of (rank, i0, i1): global chunk c = [c*chunk, min(n, (c+1)*chunk)),
+    chunk j*world + r goes to rank r in round j.  The last round may leave some
+    ranks without a chunk."""
+    if chunk <= 0 or world <= 0:
+        raise ValueError("chunk and world must be positive")
+    n_chunks = (n_total + chunk - 1) // chunk
+    rounds = []
+    for j in range((n_chunks + world - 1) // world):
+        rnd = []
+        for r in range(world):
+            c = j * world + r
+            if c < n_chunks:
+                rnd.append((r, c * chunk, min(n_total, (c + 1) * chunk)))
+        rounds.append(rnd)
+    return rounds
+
+
+def known_key_ranks(rank_table, key_bytes) -> list[int]:
+    """Rank (1 = best) of the known sub-key of each byte, from the 4096-entry
+    rank table cpa_finalize returns (h = 256*b + k)."""
+    return [int(rank_table[256 * b + int(key_bytes[b])]) for b in range(16)]
+
+
+@dataclass
+class Curve:
+    """(traces so far, rank of the known key byte per byte) at each checkpoint."""
+    points: list[tuple[int, list[int]]] = field(default_factory=list)
+
+    def add(self, n: int, ranks: list[int]):
+        self.points.append((n, list(ranks)))
+
+    def traces_to_key(self) -> int | None:
+        """First checkpoint from which all 16 bytes stay at rank 1 (None if never)."""
+        first = None
+        for n, ranks in self.points:
+            if all(r == 1 for r in ranks):
+                if first is None:
+                    first = n
+            else:
+                first = None
+        return first
+
+    def summary(self) -> list[list[int]]:
+        """[[n, worst rank over the 16 bytes, bytes at rank 1], ...]"""
+        return [[n, max(r), sum(1 for x in r if x == 1)] for n, r in self.points]
+
+
+class StreamingAttack:
+    """Chunked accumulate + checkpoint finalize on one rank of a (possibly
+    multi-GPU) run.  `group` is a torch.distributed group (None = default when
+    initialized; single process otherwise)."""
+
+    def __init__(self, M: int, dtype: int, model: int, device: int = 0, group=None):
+        import torch.distributed as dist
+
+        from .engine import Engine
+        self.group = group
+        self.world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+        self.eng = Engine(M, dtype, model, device)
+        # multi-GPU checkpoints finalize from an all-reduced copy of the partials
+        self.view = Engine(M, dtype, model, device, stream=self.eng.stream) if self.world > 1 else None
+        self.n_local = 0
+
+    def add(self, traces, texts):
+        self.eng.accumulate(traces, texts)
+        self.n_local += traces.shape[0]
+
+    def checkpoint(self, want_rho: bool = False) -> dict:
+        if self.view is None:
+            return self.eng.finalize(want_rho=want_rho)
+        import torch
+
+        from .multigpu import combined_copy
+        with torch.cuda.stream(self.eng.stream):
+            combined_copy(self.eng.accum, self.view.accum, self.group)
+        return self.view.finalize(want_rho=want_rho)
+
+    def reset(self):
+        self.eng.reset()
+        self.n_local = 0
+
+    @property
+    def launches(self) -> int:
+        return self.eng.launches + (self.view.launches if self.view is not None else 0)
+
+    def close(self):
+        if self.view is not None:
+            self.view.close()
+        self.eng.close()
