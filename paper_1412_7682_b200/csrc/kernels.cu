@@ -212,6 +212,7 @@ __device__ __forceinline__ Best warp_best(Best x)
 }
 
 constexpr int FIN_THREADS = 256;
+constexpr int FIN_UNROLL = 4;
 
 __device__ __forceinline__ void block_best_store(Best best, int h, const FinalizeOut &o)
 {
@@ -244,7 +245,31 @@ k_finalize_i8(const int64_t *__restrict__ hw, const int64_t *__restrict__ sw,
     const int64_t *row = hw + (int64_t)h * M;
     double *rrow = o.rho ? o.rho + (int64_t)h * M : nullptr;
     Best best{-1.0, 0.0, 0x7fffffff};
-    for (int j = threadIdx.x; j < M; j += FIN_THREADS) {
+    // HBM-bound: FIN_UNROLL independent row loads in flight per thread before the
+    // (long-latency) fp64 division chains; j ascending per thread keeps the
+    // lowest-j tie rule with a strict '>'
+    constexpr int U = FIN_UNROLL;
+    int j0 = threadIdx.x;
+    for (; j0 + (U - 1) * FIN_THREADS < M; j0 += U * FIN_THREADS) {
+        int64_t v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) v[u] = __ldcs(row + j0 + u * FIN_THREADS);
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int j = j0 + u * FIN_THREADS;
+            const double den_w = sqrt_dw[j];
+            double r = 0.0;
+            if (den_w != 0.0 && den_h != 0.0) {
+                const int64_t num = n * v[u] - s_h * sw[j];
+                r = __ddiv_rn(__ll2double_rn(num), __dmul_rn(den_w, den_h));
+                r = fmin(1.0, fmax(-1.0, r));
+            }
+            if (rrow) __stcs(rrow + j, r);
+            const double a = fabs(r);
+            if (a > best.v) best = Best{a, r, j};
+        }
+    }
+    for (int j = j0; j < M; j += FIN_THREADS) {
         const double den_w = sqrt_dw[j];
         double r = 0.0;
         if (den_w != 0.0 && den_h != 0.0) {
