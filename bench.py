@@ -193,10 +193,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks (tests/test_bench_gpu.py): run a multi-rank bench on ONE GPU with
+    # every rank on cuda:0 over gloo.  Production runs use NCCL, one GPU per rank.
+    if os.environ.get("CPA_BENCH_SAME_DEVICE") == "1":
+        local = 0
+    backend = os.environ.get("CPA_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_1412_7682_b200 as P
 
     from paper_1412_7682_b200.multigpu import shard_range
