@@ -44,12 +44,27 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--combine", choices=["rows", "allreduce"], default="rows",
+                    help="N>1: 'rows' = reduce-scatter of the sum_hw rows + all-reduce of the small "
+                         "fields, row-sharded finalize, gather of the maxima; 'allreduce' = one "
+                         "all-reduce of the whole accumulator, finalize on every rank")
+    ap.add_argument("--shard", choices=["auto", "traces", "samples"], default="auto",
+                    help="N>1: split the traces (partial sums combined per --combine) or the sample "
+                         "columns (every rank all traces of M/G columns; only the per-hypothesis maxima "
+                         "are exchanged).  auto: samples for the wide-trace W48 workload, else traces")
     ap.add_argument("--no-overlap", action="store_true",
                     help="serialise the a4 moments pass with the cross term")
     ap.add_argument("--chunk", type=int, default=0,
                     help="stream the traces in chunks of this many, finalizing after every round "
                          "(key-rank curve); default for C5: 65536")
     return ap.parse_args()
+
+
+def metric_name(w) -> str:
+    """BASELINE.json's metric (quoted at N = 1.5M traces: C4, C5); other
+    configs state their own N."""
+    at = "1.5M" if w.n == 1_500_000 else f"{w.n}"
+    return f"hypothesis x sample correlations/s at {at} traces"
 
 
 def load_peaks():
@@ -167,7 +182,7 @@ def run_reference(args, w):
     t = sum(ts) / len(ts)
     val = 4096 * len(cols) / t
     sample = f"{len(cols)} sample columns x first {n} traces of {w.name}; time x{w.n / n:.2f} to N={w.n}"
-    line = {"metric": "hypothesis x sample correlations/s at 1.5M traces", "impl": "reference", "value": val,
+    line = {"metric": metric_name(w), "impl": "reference", "value": val,
             "unit": "correlations/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "int64", "data": "synthetic",
@@ -207,12 +222,22 @@ def main():
             dist.init_process_group(backend)
     import paper_1412_7682_b200 as P
 
+    from paper_1412_7682_b200 import multigpu as MG
     from paper_1412_7682_b200.multigpu import shard_range
     dev = torch.device("cuda", local)
     if args.chunk or w.name == "C5":
         return run_stream(args, w, dev, world, rank, local)
-    i0, i1 = shard_range(w.n, rank, world)
-    n_local = i1 - i0
+    shard = args.shard if args.shard != "auto" else ("samples" if w.name == "W48" else "traces")
+    if world == 1:
+        shard = "traces"
+    if shard == "samples":      # all traces, this rank's columns [j0, j1) (16-aligned)
+        i0, i1 = 0, w.n
+        j0, j1 = MG.column_range(w.m, rank, world)
+        assert j1 > j0, f"M={w.m} too small for {world} column shards"
+    else:
+        i0, i1 = shard_range(w.n, rank, world)
+        j0, j1 = 0, w.m
+    n_local, m_local = i1 - i0, j1 - j0
     # ---- inputs: texts + planted leakage on the host, traces generated on device
     is_f32 = w.dtype == S.F32
     tdt = torch.float32 if is_f32 else torch.int8
@@ -221,15 +246,19 @@ def main():
     dW = torch.empty((n_local, ld), dtype=tdt, device=dev)
     dT = torch.from_numpy(texts).to(dev)
     S.dev_traces(w, torch.from_numpy(lv).to(dev), i0, n_local, dW, ld)
-    dWv = dW[:, :w.m]
+    dWv = dW[:, j0:j1]
     torch.cuda.synchronize()
 
-    eng = P.Engine(w.m, P.CPA_F32 if is_f32 else P.CPA_S8, P.CPA_HD_LAST, local)
+    eng = P.Engine(m_local, P.CPA_F32 if is_f32 else P.CPA_S8, P.CPA_HD_LAST, local)
+    eng.set_col0(j0)
     if args.no_overlap:
         eng.set_overlap(False)
-    rho = torch.empty((4096, w.m), dtype=torch.float64, device=dev)
+    combine = ("columns" if shard == "samples" else args.combine) if world > 1 else "none"
+    h0, h1 = MG.row_range(rank, world) if combine == "rows" else (0, 4096)
+    rho = torch.empty((h1 - h0, m_local), dtype=torch.float64, device=dev)   # this rank's block of rho
     maxabs = torch.empty(4096, dtype=torch.float64, device=dev)
     argmax = torch.empty(4096, dtype=torch.int32, device=dev)
+    peak = torch.empty(4096, dtype=torch.float64, device=dev)
     rank_t = torch.empty(4096, dtype=torch.int32, device=dev)
     stream = eng.stream
 
@@ -239,7 +268,15 @@ def main():
             eng.accumulate(dWv, dT)
         else:
             eng.accumulate_host(*host)
-        if world > 1:
+        if combine == "rows":   # reduce-scatter rows, sharded Eq. (1), gather maxima, select
+            MG.reduce_scatter_rows(eng.accum, w.m)
+            P.cpa_finalize_rows(eng.ctx, h0, h1, rho, maxabs, argmax, peak)
+            MG.gather_rows(maxabs, argmax, peak, h0, h1)
+            return P.cpa_select(eng.ctx, 1, maxabs, argmax, peak, rank_t)
+        if combine == "columns":    # local Eq. (1) over this rank's columns, gather maxima, merge
+            P.cpa_finalize_rows(eng.ctx, 0, 4096, rho, maxabs, argmax, peak)
+            return P.cpa_select(eng.ctx, world, *MG.gather_shards(maxabs, argmax, peak), rank_t)
+        if combine == "allreduce":
             eng.allreduce()
         return P.cpa_finalize(eng.ctx, rho, maxabs, argmax, rank_t)
 
@@ -277,7 +314,7 @@ def main():
     # ---- roofline of the dominant kernel (cross term, tensor-bound)
     peaks, src = load_peaks()
     xt_ms = phase_ms["xterm"] / max(1, phase_n["xterm"])
-    ops = 2.0 * 4096 * n_local * w.m   # algorithmic: one multiply-add per (h, i, j)
+    ops = 2.0 * 4096 * n_local * m_local   # algorithmic: one multiply-add per (h, i, j)
     achieved = ops / (xt_ms * 1e-3) / 1e12
     ratio = 1.0 if is_f32 else INT8_PER_BF16
     # the burst figure: the measured sustained bf16 one (a power-capped cuBLAS
@@ -302,15 +339,15 @@ def main():
     step_phase_ms = {k: v / args.steps for k, v in phase_ms.items()}
     tot = sum(step_phase_ms.values()) or 1.0
     # HBM-bound kernels: achieved GB/s on their algorithmic bytes
-    hbm = {"moments_GBps": (n_local * w.m) / (step_phase_ms["moments"] * 1e-3) / 1e9 if step_phase_ms["moments"] else None,
-           "finalize_GBps": (4096 * w.m * 16) / (step_phase_ms["finalize"] * 1e-3) / 1e9 if step_phase_ms["finalize"] else None,
+    hbm = {"moments_GBps": (n_local * m_local) / (step_phase_ms["moments"] * 1e-3) / 1e9 if step_phase_ms["moments"] else None,
+           "finalize_GBps": ((h1 - h0) * m_local * 16) / (step_phase_ms["finalize"] * 1e-3) / 1e9 if step_phase_ms["finalize"] else None,
            "hbm_peak_GBps": peaks["hbm_gbs"]}
 
     # ---- end to end through the public API: host (pinned) buffers -> key on host
     e2e = None
     if not args.no_e2e:
         try:
-            hW = torch.empty((n_local, w.m), dtype=tdt, pin_memory=True)
+            hW = torch.empty((n_local, m_local), dtype=tdt, pin_memory=True)
             hW.copy_(dWv)
             hT = torch.from_numpy(texts).pin_memory()
             step((hW, hT))  # warm the staging buffers
@@ -330,7 +367,7 @@ def main():
             else:
                 te = statistics.mean(ts)
             e2e = {"value": 4096 * w.m / te, "unit": "correlations/s",
-                   "h2d_bytes_per_step": n_local * (w.m * hW.element_size() + 16),
+                   "h2d_bytes_per_step": n_local * (m_local * hW.element_size() + 16),
                    "d2h_bytes_per_step": 8 + 32 * 4 + 16 * 8,
                    "ms_per_step": te * 1e3, "time_to_key_s": te, "key_recovered": bytes(r2.master_key) == w.key,
                    "host_buffers": "pinned"}
@@ -344,7 +381,7 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "hypothesis x sample correlations/s at 1.5M traces", "value": value,
+            "metric": metric_name(w), "value": value,
             "unit": "correlations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16x2 (f32 traces, fp32 accum, fp64 sums)" if is_f32 else "s8",
@@ -352,8 +389,10 @@ def main():
             "config": {"workload": f"{w.name}: {w.n} traces x {w.m} samples "
                                    f"{'float32' if is_f32 else 'int8 (s8)'}, HD last-round model, "
                                    f"AES-128 key {w.key.hex()}",
-                       "n_traces": w.n, "n_samples": w.m, "hypotheses": 4096, "parallelism": f"trace-shard x{world}",
-                       "l2": f"inputs {n_local * w.m * dW.element_size() / 1e9:.1f} GB > 126 MB L2, no flush needed",
+                       "n_traces": w.n, "n_samples": w.m, "hypotheses": 4096, "parallelism": (f"{'sample' if shard == 'samples' else 'trace'}-shard x{world}"
+                                       + (f", {combine} combine" if world > 1 else "")),
+                       "l2": f"inputs {n_local * m_local * dW.element_size() / 1e9:.2f} GB per rank > 126 MB L2, "
+                             "no flush needed",
                        "rho_written": True},
             "key_recovered": key_ok, "gpu_launches": launches,
             "phases_ms_per_step": step_phase_ms,
@@ -458,7 +497,7 @@ def run_stream(args, w, dev, world, rank, local):
     peak = peaks["bf16_tflops"] * INT8_PER_BF16
     if rank == 0:
         line = {
-            "metric": "hypothesis x sample correlations/s at 1.5M traces", "value": 4096 * w.m / (ms_step * 1e-3),
+            "metric": metric_name(w), "value": 4096 * w.m / (ms_step * 1e-3),
             "unit": "correlations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "s8", "data": "synthetic",

@@ -135,6 +135,42 @@ typedef struct {
 CPA_API cpa_status cpa_finalize(cpa_ctx *ctx, double *d_rho, double *d_maxabs,
                         int32_t *d_argmax, int32_t *d_rank, cpa_result *res);
 
+/* ---- sharded Phase 3/4 (multi-GPU) ---------------------------
+ * Two ways to split the work of Phase 3 [P:81-83] over G ranks:
+ *  (rows)    trace-sharded accumulation; ONE reduce-scatter of the sum_hw rows
+ *            (rank r receives hypothesis rows [4096 r/G, 4096 (r+1)/G)) plus an
+ *            all-reduce of the small fields (sum_w, sum_w2, sum_h, sum_h2, N);
+ *            each rank runs cpa_finalize_rows on its rows; the per-hypothesis
+ *            maxima are all-gathered and cpa_select(G = 1) ranks them.
+ *  (columns) sample-axis sharding for wide traces: rank r accumulates ALL
+ *            traces over its own sample columns (CPA_OPT_COL0 = its first
+ *            column), so no sums are exchanged; cpa_finalize_rows(0, 4096) on
+ *            every rank, an all-gather of the maxima into [G][4096], then
+ *            cpa_select(G) merges them and ranks.
+ *
+ * cpa_finalize_rows: Eq. (1) [P:69] and max|rho| over this context's samples
+ * (Phase 3) for hypotheses h in [h0, h1) only, from the accumulator (whose
+ * sum_hw rows [h0, h1) and small fields must hold the combined sums).  Blocks
+ * until done.  Same arithmetic as cpa_finalize, bit for bit.
+ *   d_rho     optional [h1-h0][M] double (row h at (h-h0)*M)
+ *   d_maxabs  [4096] double, d_argmax [4096] int32, d_peak [4096] double
+ *             (signed rho at the argmax): only entries h0..h1-1 are written;
+ *             argmax is the GLOBAL sample index (local j + CPA_OPT_COL0).
+ * Errors as cpa_finalize; CPA_E_INVALID_ARG for a bad row range or a NULL
+ * maxabs/argmax/peak.                                                        */
+CPA_API cpa_status cpa_finalize_rows(cpa_ctx *ctx, int32_t h0, int32_t h1, double *d_rho,
+                                     double *d_maxabs, int32_t *d_argmax, double *d_peak);
+
+/* cpa_select: Phase 4 [P:85-87] from per-hypothesis maxima.  Inputs are G
+ * stacked shards, d_maxabs/d_peak [G][4096] double and d_argmax [G][4096]
+ * int32 (global sample indices).  For G > 1 the shards are first merged IN
+ * PLACE into shard 0 (largest max|rho|; ties to the lowest sample index
+ * [S:298]).  Then, as in cpa_finalize: d_rank [4096] (optional) receives the
+ * rank of k within byte b, and res (host, optional) the key, peak samples,
+ * signed peak rho and N (read from this context's accumulator).  Blocks.     */
+CPA_API cpa_status cpa_select(cpa_ctx *ctx, int32_t G, double *d_maxabs, int32_t *d_argmax,
+                              double *d_peak, int32_t *d_rank, cpa_result *res);
+
 /* CPA_F32 only: per-sample offsets o_j (device pointer, M floats; NULL = 0)
  * subtracted from every sample before the bf16 hi/lo split.  rho is invariant
  * to per-sample offsets [S:285]; centring keeps the split and the fp32 tensor-
@@ -158,8 +194,12 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *                   0 = serialise everything on the context's stream.
  *   CPA_OPT_STAGE_BYTES: bytes of trace rows per staging chunk of
  *                   cpa_accumulate_host / unaligned cpa_accumulate
- *                   (0 = default 256 MiB; at least one row per chunk).      */
-enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2, CPA_OPT_OVERLAP = 3, CPA_OPT_STAGE_BYTES = 4 };
+ *                   (0 = default 256 MiB; at least one row per chunk).
+ *   CPA_OPT_COL0:   global index of this context's sample 0 (sample-axis
+ *                   sharding); added to every reported sample index
+ *                   (argmax, peak_sample).  Default 0.                      */
+enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2, CPA_OPT_OVERLAP = 3, CPA_OPT_STAGE_BYTES = 4,
+       CPA_OPT_COL0 = 5 };
 CPA_API cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value);
 
 /* Per-phase device time (ms) and launch count since the last call, from the

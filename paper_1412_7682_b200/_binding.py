@@ -17,7 +17,7 @@ CPA_E_INVALID_ARG, CPA_E_BAD_STATE, CPA_E_CUDA, CPA_E_NO_MEMORY = 1, 2, 3, 4
 CPA_E_TOO_FEW_TRACES, CPA_E_OVERFLOW, CPA_E_UNSUPPORTED_DEVICE, CPA_E_NONFINITE = 5, 6, 7, 8
 CPA_S8, CPA_U8, CPA_F32 = 0, 1, 2
 CPA_HD_LAST, CPA_HW_LAST, CPA_HW_FIRST = 0, 1, 2
-CPA_OPT_KCHUNK, CPA_OPT_TIMING, CPA_OPT_OVERLAP, CPA_OPT_STAGE_BYTES = 1, 2, 3, 4
+CPA_OPT_KCHUNK, CPA_OPT_TIMING, CPA_OPT_OVERLAP, CPA_OPT_STAGE_BYTES, CPA_OPT_COL0 = 1, 2, 3, 4, 5
 CPA_NUM_PHASES = 5
 PHASE_NAMES = ("modelsums", "moments", "xterm", "finalize", "phase4")
 FIELD_HW, FIELD_W, FIELD_W2, FIELD_H, FIELD_H2, FIELD_N = range(6)
@@ -25,7 +25,7 @@ FIELD_HW, FIELD_W, FIELD_W2, FIELD_H, FIELD_H2, FIELD_N = range(6)
 # every symbol include/cpa.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = (
     "cpa_accum_words", "cpa_accum_bytes", "cpa_accum_offset", "cpa_init", "cpa_accumulate",
-    "cpa_accumulate_host", "cpa_finalize", "cpa_reset", "cpa_sync", "cpa_destroy",
+    "cpa_accumulate_host", "cpa_finalize", "cpa_finalize_rows", "cpa_select", "cpa_reset", "cpa_sync", "cpa_destroy",
     "cpa_set_offsets", "cpa_set_option", "cpa_phase_times", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
     "cpa_aes_expand_key", "cpa_aes_invert_key_schedule",
 )
@@ -58,6 +58,8 @@ def _load():
         "cpa_accumulate": (ST, [P, P, I64, P, I64]),
         "cpa_accumulate_host": (ST, [P, P, I64, P, I64]),
         "cpa_finalize": (ST, [P, P, P, P, P, C.POINTER(cpa_result)]),
+        "cpa_finalize_rows": (ST, [P, I32, I32, P, P, P, P]),
+        "cpa_select": (ST, [P, I32, P, P, P, P, C.POINTER(cpa_result)]),
         "cpa_reset": (ST, [P]),
         "cpa_sync": (ST, [P]),
         "cpa_destroy": (ST, [P]),
@@ -128,6 +130,18 @@ def cpa_finalize(ctx, d_rho=None, d_maxabs=None, d_argmax=None, d_rank=None) -> 
     res = cpa_result()
     _check(_lib.cpa_finalize(ctx, _ptr(d_rho), _ptr(d_maxabs), _ptr(d_argmax), _ptr(d_rank),
                              C.byref(res)), "cpa_finalize")
+    return res
+
+
+def cpa_finalize_rows(ctx, h0: int, h1: int, d_rho, d_maxabs, d_argmax, d_peak):
+    _check(_lib.cpa_finalize_rows(ctx, h0, h1, _ptr(d_rho), _ptr(d_maxabs), _ptr(d_argmax), _ptr(d_peak)),
+           "cpa_finalize_rows")
+
+
+def cpa_select(ctx, G: int, d_maxabs, d_argmax, d_peak, d_rank=None) -> cpa_result:
+    res = cpa_result()
+    _check(_lib.cpa_select(ctx, G, _ptr(d_maxabs), _ptr(d_argmax), _ptr(d_peak), _ptr(d_rank), C.byref(res)),
+           "cpa_select")
     return res
 
 

@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdarg>
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -74,6 +75,7 @@ struct cpa_ctx {
     int32_t *d_argmax = nullptr, *d_rank = nullptr, *d_best = nullptr;
     int *d_counter = nullptr;  // work-unit counter of the cross-term scheduler
     int64_t kchunk = 0;
+    int32_t col0 = 0;  // CPA_OPT_COL0: global index of sample 0 (sample-axis sharding)
     int64_t launches = 0;
     // cpa_accumulate_host staging
     void *d_stage[2] = {nullptr, nullptr};
@@ -262,6 +264,12 @@ cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
     }
     if (option == CPA_OPT_OVERLAP) {
         ctx->overlap = value != 0;
+        return CPA_OK;
+    }
+    if (option == CPA_OPT_COL0) {
+        if (value < 0 || value + ctx->M > (int64_t)INT32_MAX)
+            return fail(CPA_E_INVALID_ARG, "COL0=%lld: sample indices must fit int32", (long long)value);
+        ctx->col0 = (int32_t)value;
         return CPA_OK;
     }
     if (option == CPA_OPT_TIMING) {
@@ -508,24 +516,27 @@ cpa_status cpa_accumulate_host(cpa_ctx *c, const void *h_traces, int64_t ld, con
     return CPA_OK;
 }
 
-cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_argmax, int32_t *d_rank,
-                        cpa_result *res)
+// N from the accumulator, with the preconditions of Eq. (1) [P:69]
+static cpa_status read_n(cpa_ctx *c, int64_t *n_out)
 {
-    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
-    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
-    const int M = c->M;
-    int64_t n = 0;
+    const size_t off = cpa_accum_offset(c->M, 5);
     if (c->dtype == CPA_F32) {
         double dn = 0;
-        CUDA_TRY(cudaMemcpyAsync(&dn, (double *)c->accum + cpa_accum_offset(M, 5), 8, cudaMemcpyDeviceToHost, c->stream),
-                 "read N");
+        CUDA_TRY(cudaMemcpyAsync(&dn, (double *)c->accum + off, 8, cudaMemcpyDeviceToHost, c->stream), "read N");
         CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
-        n = (int64_t)dn;
+        *n_out = (int64_t)dn;
     } else {
-        CUDA_TRY(cudaMemcpyAsync(&n, (int64_t *)c->accum + cpa_accum_offset(M, 5), 8, cudaMemcpyDeviceToHost, c->stream),
-                 "read N");
+        CUDA_TRY(cudaMemcpyAsync(n_out, (int64_t *)c->accum + off, 8, cudaMemcpyDeviceToHost, c->stream), "read N");
         CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
     }
+    return CPA_OK;
+}
+
+static cpa_status finalize_checks(cpa_ctx *c, int64_t *n_out)
+{
+    int64_t n = 0;
+    cpa_status st = read_n(c, &n);
+    if (st != CPA_OK) return st;
     if (n < 2) return fail(CPA_E_TOO_FEW_TRACES, "N=%lld < 2: Eq. (1) undefined", (long long)n);
     if (c->dtype == CPA_F32) {
         int bad = 0;
@@ -534,25 +545,29 @@ cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_
     }
     if (c->dtype != CPA_F32 && n > kMaxTraces)
         return fail(CPA_E_OVERFLOW, "N=%lld > 2^23: Eq. (1) intermediates may overflow int64", (long long)n);
-    cpa::FinalizeOut o;
-    o.rho = d_rho;
-    o.maxabs = d_maxabs ? d_maxabs : c->d_maxabs;
-    o.argmax = d_argmax ? d_argmax : c->d_argmax;
-    o.rank = d_rank ? d_rank : c->d_rank;
-    o.peak = c->d_peak;
-    o.best = c->d_best;
-    o.best_rho = c->d_best_rho;
-    int launches = 0;
+    *n_out = n;
+    return CPA_OK;
+}
+
+// a8 for hypothesis rows [o.h0, o.h1)
+static cpa_status phase3(cpa_ctx *c, const cpa::FinalizeOut &o, int *launches)
+{
+    if (o.h1 <= o.h0) return CPA_OK;
     CUDA_TRY(c->timed(3, [&] {
                  return c->dtype == CPA_F32
-                            ? cpa::launch_finalize_f64((const double *)c->accum, M, c->d_sqrt_dw, o, c->stream,
-                                                       &launches)
-                            : cpa::launch_finalize_i8((const int64_t *)c->accum, M, c->d_sqrt_dw, o, c->stream,
-                                                      &launches);
+                            ? cpa::launch_finalize_f64((const double *)c->accum, c->M, c->d_sqrt_dw, o, c->stream,
+                                                       launches)
+                            : cpa::launch_finalize_i8((const int64_t *)c->accum, c->M, c->d_sqrt_dw, o, c->stream,
+                                                      launches);
              }),
              "finalize");
-    CUDA_TRY(c->timed(4, [&] { return cpa::launch_phase4(o, c->stream, &launches); }), "phase4");
-    c->launches += launches;
+    return CPA_OK;
+}
+
+// a9 on o.maxabs/argmax/peak, then the key D2H
+static cpa_status phase4(cpa_ctx *c, const cpa::FinalizeOut &o, int64_t n, int *launches, cpa_result *res)
+{
+    CUDA_TRY(c->timed(4, [&] { return cpa::launch_phase4(o, c->stream, launches); }), "phase4");
     int32_t best[32];
     double brho[16];
     CUDA_TRY(cudaMemcpyAsync(best, c->d_best, sizeof best, cudaMemcpyDeviceToHost, c->stream), "D2H best");
@@ -571,6 +586,78 @@ cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_
         res->n_traces = n;
     }
     return CPA_OK;
+}
+
+static cpa::FinalizeOut outputs(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_argmax, double *d_peak,
+                                int32_t *d_rank)
+{
+    cpa::FinalizeOut o;
+    o.rho = d_rho;
+    o.maxabs = d_maxabs ? d_maxabs : c->d_maxabs;
+    o.argmax = d_argmax ? d_argmax : c->d_argmax;
+    o.peak = d_peak ? d_peak : c->d_peak;
+    o.rank = d_rank ? d_rank : c->d_rank;
+    o.best = c->d_best;
+    o.best_rho = c->d_best_rho;
+    o.col0 = c->col0;
+    return o;
+}
+
+cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_argmax, int32_t *d_rank,
+                        cpa_result *res)
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    int64_t n = 0;
+    cpa_status st = finalize_checks(c, &n);
+    if (st != CPA_OK) return st;
+    cpa::FinalizeOut o = outputs(c, d_rho, d_maxabs, d_argmax, nullptr, d_rank);
+    int launches = 0;
+    st = phase3(c, o, &launches);
+    if (st == CPA_OK) st = phase4(c, o, n, &launches, res);
+    c->launches += launches;
+    return st;
+}
+
+cpa_status cpa_finalize_rows(cpa_ctx *c, int32_t h0, int32_t h1, double *d_rho, double *d_maxabs,
+                             int32_t *d_argmax, double *d_peak)
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    if (h0 < 0 || h1 > 4096 || h0 > h1) return fail(CPA_E_INVALID_ARG, "rows [%d, %d) outside [0, 4096]", h0, h1);
+    if (!d_maxabs || !d_argmax || !d_peak) return fail(CPA_E_INVALID_ARG, "d_maxabs, d_argmax and d_peak are required");
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    int64_t n = 0;
+    cpa_status st = finalize_checks(c, &n);
+    if (st != CPA_OK) return st;
+    cpa::FinalizeOut o = outputs(c, d_rho, d_maxabs, d_argmax, d_peak, nullptr);
+    o.h0 = h0;
+    o.h1 = h1;
+    int launches = 0;
+    st = phase3(c, o, &launches);
+    c->launches += launches;
+    if (st == CPA_OK) CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+    return st;
+}
+
+cpa_status cpa_select(cpa_ctx *c, int32_t G, double *d_maxabs, int32_t *d_argmax, double *d_peak, int32_t *d_rank,
+                      cpa_result *res)
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    if (G < 1 || G > 65536) return fail(CPA_E_INVALID_ARG, "G=%d outside [1, 65536]", G);
+    if (!d_maxabs || !d_argmax || !d_peak) return fail(CPA_E_INVALID_ARG, "d_maxabs, d_argmax and d_peak are required");
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    int64_t n = 0;
+    cpa_status st = read_n(c, &n);
+    if (st != CPA_OK) return st;
+    cpa::FinalizeOut o = outputs(c, nullptr, d_maxabs, d_argmax, d_peak, d_rank);
+    int launches = 0;
+    if (G > 1)
+        CUDA_TRY(c->timed(4, [&] { return cpa::launch_merge_shards(G, d_maxabs, d_argmax, d_peak, c->stream,
+                                                                   &launches); }),
+                 "merge shards");
+    st = phase4(c, o, n, &launches, res);
+    c->launches += launches;
+    return st;
 }
 
 cpa_status cpa_phase_times(cpa_ctx *c, double ms[CPA_NUM_PHASES], int64_t launches[CPA_NUM_PHASES])

@@ -225,7 +225,7 @@ __device__ __forceinline__ void block_best_store(Best best, int h, const Finaliz
         x = warp_best(x);
         if (threadIdx.x == 0) {
             o.maxabs[h] = x.v;
-            o.argmax[h] = x.j;
+            o.argmax[h] = x.j + o.col0;
             o.peak[h] = x.r;
         }
     }
@@ -237,13 +237,13 @@ k_finalize_i8(const int64_t *__restrict__ hw, const int64_t *__restrict__ sw,
               const int64_t *__restrict__ count, const double *__restrict__ sqrt_dw, int32_t M,
               FinalizeOut o)
 {
-    const int h = blockIdx.x;
+    const int h = o.h0 + blockIdx.x;
     const int64_t n = *count;
     const int64_t s_h = sh[h];
     const int64_t dh = n * sh2[h] - s_h * s_h;
     const double den_h = __dsqrt_rn(__ll2double_rn(dh));
     const int64_t *row = hw + (int64_t)h * M;
-    double *rrow = o.rho ? o.rho + (int64_t)h * M : nullptr;
+    double *rrow = o.rho ? o.rho + (int64_t)(h - o.h0) * M : nullptr;
     Best best{-1.0, 0.0, 0x7fffffff};
     // HBM-bound: FIN_UNROLL independent row loads in flight per thread before the
     // (long-latency) fp64 division chains; j ascending per thread keeps the
@@ -302,13 +302,13 @@ k_finalize_f64(const double *__restrict__ hw, const double *__restrict__ sw,
                const double *__restrict__ count, const double *__restrict__ sqrt_dw, int32_t M,
                FinalizeOut o)
 {
-    const int h = blockIdx.x;
+    const int h = o.h0 + blockIdx.x;
     const double n = *count;
     const double s_h = sh[h];
     const double dh = __dsub_rn(__dmul_rn(n, sh2[h]), __dmul_rn(s_h, s_h));
     const double den_h = dh > 0.0 ? __dsqrt_rn(dh) : 0.0;
     const double *row = hw + (int64_t)h * M;
-    double *rrow = o.rho ? o.rho + (int64_t)h * M : nullptr;
+    double *rrow = o.rho ? o.rho + (int64_t)(h - o.h0) * M : nullptr;
     Best best{-1.0, 0.0, 0x7fffffff};
     for (int j = threadIdx.x; j < M; j += FIN_THREADS) {
         const double den_w = sqrt_dw[j];
@@ -346,6 +346,31 @@ __global__ void __launch_bounds__(256) k_phase4(FinalizeOut o)
         o.best[16 + b] = o.argmax[b * 256 + k];
         o.best_rho[b] = o.peak[b * 256 + k];
     }
+}
+
+// ---------------------------------------------------------------------------
+// Phase-3 merge over sample-axis shards: per hypothesis h, the shard with the
+// largest max|rho| wins, ties to the lowest global sample index [S:298] (the
+// shards' argmax already carry their column base).  In place into shard 0.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_merge_shards(int32_t G, double *maxabs, int32_t *argmax, double *peak)
+{
+    const int h = blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= 4096) return;
+    double v = maxabs[h], r = peak[h];
+    int32_t j = argmax[h];
+    for (int g = 1; g < G; g++) {
+        const double v2 = maxabs[(int64_t)g * 4096 + h];
+        const int32_t j2 = argmax[(int64_t)g * 4096 + h];
+        if (v2 > v || (v2 == v && j2 < j)) {
+            v = v2;
+            j = j2;
+            r = peak[(int64_t)g * 4096 + h];
+        }
+    }
+    maxabs[h] = v;
+    argmax[h] = j;
+    peak[h] = r;
 }
 
 // ---------------------------------------------------------------------------
@@ -494,7 +519,7 @@ cudaError_t launch_finalize_i8(const int64_t *d_accum, int32_t M, double *d_sqrt
     const int64_t *sh2 = sh + 4096;
     const int64_t *cnt = sh2 + 4096;
     k_sqrt_dw_i8<<<(M + 255) / 256, 256, 0, s>>>(sw, sw2, cnt, M, d_sqrt_dw);
-    k_finalize_i8<<<4096, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o);
+    k_finalize_i8<<<o.h1 - o.h0, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o);
     if (launches) (*launches) += 2;
     return cudaGetLastError();
 }
@@ -509,8 +534,16 @@ cudaError_t launch_finalize_f64(const double *d_accum, int32_t M, double *d_sqrt
     const double *sh2 = sh + 4096;
     const double *cnt = sh2 + 4096;
     k_sqrt_dw_f64<<<(M + 255) / 256, 256, 0, s>>>(sw, sw2, cnt, M, d_sqrt_dw);
-    k_finalize_f64<<<4096, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o);
+    k_finalize_f64<<<o.h1 - o.h0, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o);
     if (launches) (*launches) += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge_shards(int32_t G, double *maxabs, int32_t *argmax, double *peak, cudaStream_t s,
+                                int *launches)
+{
+    k_merge_shards<<<16, 256, 0, s>>>(G, maxabs, argmax, peak);
+    if (launches) (*launches)++;
     return cudaGetLastError();
 }
 

@@ -48,7 +48,10 @@ cudaError_t launch_repack(const uint8_t *d_src, int64_t rb, uint8_t *d_dst, int6
 
 // a8/a9: Phase 3 + 4 [P:81-87]
 struct FinalizeOut {
-    double *rho;       // optional [4096][M]
+    double *rho;       // optional [h1-h0][M]: row h at (h - h0) * M
+    int32_t h0 = 0;    // hypothesis rows [h0, h1) of this launch
+    int32_t h1 = 4096;
+    int32_t col0 = 0;  // global index of sample 0 (sample-axis sharding); added to argmax
     double *maxabs;    // [4096]
     int32_t *argmax;   // [4096]
     double *peak;      // [4096] signed rho at argmax
@@ -61,5 +64,9 @@ cudaError_t launch_finalize_i8(const int64_t *d_accum, int32_t M, double *d_sqrt
 cudaError_t launch_finalize_f64(const double *d_accum, int32_t M, double *d_sqrt_dw,
                                 const FinalizeOut &o, cudaStream_t s, int *launches);
 cudaError_t launch_phase4(const FinalizeOut &o, cudaStream_t s, int *launches);
+// Phase-3 merge of G shards' per-hypothesis maxima (stacked [G][4096]) into
+// shard 0's slots: max |rho|, ties to the lowest (global) sample index
+cudaError_t launch_merge_shards(int32_t G, double *maxabs, int32_t *argmax, double *peak, cudaStream_t s,
+                                int *launches);
 
 }  // namespace cpa

@@ -65,6 +65,10 @@ class Engine:
     def set_stage_bytes(self, nbytes: int):
         B.cpa_set_option(self.ctx, B.CPA_OPT_STAGE_BYTES, nbytes)
 
+    def set_col0(self, col0: int):
+        """Global index of this context's sample 0 (sample-axis sharding)."""
+        B.cpa_set_option(self.ctx, B.CPA_OPT_COL0, col0)
+
     def set_overlap(self, on: bool = True):
         B.cpa_set_option(self.ctx, B.CPA_OPT_OVERLAP, int(on))
 
@@ -100,6 +104,33 @@ class Engine:
         rank = torch.empty(4096, dtype=torch.int32, device=dev)
         res = B.cpa_finalize(self.ctx, rho, maxabs, argmax, rank)
         return dict(rho=rho, maxabs=maxabs, argmax=argmax, rank=rank,
+                    round_key=bytes(res.round_key), master_key=bytes(res.master_key),
+                    peak_sample=list(res.peak_sample), peak_rho=list(res.peak_rho),
+                    n_traces=res.n_traces)
+
+    def maxima_buffers(self, G: int = 1):
+        """Zeroed per-hypothesis maxima (maxabs, argmax, peak) for G stacked shards."""
+        dev = self.device
+        return (torch.zeros((G, 4096), dtype=torch.float64, device=dev),
+                torch.zeros((G, 4096), dtype=torch.int32, device=dev),
+                torch.zeros((G, 4096), dtype=torch.float64, device=dev))
+
+    def finalize_rows(self, h0: int, h1: int, maxabs, argmax, peak, want_rho: bool = False):
+        """Phase 3 for hypothesis rows [h0, h1) into the [4096] maxima arrays
+        (sharded finalize, include/cpa.h); returns rho [h1-h0][M] or None."""
+        rho = (torch.empty((h1 - h0, self.M), dtype=torch.float64, device=self.device)
+               if want_rho else None)
+        B.cpa_finalize_rows(self.ctx, h0, h1, rho, maxabs, argmax, peak)
+        return rho
+
+    def select(self, maxabs, argmax, peak):
+        """Phase 4 from G stacked shards of maxima ([G][4096]; merged in place
+        into shard 0 when G > 1)."""
+        G = maxabs.shape[0] if maxabs.dim() == 2 else 1
+        rank = torch.empty(4096, dtype=torch.int32, device=self.device)
+        res = B.cpa_select(self.ctx, G, maxabs, argmax, peak, rank)
+        m = (lambda t: t[0] if t.dim() == 2 else t)
+        return dict(maxabs=m(maxabs), argmax=m(argmax), peak=m(peak), rank=rank,
                     round_key=bytes(res.round_key), master_key=bytes(res.master_key),
                     peak_sample=list(res.peak_sample), peak_rho=list(res.peak_rho),
                     n_traces=res.n_traces)

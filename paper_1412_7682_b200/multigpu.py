@@ -59,9 +59,125 @@ def allreduce_accumulator(acc, group=None):
     return acc
 
 
-def combined_copy(acc, scratch, group=None):
-    """Checkpoint of a running multi-rank accumulation: copy this rank's partial
-    sums into `scratch` and all-reduce the copy, leaving `acc` (the running
-    partials) untouched so later chunks are not double counted."""
-    scratch.copy_(acc)
-    return allreduce_accumulator(scratch, group)
+# ---- sharded Phase 3/4 (include/cpa.h "sharded Phase 3/4") -------
+# The engine protocol used below (paper_1412_7682_b200.Engine implements it):
+#   .accum, .M, .maxima_buffers(G), .finalize_rows(h0, h1, mx, am, pk, want_rho),
+#   .select(mx, am, pk)
+# Only index ranges and collectives live here; Eq. (1), the shard merge and the
+# ranking run in the library.
+
+def row_range(rank: int, world: int) -> tuple[int, int]:
+    """Hypothesis rows [h0, h1) whose Phase 3 `rank` computes."""
+    return shard_range(4096, rank, world)
+
+
+def column_range(M: int, rank: int, world: int, align: int = 16) -> tuple[int, int]:
+    """Sample columns [j0, j1) of `rank` for sample-axis sharding: balanced in
+    units of `align` columns so every shard starts 16-byte aligned (the TMA
+    fast path reads an int8 column slice in place).  Empty when
+    M < world * align (callers require M >= world * align)."""
+    units = -(-M // align)
+    u0, u1 = shard_range(units, rank, world)
+    return min(M, u0 * align), min(M, u1 * align)
+
+
+def _world(group):
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def reduce_scatter_rows(acc, M: int, group=None, out=None) -> tuple[int, int]:
+    """Combine trace-sharded partial sums for a row-sharded finalize: ONE
+    reduce-scatter of the sum_hw rows (this rank receives its rows) and an
+    all-reduce of the small fields (sum_w, sum_w2, sum_h, sum_h2, N).  Moves
+    (G-1)/G of sum_hw per rank instead of the all-reduce's 2(G-1)/G.
+    In place by default; with `out` (another packed accumulator) the combined
+    rows and small fields land there and `acc` is left untouched (checkpoints
+    of a running accumulation).  Returns this rank's rows [h0, h1)."""
+    import torch.distributed as dist
+    world, rank = _world(group)
+    dst = acc if out is None else out
+    n_hw = 4096 * M
+    if world == 1:
+        if out is not None:
+            out.copy_(acc)
+        return 0, 4096
+    if out is not None:
+        out[n_hw:].copy_(acc[n_hw:])
+    dist.all_reduce(dst[n_hw:], op=dist.ReduceOp.SUM, group=group)
+    h0, h1 = row_range(rank, world)
+    if 4096 % world == 0:
+        inp = acc[:n_hw]
+        if out is None and dist.get_backend(group) != "nccl":
+            inp = inp.clone()     # NCCL reduce-scatters in place; gloo gets a copy
+        dist.reduce_scatter_tensor(dst[h0 * M:h1 * M], inp, op=dist.ReduceOp.SUM, group=group)
+    else:                         # unequal row blocks: plain all-reduce of the rows
+        if out is not None:
+            out[:n_hw].copy_(acc[:n_hw])
+        dist.all_reduce(dst[:n_hw], op=dist.ReduceOp.SUM, group=group)
+    return h0, h1
+
+
+def _pack_maxima(mx, am, pk):
+    import torch
+    return torch.stack([mx, am.to(torch.float64), pk])   # int32 -> f64 is exact
+
+
+def gather_rows(mx, am, pk, h0: int, h1: int, group=None):
+    """After each rank wrote rows [h0, h1) of the [4096] maxima: one
+    all-reduce(SUM) of the packed rows, zero elsewhere, fills in every row
+    (each entry has exactly one nonzero contributor, so the sum is exact)."""
+    import torch
+    import torch.distributed as dist
+    world, _ = _world(group)
+    if world == 1:
+        return mx, am, pk
+    buf = torch.zeros((3, 4096), dtype=torch.float64, device=mx.device)
+    buf[:, h0:h1] = _pack_maxima(mx[h0:h1], am[h0:h1], pk[h0:h1])
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    mx.copy_(buf[0])
+    am.copy_(buf[1].to(torch.int32))
+    pk.copy_(buf[2])
+    return mx, am, pk
+
+
+def gather_shards(mx, am, pk, group=None):
+    """Sample-axis sharding: all-gather every rank's [4096] maxima into
+    stacked [G][4096] arrays (rank order = column order)."""
+    import torch
+    import torch.distributed as dist
+    world, _ = _world(group)
+    if world == 1:
+        return mx.view(1, -1), am.view(1, -1), pk.view(1, -1)
+    buf = _pack_maxima(mx, am, pk)
+    out = torch.empty((world * buf.shape[0], buf.shape[1]), dtype=buf.dtype, device=buf.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    out = out.view(world, buf.shape[0], buf.shape[1])
+    return (out[:, 0].contiguous(), out[:, 1].to(torch.int32).contiguous(), out[:, 2].contiguous())
+
+
+def finalize_rows_sharded(engine, group=None, want_rho: bool = False) -> dict:
+    """Trace-sharded run, row-sharded finalize: reduce-scatter + all-reduce of
+    the sums, Phase 3 on this rank's hypothesis rows, gather of the maxima,
+    Phase 4.  Every rank returns the same key; rho (if wanted) covers only
+    this rank's rows (`rows`)."""
+    h0, h1 = reduce_scatter_rows(engine.accum, engine.M, group)
+    mx, am, pk = (t[0] for t in engine.maxima_buffers(1))
+    rho = engine.finalize_rows(h0, h1, mx, am, pk, want_rho)
+    gather_rows(mx, am, pk, h0, h1, group)
+    out = engine.select(mx, am, pk)
+    out.update(rows=(h0, h1), rho=rho)
+    return out
+
+
+def finalize_columns_sharded(engine, group=None, want_rho: bool = False) -> dict:
+    """Sample-axis sharded run (engine holds ALL traces over its columns, its
+    CPA_OPT_COL0 set): local Phase 3, all-gather of the maxima, merge + Phase 4."""
+    mx, am, pk = (t[0] for t in engine.maxima_buffers(1))
+    rho = engine.finalize_rows(0, 4096, mx, am, pk, want_rho)
+    out = engine.select(*gather_shards(mx, am, pk, group))
+    out.update(rho=rho)
+    return out
+

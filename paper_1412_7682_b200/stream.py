@@ -9,9 +9,10 @@ The traces-to-key point is the first checkpoint from which every byte ranks 1.
 
 Multi-GPU [P:230]: global chunk c covers traces [c*chunk, (c+1)*chunk); round j
 gives chunk j*G + r to rank r.  Each rank keeps its own partial sums; a
-checkpoint copies them into a scratch accumulator, all-reduces the copy (one
-NCCL all-reduce, exact for the int path) and finalizes from it, so the running
-partials are never double counted.
+checkpoint reduce-scatters them (out of place) into a scratch accumulator, so
+the running partials are never double counted: each rank then finalizes its
+4096/G hypothesis rows, the maxima are gathered and Phase 4 ranks them
+(multigpu.reduce_scatter_rows).
 
 Only index bookkeeping and orchestration live here; every sum, rho and rank is
 computed by libcpa through the C ABI."""
@@ -93,10 +94,15 @@ class StreamingAttack:
             return self.eng.finalize(want_rho=want_rho)
         import torch
 
-        from .multigpu import combined_copy
+        from . import multigpu as MG
         with torch.cuda.stream(self.eng.stream):
-            combined_copy(self.eng.accum, self.view.accum, self.group)
-        return self.view.finalize(want_rho=want_rho)
+            h0, h1 = MG.reduce_scatter_rows(self.eng.accum, self.eng.M, self.group, out=self.view.accum)
+            mx, am, pk = (t[0] for t in self.view.maxima_buffers(1))
+            rho = self.view.finalize_rows(h0, h1, mx, am, pk, want_rho)
+            MG.gather_rows(mx, am, pk, h0, h1, self.group)
+            out = self.view.select(mx, am, pk)
+        out.update(rows=(h0, h1), rho=rho)
+        return out
 
     def reset(self):
         self.eng.reset()

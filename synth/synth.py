@@ -76,6 +76,9 @@ CONFIGS = {
     "C3": Workload("C3", 100_000, 5000, F32, 1e-3, 0.045, 0.5, 1.5),
     "C4": Workload("C4", 1_500_000, 5000, S8, 0.25, 32.0, -40, 40),
     "C5": Workload("C5", 1_500_000, 20000, S8, 0.25, 32.0, -40, 40),
+    # the paper's wide-trace shape (dataset2: 48000 samples
+    # per trace [P:168]; Fig. 5's largest run, 8000 traces [P:188, P:199])
+    "W48": Workload("W48", 8000, 48000, S8, 3.0, 16.0, -40, 40),
 }
 
 

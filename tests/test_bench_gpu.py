@@ -36,13 +36,14 @@ def test_bench_single_gpu_line():
 
 
 @pytest.mark.gpu
-def test_bench_two_ranks_one_gpu_gloo():
+@pytest.mark.parametrize("combine,port", [("rows", 29533), ("allreduce", 29535)])
+def test_bench_two_ranks_one_gpu_gloo(combine, port):
     d = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-              "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2", "--config", "C2",
-              "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e"],
+              "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--config", "C2",
+              "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--combine", combine],
              env={"CPA_BENCH_SAME_DEVICE": "1", "CPA_BENCH_BACKEND": "gloo"})
     assert d["n_gpus"] == 2 and d["key_recovered"] is True
-    assert KEYS <= set(d)
+    assert KEYS <= set(d) and combine in d["config"]["parallelism"]
 
 
 @pytest.mark.gpu
@@ -54,3 +55,14 @@ def test_bench_stream_two_ranks_one_gpu_gloo():
     assert d["n_gpus"] == 2 and d["key_recovered"] is True
     pts = d["rank_curve"]["points"]
     assert pts[-1][0] == 500 and d["config"]["checkpoints"] == len(pts)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config,port", [("C2", 29536), ("W48", 29537)])
+def test_bench_sample_shards_two_ranks_one_gpu_gloo(config, port):
+    d = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+              "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--config", config,
+              "--shard", "samples", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e"],
+             env={"CPA_BENCH_SAME_DEVICE": "1", "CPA_BENCH_BACKEND": "gloo"})
+    assert d["n_gpus"] == 2 and d["key_recovered"] is True
+    assert d["config"]["parallelism"].startswith("sample-shard x2")

@@ -23,6 +23,20 @@ def _free_port():
     return p
 
 
+def _collect(q, procs, n, timeout=300):
+    """n results from the workers; fails fast if one of them died."""
+    import queue
+    import time
+    out, t_end = [], time.time() + timeout
+    while len(out) < n:
+        try:
+            out.append(q.get(timeout=2))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            assert not dead and time.time() < t_end, f"worker exit codes {dead}"
+    return out
+
+
 def _worker(rank, world, port, name, ret):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -91,3 +105,106 @@ def test_layout_matches_library():
         assert MG.accum_words(M) == P.cpa_accum_words(M)
         for i, k in enumerate(("sum_hw", "sum_w", "sum_w2", "sum_h", "sum_h2", "n")):
             assert f[k][0] == P.cpa_accum_offset(M, i)
+
+
+# ---- sharded Phase 3/4: row-sharded finalize and sample-axis sharding ---------
+class OracleEngine:
+    """Stands in for paper_1412_7682_b200.Engine on CPU: the accumulator holds
+    the oracle's exact partial sums of this rank's data; finalize_rows / select
+    follow include/cpa.h with the oracle's Eq. (1), phase 3 and phase 4 (the
+    shard merge written out in numpy).  Exercises multigpu's collectives and
+    index ranges; the library's own kernels are checked in test_sharded_gpu."""
+
+    def __init__(self, texts, W, cols):
+        from oracle import oracle as O
+        self.O, self.cols, self.M = O, np.asarray(cols, np.int32), len(cols)
+        sh, sh2 = O.model_sums(O.HD_LAST, texts)
+        sw, sw2 = O.trace_sums_i8(W, self.cols)
+        shw = O.cross_sums_i8(O.HD_LAST, texts, W, self.cols)
+        self.accum = MG.pack(self.M, dict(sum_hw=shw, sum_w=sw, sum_w2=sw2, sum_h=sh, sum_h2=sh2,
+                                          n=[W.shape[0]]), torch.zeros(1, dtype=torch.int64))
+
+    def maxima_buffers(self, G=1):
+        return (torch.zeros((G, 4096), dtype=torch.float64), torch.zeros((G, 4096), dtype=torch.int32),
+                torch.zeros((G, 4096), dtype=torch.float64))
+
+    def finalize_rows(self, h0, h1, mx, am, pk, want_rho=False):
+        s = MG.unpack(self.M, self.accum)
+        rho = self.O.rho_eq1_grid(int(s["n"][0]), s["sum_hw"].numpy(), s["sum_h"].numpy(), s["sum_h2"].numpy(),
+                                  s["sum_w"].numpy(), s["sum_w2"].numpy())
+        m, a, p = self.O.phase3(rho, self.cols)
+        mx[h0:h1], am[h0:h1], pk[h0:h1] = (torch.from_numpy(x[h0:h1]) for x in (m, a, p))
+        return torch.from_numpy(rho[h0:h1]) if want_rho else None
+
+    def select(self, mx, am, pk):
+        mx, am, pk = (t.reshape(-1, 4096).clone() for t in (mx, am, pk))
+        for g in range(1, mx.shape[0]):     # largest max|rho|, ties to the lowest sample
+            win = (mx[g] > mx[0]) | ((mx[g] == mx[0]) & (am[g] < am[0]))
+            mx[0][win], am[0][win], pk[0][win] = mx[g][win], am[g][win], pk[g][win]
+        best, rank = self.O.phase4(mx[0].numpy())
+        return dict(maxabs=mx[0], argmax=am[0], peak=pk[0], rank=torch.from_numpy(rank), round_key=best.tobytes())
+
+
+def _sharded_worker(rank, world, port, mode, ret):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from synth import synth as S
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = S.CONFIGS["C1"]
+    if mode == "rows":              # trace shard, all columns
+        i0, i1 = MG.shard_range(w.n, rank, world)
+        texts, lv = S.texts(w, i0, i1 - i0)
+        eng = OracleEngine(texts, S.traces(w, lv, i0), np.arange(w.m))
+        out = MG.finalize_rows_sharded(eng, want_rho=True)
+    else:                           # all traces, this rank's columns
+        j0, j1 = MG.column_range(w.m, rank, world)
+        texts, W = S.dataset(w)
+        eng = OracleEngine(texts, W, np.arange(j0, j1))
+        out = MG.finalize_columns_sharded(eng)
+    ret.put((rank, {k: (v.numpy() if torch.is_tensor(v) else v) for k, v in out.items() if k != "rows"},
+             out.get("rows")))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode,world", [("rows", 2), ("rows", 3), ("rows", 4), ("columns", 2), ("columns", 3)])
+def test_gloo_sharded_finalize_equals_single_process(mode, world):
+    from oracle import oracle as O
+    from synth import synth as S
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = _collect(q, procs, world)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    w = S.CONFIGS["C1"]
+    texts, W = S.dataset(w)
+    ref = O.attack_i8(O.HD_LAST, texts, W)
+    for rank, out, rows in outs:        # every rank holds the full, identical selection
+        assert np.array_equal(out["maxabs"], ref["maxabs"])
+        assert np.array_equal(out["argmax"], ref["argmax"])
+        assert np.array_equal(out["peak"], ref["peak"])
+        assert np.array_equal(out["rank"], ref["rank"])
+        assert out["round_key"] == ref["best"].tobytes()
+        if mode == "rows":
+            h0, h1 = rows
+            assert (h0, h1) == MG.row_range(rank, world)
+            assert np.array_equal(out["rho"], ref["rho"][h0:h1])
+
+
+def test_column_ranges_aligned_cover():
+    for M in (16, 500, 5000, 48000, 20000):
+        for world in (1, 2, 3, 4, 8):
+            if M < 16 * world:
+                continue
+            rs = [MG.column_range(M, r, world) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == M
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            assert all(j0 % 16 == 0 and j1 > j0 for j0, j1 in rs)
+    assert [MG.row_range(r, 8) for r in range(8)][3] == (1536, 2048)

@@ -77,8 +77,10 @@ def _worker(rank, world, port, chunk, ret):
                 shw = O.cross_sums_i8(O.HD_LAST, texts, W)
                 acc += MG.pack(w.m, dict(sum_hw=shw, sum_w=sw, sum_w2=sw2, sum_h=sh, sum_h2=sh2,
                                          n=[i1 - i0]), acc)
-        MG.combined_copy(acc, scratch)
-        outs.append(scratch.clone().numpy())
+        before = acc.clone()
+        rows = MG.reduce_scatter_rows(acc, w.m, out=scratch)
+        assert torch.equal(acc, before)            # running partials untouched
+        outs.append((rows, scratch.clone().numpy()))
     if rank == 0:
         ret.put(outs)
     dist.barrier()
@@ -87,8 +89,10 @@ def _worker(rank, world, port, chunk, ret):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_gloo_checkpoints_equal_prefix_sums(world):
-    """Every checkpoint of a world-G streamed run holds exactly the sums of the
-    trace prefix processed so far (no double counting of the running partials)."""
+    """Every checkpoint of a world-G streamed run (out-of-place reduce-scatter
+    of the running partials) holds exactly the sums of the trace prefix
+    processed so far in this rank's rows and the small fields (no double
+    counting of the running partials)."""
     from oracle import oracle as O
     from synth import synth as S
     chunk = 64
@@ -106,11 +110,16 @@ def test_gloo_checkpoints_equal_prefix_sums(world):
     texts, W = S.dataset(w)
     rounds = chunk_rounds(w.n, chunk, world)
     assert len(outs) == len(rounds)
-    for rnd, got in zip(rounds, outs):
+    for rnd, ((h0, h1), got) in zip(rounds, outs):
         n = rnd[-1][2]
+        assert (h0, h1) == MG.row_range(0, world)
         ref_hw = O.cross_sums_i8(O.HD_LAST, texts[:n], W[:n])
+        sh, sh2 = O.model_sums(O.HD_LAST, texts[:n])
+        sw, sw2 = O.trace_sums_i8(W[:n])
         g = MG.unpack(w.m, torch.from_numpy(got))
-        assert np.array_equal(g["sum_hw"].numpy(), ref_hw)
+        assert np.array_equal(g["sum_hw"].numpy()[h0:h1], ref_hw[h0:h1])   # this rank's rows
+        for k, v in (("sum_h", sh), ("sum_h2", sh2), ("sum_w", sw), ("sum_w2", sw2)):
+            assert np.array_equal(g[k].numpy(), v), k
         assert int(g["n"][0]) == n
 
 
