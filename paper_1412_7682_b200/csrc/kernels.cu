@@ -21,12 +21,13 @@ __device__ __forceinline__ int shiftrows_src(int b) { return (b & 3) + 4 * (((b 
 // H = V[c_s][c_b ^ k]; per-thread int32 partials, one int64 atomic per (b,k).
 // ---------------------------------------------------------------------------
 constexpr int MS_THREADS = 512;
-constexpr int MS_CHUNK = 2048;  // traces per block (int32-exact: 64 * 2048)
+constexpr int MS_CHUNK = 2048;  // max traces per block (int32-exact: 64 * 2048)
+constexpr int MS_MIN_BLOCKS = 296;  // 2 per SM: spread small N over the GPU
 constexpr int MS_STAGE = 256;   // traces staged in smem at a time
 
 template <typename Acc>
 __global__ void __launch_bounds__(MS_THREADS)
-k_modelsums(const uint8_t *__restrict__ texts, int64_t n, const uint8_t *__restrict__ vtab,
+k_modelsums(const uint8_t *__restrict__ texts, int64_t n, int chunk, const uint8_t *__restrict__ vtab,
             Acc *sum_h, Acc *sum_h2, Acc *count)
 {
     extern __shared__ uint8_t sm[];
@@ -38,8 +39,8 @@ k_modelsums(const uint8_t *__restrict__ texts, int64_t n, const uint8_t *__restr
     int32_t s1[8], s2[8];
 #pragma unroll
     for (int q = 0; q < 8; q++) s1[q] = s2[q] = 0;
-    const int64_t i0 = (int64_t)blockIdx.x * MS_CHUNK;
-    const int64_t i1 = min(n, i0 + MS_CHUNK);
+    const int64_t i0 = (int64_t)blockIdx.x * chunk;
+    const int64_t i1 = min(n, i0 + chunk);
     for (int64_t base = i0; base < i1; base += MS_STAGE) {
         __syncthreads();
         const int cnt = (int)min((int64_t)MS_STAGE, i1 - base);
@@ -455,8 +456,11 @@ cudaError_t modelsums(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab, 
         if (launches) (*launches) += 2;
         return cudaGetLastError();
     }
-    const int blocks = (int)((n + MS_CHUNK - 1) / MS_CHUNK);
-    k_modelsums<Acc><<<blocks, MS_THREADS, 65536 + MS_STAGE * 16, s>>>(d_texts, n, d_vtab, d_sum_h, d_sum_h2, d_count);
+    int64_t chunk = (n + MS_MIN_BLOCKS - 1) / MS_MIN_BLOCKS;
+    chunk = chunk < 16 ? 16 : (chunk > MS_CHUNK ? MS_CHUNK : chunk);
+    const int blocks = (int)((n + chunk - 1) / chunk);
+    k_modelsums<Acc><<<blocks, MS_THREADS, 65536 + MS_STAGE * 16, s>>>(d_texts, n, (int)chunk, d_vtab, d_sum_h,
+                                                                         d_sum_h2, d_count);
     if (launches) (*launches)++;
     return cudaGetLastError();
 }

@@ -252,10 +252,12 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
         }
         fence_mbar_init();
     }
+    __syncthreads();
+    cluster_sync_all();  // peer barriers initialised before any remote arrive; both CTAs
+                         // past their launch prologue before the pair TMEM allocation
     if (warp == 2) tmem_alloc_pair<TMEM_COLS>(smem_u32(tmem_slot));
     tc_fence_before();
     __syncthreads();
-    cluster_sync_all();  // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 

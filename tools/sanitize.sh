@@ -1,0 +1,14 @@
+# compute-sanitizer over the whole path (run under gpurun): int path (C1, and C2
+# with split-K units) and float path (C3 at 4000 traces); summary -> gpurun_out/
+mkdir -p gpurun_out
+CS=/usr/local/cuda/bin/compute-sanitizer
+for tool in memcheck racecheck synccheck initcheck; do
+  for cfg in "C1" "C2 2000 512" "C3 4000 0 0.02"; do
+    echo "== $tool $cfg" >> gpurun_out/sanitize.log
+    timeout -s KILL 900 $CS --tool $tool --error-exitcode 99 --print-limit 20 python tools/repro.py $cfg \
+        > gpurun_out/san_tmp.log 2>&1
+    echo "exit $?" >> gpurun_out/sanitize.log
+    grep -E "ERROR SUMMARY|RACECHECK SUMMARY|========= (Invalid|Race|Barrier|Uninit)|key " gpurun_out/san_tmp.log | head -12 >> gpurun_out/sanitize.log
+  done
+done
+cat gpurun_out/sanitize.log
