@@ -31,6 +31,7 @@ PEAK_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustaine
 INT8_PER_BF16 = 4.5 / 2.25  # nominal dense int8 : bf16 ratio (B200_PROFILING.md)
 CPU_SAMPLE_TRACES = 131072
 CPU_SAMPLE_COLS = 4
+OVERLAP_DEFAULT = 1   # CPA_OPT_OVERLAP: a4 on a low-priority side stream after the cross term
 
 
 def parse():
@@ -54,6 +55,8 @@ def parse():
                          "are exchanged).  auto: samples for the wide-trace W48 workload, else traces")
     ap.add_argument("--no-overlap", action="store_true",
                     help="serialise the a4 moments pass with the cross term")
+    ap.add_argument("--overlap-mode", type=int, default=None, choices=[0, 1, 2],
+                    help="CPA_OPT_OVERLAP (include/cpa.h); default: the library's")
     ap.add_argument("--chunk", type=int, default=0,
                     help="stream the traces in chunks of this many, finalizing after every round "
                          "(key-rank curve); default for C5: 65536")
@@ -251,8 +254,8 @@ def main():
 
     eng = P.Engine(m_local, P.CPA_F32 if is_f32 else P.CPA_S8, P.CPA_HD_LAST, local)
     eng.set_col0(j0)
-    if args.no_overlap:
-        eng.set_overlap(False)
+    ovl_mode = 0 if args.no_overlap else (args.overlap_mode if args.overlap_mode is not None else OVERLAP_DEFAULT)
+    eng.set_overlap(ovl_mode)
     combine = ("columns" if shard == "samples" else args.combine) if world > 1 else "none"
     h0, h1 = MG.row_range(rank, world) if combine == "rows" else (0, 4096)
     rho = torch.empty((h1 - h0, m_local), dtype=torch.float64, device=dev)   # this rank's block of rho
@@ -310,8 +313,8 @@ def main():
     # a4 alone: the timed steps overlap it with a5 on a low-priority side stream,
     # which hides its own HBM rate; two untimed extra steps serialise it
     solo = None
-    if not args.no_overlap:
-        eng.set_overlap(False)
+    if ovl_mode:
+        eng.set_overlap(0)
         eng.set_timing(True)
         eng.phase_times()
         for _ in range(2):
@@ -320,7 +323,7 @@ def main():
         sm, sn = eng.phase_times()
         solo = sm["moments"] / max(1, sn["moments"])
         eng.set_timing(False)
-        eng.set_overlap(True)
+        eng.set_overlap(ovl_mode)
     ms_step = ms_total / args.steps
     value = 4096 * w.m / (ms_step * 1e-3)
     key_ok = bytes(res.master_key) == w.key

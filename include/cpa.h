@@ -189,9 +189,11 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *                   (multiple of 128, <= 2^20; 0 = automatic).
  *   CPA_OPT_TIMING: nonzero = record CUDA events on the context's stream
  *                   around every kernel launch (read with cpa_phase_times).
- *   CPA_OPT_OVERLAP: nonzero (default) = run the trace-moment pass (a4) on a
- *                   low-priority side stream concurrently with the cross term;
- *                   0 = serialise everything on the context's stream.
+ *   CPA_OPT_OVERLAP: how the trace-moment pass (a4) runs next to the cross
+ *                   term: 0 = serialised on the context's stream; 1 (default)
+ *                   = launched after it on a low-priority side stream; 2 =
+ *                   launched before it on a high-priority side stream, one
+ *                   block per SM, co-resident with the cross-term CTAs.
  *   CPA_OPT_STAGE_BYTES: bytes of trace rows per staging chunk of
  *                   cpa_accumulate_host / unaligned cpa_accumulate
  *                   (0 = default 256 MiB; at least one row per chunk).

@@ -114,8 +114,8 @@ struct cpa_ctx {
         return e;
     }
     // a4 on a low-priority side stream, overlapped with the cross term
-    bool overlap = true;
-    cudaStream_t side = nullptr;
+    int overlap = 1;   // CPA_OPT_OVERLAP mode (0 serial, 1 low-priority after, 2 high-priority before)
+    cudaStream_t side = nullptr, side_hi = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
@@ -220,6 +220,7 @@ cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, 
         int lo = 0, hi = 0;  // numerically greatest = lowest priority
         e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
         if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo);
+        if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->side_hi, cudaStreamNonBlocking, hi);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
     }
@@ -263,7 +264,8 @@ cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
         return CPA_OK;
     }
     if (option == CPA_OPT_OVERLAP) {
-        ctx->overlap = value != 0;
+        if (value < 0 || value > 2) return fail(CPA_E_INVALID_ARG, "OVERLAP=%lld outside [0, 2]", (long long)value);
+        ctx->overlap = (int)value;
         return CPA_OK;
     }
     if (option == CPA_OPT_COL0) {
@@ -358,21 +360,24 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                               &launches);
              }),
              "modelsums");
-    // a4 (HBM-bound) runs on a low-priority side stream concurrently with the
-    // tensor-bound cross term: its blocks fill the registers/threads the
-    // cross-term CTAs leave free on each SM
-    const bool ovl = c->overlap && c->side;
-    if (ovl) {
+    // a4 (HBM-bound) runs concurrently with the tensor-bound cross term:
+    //   overlap 1: launched after it on a low-priority side stream (its blocks
+    //              fill whatever registers/threads the cross-term CTAs leave);
+    //   overlap 2: launched BEFORE it on a high-priority side stream, one block
+    //              per SM, so both kernels are co-resident from the start.
+    const int mode = c->side ? c->overlap : 0;
+    cudaStream_t mst = mode == 2 ? c->side_hi : (mode == 1 ? c->side : c->stream);
+    if (mode) {
         CUDA_TRY(cudaEventRecord(c->ev_fork, c->stream), "fork");
-        CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_fork, 0), "fork");
+        CUDA_TRY(cudaStreamWaitEvent(mst, c->ev_fork, 0), "fork");
     }
     auto moments = [&] {
-        return c->timed_on(1, ovl ? c->side : c->stream, [&] {
+        return c->timed_on(1, mst, [&] {
             return cpa::launch_moments_i8(d_w, ld, n, M, sgn, acc + cpa_accum_offset(M, 1),
-                                          acc + cpa_accum_offset(M, 2), ovl ? c->side : c->stream, &launches);
+                                          acc + cpa_accum_offset(M, 2), mode == 2 ? 1 : 0, mst, &launches);
         });
     };
-    if (!ovl) CUDA_TRY(moments(), "moments");
+    if (mode != 1) CUDA_TRY(moments(), "moments");
     CUtensorMap tmap;
     cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)n};
     cuuint64_t strides[1] = {(cuuint64_t)ld};
@@ -389,9 +394,9 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                              &launches);
              }),
              "xterm_i8");
-    if (ovl) {
-        CUDA_TRY(moments(), "moments");
-        CUDA_TRY(cudaEventRecord(c->ev_join, c->side), "join");
+    if (mode == 1) CUDA_TRY(moments(), "moments");
+    if (mode) {
+        CUDA_TRY(cudaEventRecord(c->ev_join, mst), "join");
         CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "join");
     }
     c->launches += launches;
@@ -710,6 +715,10 @@ cpa_status cpa_destroy(cpa_ctx *c)
     }
     cudaFree(c->d_pack);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->side_hi) {
+        cudaStreamSynchronize(c->side_hi);
+        cudaStreamDestroy(c->side_hi);
+    }
     if (c->side) {
         cudaStreamSynchronize(c->side);
         cudaStreamDestroy(c->side);

@@ -246,41 +246,53 @@ k_finalize_i8(const int64_t *__restrict__ hw, const int64_t *__restrict__ sw,
     const int64_t *row = hw + (int64_t)h * M;
     double *rrow = o.rho ? o.rho + (int64_t)(h - o.h0) * M : nullptr;
     Best best{-1.0, 0.0, 0x7fffffff};
-    // HBM-bound: FIN_UNROLL independent row loads in flight per thread before the
-    // (long-latency) fp64 division chains; j ascending per thread keeps the
-    // lowest-j tie rule with a strict '>'
-    constexpr int U = FIN_UNROLL;
-    int j0 = threadIdx.x;
-    for (; j0 + (U - 1) * FIN_THREADS < M; j0 += U * FIN_THREADS) {
-        int64_t v[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) v[u] = __ldcs(row + j0 + u * FIN_THREADS);
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int j = j0 + u * FIN_THREADS;
-            const double den_w = sqrt_dw[j];
-            double r = 0.0;
-            if (den_w != 0.0 && den_h != 0.0) {
-                const int64_t num = n * v[u] - s_h * sw[j];
-                r = __ddiv_rn(__ll2double_rn(num), __dmul_rn(den_w, den_h));
-                r = fmin(1.0, fmax(-1.0, r));
-            }
-            if (rrow) __stcs(rrow + j, r);
-            const double a = fabs(r);
-            if (a > best.v) best = Best{a, r, j};
-        }
-    }
-    for (int j = j0; j < M; j += FIN_THREADS) {
+    auto cell = [&](int64_t v, int j) {  // Eq. (1), fixed FMA-free sequence
         const double den_w = sqrt_dw[j];
         double r = 0.0;
         if (den_w != 0.0 && den_h != 0.0) {
-            const int64_t num = n * row[j] - s_h * sw[j];
+            const int64_t num = n * v - s_h * sw[j];
             r = __ddiv_rn(__ll2double_rn(num), __dmul_rn(den_w, den_h));
             r = fmin(1.0, fmax(-1.0, r));
         }
-        if (rrow) rrow[j] = r;
         const double a = fabs(r);
         if (a > best.v) best = Best{a, r, j};
+        return r;
+    };
+    // HBM-bound: FIN_UNROLL independent 16-byte row loads (2 samples each) in
+    // flight per thread before the long-latency fp64 division chains; j
+    // ascending per thread keeps the lowest-j tie rule with a strict '>'
+    constexpr int U = FIN_UNROLL;
+    int j = 0;
+    if ((M & 1) == 0 && ((uintptr_t)o.rho & 15) == 0) {  // 16-byte aligned rows (M even)
+        const longlong2 *row2 = (const longlong2 *)row;
+        double2 *rrow2 = (double2 *)rrow;
+        const int M2 = M >> 1;
+        int p0 = threadIdx.x;
+        for (; p0 + (U - 1) * FIN_THREADS < M2; p0 += U * FIN_THREADS) {
+            longlong2 v[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) v[u] = __ldcs(row2 + p0 + u * FIN_THREADS);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int jj = 2 * (p0 + u * FIN_THREADS);
+                double2 r;
+                r.x = cell(v[u].x, jj);
+                r.y = cell(v[u].y, jj + 1);
+                if (rrow2) __stcs(rrow2 + p0 + u * FIN_THREADS, r);
+            }
+        }
+        for (; p0 < M2; p0 += FIN_THREADS) {
+            const longlong2 v = __ldcs(row2 + p0);
+            double2 r;
+            r.x = cell(v.x, 2 * p0);
+            r.y = cell(v.y, 2 * p0 + 1);
+            if (rrow2) __stcs(rrow2 + p0, r);
+        }
+        j = M;  // done
+    }
+    for (j += threadIdx.x; j < M; j += FIN_THREADS) {
+        const double r = cell(row[j], j);
+        if (rrow) rrow[j] = r;
     }
     block_best_store(best, h, o);
 }
@@ -480,18 +492,22 @@ cudaError_t launch_modelsums_f64(const uint8_t *d_texts, int64_t n, const uint8_
 }
 
 cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M, bool w_signed,
-                              int64_t *d_sum_w, int64_t *d_sum_w2, cudaStream_t s, int *launches)
+                              int64_t *d_sum_w, int64_t *d_sum_w2, int blocks_per_sm, cudaStream_t s,
+                              int *launches)
 {
     // one resident wave: rows per item so that (groups x chunks) fills the
-    // GPU's resident threads exactly once (no wave-quantisation tail)
-    static int resident = 0;
-    if (!resident) {
-        int dev = 0, sms = 0, per_sm = 0;
+    // GPU's resident threads exactly once (no wave-quantisation tail);
+    // blocks_per_sm > 0 caps the wave (room for a concurrent cross term)
+    static int sms = 0, per_sm = 0;
+    if (!sms) {
+        int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_moments_i8<true>, MO_THREADS, 0);
-        resident = sms * (per_sm > 0 ? per_sm : 1) * MO_THREADS;
+        if (per_sm < 1) per_sm = 1;
     }
+    const int bps = (blocks_per_sm > 0 && blocks_per_sm < per_sm) ? blocks_per_sm : per_sm;
+    const int64_t resident = (int64_t)sms * bps * MO_THREADS;
     const int64_t groups = (M + 15) / 16;
     int64_t chunks = resident / groups;
     if (chunks < 1) chunks = 1;

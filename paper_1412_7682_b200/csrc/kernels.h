@@ -20,7 +20,8 @@ cudaError_t launch_modelsums_f64(const uint8_t *d_texts, int64_t n, const uint8_
 
 // a4: Phase 2 trace moments sum W, sum W^2 [P:79] (int8 traces, exact int64)
 cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M, bool w_signed,
-                              int64_t *d_sum_w, int64_t *d_sum_w2, cudaStream_t s, int *launches);
+                              int64_t *d_sum_w, int64_t *d_sum_w2, int blocks_per_sm, cudaStream_t s,
+                              int *launches);
 
 // a5: cross term (tcgen05 kind::i8, CTA pairs)
 int xterm_smem_bytes();

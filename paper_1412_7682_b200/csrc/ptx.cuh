@@ -145,6 +145,15 @@ __device__ __forceinline__ void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&v)[
                  : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// wait for the outstanding tcgen05.ld into v: the registers are in/out operands
+// so the compiler cannot read them before the wait
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&v)[8])
+{
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7])
+                 :
+                 : "memory");
+}
 
 // ---- UMMA descriptors (PTX ISA "Shared memory descriptor" / "Instruction
 // descriptor" for tcgen05.mma; field layout as in CUTLASS cute/arch/mma_sm100_desc.hpp)

@@ -272,7 +272,9 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     u = atomicAdd(p.unit_counter, 1);
                     if (u >= p.units) u = -1;
                     const int q = t % SCHED_Q;
-                    mbar_wait(sempty_bar(q), ((t / SCHED_Q) & 1) ^ 1);
+                    // acquire.cluster: pairs with the consumers' release.cluster arrivals
+                    // (both CTAs' reads of slot q happen before it is overwritten)
+                    mbar_wait_cluster(sempty_bar(q), ((t / SCHED_Q) & 1) ^ 1);
                     sched[q] = u;
                     st_cluster_u32(peer_sched + 4 * q, (uint32_t)u);
                     mbar_arrive(sfull_bar(q));                       // release: ids visible to waiters
@@ -410,15 +412,20 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             mbar_wait(tfull_bar(acc), (t / C::NBUF) & 1);  // multicast commit: CTA-scope wait
             tc_fence_after();
             constexpr int CPB = C::NT * BN / 8;  // 8-column groups per key byte
+            constexpr int NC = C::NACC * BN / 8;
+            const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + acc * (C::NACC * BN);
             // 8 columns at a time through a small transpose buffer: each warp-wide
-            // atomic covers 4 rows x 8 consecutive samples = 8 full 32-byte sectors
+            // atomic covers 4 rows x 8 consecutive samples = 8 full 32-byte sectors.
+            // The TMEM load of the next 8 columns is in flight during the atomics.
+            uint32_t v[8];
+            tmem_ld_32x32b_x8(tcol, v);
+            tmem_ld_wait(v);
 #pragma unroll 1
-            for (int c = 0; c < C::NACC * BN / 8; c++) {
+            for (int c = 0; c < NC; c++) {
                 const int kb = c / CPB, cc = c % CPB;
                 const int hrow0 = (b + kb) * 256 + (int)rank * BMC + q * 32;
-                uint32_t v[8];
-                tmem_ld_32x32b_x8(tmem_base + ((uint32_t)(q * 32) << 16) + acc * (C::NACC * BN) + c * 8, v);
-                tmem_ld_wait();
+                uint32_t vn[8];
+                if (c + 1 < NC) tmem_ld_32x32b_x8(tcol + (c + 1) * 8, vn);
 #pragma unroll
                 for (int x = 0; x < 8; x++) tbuf[lane * TB_LD + x] = v[x];
                 __syncwarp();
@@ -437,6 +444,11 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     }
                 }
                 __syncwarp();
+                if (c + 1 < NC) {
+                    tmem_ld_wait(vn);
+#pragma unroll
+                    for (int x = 0; x < 8; x++) v[x] = vn[x];
+                }
             }
             tc_fence_before();
             __syncwarp();

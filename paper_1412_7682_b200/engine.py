@@ -69,8 +69,9 @@ class Engine:
         """Global index of this context's sample 0 (sample-axis sharding)."""
         B.cpa_set_option(self.ctx, B.CPA_OPT_COL0, col0)
 
-    def set_overlap(self, on: bool = True):
-        B.cpa_set_option(self.ctx, B.CPA_OPT_OVERLAP, int(on))
+    def set_overlap(self, mode: int | bool = True):
+        """CPA_OPT_OVERLAP: 0 serial, 1 (True) low-priority side stream, 2 co-resident."""
+        B.cpa_set_option(self.ctx, B.CPA_OPT_OVERLAP, int(mode))
 
     def phase_times(self):
         """({phase: ms}, {phase: launches}) of the CUDA-event-timed launches

@@ -154,3 +154,20 @@ def test_wide_traces_w48_sampled_parity_and_column_shards(P):
         assert torch.equal(sh[k], out[k]), k
     assert sh["round_key"] == out["round_key"]
     eng.close()
+
+
+def test_finalize_rho_buffer_alignment(P, c1):
+    """The finalize kernel's 16-byte vector path (M even, aligned rho) and its
+    scalar path (rho only 8-byte aligned) give bit-identical results."""
+    w, texts, W, ref = c1
+    eng = P.Engine(w.m, P.CPA_S8, P.CPA_HD_LAST, 0)
+    eng.accumulate(_padded(W)[:, :w.m], torch.from_numpy(texts).cuda())
+    buf = torch.zeros(4096 * w.m + 1, dtype=torch.float64, device="cuda")
+    mx = torch.empty(4096, dtype=torch.float64, device="cuda")
+    am = torch.empty(4096, dtype=torch.int32, device="cuda")
+    for off in (0, 1):
+        rho = buf[off:off + 4096 * w.m]
+        P.cpa_finalize(eng.ctx, rho, mx, am)
+        assert np.array_equal(rho.view(4096, w.m).cpu().numpy(), ref["rho"]), off
+        assert np.array_equal(mx.cpu().numpy(), ref["maxabs"]) and np.array_equal(am.cpu().numpy(), ref["argmax"])
+    eng.close()
