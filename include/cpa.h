@@ -190,10 +190,13 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *   CPA_OPT_TIMING: nonzero = record CUDA events on the context's stream
  *                   around every kernel launch (read with cpa_phase_times).
  *   CPA_OPT_OVERLAP: how the trace-moment pass (a4) runs next to the cross
- *                   term: 0 = serialised on the context's stream; 1 (default)
- *                   = launched after it on a low-priority side stream; 2 =
- *                   launched before it on a high-priority side stream, one
- *                   block per SM, co-resident with the cross-term CTAs.
+ *                   term (int8 traces): 0 = serialised on the context's
+ *                   stream; 1 = launched after it on a low-priority side
+ *                   stream; 2 = launched before it on a high-priority side
+ *                   stream, one block per SM, co-resident with the cross-term
+ *                   CTAs; 3 (default) = fused: the cross-term kernel sums the
+ *                   W tiles it stages anyway (no separate pass, no extra HBM
+ *                   reads).  All modes give identical (exact) sums.
  *   CPA_OPT_STAGE_BYTES: bytes of trace rows per staging chunk of
  *                   cpa_accumulate_host / unaligned cpa_accumulate
  *                   (0 = default 256 MiB; at least one row per chunk).

@@ -114,7 +114,8 @@ struct cpa_ctx {
         return e;
     }
     // a4 on a low-priority side stream, overlapped with the cross term
-    int overlap = 1;   // CPA_OPT_OVERLAP mode (0 serial, 1 low-priority after, 2 high-priority before)
+    int overlap = 3;   // CPA_OPT_OVERLAP mode (0 serial, 1 low-priority after, 2 high-priority before,
+                       // 3 fused into the cross-term kernel)
     cudaStream_t side = nullptr, side_hi = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -264,7 +265,7 @@ cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
         return CPA_OK;
     }
     if (option == CPA_OPT_OVERLAP) {
-        if (value < 0 || value > 2) return fail(CPA_E_INVALID_ARG, "OVERLAP=%lld outside [0, 2]", (long long)value);
+        if (value < 0 || value > 3) return fail(CPA_E_INVALID_ARG, "OVERLAP=%lld outside [0, 3]", (long long)value);
         ctx->overlap = (int)value;
         return CPA_OK;
     }
@@ -365,7 +366,10 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     //              fill whatever registers/threads the cross-term CTAs leave);
     //   overlap 2: launched BEFORE it on a high-priority side stream, one block
     //              per SM, so both kernels are co-resident from the start.
-    const int mode = c->side ? c->overlap : 0;
+    //   overlap 3: no separate pass: the cross-term kernel's epilogue warps sum
+    //              the W tiles it loads anyway (no extra HBM traffic).
+    const bool fused = c->overlap == 3;
+    const int mode = (c->side && !fused) ? c->overlap : 0;
     cudaStream_t mst = mode == 2 ? c->side_hi : (mode == 1 ? c->side : c->stream);
     if (mode) {
         CUDA_TRY(cudaEventRecord(c->ev_fork, c->stream), "fork");
@@ -377,7 +381,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                           acc + cpa_accum_offset(M, 2), mode == 2 ? 1 : 0, mst, &launches);
         });
     };
-    if (mode != 1) CUDA_TRY(moments(), "moments");
+    if (!fused && mode != 1) CUDA_TRY(moments(), "moments");
     CUtensorMap tmap;
     cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)n};
     cuuint64_t strides[1] = {(cuuint64_t)ld};
@@ -390,11 +394,11 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     const int64_t kc = c->kchunk ? c->kchunk : cpa::xterm_i8_auto_kchunk(M, n, c->num_sms);
     CUDA_TRY(c->timed(2, [&] {
                  return cpa::launch_xterm_i8(tmap, d_tx, c->d_vtab, acc, c->d_counter, M, n, kc, sgn, c->num_sms,
-                                             c->stream,
-                                             &launches);
+                                             c->stream, &launches, fused ? acc + cpa_accum_offset(M, 1) : nullptr,
+                                             fused ? acc + cpa_accum_offset(M, 2) : nullptr);
              }),
              "xterm_i8");
-    if (mode == 1) CUDA_TRY(moments(), "moments");
+    if (!fused && mode == 1) CUDA_TRY(moments(), "moments");
     if (mode) {
         CUDA_TRY(cudaEventRecord(c->ev_join, mst), "join");
         CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "join");

@@ -23,12 +23,14 @@ cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M,
                               int64_t *d_sum_w, int64_t *d_sum_w2, int blocks_per_sm, cudaStream_t s,
                               int *launches);
 
-// a5: cross term (tcgen05 kind::i8, CTA pairs)
+// a5: cross term (tcgen05 kind::i8, CTA pairs).  With d_sum_w / d_sum_w2 set,
+// the kernel also adds a4's sum W, sum W^2 (fused moments).
 int xterm_smem_bytes();
 int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms);
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
                             int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
-                            int num_sms, cudaStream_t stream, int *launches);
+                            int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr,
+                            int64_t *d_sum_w2 = nullptr);
 
 // a6: float traces.  Split pre-pass: w' = w - offset[j] (fp32), hi = bf16(w'),
 // lo = bf16(w' - hi) into [n][ldh] bf16 planes; fp64 sum w', sum w'^2; sets

@@ -10,26 +10,27 @@
 //
 // The paper computed this serially per (k, b, j) thread [P:121]; here a CTA
 // PAIR (cluster of 2, tcgen05 cta_group::2) owns one key byte b (M = 256
-// sub-keys, 128 per CTA) and 512 (I8) / 256 (F32) samples:
+// sub-keys, 128 per CTA) and NT = 2 N tiles of 256 samples (I8; F32: one):
 //   * A = H (128 sub-keys x BK traces per CTA, MN-major, 128B swizzle) is
 //     GENERATED in shared memory from the ciphertext bytes: H[k] = V[c_s][c_b^k]
-//     with V[y][x] = HW(InvS[x] ^ y) (64 KB table in smem): one 16-byte chunk
-//     of 16 consecutive keys = one 16-byte chunk of row V[c_s], byte-permuted by
-//     (c_b & 15) -- LDS.128 + 4 SEL + 4 PRMT (+ 8 PRMT + 8 HSUB2.BF16 to widen to
-//     bf16 for F32) + STS.128.
+//     with V[y][x] = HW(InvS[x] ^ y) (nibble-packed 32 KB table in smem), see the
+//     generator section.  One A tile feeds NT accumulators, so the generation
+//     cost per MAC halves (KB=2, NT=1 -- two key bytes sharing one W tile -- was
+//     measured 1.3 ms slower at C4: generation costs issue slots, TMA does not).
 //   * B = W (MN-major = the caller's trace-major layout, no transpose): each CTA
-//     TMA-loads HALF of each N=256 tile, so the pair reads W once per 256 keys.
-//   * 8 MMAs per pipeline stage and per tcgen05.commit (a commit costs ~45 clk of
-//     tensor-pipe time, tools/mma_bench), 3 stages of 48 KB.
-//   * Per stage and SM: TMA 32 KB + tensor-core operand reads 64 KB + generation
-//     32 KB of shared-memory traffic for 1024 clk of MMA.
-//   * Work unit = (byte, trace chunk, N tile), byte fastest, handed out IN ORDER
-//     by a global atomic counter (leader CTA) so the units in flight share a
-//     few W blocks in L2 (W streams from HBM about once).
+//     TMA-loads HALF of each N=256 tile.
+//   * Per 128-trace stage: 4 K steps x NT MMAs, one tcgen05.commit per ring
+//     (a commit costs ~45 clk of tensor-pipe time, tools/mma_bench); A ring 3 x
+//     16 KB, W ring 4 x 32 KB.
+//   * Work unit = (byte, trace chunk, N tile group), byte fastest, handed out IN
+//     ORDER by a global atomic counter (leader CTA) so the units in flight share
+//     a few W blocks in L2 (W streams from HBM about once).
+//   * Fused a4 (moments_pass): the epilogue warps, idle during the mainloop,
+//     sum W and W^2 over 1/16 of the rows of every W stage they see.
 // Warp roles (768 threads per CTA): w0 scheduler (leader) + W TMA producer,
 // w1 MMA issuer (leader), w2 TMEM owner, w3
-// ciphertext producer, w4-7 epilogue (TMEM lanes 32*(w%4)...), w8-23 H
-// generators.
+// ciphertext producer, w4-7 epilogue (TMEM lanes 32*(w%4)...) + fused moments,
+// w8-23 H generators.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -47,11 +48,17 @@
 #ifndef XT_EXP
 #define XT_EXP 0
 #endif
+#ifndef XT_KB_I8
+#define XT_KB_I8 1
+#endif
+#ifndef XT_NT_I8
+#define XT_NT_I8 2
+#endif
 #ifndef XT_A_STAGES_I8
 #define XT_A_STAGES_I8 3
 #endif
 #ifndef XT_B_STAGES_I8
-#define XT_B_STAGES_I8 5
+#define XT_B_STAGES_I8 4
 #endif
 #ifndef XT_A_STAGES_F32
 #define XT_A_STAGES_F32 3
@@ -68,8 +75,8 @@ struct Cfg {
     static constexpr int ESZ = F32 ? 2 : 1;         // bytes per operand element
     static constexpr int KMMA = F32 ? 16 : 32;      // K per MMA instruction
     static constexpr int NB = F32 ? 2 : 1;          // B operands (hi, lo)
-    static constexpr int KB = F32 ? 1 : 2;          // key bytes per unit (A tiles sharing one W tile)
-    static constexpr int NT = 1;                    // N=256 sample tiles per unit
+    static constexpr int KB = F32 ? 1 : XT_KB_I8;   // key bytes per unit (A tiles sharing one W tile)
+    static constexpr int NT = F32 ? 1 : XT_NT_I8;   // N=256 sample tiles per unit (W tiles sharing one A tile)
     static constexpr int NBUF = F32 ? 2 : 1;        // TMEM accumulator buffers
     static constexpr int NACC = KB * NT;            // N=256 accumulators per unit
     static constexpr int BK = F32 ? 64 : 128;       // traces per pipeline stage
@@ -115,7 +122,7 @@ constexpr int RINGS_BYTES = 180224;           // A_STAGES*A_STAGE + B_STAGES*B_S
 constexpr int SMEM_TX = SMEM_A + RINGS_BYTES;
 constexpr int SMEM_TB = SMEM_TX + TX_STAGES * TX_BYTES;
 constexpr int SMEM_BAR = SMEM_TB + TB_BYTES;
-constexpr int NUM_BARS = 4 * MAX_RING + 2 * TX_STAGES + 4 + 2 * SCHED_Q;
+constexpr int NUM_BARS = 4 * MAX_RING + 2 * TX_STAGES + 4 + 2 * SCHED_Q + 2 * MAX_RING;
 constexpr int SMEM_SCHED = SMEM_BAR + NUM_BARS * 8;
 constexpr int SMEM_TOTAL = SMEM_SCHED + SCHED_Q * 4 + 16;
 constexpr int SMEM_ALLOC = SMEM_TOTAL;
@@ -144,6 +151,11 @@ struct Params {
     int64_t N;
     int64_t kc_len;
     uint32_t idesc;
+    // fused a4 (I8 only; null = off): the epilogue warps add sum W, sum W^2 of
+    // 1/8 of the rows of every W tile they stage (moments_pass)
+    int64_t *sum_w;
+    int64_t *sum_w2;
+    int32_t w_signed;
 };
 
 template <bool F32>
@@ -173,6 +185,84 @@ __device__ __forceinline__ uint32_t bf16x2_of_bytes(uint32_t w, uint32_t sel)
     return *reinterpret_cast<const uint32_t *>(&v);
 }
 
+// Fused a4 [P:79]: sum W_ij and sum W_ij^2, read from the W ring while the MMAs
+// consume it.  Each W tile (trace chunk x NT*256 samples) is staged by the units
+// of all G = 16 / KB key-byte groups; the unit of group g sums rows
+// g*128/G .. (g+1)*128/G - 1 of every 128-trace stage over its CTA's NT x 128
+// samples, so every (trace, sample) is counted exactly once and the work is
+// spread evenly over all units (KB * NT == 2: 4 warps x 32 lanes x 4 rows x 4
+// samples = 128/G rows x NT*128 samples).  Thread (warp q, lane) owns samples
+// 4 lane .. 4 lane + 3 of N tile q % NT, rows 4 (q / NT) .. + 3 of the group's
+// slice: 4 LDS.32 (one 128-byte row per warp instruction, conflict-free), a 4x4
+// byte transpose (8 PRMT) puts the 4 traces of one sample in a word, and IDP4A
+// adds 4 values (x 1) or 4 squares (x itself) per instruction.  Per-thread sums
+// are exact in 32 bits (a unit of <= 2^20 traces gives a thread <= 2^15 rows:
+// |sum W| <= 2^22, sum W^2 <= 65025 * 2^15 < 2^31); they are added to the int64
+// sums with atomics (exact, order-independent).  TMA zero fill (rows >= N,
+// samples >= M) adds nothing.
+template <bool SIGNED>
+__device__ __forceinline__ uint32_t dp4(uint32_t a, uint32_t b, uint32_t c)
+{
+    if constexpr (SIGNED) return (uint32_t)__dp4a((int)a, (int)b, (int)c);
+    else return __dp4a(a, b, c);
+}
+template <bool SIGNED>
+__device__ __forceinline__ void moments_pass(const Params &p, uint32_t bring, uint32_t eit, uint32_t nst, bool leader,
+                                             int g, int q, int lane, int j0, uint32_t bfull0, uint32_t mready0,
+                                             uint32_t mdone0)
+{
+    using C = Cfg<false>;
+    static_assert(C::KB * C::NT == 2 && C::NB == 1 && C::ESZ == 1 && C::BK == 128, "moments_pass thread map");
+    constexpr int BS = C::B_STAGES;
+    uint32_t s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+    const int n = q % C::NT;
+    const int row0 = (C::BK * C::KB / 16) * g + 4 * (q / C::NT);
+    const uint32_t off0 = n * C::BH_BYTES + row0 * 128 + (lane & 3) * 4;
+    for (uint32_t k = 0; k < nst; k++) {
+        const uint32_t git = eit + k;
+        const int s = (int)(git % BS);
+        const uint32_t ph = (git / BS) & 1;
+        // CTA-scope waits and a release.cta remote relay, as the MMA issuer's: the
+        // cluster-scope forms compile to CCTL.IVALL / MEMBAR.ALL.GPU per stage,
+        // which made this warp the pipeline's bottleneck (27 vs 19.5 ms at C4).
+        // The TMA engine has written this CTA's half before it completes the tx
+        // on the leader's barrier, and shared memory has no cache to go stale.
+        if (leader) {
+            mbar_wait(bfull0 + 8 * s, ph);  // both halves landed
+            if (q == 0 && lane == 0) mbar_arrive_remote(mapa_shared(mready0 + 8 * s, 1));
+        } else {
+            mbar_wait(mready0 + 8 * s, ph);  // relayed by the leader
+        }
+        const uint32_t tile = bring + s * Cfg<false>::B_STAGE + off0;
+        uint32_t x[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const uint32_t a = tile + r * 128 + ((((uint32_t)lane >> 2) ^ (uint32_t)((row0 + r) & 7)) << 4);
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x[r]) : "r"(a));
+        }
+        const uint32_t t0 = __byte_perm(x[0], x[1], 0x5140), t1 = __byte_perm(x[0], x[1], 0x7362);
+        const uint32_t t2 = __byte_perm(x[2], x[3], 0x5140), t3 = __byte_perm(x[2], x[3], 0x7362);
+        const uint32_t y[4] = {__byte_perm(t0, t2, 0x5410), __byte_perm(t0, t2, 0x7632),
+                               __byte_perm(t1, t3, 0x5410), __byte_perm(t1, t3, 0x7632)};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            s1[e] = dp4<SIGNED>(y[e], 0x01010101u, s1[e]);
+            s2[e] = dp4<SIGNED>(y[e], y[e], s2[e]);
+        }
+        __syncwarp();  // every lane's loads have returned (their values are consumed above)
+        if (lane == 0) mbar_arrive(mdone0 + 8 * s);  // this warp is done with slot s
+    }
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        const int j = j0 + n * BN + 4 * lane + e;
+        if (j < p.M) {
+            const int64_t a1 = SIGNED ? (int64_t)(int32_t)s1[e] : (int64_t)s1[e];
+            atomicAdd((unsigned long long *)p.sum_w + j, (unsigned long long)a1);
+            atomicAdd((unsigned long long *)p.sum_w2 + j, (unsigned long long)s2[e]);
+        }
+    }
+}
+
 template <bool F32>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUtensorMap tmap_b1, const Params p)
@@ -198,6 +288,11 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
     auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + 2 + a); }; // leader's
     auto sfull_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + q); };        // both CTAs
     auto sempty_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + SCHED_Q + q); };  // leader's
+    constexpr int BAR_M = BAR_S + 2 * SCHED_Q;
+    // fused moments: W slot s landed (peer: relayed by the leader's epilogue), and
+    // this CTA's epilogue warps are done reading it (gates the W producer's refill)
+    auto mready_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (BAR_M + s); };             // peer's
+    auto mdone_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (BAR_M + MAX_RING + s); };   // both CTAs
     volatile int *sched = (volatile int *)(smem + SMEM_SCHED);
     uint32_t *tmem_slot = (uint32_t *)(smem + SMEM_SCHED + SCHED_Q * 4);
     auto to_leader = [&](uint32_t a) { return mapa_shared(a, 0); };
@@ -237,6 +332,8 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
         for (int s = 0; s < BS; s++) {
             mbar_init(bfull_bar(s), 1);   // leader's W producer: arrive + tx of both CTAs' loads
             mbar_init(bempty_bar(s), 1);  // multicast tcgen05.commit
+            mbar_init(mready_bar(s), 1);  // the leader's epilogue relay
+            mbar_init(mdone_bar(s), EPI_WARPS);
         }
         for (int x = 0; x < TX_STAGES; x++) {
             mbar_init(txfull_bar(x), 1);            // ciphertext rows landed
@@ -266,6 +363,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
         if (lane == 0) {
             const uint32_t peer_sched = mapa_shared(smem_u32((const void *)sched), 1);
             uint32_t it = 0;
+            uint32_t mpend = 0, mph = 0;  // slots holding a moments stage not yet released, their mdone parities
             for (uint32_t t = 0;; t++) {
                 int u;
                 if (leader) {
@@ -287,9 +385,16 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 int64_t t0, t1;
                 unit_coords<F32>(p, u, b, nt, t0, t1);
                 const int x0 = nt * (C::NT * BN) + (int)rank * (BN / 2);  // this CTA's half of N tile 0
+                const bool mom = !F32 && p.sum_w != nullptr;
                 for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
                     const int s = it % BS;
                     mbar_wait(bempty_bar(s), ((it / BS) & 1) ^ 1);
+                    if ((mpend >> s) & 1u) {  // the epilogue's moment pass over the old contents
+                        mbar_wait(mdone_bar(s), (mph >> s) & 1u);
+                        mph ^= 1u << s;
+                        mpend &= ~(1u << s);
+                    }
+                    if (mom) mpend |= 1u << s;
                     // the leader's arrival carries the tx bytes of BOTH CTAs' loads; the
                     // peer's loads only complete tx on it (they cannot land in an earlier
                     // phase: the peer waited for this slot's commit, which follows it)
@@ -402,12 +507,24 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         uint32_t *tbuf = (uint32_t *)(smem + SMEM_TB) + q * 32 * TB_LD;
         const int rsub = lane >> 3, csub = lane & 7;
+        uint32_t eit = 0;     // W ring stage counter (same sequence as the producer's)
         for (uint32_t t = 0;; t++) {
             const int u = next_unit(t, false);
             if (u < 0) break;
             int b, nt;
             int64_t t0, t1;
             unit_coords<F32>(p, u, b, nt, t0, t1);
+            const uint32_t nst = (uint32_t)((t1 - t0 + C::BK - 1) / C::BK);
+            if constexpr (!F32) {
+                if (p.sum_w != nullptr) {
+                    const int j0 = nt * (C::NT * BN) + (int)rank * (BN / 2);  // this CTA's half of N tile 0
+                    if (p.w_signed) moments_pass<true>(p, sbase + smem_b<F32>(), eit, nst, leader, b / C::KB, q, lane,
+                                                       j0, bfull_bar(0), mready_bar(0), mdone_bar(0));
+                    else moments_pass<false>(p, sbase + smem_b<F32>(), eit, nst, leader, b / C::KB, q, lane, j0,
+                                             bfull_bar(0), mready_bar(0), mdone_bar(0));
+                }
+            }
+            eit += nst;
             const uint32_t acc = t % C::NBUF;
             mbar_wait(tfull_bar(acc), (t / C::NBUF) & 1);  // multicast commit: CTA-scope wait
             tc_fence_after();
@@ -572,7 +689,8 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
 template <bool F32>
 cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *d_texts, const uint8_t *d_vtab,
                    void *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, uint32_t idesc, int num_sms,
-                   cudaStream_t stream, int *launches)
+                   cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr, int64_t *d_sum_w2 = nullptr,
+                   bool w_signed = true)
 {
     using Cf = Cfg<F32>;
     Params p;
@@ -588,6 +706,9 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *
     p.kc_count = (int32_t)((N + kc_len - 1) / kc_len);
     p.units = p.groups * p.n_tiles * p.kc_count;
     p.idesc = idesc;
+    p.sum_w = d_sum_w;
+    p.sum_w2 = d_sum_w2;
+    p.w_signed = w_signed ? 1 : 0;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_xterm<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
@@ -650,10 +771,10 @@ int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms)
 
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
                             int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
-                            int num_sms, cudaStream_t stream, int *launches)
+                            int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w, int64_t *d_sum_w2)
 {
     return launch<false>(tmap_w, tmap_w, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
-                         idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches);
+                         idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, d_sum_w, d_sum_w2, w_signed);
 }
 
 cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,

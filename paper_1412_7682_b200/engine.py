@@ -70,7 +70,7 @@ class Engine:
         B.cpa_set_option(self.ctx, B.CPA_OPT_COL0, col0)
 
     def set_overlap(self, mode: int | bool = True):
-        """CPA_OPT_OVERLAP: 0 serial, 1 (True) low-priority side stream, 2 co-resident."""
+        """CPA_OPT_OVERLAP: 0 serial, 1 (True) low-priority side stream, 2 co-resident, 3 fused (default)."""
         B.cpa_set_option(self.ctx, B.CPA_OPT_OVERLAP, int(mode))
 
     def phase_times(self):

@@ -23,13 +23,15 @@ def P():
 MODEL = {O.HD_LAST: 0, O.HW_LAST: 1, O.HW_FIRST: 2}
 
 
-def run_gpu(P, texts, W, model=0, kchunk=0, chunks=None, want_rho=True, overlap=True):
+def run_gpu(P, texts, W, model=0, kchunk=0, chunks=None, want_rho=True, overlap=True, mode=None):
     dtype = {np.int8: P.CPA_S8, np.uint8: P.CPA_U8}[W.dtype.type]
     eng = P.Engine(W.shape[1], dtype, model, 0)
     if kchunk:
         eng.set_kchunk(kchunk)
     if not overlap:
         eng.set_overlap(False)
+    if mode is not None:
+        eng.set_overlap(mode)
     bounds = chunks or [0, W.shape[0]]
     # pad rows to a 16-byte multiple (TMA stride rule); ld > M exercises strides
     ld = (W.shape[1] + 15) // 16 * 16
@@ -259,3 +261,44 @@ def test_model_sums_histogram_path(P, model):
         assert np.array_equal(s["sum_h"], sh) and np.array_equal(s["sum_h2"], sh2)
         assert s["n"] == n
     assert np.array_equal(one["sum_hw"], chunked["sum_hw"])
+
+
+@pytest.mark.parametrize("dt", [np.int8, np.uint8])
+def test_moment_modes_exact(P, dt):
+    """a4 trace moments in every CPA_OPT_OVERLAP mode (0 serial, 1 low-priority
+    side stream, 2 co-resident, 3 fused into the cross-term kernel) equal the
+    oracle's exact sums [P:79], including the extreme values (-128/127, 0/255)
+    whose squares bound the per-thread 32-bit partials, a ragged last sample
+    tile (M = 300: the second CTA of the second tile is entirely past M) and
+    ragged trace counts / split-K units."""
+    rng = np.random.default_rng(21)
+    n, m = 5 * 128 + 77, 300
+    lo, hi = (-128, 128) if dt is np.int8 else (0, 256)
+    texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    W = rng.integers(lo, hi, (n, m)).astype(dt)
+    W[:, 7] = lo                     # constant extreme columns
+    W[:, 299] = hi - 1
+    W[:300, 11] = lo
+    sw, sw2 = O.trace_sums_i8(W)
+    ref_hw = O.cross_sums_i8(O.HD_LAST, texts, W, np.array([0, 7, 11, 255, 256, 299], np.int32))
+    for mode in (0, 1, 2, 3):
+        for kw in (dict(), dict(kchunk=128), dict(chunks=[0, 3, 400, n])):
+            s, _ = run_gpu(P, texts, W, mode=mode, want_rho=False, **kw)
+            assert np.array_equal(s["sum_w"], sw), (mode, kw)
+            assert np.array_equal(s["sum_w2"], sw2), (mode, kw)
+            assert np.array_equal(s["sum_hw"][:, [0, 7, 11, 255, 256, 299]], ref_hw), (mode, kw)
+
+
+@pytest.mark.parametrize("dt,v", [(np.int8, -128), (np.uint8, 255)])
+def test_fused_moments_32bit_bound(P, dt, v):
+    """Worst case of the fused a4 partials (xterm.cu moments_pass): constant
+    extreme traces over one 2^20-trace split-K unit, the largest allowed, so a
+    thread's 32-bit sum W^2 reaches 2^15 * 65025 (u8) / 2^29 (s8).  Closed form:
+    sum W = N v, sum W^2 = N v^2, and sum_k sum HW = 1024 sum W per byte."""
+    n, m = (1 << 20) + 5, 16
+    texts = np.random.default_rng(3).integers(0, 256, (n, 16), dtype=np.uint8)
+    W = np.full((n, m), v, dt)
+    s, _ = run_gpu(P, texts, W, kchunk=1 << 20, mode=3, want_rho=False)
+    assert np.all(s["sum_w"] == n * v) and np.all(s["sum_w2"] == n * v * v)
+    hw = s["sum_hw"].reshape(16, 256, m).sum(axis=1)
+    assert np.all(hw == 1024 * n * v)
