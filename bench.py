@@ -31,6 +31,7 @@ PEAK_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustaine
 INT8_PER_BF16 = 4.5 / 2.25  # nominal dense int8 : bf16 ratio (B200_PROFILING.md)
 CPU_SAMPLE_TRACES = 131072
 CPU_SAMPLE_COLS = 4
+MODEL_NAMES = ("HD last-round", "HW last-round", "HW first-round")
 OVERLAP_DEFAULT = 3   # CPA_OPT_OVERLAP: a4 fused into the cross-term kernel (int8 traces)
 
 
@@ -57,6 +58,9 @@ def parse():
                     help="serialise the a4 moments pass with the cross term")
     ap.add_argument("--overlap-mode", type=int, default=None, choices=[0, 1, 2, 3],
                     help="CPA_OPT_OVERLAP (include/cpa.h); default: the library's")
+    ap.add_argument("--class-sums", choices=["0", "1"], default="0",
+                    help="CPA_OPT_CLASS_SUMS=1: class-sum cross term for HW_LAST/HW_FIRST workloads "
+                         "(C4-HW); default: the tensor-core contraction (faster on B200, DESIGN.md)")
     ap.add_argument("--chunk", type=int, default=0,
                     help="stream the traces in chunks of this many, finalizing after every round "
                          "(key-rank curve); default for C5: 65536")
@@ -130,17 +134,17 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- cpu baseline ----
-def oracle_attack(O, texts, Ws):
+def oracle_attack(O, texts, Ws, model=0):
     """The oracle's Phases 1-4 on the sampled columns (int or float traces)."""
     import numpy as np
     if Ws.dtype == np.float32:
-        sh, sh2 = O.model_sums(O.HD_LAST, texts)
-        shw, sw, sw2 = O.sums_f32(O.HD_LAST, texts, Ws)
+        sh, sh2 = O.model_sums(model, texts)
+        shw, sw, sw2 = O.sums_f32(model, texts, Ws)
         rho = O.rho_eq1_f64_grid(Ws.shape[0], shw, sh, sh2, sw, sw2)
         mx, am, pk = O.phase3(rho)
         best, rank = O.phase4(mx)
         return {"best": best}
-    return O.attack_i8(O.HD_LAST, texts, Ws, np.arange(Ws.shape[1], dtype=np.int32))
+    return O.attack_i8(model, texts, Ws, np.arange(Ws.shape[1], dtype=np.int32))
 
 
 def cpu_baseline(w, sample_traces=CPU_SAMPLE_TRACES, ncols=CPU_SAMPLE_COLS):
@@ -154,7 +158,7 @@ def cpu_baseline(w, sample_traces=CPU_SAMPLE_TRACES, ncols=CPU_SAMPLE_COLS):
     cols = np.array(sorted(w.leak_positions()[:2] + [w.m // 5, (3 * w.m) // 5]), np.int32)[:ncols]
     Ws = S.traces(w, lv, 0, cols)
     t0 = time.perf_counter()
-    a = oracle_attack(O, texts, Ws)
+    a = oracle_attack(O, texts, Ws, w.leak_model)
     t = time.perf_counter() - t0
     t_full = t * (w.n / n)
     return {"value": 4096 * len(cols) / t_full, "unit": "correlations/s", "cores": 1, "kind": "oracle",
@@ -178,7 +182,7 @@ def run_reference(args, w):
     ts = []
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        oracle_attack(O, texts, Ws)
+        oracle_attack(O, texts, Ws, w.leak_model)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             ts.append(dt * (w.n / n))
@@ -189,7 +193,7 @@ def run_reference(args, w):
             "unit": "correlations/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "int64", "data": "synthetic",
-            "config": {"workload": f"{w.name}: {w.n} traces x {w.m} samples int8, HD last-round model",
+            "config": {"workload": f"{w.name}: {w.n} traces x {w.m} samples int8, {MODEL_NAMES[w.leak_model]} model",
                        "n_traces": w.n, "n_samples": w.m},
             "cpu_baseline": {"value": val, "unit": "correlations/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": "correlations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -252,7 +256,10 @@ def main():
     dWv = dW[:, j0:j1]
     torch.cuda.synchronize()
 
-    eng = P.Engine(m_local, P.CPA_F32 if is_f32 else P.CPA_S8, P.CPA_HD_LAST, local)
+    eng = P.Engine(m_local, P.CPA_F32 if is_f32 else P.CPA_S8, w.leak_model, local)  # model = the leakage's
+    class_sums = args.class_sums == "1" and not is_f32
+    if class_sums:
+        eng.set_class_sums(True)
     eng.set_col0(j0)
     ovl_mode = 0 if args.no_overlap else (args.overlap_mode if args.overlap_mode is not None else OVERLAP_DEFAULT)
     eng.set_overlap(ovl_mode)
@@ -350,6 +357,12 @@ def main():
                                 f"{src} bf16_tflops (burst) x {INT8_PER_BF16:g} (int8:bf16 nominal ratio)"),
                 "frac_of_sustained": achieved / (peaks["bf16_tflops_sustained"] * ratio),
                 "algorithmic_ops_per_launch": ops, "ms_per_launch": xt_ms}
+    if class_sums:  # NEXT-4 path: HBM-bound by design (16 adds per trace byte), so report it as such
+        gbs = n_local * m_local / (xt_ms * 1e-3) / 1e9
+        roofline = {"kernel": "class sums (k_cs_sort + k_cs_sum + k_cs_contract)", "bound": "hbm",
+                    "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"],
+                    "traffic": None, "algorithmic_bytes_per_launch": n_local * m_local, "ms_per_launch": xt_ms,
+                    "note": "each trace byte is gathered once per key byte (16x) through L2; see DESIGN.md"}
     if is_f32:
         roofline["executed_ops_per_launch"] = 2 * ops  # bf16 hi + lo MMAs
         roofline["executed_frac"] = 2 * achieved / peak
@@ -357,7 +370,7 @@ def main():
     tot = sum(step_phase_ms.values()) or 1.0
     # HBM-bound kernels: achieved GB/s on their algorithmic bytes
     mo_launch_ms = phase_ms["moments"] / max(1, phase_n["moments"])
-    fused = ovl_mode == 3 and not is_f32
+    fused = ovl_mode == 3 and not is_f32 and not class_sums
     mo_solo = solo or mo_launch_ms
     hbm = {"moments_GBps": (n_local * m_local) / (mo_solo * 1e-3) / 1e9 if mo_solo else None,
            "moments_GBps_overlapped": (n_local * m_local) / (mo_launch_ms * 1e-3) / 1e9 if (solo and mo_launch_ms) else None,
@@ -410,7 +423,8 @@ def main():
             "dtype": "bf16x2 (f32 traces, fp32 accum, fp64 sums)" if is_f32 else "s8",
             "data": "synthetic",
             "config": {"workload": f"{w.name}: {w.n} traces x {w.m} samples "
-                                   f"{'float32' if is_f32 else 'int8 (s8)'}, HD last-round model, "
+                                   f"{'float32' if is_f32 else 'int8 (s8)'}, {MODEL_NAMES[w.leak_model]} model"
+                                   f"{' (class-sum cross term)' if class_sums else ''}, "
                                    f"AES-128 key {w.key.hex()}",
                        "n_traces": w.n, "n_samples": w.m, "hypotheses": 4096, "parallelism": (f"{'sample' if shard == 'samples' else 'trace'}-shard x{world}"
                                        + (f", {combine} combine" if world > 1 else "")),

@@ -202,9 +202,18 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *                   (0 = default 256 MiB; at least one row per chunk).
  *   CPA_OPT_COL0:   global index of this context's sample 0 (sample-axis
  *                   sharding); added to every reported sample index
- *                   (argmax, peak_sample).  Default 0.                      */
+ *                   (argmax, peak_sample).  Default 0.
+ *   CPA_OPT_CLASS_SUMS: 1 = compute the cross term sum H*W by class sums
+ *                   (SURVEY 8f NEXT-4): for HW_LAST / HW_FIRST, H depends on
+ *                   one text byte x, so sum_i H W_ij = sum_x f(x ^ k) S_b[x][j]
+ *                   with S_b[x][j] the sum of W_ij over the traces whose byte b
+ *                   is x [P:63, P:79].  Exact (bit-identical to 0).  Needs a
+ *                   single-byte model and s8/u8 traces, else
+ *                   CPA_E_INVALID_ARG.  Allocates 64 B per trace (<= 2^17
+ *                   traces per chunk) + 16 KB per sample (<= 8192 samples per
+ *                   block) of scratch on first use.  Default 0 (tensor cores). */
 enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2, CPA_OPT_OVERLAP = 3, CPA_OPT_STAGE_BYTES = 4,
-       CPA_OPT_COL0 = 5 };
+       CPA_OPT_COL0 = 5, CPA_OPT_CLASS_SUMS = 6 };
 CPA_API cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value);
 
 /* Per-phase device time (ms) and launch count since the last call, from the

@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcpa.so")
-SOURCES = ["cpa_api.cu", "kernels.cu", "xterm.cu", "aes_host.cpp"]
+SOURCES = ["cpa_api.cu", "kernels.cu", "xterm.cu", "classsum.cu", "aes_host.cpp"]
 HEADERS = ["ptx.cuh", "kernels.h", "tables.h"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-shared"]

@@ -93,6 +93,11 @@ struct cpa_ctx {
     int64_t plane_rows = 0;
     int *d_nonfinite = nullptr;
     uint32_t *d_hist = nullptr;  // a3 byte-pair histogram scratch (16 x 65536)
+    // CPA_OPT_CLASS_SUMS (HW_LAST / HW_FIRST, int8 traces): class-sum cross term
+    // (classsum.cu); scratch allocated on first use
+    int class_sums = 0;
+    int32_t *d_cs_cnt = nullptr, *d_cs_off = nullptr, *d_cs_cur = nullptr, *d_cs_perm = nullptr, *d_cs_S = nullptr;
+    int64_t cs_perm_n = 0, cs_S_words = 0;
     // CPA_OPT_TIMING: CUDA events recorded on `stream` around every launch
     bool timing = false;
     struct Rec { int phase; cudaEvent_t a, b; };
@@ -285,7 +290,89 @@ cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
         ctx->kchunk = value;
         return CPA_OK;
     }
+    if (option == CPA_OPT_CLASS_SUMS) {
+        if (value < 0 || value > 1) return fail(CPA_E_INVALID_ARG, "CLASS_SUMS=%lld outside [0, 1]", (long long)value);
+        if (value && (ctx->model == CPA_HD_LAST || ctx->dtype == CPA_F32))
+            return fail(CPA_E_INVALID_ARG, "class sums need a single-byte model (HW_LAST/HW_FIRST) and int8 traces");
+        ctx->class_sums = (int)value;
+        return CPA_OK;
+    }
     return fail(CPA_E_INVALID_ARG, "unknown option %d", option);
+}
+
+// Cross term by class sums (classsum.cu).  The call's traces are taken in
+// super-chunks of <= kCsSuper; each is counting-sorted by class per byte in
+// chunks of kCsChunk traces (a chunk's rows span < 256 MB: TLB reach), then per
+// block of <= kCsCols samples the class sums S of the super-chunk are built
+// column tile by column tile (k_cs_sum) and contracted into sum_hw.  Scratch:
+// 64 B per super-chunk trace + 16 KB per sample.
+#ifndef CS_CHUNK_LOG2
+#define CS_CHUNK_LOG2 15
+#endif
+constexpr int64_t kCsChunk = 1 << CS_CHUNK_LOG2;
+constexpr int64_t kCsSuper = 1 << 20;
+constexpr int32_t kCsCols = 8192;
+static cpa_status accumulate_class_sums(cpa_ctx *c, const void *d_w, int64_t ld, const uint8_t *d_tx, int64_t n,
+                                        int *launches)
+{
+    const int M = c->M;
+    const int64_t sup = n < kCsSuper ? n : kCsSuper;
+    const int64_t clen = sup < kCsChunk ? sup : kCsChunk;
+    const int64_t max_ch = (sup + clen - 1) / clen;
+    const int32_t cols = M < kCsCols ? M : kCsCols;
+    if (c->cs_perm_n < max_ch * clen) {
+        CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+        for (int32_t **p : {&c->d_cs_cnt, &c->d_cs_off, &c->d_cs_cur, &c->d_cs_perm}) {
+            cudaFree(*p);
+            *p = nullptr;
+        }
+        c->cs_perm_n = 0;
+        cudaError_t e = cudaMalloc(&c->d_cs_cnt, sizeof(int32_t) * 4096);
+        if (e == cudaSuccess) e = cudaMalloc(&c->d_cs_cur, sizeof(int32_t) * 4096);
+        if (e == cudaSuccess) e = cudaMalloc(&c->d_cs_off, sizeof(int32_t) * 16 * 257 * max_ch);
+        if (e == cudaSuccess) e = cudaMalloc(&c->d_cs_perm, sizeof(int32_t) * 16 * max_ch * clen);
+        if (e != cudaSuccess) return fail(CPA_E_NO_MEMORY, "class-sum scratch: %s", cudaGetErrorString(e));
+        c->cs_perm_n = max_ch * clen;
+    }
+    if (c->cs_S_words < (int64_t)4096 * cols) {
+        CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+        cudaFree(c->d_cs_S);
+        c->d_cs_S = nullptr;
+        c->cs_S_words = 0;
+        cudaError_t e = cudaMalloc(&c->d_cs_S, sizeof(int32_t) * 4096 * cols);
+        if (e != cudaSuccess) return fail(CPA_E_NO_MEMORY, "class sums: %s", cudaGetErrorString(e));
+        c->cs_S_words = (int64_t)4096 * cols;
+    }
+    const bool sgn = c->dtype == CPA_S8;
+    int64_t *hw = (int64_t *)c->accum;
+    CUDA_TRY(c->timed(2, [&] {
+                 cudaError_t e = cudaSuccess;
+                 for (int64_t s0 = 0; e == cudaSuccess && s0 < n; s0 += sup) {
+                     const int64_t sn = (n - s0) < sup ? (n - s0) : sup;
+                     // uniform chunks of clen traces (the last one shorter)
+                     const int32_t nch = (int32_t)((sn + clen - 1) / clen);
+                     for (int32_t ch = 0; e == cudaSuccess && ch < nch; ch++) {
+                         const int64_t i0 = s0 + ch * clen;
+                         const int64_t m = (s0 + sn - i0) < clen ? (s0 + sn - i0) : clen;
+                         e = cpa::launch_cs_sort(d_tx + i0 * 16, m, clen, c->d_cs_cnt, c->d_cs_off + ch * 16 * 257,
+                                                 c->d_cs_cur, c->d_cs_perm + (int64_t)ch * 16 * clen, c->num_sms,
+                                                 c->stream, launches);
+                     }
+                     for (int32_t j0 = 0; e == cudaSuccess && j0 < M; j0 += cols) {
+                         const int32_t mc = (M - j0) < cols ? (M - j0) : cols;
+                         e = cudaMemsetAsync(c->d_cs_S, 0, sizeof(int32_t) * 4096 * mc, c->stream);
+                         if (e == cudaSuccess)
+                             e = cpa::launch_cs_sum((const uint8_t *)d_w + s0 * ld, ld, nch, clen, j0, mc, sgn,
+                                                    c->d_cs_perm, c->d_cs_off, c->d_cs_S, c->num_sms, c->stream,
+                                                    launches);
+                         if (e == cudaSuccess)
+                             e = cpa::launch_cs_contract(c->d_cs_S, M, j0, mc, c->d_vtab, hw, c->stream, launches);
+                     }
+                 }
+                 return e;
+             }),
+             "class sums");
+    return CPA_OK;
 }
 
 static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, const uint8_t *d_tx, int64_t n)
@@ -361,6 +448,16 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                               &launches);
              }),
              "modelsums");
+    if (c->class_sums) {  // a4 serialised, then the class-sum cross term
+        CUDA_TRY(c->timed(1, [&] {
+                     return cpa::launch_moments_i8(d_w, ld, n, M, sgn, acc + cpa_accum_offset(M, 1),
+                                                   acc + cpa_accum_offset(M, 2), 0, c->stream, &launches);
+                 }),
+                 "moments");
+        cpa_status st = accumulate_class_sums(c, d_w, ld, d_tx, n, &launches);
+        c->launches += launches;
+        return st;
+    }
     // a4 (HBM-bound) runs concurrently with the tensor-bound cross term:
     //   overlap 1: launched after it on a low-priority side stream (its blocks
     //              fill whatever registers/threads the cross-term CTAs leave);
@@ -734,6 +831,11 @@ cpa_status cpa_destroy(cpa_ctx *c)
     cudaFree(c->d_lo);
     cudaFree(c->d_nonfinite);
     cudaFree(c->d_hist);
+    cudaFree(c->d_cs_cnt);
+    cudaFree(c->d_cs_off);
+    cudaFree(c->d_cs_cur);
+    cudaFree(c->d_cs_perm);
+    cudaFree(c->d_cs_S);
     for (auto &r : c->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);

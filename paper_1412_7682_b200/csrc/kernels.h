@@ -44,6 +44,20 @@ cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &t
                                 const uint8_t *d_vtab, double *d_hw, int *d_counter, int32_t M, int64_t N,
                                 int64_t kc_len, int num_sms, cudaStream_t stream, int *launches);
 
+// a5 for the single-byte models (HW_LAST / HW_FIRST), class sums (classsum.cu):
+// counting sort of n traces by text byte per byte (perm: 16 x n int32, off: 16 x
+// 257), per chunk of clen traces; then
+// per block of mc samples from jc0 (jc0 % 16 == 0, 16-byte rows): S [4096][mc]
+// int32 class sums += (launch_cs_sum, per trace chunk) and then sum_hw[256 b + k]
+// [jc0 + j] += sum_x f(x ^ k) S_b[x][j] (launch_cs_contract), f = row 0 of d_vtab.
+cudaError_t launch_cs_sort(const uint8_t *d_texts, int64_t n, int64_t pstride, int32_t *d_cnt, int32_t *d_off,
+                           int32_t *d_cur, int32_t *d_perm, int num_sms, cudaStream_t s, int *launches);
+cudaError_t launch_cs_sum(const uint8_t *d_w, int64_t ld, int32_t nch, int64_t clen, int32_t jc0, int32_t mc,
+                          bool w_signed, const int32_t *d_perm, const int32_t *d_off, int32_t *d_S, int num_sms,
+                          cudaStream_t s, int *launches);
+cudaError_t launch_cs_contract(const int32_t *d_S, int32_t M, int32_t jc0, int32_t mc, const uint8_t *d_f,
+                               int64_t *d_hw, cudaStream_t s, int *launches);
+
 // a1 staging: n rows of rb contiguous bytes -> rows of `pitch` bytes (multiple
 // of 16).  d_src needs >= 20 bytes of readable slack past n*rb.
 cudaError_t launch_repack(const uint8_t *d_src, int64_t rb, uint8_t *d_dst, int64_t pitch, int64_t n,

@@ -107,7 +107,10 @@ constexpr int SCHED_Q = 4;        // depth of the unit-id ring
 constexpr int V_BYTES = 32768;
 constexpr int TX_BYTES = 128 * 16;            // ciphertext rows of one stage (max BK)
 constexpr int EPI_WARPS = 4;
-constexpr int GEN_WARPS = 16;                 // every generator warp works on every stage, so
+#ifndef XT_GEN_WARPS
+#define XT_GEN_WARPS 16
+#endif
+constexpr int GEN_WARPS = XT_GEN_WARPS;       // every generator warp works on every stage, so
                                               // each waits every phase of every slot in order
                                               // (mbarrier parity waits are 1-bit)
 // readers of the unit-id ring: leader = MMA + text producer + epilogue + generators,

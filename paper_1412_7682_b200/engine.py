@@ -69,6 +69,10 @@ class Engine:
         """Global index of this context's sample 0 (sample-axis sharding)."""
         B.cpa_set_option(self.ctx, B.CPA_OPT_COL0, col0)
 
+    def set_class_sums(self, on: bool = True):
+        """CPA_OPT_CLASS_SUMS: class-sum cross term for HW_LAST / HW_FIRST (exact)."""
+        B.cpa_set_option(self.ctx, B.CPA_OPT_CLASS_SUMS, int(bool(on)))
+
     def set_overlap(self, mode: int | bool = True):
         """CPA_OPT_OVERLAP: 0 serial, 1 (True) low-priority side stream, 2 co-resident, 3 fused (default)."""
         B.cpa_set_option(self.ctx, B.CPA_OPT_OVERLAP, int(mode))

@@ -79,6 +79,10 @@ CONFIGS = {
     # the paper's wide-trace shape (dataset2: 48000 samples
     # per trace [P:168]; Fig. 5's largest run, 8000 traces [P:188, P:199])
     "W48": Workload("W48", 8000, 48000, S8, 3.0, 16.0, -40, 40),
+    # C4 / C2 with last-round Hamming-WEIGHT leakage, attacked
+    # with the HW_LAST model (class-sum cross term)
+    "C4-HW": Workload("C4-HW", 1_500_000, 5000, S8, 0.25, 32.0, -40, 40, leak_model=LEAK_HW_LAST),
+    "C2-HW": Workload("C2-HW", 2000, 5000, S8, 3.0, 16.0, -40, 40, leak_model=LEAK_HW_LAST),
 }
 
 

@@ -302,3 +302,77 @@ def test_fused_moments_32bit_bound(P, dt, v):
     assert np.all(s["sum_w"] == n * v) and np.all(s["sum_w2"] == n * v * v)
     hw = s["sum_hw"].reshape(16, 256, m).sum(axis=1)
     assert np.all(hw == 1024 * n * v)
+
+
+def run_cs(P, texts, W, model, chunks=None, class_sums=True):
+    dtype = {np.int8: P.CPA_S8, np.uint8: P.CPA_U8}[W.dtype.type]
+    eng = P.Engine(W.shape[1], dtype, model, 0)
+    eng.set_class_sums(class_sums)
+    ld = (W.shape[1] + 15) // 16 * 16
+    Wp = np.zeros((W.shape[0], ld), W.dtype)
+    Wp[:, :W.shape[1]] = W
+    dW = torch.from_numpy(Wp).cuda()
+    dT = torch.from_numpy(np.ascontiguousarray(texts)).cuda()
+    bounds = chunks or [0, W.shape[0]]
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        eng.accumulate(dW[a:b, :W.shape[1]], dT[a:b])
+    out = eng.finalize(want_rho=True)
+    sums = dict(sum_hw=eng.sum_hw.cpu().numpy(), sum_w=eng.sum_w.cpu().numpy(),
+                sum_w2=eng.sum_w2.cpu().numpy(), sum_h=eng.sum_h.cpu().numpy(),
+                sum_h2=eng.sum_h2.cpu().numpy(), n=int(eng.n.cpu().numpy()[0]))
+    eng.close()
+    return sums, out
+
+
+@pytest.mark.parametrize("model", [O.HW_LAST, O.HW_FIRST])
+@pytest.mark.parametrize("dt", [np.int8, np.uint8])
+def test_class_sums_exact(P, model, dt):
+    """Class-sum cross term (CPA_OPT_CLASS_SUMS): for the
+    single-byte models sum_i H W = sum_x f(x ^ k) S_b[x][j] exactly, so every
+    sum, rho, maximum and rank equals the oracle's (and the tensor-core path's)
+    bit for bit.  Ragged N and M (half-empty last column tile), several calls."""
+    rng = np.random.default_rng(31 + model)
+    n, m = 3 * 128 + 61, 300
+    lo, hi = (-128, 128) if dt is np.int8 else (0, 256)
+    texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    texts[:40, 3] = 7                                  # a heavy class
+    W = rng.integers(lo, hi, (n, m)).astype(dt)
+    W[:, 5] = lo
+    ref = O.attack_i8(model, texts, W)
+    for chunks in (None, [0, 1, 200, n]):
+        sums, out = run_cs(P, texts, W, MODEL[model], chunks)
+        assert_parity(sums, out, ref)
+    s0, o0 = run_cs(P, texts, W, MODEL[model], class_sums=False)
+    assert np.array_equal(s0["sum_hw"], sums["sum_hw"])
+
+
+def test_class_sums_column_blocks_and_key(P):
+    """M > 8192 (two column blocks of the class-sum scratch) on HW_LAST leakage:
+    closed form over every column, oracle on sampled columns, key recovered."""
+    w = S.CONFIGS["C2-HW"].replace(n=600, m=8200, a=6.0)
+    texts, W = S.dataset(w)
+    sums, out = run_cs(P, texts, W, 1)
+    cols = np.array(sorted(set(w.leak_positions()) | {0, 8191, 8192, 8199}), np.int32)
+    assert np.array_equal(sums["sum_hw"][:, cols], O.cross_sums_i8(O.HW_LAST, texts, W, cols))
+    sw, _ = O.trace_sums_i8(W)
+    assert np.array_equal(sums["sum_hw"].reshape(16, 256, -1).sum(axis=1), 1024 * np.broadcast_to(sw, (16, w.m)))
+    assert out["master_key"] == w.key
+
+
+def test_class_sums_chunked_sort_and_errors(P):
+    """> 2^20 traces in one call (two super-chunks, ragged sort chunks), closed form; class sums on
+    an HD_LAST context are refused with CPA_E_INVALID_ARG."""
+    n, m = (1 << 20) + 300, 16
+    rng = np.random.default_rng(5)
+    texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    W = rng.integers(-128, 128, (n, m)).astype(np.int8)
+    sums, _ = run_cs(P, texts, W, 1)
+    sw, sw2 = O.trace_sums_i8(W)
+    assert np.array_equal(sums["sum_w"], sw)
+    assert np.array_equal(sums["sum_hw"].reshape(16, 256, m).sum(axis=1), 1024 * np.broadcast_to(sw, (16, m)))
+    ref = O.cross_sums_i8(O.HW_LAST, texts, W, np.array([15], np.int32))
+    assert np.array_equal(sums["sum_hw"][:, [15]], ref)
+    eng = P.Engine(16, P.CPA_S8, 0, 0)
+    with pytest.raises(Exception):
+        eng.set_class_sums(True)
+    eng.close()
