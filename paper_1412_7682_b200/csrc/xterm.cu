@@ -27,10 +27,10 @@
 //     a few W blocks in L2 (W streams from HBM about once).
 //   * Fused a4 (moments_pass): the epilogue warps, idle during the mainloop,
 //     sum W and W^2 over 1/16 of the rows of every W stage they see.
-// Warp roles (768 threads per CTA): w0 scheduler (leader) + W TMA producer,
+// Warp roles (512 threads per CTA): w0 scheduler (leader) + W TMA producer,
 // w1 MMA issuer (leader), w2 TMEM owner, w3
 // ciphertext producer, w4-7 epilogue (TMEM lanes 32*(w%4)...) + fused moments,
-// w8-23 H generators.
+// w8-15 H generators (8: measured ~1% faster than 16 once NT = 2 halved the generation).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -108,7 +108,7 @@ constexpr int V_BYTES = 32768;
 constexpr int TX_BYTES = 128 * 16;            // ciphertext rows of one stage (max BK)
 constexpr int EPI_WARPS = 4;
 #ifndef XT_GEN_WARPS
-#define XT_GEN_WARPS 16
+#define XT_GEN_WARPS 8
 #endif
 constexpr int GEN_WARPS = XT_GEN_WARPS;       // every generator warp works on every stage, so
                                               // each waits every phase of every slot in order
