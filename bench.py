@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--class-sums", choices=["0", "1"], default="0",
                     help="CPA_OPT_CLASS_SUMS=1: class-sum cross term for HW_LAST/HW_FIRST workloads "
                          "(C4-HW); default: the tensor-core contraction (faster on B200, DESIGN.md)")
+    ap.add_argument("--fuse-hist", choices=["0", "1"], default="0",
+                    help="CPA_OPT_FUSE_HIST: a3's byte-pair histogram counted inside the cross-term kernel")
     ap.add_argument("--chunk", type=int, default=0,
                     help="stream the traces in chunks of this many, finalizing after every round "
                          "(key-rank curve); default for C5: 65536")
@@ -260,6 +262,7 @@ def main():
     class_sums = args.class_sums == "1" and not is_f32
     if class_sums:
         eng.set_class_sums(True)
+    eng.set_fuse_hist(args.fuse_hist == "1")
     eng.set_col0(j0)
     ovl_mode = 0 if args.no_overlap else (args.overlap_mode if args.overlap_mode is not None else OVERLAP_DEFAULT)
     eng.set_overlap(ovl_mode)

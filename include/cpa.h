@@ -211,9 +211,15 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *                   single-byte model and s8/u8 traces, else
  *                   CPA_E_INVALID_ARG.  Allocates 64 B per trace (<= 2^17
  *                   traces per chunk) + 16 KB per sample (<= 8192 samples per
- *                   block) of scratch on first use.  Default 0 (tensor cores). */
+ *                   block) of scratch on first use.  Default 0 (tensor cores).
+ *   CPA_OPT_FUSE_HIST: 1 = for calls of >= 65536 traces the cross-term kernel
+ *                   counts the (c_b, c_SR(b)) byte pairs that a3's sum H,
+ *                   sum H^2 are contracted from [P:75] as it generates H (no
+ *                   separate histogram pass); 0 (default) = separate pass
+ *                   (the fused counting cost the cross term what the pass
+ *                   cost).  Same exact sums either way.           */
 enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2, CPA_OPT_OVERLAP = 3, CPA_OPT_STAGE_BYTES = 4,
-       CPA_OPT_COL0 = 5, CPA_OPT_CLASS_SUMS = 6 };
+       CPA_OPT_COL0 = 5, CPA_OPT_CLASS_SUMS = 6, CPA_OPT_FUSE_HIST = 7 };
 CPA_API cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value);
 
 /* Per-phase device time (ms) and launch count since the last call, from the

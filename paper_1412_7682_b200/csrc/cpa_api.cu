@@ -96,6 +96,7 @@ struct cpa_ctx {
     // CPA_OPT_CLASS_SUMS (HW_LAST / HW_FIRST, int8 traces): class-sum cross term
     // (classsum.cu); scratch allocated on first use
     int class_sums = 0;
+    int fuse_hist = 0;  // CPA_OPT_FUSE_HIST: a3 byte-pair histogram counted by the cross-term kernel (measured neutral)
     int32_t *d_cs_cnt = nullptr, *d_cs_off = nullptr, *d_cs_cur = nullptr, *d_cs_perm = nullptr, *d_cs_S = nullptr;
     int64_t cs_perm_n = 0, cs_S_words = 0;
     // CPA_OPT_TIMING: CUDA events recorded on `stream` around every launch
@@ -290,6 +291,11 @@ cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
         ctx->kchunk = value;
         return CPA_OK;
     }
+    if (option == CPA_OPT_FUSE_HIST) {
+        if (value < 0 || value > 1) return fail(CPA_E_INVALID_ARG, "FUSE_HIST=%lld outside [0, 1]", (long long)value);
+        ctx->fuse_hist = (int)value;
+        return CPA_OK;
+    }
     if (option == CPA_OPT_CLASS_SUMS) {
         if (value < 0 || value > 1) return fail(CPA_E_INVALID_ARG, "CLASS_SUMS=%lld outside [0, 1]", (long long)value);
         if (value && (ctx->model == CPA_HD_LAST || ctx->dtype == CPA_F32))
@@ -379,14 +385,19 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
 {
     const int M = c->M;
     int launches = 0;
+    // a3 for large N: the cross-term kernel counts the byte pairs as it
+    // generates H (CPA_OPT_FUSE_HIST), only the contraction runs here
+    const bool fhist = c->fuse_hist && !c->class_sums && n >= cpa::kHistMinTraces;
+    if (fhist) CUDA_TRY(cpa::launch_hist_clear(c->d_hist, c->stream), "hist clear");
     if (c->dtype == CPA_F32) {
         double *acc = (double *)c->accum;
-        CUDA_TRY(c->timed(0, [&] {
-                     return cpa::launch_modelsums_f64(d_tx, n, c->d_vtab, c->d_hist, acc + cpa_accum_offset(M, 3),
-                                                      acc + cpa_accum_offset(M, 4), acc + cpa_accum_offset(M, 5),
-                                                      c->stream, &launches);
-                 }),
-                 "modelsums");
+        if (!fhist)
+            CUDA_TRY(c->timed(0, [&] {
+                         return cpa::launch_modelsums_f64(d_tx, n, c->d_vtab, c->d_hist, acc + cpa_accum_offset(M, 3),
+                                                          acc + cpa_accum_offset(M, 4), acc + cpa_accum_offset(M, 5),
+                                                          c->stream, &launches);
+                     }),
+                     "modelsums");
         // per-sample offsets (centring keeps the bf16 hi/lo split and the fp32
         // accumulation accurate; rho is invariant to them [S:285]): unless the
         // caller set them, take the first trace of the first accumulate call
@@ -433,21 +444,30 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                          : cpa::xterm_f32_auto_kchunk(M, m, c->num_sms);
             CUDA_TRY(c->timed(2, [&] {
                          return cpa::launch_xterm_bf16x2(mh, ml, d_tx + i0 * 16, c->d_vtab, acc, c->d_counter, M, m,
-                                                         kc, c->num_sms, c->stream, &launches);
+                                                         kc, c->num_sms, c->stream, &launches,
+                                                         fhist ? c->d_hist : nullptr);
                      }),
                      "xterm_bf16x2");
         }
+        if (fhist)
+            CUDA_TRY(c->timed(0, [&] {
+                         return cpa::launch_hist_contract_f64(c->d_hist, n, c->d_vtab, acc + cpa_accum_offset(M, 3),
+                                                              acc + cpa_accum_offset(M, 4),
+                                                              acc + cpa_accum_offset(M, 5), c->stream, &launches);
+                     }),
+                     "hist contract");
         c->launches += launches;
         return CPA_OK;
     }
     int64_t *acc = (int64_t *)c->accum;
     const bool sgn = c->dtype == CPA_S8;
-    CUDA_TRY(c->timed(0, [&] {
-                 return cpa::launch_modelsums(d_tx, n, c->d_vtab, c->d_hist, acc + cpa_accum_offset(M, 3),
-                                              acc + cpa_accum_offset(M, 4), acc + cpa_accum_offset(M, 5), c->stream,
-                                              &launches);
-             }),
-             "modelsums");
+    if (!fhist)
+        CUDA_TRY(c->timed(0, [&] {
+                     return cpa::launch_modelsums(d_tx, n, c->d_vtab, c->d_hist, acc + cpa_accum_offset(M, 3),
+                                                  acc + cpa_accum_offset(M, 4), acc + cpa_accum_offset(M, 5),
+                                                  c->stream, &launches);
+                 }),
+                 "modelsums");
     if (c->class_sums) {  // a4 serialised, then the class-sum cross term
         CUDA_TRY(c->timed(1, [&] {
                      return cpa::launch_moments_i8(d_w, ld, n, M, sgn, acc + cpa_accum_offset(M, 1),
@@ -492,10 +512,18 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     CUDA_TRY(c->timed(2, [&] {
                  return cpa::launch_xterm_i8(tmap, d_tx, c->d_vtab, acc, c->d_counter, M, n, kc, sgn, c->num_sms,
                                              c->stream, &launches, fused ? acc + cpa_accum_offset(M, 1) : nullptr,
-                                             fused ? acc + cpa_accum_offset(M, 2) : nullptr);
+                                             fused ? acc + cpa_accum_offset(M, 2) : nullptr,
+                                             fhist ? c->d_hist : nullptr);
              }),
              "xterm_i8");
     if (!fused && mode == 1) CUDA_TRY(moments(), "moments");
+    if (fhist)
+        CUDA_TRY(c->timed(0, [&] {
+                     return cpa::launch_hist_contract(c->d_hist, n, c->d_vtab, acc + cpa_accum_offset(M, 3),
+                                                      acc + cpa_accum_offset(M, 4), acc + cpa_accum_offset(M, 5),
+                                                      c->stream, &launches);
+                 }),
+                 "hist contract");
     if (mode) {
         CUDA_TRY(cudaEventRecord(c->ev_join, mst), "join");
         CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "join");

@@ -446,6 +446,23 @@ k_hist_contract(const uint32_t *__restrict__ hist, const uint8_t *__restrict__ v
 }
 
 template <typename Acc>
+cudaError_t hist_contract(const uint32_t *d_hist, int64_t n, const uint8_t *d_vtab, Acc *d_sum_h, Acc *d_sum_h2,
+                          Acc *d_count, cudaStream_t s, int *launches)
+{
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_hist_contract<Acc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             65536 + HC_X * 256 * 4);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_hist_contract<Acc><<<dim3(256 / HC_X, 16), 256, 65536 + HC_X * 256 * 4, s>>>(d_hist, d_vtab, d_sum_h, d_sum_h2,
+                                                                                   d_count, n);
+    if (launches) (*launches)++;
+    return cudaGetLastError();
+}
+
+template <typename Acc>
 cudaError_t modelsums(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab, uint32_t *d_hist, Acc *d_sum_h,
                       Acc *d_sum_h2, Acc *d_count, cudaStream_t s, int *launches)
 {
@@ -489,6 +506,23 @@ cudaError_t launch_modelsums_f64(const uint8_t *d_texts, int64_t n, const uint8_
                                  double *d_sum_h, double *d_sum_h2, double *d_count, cudaStream_t s, int *launches)
 {
     return modelsums<double>(d_texts, n, d_vtab, d_hist, d_sum_h, d_sum_h2, d_count, s, launches);
+}
+
+cudaError_t launch_hist_clear(uint32_t *d_hist, cudaStream_t s)
+{
+    return cudaMemsetAsync(d_hist, 0, sizeof(uint32_t) * 16 * 65536, s);
+}
+
+cudaError_t launch_hist_contract(const uint32_t *d_hist, int64_t n, const uint8_t *d_vtab, int64_t *d_sum_h,
+                                 int64_t *d_sum_h2, int64_t *d_count, cudaStream_t s, int *launches)
+{
+    return hist_contract<int64_t>(d_hist, n, d_vtab, d_sum_h, d_sum_h2, d_count, s, launches);
+}
+
+cudaError_t launch_hist_contract_f64(const uint32_t *d_hist, int64_t n, const uint8_t *d_vtab, double *d_sum_h,
+                                     double *d_sum_h2, double *d_count, cudaStream_t s, int *launches)
+{
+    return hist_contract<double>(d_hist, n, d_vtab, d_sum_h, d_sum_h2, d_count, s, launches);
 }
 
 cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M, bool w_signed,

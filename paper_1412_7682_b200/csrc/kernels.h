@@ -18,6 +18,14 @@ cudaError_t launch_modelsums_f64(const uint8_t *d_texts, int64_t n, const uint8_
                                  double *d_sum_h, double *d_sum_h2, double *d_count,
                                  cudaStream_t s, int *launches);
 
+// a3 with the histogram filled by the cross-term kernel (d_hist passed to
+// launch_xterm_*, cleared first): only the contraction (+ n to the count)
+cudaError_t launch_hist_clear(uint32_t *d_hist, cudaStream_t s);
+cudaError_t launch_hist_contract(const uint32_t *d_hist, int64_t n, const uint8_t *d_vtab, int64_t *d_sum_h,
+                                 int64_t *d_sum_h2, int64_t *d_count, cudaStream_t s, int *launches);
+cudaError_t launch_hist_contract_f64(const uint32_t *d_hist, int64_t n, const uint8_t *d_vtab, double *d_sum_h,
+                                     double *d_sum_h2, double *d_count, cudaStream_t s, int *launches);
+
 // a4: Phase 2 trace moments sum W, sum W^2 [P:79] (int8 traces, exact int64)
 cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M, bool w_signed,
                               int64_t *d_sum_w, int64_t *d_sum_w2, int blocks_per_sm, cudaStream_t s,
@@ -30,7 +38,7 @@ int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms);
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
                             int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
                             int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr,
-                            int64_t *d_sum_w2 = nullptr);
+                            int64_t *d_sum_w2 = nullptr, uint32_t *d_hist = nullptr);
 
 // a6: float traces.  Split pre-pass: w' = w - offset[j] (fp32), hi = bf16(w'),
 // lo = bf16(w' - hi) into [n][ldh] bf16 planes; fp64 sum w', sum w'^2; sets
@@ -42,7 +50,8 @@ cudaError_t launch_split_f32(const float *d_w, int64_t ld, int64_t n, int32_t M,
 int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms);
 cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
                                 const uint8_t *d_vtab, double *d_hw, int *d_counter, int32_t M, int64_t N,
-                                int64_t kc_len, int num_sms, cudaStream_t stream, int *launches);
+                                int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
+                                uint32_t *d_hist = nullptr);
 
 // a5 for the single-byte models (HW_LAST / HW_FIRST), class sums (classsum.cu):
 // counting sort of n traces by text byte per byte (perm: 16 x n int32, off: 16 x

@@ -159,6 +159,10 @@ struct Params {
     int64_t *sum_w;
     int64_t *sum_w2;
     int32_t w_signed;
+    // fused a3 histogram (null = off): the leader's generators of the units of
+    // N tile group 0 count each trace's (c_b, c_SR(b)) pair of their key byte
+    // (k_hist_contract turns the counts into sum H, sum H^2 afterwards)
+    uint32_t *hist;
 };
 
 template <bool F32>
@@ -612,6 +616,8 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 uint32_t desc = 0;
                 if (lane < ROWS * C::KB) {
                     const uint32_t cb = tx[drow * 16 + b + dkb], cs = tx[drow * 16 + dsrc];
+                    if (p.hist != nullptr && nt == 0 && leader && tb + drow < t1)  // each (trace, byte) once
+                        atomicAdd(p.hist + (((uint32_t)(b + dkb) << 16) | (cb << 8) | cs), 1u);
                     const uint32_t hi = cb >> 4, lo = cb & 15;
                     // output byte jj of an even word takes nibble m = jj ^ (lo & 7) of its
                     // 8-nibble group: even m from the low-nibble word (PRMT 0-3), odd from
@@ -693,7 +699,7 @@ template <bool F32>
 cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *d_texts, const uint8_t *d_vtab,
                    void *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, uint32_t idesc, int num_sms,
                    cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr, int64_t *d_sum_w2 = nullptr,
-                   bool w_signed = true)
+                   bool w_signed = true, uint32_t *d_hist = nullptr)
 {
     using Cf = Cfg<F32>;
     Params p;
@@ -712,6 +718,7 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *
     p.sum_w = d_sum_w;
     p.sum_w2 = d_sum_w2;
     p.w_signed = w_signed ? 1 : 0;
+    p.hist = d_hist;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_xterm<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
@@ -774,18 +781,20 @@ int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms)
 
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
                             int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
-                            int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w, int64_t *d_sum_w2)
+                            int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w, int64_t *d_sum_w2,
+                            uint32_t *d_hist)
 {
     return launch<false>(tmap_w, tmap_w, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
-                         idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, d_sum_w, d_sum_w2, w_signed);
+                         idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, d_sum_w, d_sum_w2, w_signed,
+                         d_hist);
 }
 
 cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
                                 const uint8_t *d_vtab, double *d_hw, int *d_counter, int32_t M, int64_t N,
-                                int64_t kc_len, int num_sms, cudaStream_t stream, int *launches)
+                                int64_t kc_len, int num_sms, cudaStream_t stream, int *launches, uint32_t *d_hist)
 {
     return launch<true>(tmap_hi, tmap_lo, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len, idesc_bf16(2 * BMC, BN),
-                        num_sms, stream, launches);
+                        num_sms, stream, launches, nullptr, nullptr, true, d_hist);
 }
 
 }  // namespace cpa

@@ -69,6 +69,10 @@ class Engine:
         """Global index of this context's sample 0 (sample-axis sharding)."""
         B.cpa_set_option(self.ctx, B.CPA_OPT_COL0, col0)
 
+    def set_fuse_hist(self, on: bool = True):
+        """CPA_OPT_FUSE_HIST: a3's byte-pair histogram counted inside the cross-term kernel (default off)."""
+        B.cpa_set_option(self.ctx, B.CPA_OPT_FUSE_HIST, int(bool(on)))
+
     def set_class_sums(self, on: bool = True):
         """CPA_OPT_CLASS_SUMS: class-sum cross term for HW_LAST / HW_FIRST (exact)."""
         B.cpa_set_option(self.ctx, B.CPA_OPT_CLASS_SUMS, int(bool(on)))

@@ -23,7 +23,7 @@ def P():
 MODEL = {O.HD_LAST: 0, O.HW_LAST: 1, O.HW_FIRST: 2}
 
 
-def run_gpu(P, texts, W, model=0, kchunk=0, chunks=None, want_rho=True, overlap=True, mode=None):
+def run_gpu(P, texts, W, model=0, kchunk=0, chunks=None, want_rho=True, overlap=True, mode=None, fuse_hist=None):
     dtype = {np.int8: P.CPA_S8, np.uint8: P.CPA_U8}[W.dtype.type]
     eng = P.Engine(W.shape[1], dtype, model, 0)
     if kchunk:
@@ -32,6 +32,8 @@ def run_gpu(P, texts, W, model=0, kchunk=0, chunks=None, want_rho=True, overlap=
         eng.set_overlap(False)
     if mode is not None:
         eng.set_overlap(mode)
+    if fuse_hist is not None:
+        eng.set_fuse_hist(fuse_hist)
     bounds = chunks or [0, W.shape[0]]
     # pad rows to a 16-byte multiple (TMA stride rule); ld > M exercises strides
     ld = (W.shape[1] + 15) // 16 * 16
@@ -248,16 +250,19 @@ def test_synth_device_generator_matches_host(P):
 
 @pytest.mark.parametrize("model", [O.HD_LAST, O.HW_LAST, O.HW_FIRST])
 def test_model_sums_histogram_path(P, model):
-    """N >= 65536 in one call takes the byte-pair histogram path for a3; it must
-    equal the oracle and the direct path (chunks < 65536) bit for bit."""
+    """N >= 65536 in one call takes the byte-pair histogram path for a3, with the
+    pairs counted by a separate pass (default) or inside the cross-term kernel
+    (CPA_OPT_FUSE_HIST; M = 600 spans two N-tile groups, only group 0 counts);
+    both must equal the oracle and the direct path (chunks < 65536) bit for bit."""
     rng = np.random.default_rng(31 + model)
-    n, m = 70001, 32
+    n, m = 70001, 600
     texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
     W = rng.integers(-128, 128, (n, m)).astype(np.int8)
     one, _ = run_gpu(P, texts, W, model=MODEL[model], want_rho=False)
+    sep, _ = run_gpu(P, texts, W, model=MODEL[model], want_rho=False, fuse_hist=True)
     chunked, _ = run_gpu(P, texts, W, model=MODEL[model], chunks=[0, 30000, 60000, n], want_rho=False)
     sh, sh2 = O.model_sums(model, texts)
-    for s in (one, chunked):
+    for s in (one, sep, chunked):
         assert np.array_equal(s["sum_h"], sh) and np.array_equal(s["sum_h2"], sh2)
         assert s["n"] == n
     assert np.array_equal(one["sum_hw"], chunked["sum_hw"])
