@@ -488,18 +488,27 @@ def run_stream(args, w, dev, world, rank, local):
     st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, local)
     stream = st.eng.stream
 
+    # non-final checkpoints run without blocking (one GPU): their ranks land in
+    # rank_buf and are read once per step; multi-GPU checkpoints block
+    rank_buf = torch.empty((len(rounds), 4096), dtype=torch.int32, device=dev)
+
     def step(curve=None):
         st.reset()
         o = 0
+        sync_ranks = {}
         for j, rnd in enumerate(rounds):
             for r, i0, i1 in rnd:
                 if r == rank:
                     st.add(dW[o:o + i1 - i0, :w.m], dT[o:o + i1 - i0])
                     o += i1 - i0
-            out = st.checkpoint(want_rho=(j == len(rounds) - 1))
-            ranks = out["rank"][key_idx].tolist()
-            if curve is not None:
-                curve.add(rnd[-1][2], ranks)
+            last = j == len(rounds) - 1
+            if last or not st.checkpoint_async(rank_buf[j]):
+                out = st.checkpoint(want_rho=last)
+                sync_ranks[j] = out["rank"]
+        if curve is not None:
+            for j, rnd in enumerate(rounds):
+                rk = sync_ranks.get(j, rank_buf[j])
+                curve.add(rnd[-1][2], rk[key_idx].tolist())
         return out
 
     def barrier():

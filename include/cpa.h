@@ -135,6 +135,21 @@ typedef struct {
 CPA_API cpa_status cpa_finalize(cpa_ctx *ctx, double *d_rho, double *d_maxabs,
                         int32_t *d_argmax, int32_t *d_rank, cpa_result *res);
 
+/* Phase 3 + 4 enqueued on the context's stream WITHOUT blocking: streamed
+ * checkpoints (the key-rank curve of config C5), where a synchronous finalize
+ * after every chunk would leave the GPU idle while the host waits and then
+ * launches the next chunk.  Same kernels and arithmetic as cpa_finalize (bit
+ * for bit); results land in device memory in stream order, so a later
+ * cpa_accumulate on the same stream may run before the caller reads them.
+ *   d_rho, d_maxabs, d_argmax, d_rank: as cpa_finalize (NULL = internal
+ *             scratch for maxabs/argmax/rank);
+ *   d_best    optional [32] int32: best sub-key per byte [0..15] and its peak
+ *             sample [16..31].
+ * No host-side checks: N < 2 gives rho = 0 (zero variance), and the
+ * non-finite flag (f32) is reported only by the blocking cpa_finalize.      */
+CPA_API cpa_status cpa_finalize_async(cpa_ctx *ctx, double *d_rho, double *d_maxabs, int32_t *d_argmax,
+                                      int32_t *d_rank, int32_t *d_best);
+
 /* ---- sharded Phase 3/4 (multi-GPU) ---------------------------
  * Two ways to split the work of Phase 3 [P:81-83] over G ranks:
  *  (rows)    trace-sharded accumulation; ONE reduce-scatter of the sum_hw rows

@@ -26,7 +26,7 @@ FIELD_HW, FIELD_W, FIELD_W2, FIELD_H, FIELD_H2, FIELD_N = range(6)
 # every symbol include/cpa.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = (
     "cpa_accum_words", "cpa_accum_bytes", "cpa_accum_offset", "cpa_init", "cpa_accumulate",
-    "cpa_accumulate_host", "cpa_finalize", "cpa_finalize_rows", "cpa_select", "cpa_reset", "cpa_sync", "cpa_destroy",
+    "cpa_accumulate_host", "cpa_finalize", "cpa_finalize_async", "cpa_finalize_rows", "cpa_select", "cpa_reset", "cpa_sync", "cpa_destroy",
     "cpa_set_offsets", "cpa_set_option", "cpa_phase_times", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
     "cpa_aes_expand_key", "cpa_aes_invert_key_schedule",
 )
@@ -60,6 +60,7 @@ def _load():
         "cpa_accumulate_host": (ST, [P, P, I64, P, I64]),
         "cpa_finalize": (ST, [P, P, P, P, P, C.POINTER(cpa_result)]),
         "cpa_finalize_rows": (ST, [P, I32, I32, P, P, P, P]),
+        "cpa_finalize_async": (ST, [P, P, P, P, P, P]),
         "cpa_select": (ST, [P, I32, P, P, P, P, C.POINTER(cpa_result)]),
         "cpa_reset": (ST, [P]),
         "cpa_sync": (ST, [P]),
@@ -132,6 +133,11 @@ def cpa_finalize(ctx, d_rho=None, d_maxabs=None, d_argmax=None, d_rank=None) -> 
     _check(_lib.cpa_finalize(ctx, _ptr(d_rho), _ptr(d_maxabs), _ptr(d_argmax), _ptr(d_rank),
                              C.byref(res)), "cpa_finalize")
     return res
+
+
+def cpa_finalize_async(ctx, d_rho=None, d_maxabs=None, d_argmax=None, d_rank=None, d_best=None):
+    _check(_lib.cpa_finalize_async(ctx, _ptr(d_rho), _ptr(d_maxabs), _ptr(d_argmax), _ptr(d_rank), _ptr(d_best)),
+           "cpa_finalize_async")
 
 
 def cpa_finalize_rows(ctx, h0: int, h1: int, d_rho, d_maxabs, d_argmax, d_peak):

@@ -753,6 +753,21 @@ cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_
     return st;
 }
 
+cpa_status cpa_finalize_async(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_argmax, int32_t *d_rank,
+                              int32_t *d_best)
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    cpa::FinalizeOut o = outputs(c, d_rho, d_maxabs, d_argmax, nullptr, d_rank);
+    if (d_best) o.best = d_best;
+    int launches = 0;
+    cpa_status st = phase3(c, o, &launches);
+    if (st == CPA_OK)
+        CUDA_TRY(c->timed(4, [&] { return cpa::launch_phase4(o, c->stream, &launches); }), "phase4");
+    c->launches += launches;
+    return st;
+}
+
 cpa_status cpa_finalize_rows(cpa_ctx *c, int32_t h0, int32_t h1, double *d_rho, double *d_maxabs,
                              int32_t *d_argmax, double *d_peak)
 {

@@ -117,6 +117,11 @@ class Engine:
                     peak_sample=list(res.peak_sample), peak_rho=list(res.peak_rho),
                     n_traces=res.n_traces)
 
+    def finalize_async(self, rank, maxabs=None, argmax=None, best=None, rho=None):
+        """Phase 3 + 4 enqueued without blocking (cpa_finalize_async): rank [4096]
+        int32 (and the optional maxabs/argmax/best[32]/rho) fill in stream order."""
+        B.cpa_finalize_async(self.ctx, rho, maxabs, argmax, rank, best)
+
     def maxima_buffers(self, G: int = 1):
         """Zeroed per-hypothesis maxima (maxabs, argmax, peak) for G stacked shards."""
         dev = self.device

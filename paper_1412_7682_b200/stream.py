@@ -104,6 +104,17 @@ class StreamingAttack:
         out.update(rows=(h0, h1), rho=rho)
         return out
 
+    def checkpoint_async(self, rank_out) -> bool:
+        """Single GPU: enqueue the checkpoint's Phases 3-4 without blocking, the
+        4096 ranks into rank_out (a device int32 [4096] view), and return True;
+        the caller reads them after its last checkpoint (one D2H for the whole
+        curve).  Multi-GPU checkpoints block (collectives + sharded finalize):
+        returns False and the caller uses checkpoint()."""
+        if self.view is not None:
+            return False
+        self.eng.finalize_async(rank_out)
+        return True
+
     def reset(self):
         self.eng.reset()
         self.n_local = 0

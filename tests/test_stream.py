@@ -153,3 +153,40 @@ def test_streaming_checkpoint_ranks_match_oracle_prefixes():
     assert curve.points[-1][1] == known_key_ranks(ref["rank"], rk)
     assert curve.traces_to_key() is not None   # C1 recovers the key at N = 500
     st.close()
+
+
+@pytest.mark.gpu
+def test_async_checkpoints_equal_blocking_ones():
+    """cpa_finalize_async (the non-blocking streamed checkpoint) enqueues the
+    same Phase 3-4 kernels as cpa_finalize: the ranks written at every
+    checkpoint, while later chunks are accumulated on the same stream, equal
+    those of a blocking finalize at that prefix (and the oracle's at the end)."""
+    from oracle import oracle as O
+    from synth import synth as S
+    import paper_1412_7682_b200 as P
+    w = S.CONFIGS["C1"]
+    texts, W = S.dataset(w)
+    ld = (w.m + 15) // 16 * 16
+    Wp = np.zeros((w.n, ld), np.int8)
+    Wp[:, :w.m] = W
+    dW = torch.from_numpy(Wp).cuda()[:, :w.m]
+    dT = torch.from_numpy(texts).cuda()
+    rounds = chunk_rounds(w.n, 96)
+    a = P.StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, 0)
+    b = P.StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, 0)
+    buf = torch.full((len(rounds), 4096), -1, dtype=torch.int32, device="cuda")
+    blocking = []
+    for j, rnd in enumerate(rounds):
+        for _, i0, i1 in rnd:
+            a.add(dW[i0:i1], dT[i0:i1])
+            b.add(dW[i0:i1], dT[i0:i1])
+        assert a.checkpoint_async(buf[j])
+        blocking.append(b.checkpoint()["rank"].cpu().numpy())
+    a.eng.sync()
+    got = buf.cpu().numpy()
+    for j in range(len(rounds)):
+        assert np.array_equal(got[j], blocking[j]), j
+    ref = O.attack_i8(O.HD_LAST, texts, W)
+    assert np.array_equal(got[-1], ref["rank"])
+    a.close()
+    b.close()
