@@ -32,6 +32,8 @@ INT8_PER_BF16 = 4.5 / 2.25  # nominal dense int8 : bf16 ratio (B200_PROFILING.md
 CPU_SAMPLE_TRACES = 131072
 CPU_SAMPLE_COLS = 4
 MODEL_NAMES = ("HD last-round", "HW last-round", "HW first-round")
+# tcgen05 MAC/clk/SM (tools/pair_bench: kind::i8 8192, kind::f16 4096, both measured 100% reachable)
+MMA_MACS_PER_CLK_SM = {False: 8192, True: 4096}
 OVERLAP_DEFAULT = 3   # CPA_OPT_OVERLAP: a4 fused into the cross-term kernel (int8 traces)
 
 
@@ -348,18 +350,26 @@ def main():
     # run) is below what this int8 kernel sustains, so it cannot be a ceiling
     peak = peaks["bf16_tflops"] * ratio
     traffic = None
+    ncu_xt = None
     tp = os.path.join(ROOT, "profiles", "xterm_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)
         if tj.get("config") == w.name and tj.get("n_gpus", 1) == world:
             traffic = tj.get("dram_bytes_per_launch")
+            ncu_xt = {k: tj.get(k) for k in ("tensor_active_pct", "sm_mhz", "duration_ms", "tag")}
     roofline = {"kernel": "k_xterm<F32>" if is_f32 else "k_xterm<I8>", "bound": "tensor", "achieved": achieved,
                 "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": (f"{src} bf16_tflops (burst)" if is_f32 else
                                 f"{src} bf16_tflops (burst) x {INT8_PER_BF16:g} (int8:bf16 nominal ratio)"),
                 "frac_of_sustained": achieved / (peaks["bf16_tflops_sustained"] * ratio),
                 "algorithmic_ops_per_launch": ops, "ms_per_launch": xt_ms}
+    if ncu_xt and ncu_xt.get("sm_mhz"):
+        # the same kernel under ncu: tensor-pipe activity and its own SM clock; the
+        # tcgen05 issue ceiling at that clock is what the 1000 W cap allows
+        ceil = MMA_MACS_PER_CLK_SM[is_f32] * 2 * 148 * ncu_xt["sm_mhz"] * 1e6 / 1e12
+        roofline["ncu"] = dict(ncu_xt, mma_ceiling_at_kernel_clock=ceil,
+                               frac_of_ceiling_under_ncu=ops / (ncu_xt["duration_ms"] * 1e-3) / 1e12 / ceil)
     if class_sums:  # NEXT-4 path: HBM-bound by design (16 adds per trace byte), so report it as such
         gbs = n_local * m_local / (xt_ms * 1e-3) / 1e9
         roofline = {"kernel": "class sums (k_cs_sort + k_cs_sum + k_cs_contract)", "bound": "hbm",
@@ -375,10 +385,13 @@ def main():
     mo_launch_ms = phase_ms["moments"] / max(1, phase_n["moments"])
     fused = ovl_mode == 3 and not is_f32 and not class_sums
     mo_solo = solo or mo_launch_ms
-    hbm = {"moments_GBps": (n_local * m_local) / (mo_solo * 1e-3) / 1e9 if mo_solo else None,
-           "moments_GBps_overlapped": (n_local * m_local) / (mo_launch_ms * 1e-3) / 1e9 if (solo and mo_launch_ms) else None,
+    mo_bytes = n_local * m_local * (8 if is_f32 else 1)  # f32: k_split_f32 reads 4 B, writes 2 x 2 B
+    hbm = {"moments_GBps": mo_bytes / (mo_solo * 1e-3) / 1e9 if mo_solo else None,
+           "moments_GBps_overlapped": mo_bytes / (mo_launch_ms * 1e-3) / 1e9 if (solo and mo_launch_ms) else None,
            "moments_in_step": ("fused into k_xterm (no separate pass; moments_GBps is the unfused k_moments_i8 "
-                               "measured in two extra serialised steps)") if fused else "separate k_moments_i8 pass",
+                               "measured in two extra serialised steps)") if fused else
+                              ("k_split_f32 pre-pass (centring, bf16 hi/lo planes, fp64 sums)" if is_f32
+                               else "separate k_moments_i8 pass"),
            "finalize_GBps": ((h1 - h0) * m_local * 16) / (step_phase_ms["finalize"] * 1e-3) / 1e9 if step_phase_ms["finalize"] else None,
            "hbm_peak_GBps": peaks["hbm_gbs"]}
 
@@ -446,7 +459,7 @@ def main():
             if mhz:
                 # tcgen05 issue-rate ceiling at the observed SM clock (tools/pair_bench:
                 # kind::i8 8192, kind::f16 4096 MAC/clk/SM, both measured 100% reachable)
-                macs = 4096 if is_f32 else 8192
+                macs = MMA_MACS_PER_CLK_SM[is_f32]
                 ceil = 2.0 * macs * torch.cuda.get_device_properties(dev).multi_processor_count * mhz * 1e6 / 1e12
                 roofline["mma_rate_ceiling_at_clock"] = ceil
                 roofline["frac_of_mma_rate_ceiling"] = (roofline["executed_ops_per_launch"] if is_f32 else ops) \

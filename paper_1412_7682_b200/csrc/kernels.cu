@@ -618,6 +618,10 @@ namespace cpa {
 namespace {
 constexpr int SP_THREADS = 256;
 constexpr int SP_ROWS = 512;
+#ifndef SP_U_ROWS
+#define SP_U_ROWS 4
+#endif
+constexpr int SP_U = SP_U_ROWS;
 
 __device__ __forceinline__ uint16_t bf16_bits(float x)
 {
@@ -645,15 +649,26 @@ k_split_f32(const float *__restrict__ w, int64_t ld, int64_t n, int32_t M, const
     bool bad = false;
     const int64_t r0 = (int64_t)blockIdx.y * SP_ROWS;
     const int64_t r1 = min(n, r0 + SP_ROWS);
-    for (int64_t r = r0; r < r1; r++) {
-        float x[4];
-        if (cnt == 4) {
-            const float4 v = __ldg((const float4 *)(w + r * ld + j0));
-            x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    // SP_U rows' loads in flight per thread before any use (HBM-bound: one row
+    // at a time left too few bytes in flight for the latency)
+    for (int64_t rb = r0; rb < r1; rb += SP_U) {
+    float xs[SP_U][4];
+#pragma unroll
+    for (int u = 0; u < SP_U; u++) {
+        const int64_t r = rb + u;
+        if (r < r1 && cnt == 4) {
+            const float4 v = __ldcs((const float4 *)(w + r * ld + j0));
+            xs[u][0] = v.x; xs[u][1] = v.y; xs[u][2] = v.z; xs[u][3] = v.w;
         } else {
 #pragma unroll
-            for (int q = 0; q < 4; q++) x[q] = q < cnt ? w[r * ld + j0 + q] : 0.0f;
+            for (int q = 0; q < 4; q++) xs[u][q] = (r < r1 && q < cnt) ? w[r * ld + j0 + q] : 0.0f;
         }
+    }
+#pragma unroll
+    for (int u = 0; u < SP_U; u++) {
+        const int64_t r = rb + u;
+        if (r >= r1) break;
+        const float *x = xs[u];
         uint16_t h[4], l[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) {
@@ -674,6 +689,7 @@ k_split_f32(const float *__restrict__ w, int64_t ld, int64_t n, int32_t M, const
                 lp[q] = l[q];
             }
         }
+    }
     }
     for (int q = 0; q < cnt; q++) {
         atomicAdd(&sum_w[j0 + q], s1[q]);

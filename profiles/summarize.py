@@ -117,8 +117,15 @@ def main():
     x = res["kernels"].get("k_xterm")
     if x and "dram_read_bytes" in x:
         with open(os.path.join(ROOT, "profiles", "xterm_traffic.json"), "w") as f:
+            ms = x.get("duration_ms")
+            cyc = x.get("sm_cycles")
             json.dump({"config": "C4", "n_gpus": 1, "tag": tag,
                        "dram_bytes_per_launch": x["dram_read_bytes"] + x.get("dram_write_bytes", 0.0),
+                       "tensor_active_pct": x.get("tensor_active_pct"),
+                       "duration_ms": ms,
+                       # the kernel's own average SM clock (cycles / duration): nvidia-smi's
+                       # coarse samples overstate it under the power cap
+                       "sm_mhz": (cyc / (ms * 1e-3) / 1e6) if (cyc and ms) else None,
                        "source": f"ncu --set full capture gpurun_out/k_xterm_{tag}.ncu-rep (profiles/ncu_{tag}.md)"}, f, indent=1)
     print("\n".join(lines))
 
