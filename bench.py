@@ -48,10 +48,14 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
-    ap.add_argument("--combine", choices=["rows", "allreduce"], default="rows",
-                    help="N>1: 'rows' = reduce-scatter of the sum_hw rows + all-reduce of the small "
-                         "fields, row-sharded finalize, gather of the maxima; 'allreduce' = one "
-                         "all-reduce of the whole accumulator, finalize on every rank")
+    ap.add_argument("--combine", choices=["auto", "fused", "rows", "allreduce"], default="auto",
+                    help="N>1 trace shards: 'fused' = the cross-term kernel adds each key byte's rows "
+                         "into the owner rank's accumulator over NVLink (cpa_set_row_owners), then "
+                         "an all-reduce of the small fields, row-sharded finalize, gather of the "
+                         "maxima; 'rows' = the same with an NCCL reduce-scatter of the rows after "
+                         "the kernel; 'allreduce' = one all-reduce of the whole accumulator, "
+                         "finalize on every rank; 'auto' = fused when possible (int8, G | 16), "
+                         "else rows")
     ap.add_argument("--shard", choices=["auto", "traces", "samples"], default="auto",
                     help="N>1: split the traces (partial sums combined per --combine) or the sample "
                          "columns (every rank all traces of M/G columns; only the per-hypothesis maxima "
@@ -269,7 +273,24 @@ def main():
     ovl_mode = 0 if args.no_overlap else (args.overlap_mode if args.overlap_mode is not None else OVERLAP_DEFAULT)
     eng.set_overlap(ovl_mode)
     combine = ("columns" if shard == "samples" else args.combine) if world > 1 else "none"
-    h0, h1 = MG.row_range(rank, world) if combine == "rows" else (0, 4096)
+    fused_note = None
+    if combine == "auto":
+        combine = "fused" if (not is_f32 and not class_sums and 16 % world == 0) else "rows"
+    owners = None
+    if combine == "fused":
+        try:   # map the peers' accumulators (CUDA IPC) and route the rows to their owners
+            owners = MG.FusedOwners(eng)
+        except Exception as e:  # no peer mapping on this box: NCCL reduce-scatter instead
+            fused_note = f"fused combine unavailable ({type(e).__name__}: {e}); rows"
+            combine = "rows"
+        ok = torch.tensor([0 if owners is None else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)   # every rank or none
+        if owners is not None and int(ok.item()) == 0:
+            owners.close()
+            owners, combine = None, "rows"
+            fused_note = fused_note or "fused combine unavailable on a peer rank; rows"
+    h0, h1 = MG.row_range(rank, world) if combine in ("rows", "fused") else (0, 4096)
+    bar_t = torch.zeros(1, dtype=torch.int32, device=dev)
     rho = torch.empty((h1 - h0, m_local), dtype=torch.float64, device=dev)   # this rank's block of rho
     maxabs = torch.empty(4096, dtype=torch.float64, device=dev)
     argmax = torch.empty(4096, dtype=torch.int32, device=dev)
@@ -279,10 +300,17 @@ def main():
 
     def step(host=None):
         eng.reset()
+        if combine == "fused":  # every owner's accumulator is zero before any peer adds to it
+            MG.device_barrier(bar_t)
         if host is None:
             eng.accumulate(dWv, dT)
         else:
             eng.accumulate_host(*host)
+        if combine == "fused":  # rows already with their owners; small fields + ordering point
+            MG.allreduce_small_fields(eng.accum, w.m)
+            P.cpa_finalize_rows(eng.ctx, h0, h1, rho, maxabs, argmax, peak)
+            MG.gather_rows(maxabs, argmax, peak, h0, h1)
+            return P.cpa_select(eng.ctx, 1, maxabs, argmax, peak, rank_t)
         if combine == "rows":   # reduce-scatter rows, sharded Eq. (1), gather maxima, select
             MG.reduce_scatter_rows(eng.accum, w.m)
             P.cpa_finalize_rows(eng.ctx, h0, h1, rho, maxabs, argmax, peak)
@@ -443,7 +471,8 @@ def main():
                                    f"{' (class-sum cross term)' if class_sums else ''}, "
                                    f"AES-128 key {w.key.hex()}",
                        "n_traces": w.n, "n_samples": w.m, "hypotheses": 4096, "parallelism": (f"{'sample' if shard == 'samples' else 'trace'}-shard x{world}"
-                                       + (f", {combine} combine" if world > 1 else "")),
+                                       + (f", {combine} combine" if world > 1 else "")
+                                       + (f" [{fused_note}]" if fused_note else "")),
                        "l2": f"inputs {n_local * m_local * dW.element_size() / 1e9:.2f} GB per rank > 126 MB L2, "
                              "no flush needed",
                        "rho_written": True},
@@ -465,6 +494,9 @@ def main():
                 roofline["frac_of_mma_rate_ceiling"] = (roofline["executed_ops_per_launch"] if is_f32 else ops) \
                     / (xt_ms * 1e-3) / 1e12 / ceil
         print(json.dumps(line), flush=True)
+    if owners is not None:
+        barrier()
+        owners.close()
     eng.close()
     if world > 1:
         dist.destroy_process_group()

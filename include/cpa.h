@@ -150,6 +150,31 @@ CPA_API cpa_status cpa_finalize(cpa_ctx *ctx, double *d_rho, double *d_maxabs,
 CPA_API cpa_status cpa_finalize_async(cpa_ctx *ctx, double *d_rho, double *d_maxabs, int32_t *d_argmax,
                                       int32_t *d_rank, int32_t *d_best);
 
+/* ---- fused multi-GPU combine ([P:230]) -----------------------
+ * cpa_set_row_owners: the cross-term kernel adds its int64 partial sum_hw of key
+ * byte b (hypothesis rows [256 b, 256 b + 256)) straight into the packed
+ * accumulator owners[b] -- typically a peer GPU's, mapped with cpa_ipc_open and
+ * reached over NVLink with system-scope atomics -- instead of into this
+ * context's own accumulator.  The reduce-scatter of the rows then happens
+ * inside the kernel's epilogue, overlapped with the MMAs; only the small fields
+ * (sum_w, sum_w2, sum_h, sum_h2, N), which stay in this context's accumulator,
+ * still need an all-reduce.  owners[b] NULL = this context's accumulator;
+ * owners NULL = off.  int8 traces and the tensor-core path only
+ * (CPA_E_INVALID_ARG otherwise).  The caller zeroes every owner accumulator and
+ * synchronises the ranks before the first cpa_accumulate, and after the last
+ * one before an owner reads its rows (cpa_finalize_rows).  Exact: integer
+ * atomics are order-independent, results are bit-identical to one GPU.        */
+CPA_API cpa_status cpa_set_row_owners(cpa_ctx *ctx, void *const owners[16]);
+
+/* CUDA IPC of a device buffer (e.g. a torch-allocated accumulator inside a
+ * larger allocation): cpa_ipc_export writes a 64-byte handle of the allocation
+ * containing d_ptr and the byte offset of d_ptr in it; cpa_ipc_open maps it in
+ * another process (same or peer GPU, peer access enabled) and returns the
+ * pointer at that offset; cpa_ipc_close unmaps the BASE (pointer - offset).   */
+CPA_API cpa_status cpa_ipc_export(const void *d_ptr, uint8_t handle[64], uint64_t *offset);
+CPA_API cpa_status cpa_ipc_open(const uint8_t handle[64], uint64_t offset, void **d_ptr);
+CPA_API cpa_status cpa_ipc_close(void *d_base);
+
 /* ---- sharded Phase 3/4 (multi-GPU) ---------------------------
  * Two ways to split the work of Phase 3 [P:81-83] over G ranks:
  *  (rows)    trace-sharded accumulation; ONE reduce-scatter of the sum_hw rows

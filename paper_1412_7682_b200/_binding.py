@@ -26,7 +26,8 @@ FIELD_HW, FIELD_W, FIELD_W2, FIELD_H, FIELD_H2, FIELD_N = range(6)
 # every symbol include/cpa.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = (
     "cpa_accum_words", "cpa_accum_bytes", "cpa_accum_offset", "cpa_init", "cpa_accumulate",
-    "cpa_accumulate_host", "cpa_finalize", "cpa_finalize_async", "cpa_finalize_rows", "cpa_select", "cpa_reset", "cpa_sync", "cpa_destroy",
+    "cpa_accumulate_host", "cpa_finalize", "cpa_finalize_async", "cpa_finalize_rows", "cpa_select",
+    "cpa_set_row_owners", "cpa_ipc_export", "cpa_ipc_open", "cpa_ipc_close", "cpa_reset", "cpa_sync", "cpa_destroy",
     "cpa_set_offsets", "cpa_set_option", "cpa_phase_times", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
     "cpa_aes_expand_key", "cpa_aes_invert_key_schedule",
 )
@@ -62,6 +63,10 @@ def _load():
         "cpa_finalize_rows": (ST, [P, I32, I32, P, P, P, P]),
         "cpa_finalize_async": (ST, [P, P, P, P, P, P]),
         "cpa_select": (ST, [P, I32, P, P, P, P, C.POINTER(cpa_result)]),
+        "cpa_set_row_owners": (ST, [P, P]),
+        "cpa_ipc_export": (ST, [P, P, C.POINTER(C.c_uint64)]),
+        "cpa_ipc_open": (ST, [P, C.c_uint64, C.POINTER(P)]),
+        "cpa_ipc_close": (ST, [P]),
         "cpa_reset": (ST, [P]),
         "cpa_sync": (ST, [P]),
         "cpa_destroy": (ST, [P]),
@@ -143,6 +148,33 @@ def cpa_finalize_async(ctx, d_rho=None, d_maxabs=None, d_argmax=None, d_rank=Non
 def cpa_finalize_rows(ctx, h0: int, h1: int, d_rho, d_maxabs, d_argmax, d_peak):
     _check(_lib.cpa_finalize_rows(ctx, h0, h1, _ptr(d_rho), _ptr(d_maxabs), _ptr(d_argmax), _ptr(d_peak)),
            "cpa_finalize_rows")
+
+
+def cpa_set_row_owners(ctx, owners):
+    """owners: 16 device addresses (int; 0 = this context's accumulator) or None (off)."""
+    if owners is None:
+        _check(_lib.cpa_set_row_owners(ctx, None), "cpa_set_row_owners")
+        return
+    arr = (C.c_void_p * 16)(*[int(o) or None for o in owners])
+    _check(_lib.cpa_set_row_owners(ctx, arr), "cpa_set_row_owners")
+
+
+def cpa_ipc_export(d_ptr) -> tuple[bytes, int]:
+    h = (C.c_uint8 * 64)()
+    off = C.c_uint64(0)
+    _check(_lib.cpa_ipc_export(_ptr(d_ptr), h, C.byref(off)), "cpa_ipc_export")
+    return bytes(h), off.value
+
+
+def cpa_ipc_open(handle: bytes, offset: int) -> int:
+    h = (C.c_uint8 * 64).from_buffer_copy(bytes(handle))
+    out = C.c_void_p()
+    _check(_lib.cpa_ipc_open(h, offset, C.byref(out)), "cpa_ipc_open")
+    return out.value
+
+
+def cpa_ipc_close(d_base: int):
+    _check(_lib.cpa_ipc_close(C.c_void_p(d_base)), "cpa_ipc_close")
 
 
 def cpa_select(ctx, G: int, d_maxabs, d_argmax, d_peak, d_rank=None) -> cpa_result:

@@ -55,6 +55,20 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
     return fn;
 }
 
+using PFN_addr_range = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+PFN_addr_range get_addr_range()
+{
+    static PFN_addr_range fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_addr_range)p;
+    }
+    return fn;
+}
+
 constexpr int64_t kMaxTraces = 1LL << 23;  // exact-int64 bound of Eq. (1), see DESIGN.md
 constexpr int32_t kMaxSamples = 1 << 22;
 constexpr int64_t kStageBytes = 256LL << 20;  // bytes per staging chunk (cpa_accumulate_host / unaligned input)
@@ -96,7 +110,10 @@ struct cpa_ctx {
     // CPA_OPT_CLASS_SUMS (HW_LAST / HW_FIRST, int8 traces): class-sum cross term
     // (classsum.cu); scratch allocated on first use
     int class_sums = 0;
-    int fuse_hist = 0;  // CPA_OPT_FUSE_HIST: a3 byte-pair histogram counted by the cross-term kernel (measured neutral)
+    int fuse_hist = 0;
+    // cpa_set_row_owners: fused multi-GPU combine (key byte b's sum_hw rows go to owners[b])
+    int64_t *owners[16] = {};
+    bool owners_set = false;  // CPA_OPT_FUSE_HIST: a3 byte-pair histogram counted by the cross-term kernel (measured neutral)
     int32_t *d_cs_cnt = nullptr, *d_cs_off = nullptr, *d_cs_cur = nullptr, *d_cs_perm = nullptr, *d_cs_S = nullptr;
     int64_t cs_perm_n = 0, cs_S_words = 0;
     // CPA_OPT_TIMING: CUDA events recorded on `stream` around every launch
@@ -298,6 +315,7 @@ cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
     }
     if (option == CPA_OPT_CLASS_SUMS) {
         if (value < 0 || value > 1) return fail(CPA_E_INVALID_ARG, "CLASS_SUMS=%lld outside [0, 1]", (long long)value);
+        if (value && ctx->owners_set) return fail(CPA_E_INVALID_ARG, "class sums do not support row owners");
         if (value && (ctx->model == CPA_HD_LAST || ctx->dtype == CPA_F32))
             return fail(CPA_E_INVALID_ARG, "class sums need a single-byte model (HW_LAST/HW_FIRST) and int8 traces");
         ctx->class_sums = (int)value;
@@ -513,7 +531,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                  return cpa::launch_xterm_i8(tmap, d_tx, c->d_vtab, acc, c->d_counter, M, n, kc, sgn, c->num_sms,
                                              c->stream, &launches, fused ? acc + cpa_accum_offset(M, 1) : nullptr,
                                              fused ? acc + cpa_accum_offset(M, 2) : nullptr,
-                                             fhist ? c->d_hist : nullptr);
+                                             fhist ? c->d_hist : nullptr, c->owners_set ? c->owners : nullptr);
              }),
              "xterm_i8");
     if (!fused && mode == 1) CUDA_TRY(moments(), "moments");
@@ -751,6 +769,58 @@ cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_
     if (st == CPA_OK) st = phase4(c, o, n, &launches, res);
     c->launches += launches;
     return st;
+}
+
+cpa_status cpa_set_row_owners(cpa_ctx *c, void *const owners[16])
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    if (!owners) {
+        c->owners_set = false;
+        for (auto &o : c->owners) o = nullptr;
+        return CPA_OK;
+    }
+    if (c->dtype == CPA_F32) return fail(CPA_E_INVALID_ARG, "row owners need int8 traces");
+    if (c->class_sums) return fail(CPA_E_INVALID_ARG, "row owners do not support class sums");
+    for (int b = 0; b < 16; b++) {
+        if (owners[b] && ((uintptr_t)owners[b] & 7)) return fail(CPA_E_INVALID_ARG, "owner %d misaligned", b);
+        c->owners[b] = (int64_t *)(owners[b] ? owners[b] : c->accum);
+    }
+    c->owners_set = true;
+    return CPA_OK;
+}
+
+cpa_status cpa_ipc_export(const void *d_ptr, uint8_t handle[64], uint64_t *offset)
+{
+    if (!d_ptr || !handle || !offset) return fail(CPA_E_INVALID_ARG, "null argument");
+    PFN_addr_range range = get_addr_range();
+    if (!range) return fail(CPA_E_CUDA, "cuMemGetAddressRange entry point unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)d_ptr) != CUDA_SUCCESS) return fail(CPA_E_INVALID_ARG, "not a device pointer");
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, (void *)base), "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) <= 64, "handle size");
+    std::memset(handle, 0, 64);
+    std::memcpy(handle, &h, sizeof(h));
+    *offset = (uint64_t)((CUdeviceptr)d_ptr - base);
+    return CPA_OK;
+}
+
+cpa_status cpa_ipc_open(const uint8_t handle[64], uint64_t offset, void **d_ptr)
+{
+    if (!handle || !d_ptr) return fail(CPA_E_INVALID_ARG, "null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void *base = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    *d_ptr = (uint8_t *)base + offset;
+    return CPA_OK;
+}
+
+cpa_status cpa_ipc_close(void *d_base)
+{
+    CUDA_TRY(cudaIpcCloseMemHandle(d_base), "cudaIpcCloseMemHandle");
+    return CPA_OK;
 }
 
 cpa_status cpa_finalize_async(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_argmax, int32_t *d_rank,

@@ -145,6 +145,11 @@ struct Params {
     const uint8_t *texts;    // N x 16
     const uint8_t *vtab;     // 256 x 256 (global copy of V)
     void *hw;                // sum_hw [4096][M]: int64 (I8) or double (F32)
+    // fused multi-GPU combine (I8; all null = off): key byte b's rows go to the
+    // packed accumulator owners[b] (a peer GPU's, mapped over NVLink), with
+    // system-scope atomics, instead of to hw -- the reduce-scatter happens
+    // inside the epilogue, overlapped with the MMAs
+    int64_t *owners[16];
     int *unit_counter;       // zeroed before the launch
     int32_t M;
     int32_t n_tiles;         // tiles of NT*256 samples
@@ -538,6 +543,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             constexpr int CPB = C::NT * BN / 8;  // 8-column groups per key byte
             constexpr int NC = C::NACC * BN / 8;
             const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + acc * (C::NACC * BN);
+            int64_t *const own = F32 ? nullptr : p.owners[b];  // KB == 1 for the owner routing
             // 8 columns at a time through a small transpose buffer: each warp-wide
             // atomic covers 4 rows x 8 consecutive samples = 8 full 32-byte sectors.
             // The TMEM load of the next 8 columns is in flight during the atomics.
@@ -561,6 +567,9 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                         const uint32_t bits = tbuf[(4 * rr + rsub) * TB_LD + csub];
                         if (F32) {
                             atomicAdd((double *)p.hw + off + (int64_t)(4 * rr) * p.M, (double)__uint_as_float(bits));
+                        } else if (own != nullptr) {  // peer (or own) accumulator of the row owner
+                            atomicAdd_system((unsigned long long *)own + off + (int64_t)(4 * rr) * p.M,
+                                             (unsigned long long)(long long)(int32_t)bits);
                         } else {
                             atomicAdd((unsigned long long *)p.hw + off + (int64_t)(4 * rr) * p.M,
                                       (unsigned long long)(long long)(int32_t)bits);
@@ -699,7 +708,7 @@ template <bool F32>
 cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *d_texts, const uint8_t *d_vtab,
                    void *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, uint32_t idesc, int num_sms,
                    cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr, int64_t *d_sum_w2 = nullptr,
-                   bool w_signed = true, uint32_t *d_hist = nullptr)
+                   bool w_signed = true, uint32_t *d_hist = nullptr, int64_t *const *owners = nullptr)
 {
     using Cf = Cfg<F32>;
     Params p;
@@ -719,6 +728,7 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *
     p.sum_w2 = d_sum_w2;
     p.w_signed = w_signed ? 1 : 0;
     p.hist = d_hist;
+    for (int b = 0; b < 16; b++) p.owners[b] = owners ? owners[b] : nullptr;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_xterm<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
@@ -782,11 +792,12 @@ int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms)
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
                             int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
                             int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w, int64_t *d_sum_w2,
-                            uint32_t *d_hist)
+                            uint32_t *d_hist, int64_t *const *owners)
 {
+    static_assert(Cfg<false>::KB == 1, "owner routing assumes one key byte per unit");
     return launch<false>(tmap_w, tmap_w, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                          idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, d_sum_w, d_sum_w2, w_signed,
-                         d_hist);
+                         d_hist, owners);
 }
 
 cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,

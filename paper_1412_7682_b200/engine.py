@@ -73,6 +73,10 @@ class Engine:
         """CPA_OPT_FUSE_HIST: a3's byte-pair histogram counted inside the cross-term kernel (default off)."""
         B.cpa_set_option(self.ctx, B.CPA_OPT_FUSE_HIST, int(bool(on)))
 
+    def set_row_owners(self, owners):
+        """cpa_set_row_owners: 16 device addresses (0 = own accumulator) or None."""
+        B.cpa_set_row_owners(self.ctx, owners)
+
     def set_class_sums(self, on: bool = True):
         """CPA_OPT_CLASS_SUMS: class-sum cross term for HW_LAST / HW_FIRST (exact)."""
         B.cpa_set_option(self.ctx, B.CPA_OPT_CLASS_SUMS, int(bool(on)))

@@ -181,3 +181,76 @@ def finalize_columns_sharded(engine, group=None, want_rho: bool = False) -> dict
     out.update(rho=rho)
     return out
 
+
+
+# ---- fused combine: the cross term writes each key byte's rows to their owner ----
+# (include/cpa.h cpa_set_row_owners).  Rank r owns hypothesis rows
+# [4096 r/G, 4096 (r+1)/G), i.e. key bytes [16 r/G, 16 (r+1)/G), so G must divide
+# 16.  Each rank maps its peers' accumulators (CUDA IPC) once; per step only the
+# small fields need a collective, and that collective is also the cross-GPU
+# ordering point (a rank's kernels, and thus its peer atomics, complete before its
+# contribution enters the all-reduce).
+
+def byte_owner(b: int, world: int) -> int:
+    """Rank owning key byte b's hypothesis rows (row_range of that rank)."""
+    if 16 % world:
+        raise ValueError(f"fused combine needs world | 16, got {world}")
+    return b // (16 // world)
+
+
+def owner_table(addrs: list[int], world: int, rank: int) -> list[int]:
+    """owners[b] for cpa_set_row_owners: the mapped address of byte b's owner's
+    accumulator (0 = this rank's own)."""
+    return [0 if byte_owner(b, world) == rank else addrs[byte_owner(b, world)] for b in range(16)]
+
+
+class FusedOwners:
+    """Map the peers' accumulators into this process (CUDA IPC) and route this
+    engine's cross-term rows to their owners."""
+
+    def __init__(self, eng, group=None):
+        import torch.distributed as dist
+        from . import _binding as B
+        self.world, self.rank = _world(group)
+        byte_owner(0, self.world)                  # validates world | 16
+        h, off = B.cpa_ipc_export(eng.accum)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, (h, off), group=group)
+        self.mapped = []                           # (base, ptr) of opened peer buffers
+        addrs = []
+        for r, (hr, offr) in enumerate(allh):
+            if r == self.rank:
+                addrs.append(eng.accum.data_ptr())
+                continue
+            ptr = B.cpa_ipc_open(hr, offr)
+            self.mapped.append((ptr - offr, ptr))
+            addrs.append(ptr)
+        self.owners = owner_table(addrs, self.world, self.rank)
+        eng.set_row_owners(self.owners)
+        self.eng = eng
+
+    def close(self):
+        from . import _binding as B
+        self.eng.set_row_owners(None)
+        for base, _ in self.mapped:
+            B.cpa_ipc_close(base)
+        self.mapped = []
+
+
+def device_barrier(t, group=None):
+    """Stream-ordered cross-GPU barrier: a 1-element all-reduce.  On return (in
+    stream order) every rank's earlier work on its stream has completed."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+
+def allreduce_small_fields(acc, M: int, group=None) -> tuple[int, int]:
+    """Fused combine, after the accumulation: the sum_hw rows already sit in
+    their owners' accumulators; all-reduce only the small fields (sum_w,
+    sum_w2, sum_h, sum_h2, N).  Returns this rank's rows [h0, h1)."""
+    import torch.distributed as dist
+    world, rank = _world(group)
+    if world > 1:
+        dist.all_reduce(acc[4096 * M:], op=dist.ReduceOp.SUM, group=group)
+    return row_range(rank, world)

@@ -36,7 +36,7 @@ def test_bench_single_gpu_line():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("combine,port", [("rows", 29533), ("allreduce", 29535)])
+@pytest.mark.parametrize("combine,port", [("rows", 29533), ("allreduce", 29535), ("fused", 29538)])
 def test_bench_two_ranks_one_gpu_gloo(combine, port):
     d = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
               "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--config", "C2",
@@ -44,6 +44,7 @@ def test_bench_two_ranks_one_gpu_gloo(combine, port):
              env={"CPA_BENCH_SAME_DEVICE": "1", "CPA_BENCH_BACKEND": "gloo"})
     assert d["n_gpus"] == 2 and d["key_recovered"] is True
     assert KEYS <= set(d) and combine in d["config"]["parallelism"]
+    assert "unavailable" not in d["config"]["parallelism"]   # fused: CUDA IPC between the ranks worked
 
 
 @pytest.mark.gpu

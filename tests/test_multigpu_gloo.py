@@ -208,3 +208,17 @@ def test_column_ranges_aligned_cover():
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             assert all(j0 % 16 == 0 and j1 > j0 for j0, j1 in rs)
     assert [MG.row_range(r, 8) for r in range(8)][3] == (1536, 2048)
+
+
+def test_byte_owner_table_matches_row_ranges():
+    """Fused combine bookkeeping: byte b's owner holds rows [256 b, 256 b + 256)
+    inside its row_range, for every G dividing 16; other G are refused."""
+    for G in (1, 2, 4, 8, 16):
+        for b in range(16):
+            h0, h1 = MG.row_range(MG.byte_owner(b, G), G)
+            assert h0 <= 256 * b and 256 * (b + 1) <= h1
+        tab = MG.owner_table([1000 + r for r in range(G)], G, 0)
+        assert [0 if MG.byte_owner(b, G) == 0 else 1000 + MG.byte_owner(b, G) for b in range(16)] == tab
+    for G in (3, 5, 6):
+        with pytest.raises(ValueError):
+            MG.byte_owner(0, G)

@@ -171,3 +171,42 @@ def test_finalize_rho_buffer_alignment(P, c1):
         assert np.array_equal(rho.view(4096, w.m).cpu().numpy(), ref["rho"]), off
         assert np.array_equal(mx.cpu().numpy(), ref["maxabs"]) and np.array_equal(am.cpu().numpy(), ref["argmax"])
     eng.close()
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_fused_row_owner_combine_equals_one_gpu(P, c1, G):
+    """Fused combine (cpa_set_row_owners): G trace-shard contexts on the one GPU,
+    each routing key byte b's cross-term rows into the accumulator of its owner
+    (MG.byte_owner; same-device pointers stand in for the NVLink-mapped peer
+    buffers), then only the small fields are summed.  Each owner's rows, the
+    small fields and the Phase 3/4 results equal one context's bit for bit."""
+    w, texts, W, ref = c1
+    dW, dT = _padded(W)[:, :w.m], torch.from_numpy(texts).cuda()
+    engs = [P.Engine(w.m, P.CPA_S8, P.CPA_HD_LAST, 0) for _ in range(G)]
+    addrs = [e.accum.data_ptr() for e in engs]
+    for r, e in enumerate(engs):
+        e.set_row_owners(MG.owner_table(addrs, G, r))
+    for r, e in enumerate(engs):
+        i0, i1 = MG.shard_range(w.n, r, G)
+        e.accumulate(dW[i0:i1], dT[i0:i1])
+    torch.cuda.synchronize()
+    n_hw = 4096 * w.m
+    small = sum(e.accum[n_hw:] for e in engs)
+    for r, e in enumerate(engs):
+        e.accum[n_hw:] = small
+    torch.cuda.synchronize()
+    mx, am, pk = (t[0] for t in engs[0].maxima_buffers(1))
+    for r, e in enumerate(engs):
+        h0, h1 = MG.row_range(r, G)
+        assert np.array_equal(e.sum_hw[h0:h1].cpu().numpy(), ref["sum_hw"][h0:h1]), r
+        e.finalize_rows(h0, h1, mx, am, pk)
+    assert np.array_equal(engs[0].sum_w.cpu().numpy(), ref["sum_w"])
+    out = engs[0].select(mx, am, pk)
+    assert np.array_equal(out["maxabs"].cpu().numpy(), ref["maxabs"])
+    assert np.array_equal(out["rank"].cpu().numpy(), ref["rank"])
+    assert out["master_key"] == w.key
+    with pytest.raises(P.CpaError):
+        engs[0].set_class_sums(True)   # class sums cannot route rows
+    for e in engs:
+        e.set_row_owners(None)
+        e.close()
