@@ -526,7 +526,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    const int64_t kc = c->kchunk ? c->kchunk : cpa::xterm_i8_auto_kchunk(M, n, c->num_sms);
+    const int64_t kc = c->kchunk ? c->kchunk : cpa::xterm_i8_auto_kchunk(M, n, c->num_sms, c->owners_set);
     CUDA_TRY(c->timed(2, [&] {
                  return cpa::launch_xterm_i8(tmap, d_tx, c->d_vtab, acc, c->d_counter, M, n, kc, sgn, c->num_sms,
                                              c->stream, &launches, fused ? acc + cpa_accum_offset(M, 1) : nullptr,

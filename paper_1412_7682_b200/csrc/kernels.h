@@ -34,7 +34,7 @@ cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M,
 // a5: cross term (tcgen05 kind::i8, CTA pairs).  With d_sum_w / d_sum_w2 set,
 // the kernel also adds a4's sum W, sum W^2 (fused moments).
 int xterm_smem_bytes();
-int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms);
+int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms, bool remote_epilogue = false);
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
                             int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
                             int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr,

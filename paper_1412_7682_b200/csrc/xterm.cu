@@ -748,8 +748,11 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *
 // (model: ~25k clk per epilogue, 1024 clk per stage; with a double-buffered
 // accumulator (F32) the epilogue overlaps the next unit).  max_len bounds the
 // int32 exactness (I8: |H W| <= 8 * 255 -> 2^20 traces) or the fp32 rounding
-// (F32: 4096 traces).
-int64_t auto_kchunk(int32_t M, int64_t N, int num_sms, int kb, int nt, int bk, int64_t max_len, bool overlapped)
+// (F32: 4096 traces).  epi_clk: the epilogue's cost; 3x when it adds the rows
+// into a peer GPU's accumulator over NVLink (fused multi-GPU combine), which
+// also favours fewer, longer units (less partial-sum traffic per rank).
+int64_t auto_kchunk(int32_t M, int64_t N, int num_sms, int kb, int nt, int bk, int64_t max_len, bool overlapped,
+                    double epi_clk = 25000.0)
 {
     const int64_t tiles = (16LL / kb) * ((M + nt * BN - 1) / (nt * BN));
     const int64_t pairs = num_sms / 2;
@@ -763,7 +766,7 @@ int64_t auto_kchunk(int32_t M, int64_t N, int num_sms, int kb, int nt, int bk, i
         const int64_t units = tiles * kcount;
         const int64_t waves = (units + pairs - 1) / pairs;
         const double stage_clk = (double)((len + bk - 1) / bk) * 1024.0;
-        const double epi = overlapped ? 0.0 : 25000.0;
+        const double epi = overlapped ? 0.0 : epi_clk;
         const double eff = (double)units / (double)(waves * pairs) * stage_clk / (stage_clk + epi);
         if (eff > best + 1e-3) {
             best = eff;
@@ -779,9 +782,10 @@ int64_t auto_kchunk(int32_t M, int64_t N, int num_sms, int kb, int nt, int bk, i
 
 int xterm_smem_bytes() { return SMEM_ALLOC; }
 
-int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms)
+int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms, bool remote_epilogue)
 {
-    return auto_kchunk(M, N, num_sms, Cfg<false>::KB, Cfg<false>::NT, Cfg<false>::BK, 1 << 20, false);
+    return auto_kchunk(M, N, num_sms, Cfg<false>::KB, Cfg<false>::NT, Cfg<false>::BK, 1 << 20, false,
+                       remote_epilogue ? 75000.0 : 25000.0);
 }
 
 int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms)
