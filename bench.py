@@ -346,6 +346,7 @@ def main():
     launches = eng.launches - launches0
     phase_ms, phase_n = eng.phase_times()
     eng.set_timing(False)
+    xt_mhz = P.cpa_xterm_clock(eng.ctx)   # SM clock of the last timed cross-term launch (in-kernel probe)
     if world > 1:
         t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -392,6 +393,13 @@ def main():
                                 f"{src} bf16_tflops (burst) x {INT8_PER_BF16:g} (int8:bf16 nominal ratio)"),
                 "frac_of_sustained": achieved / (peaks["bf16_tflops_sustained"] * ratio),
                 "algorithmic_ops_per_launch": ops, "ms_per_launch": xt_ms}
+    if xt_mhz > 0 and not class_sums:
+        # the tcgen05 issue ceiling at the clock the kernel itself measured (clock64 over
+        # %globaltimer in its first CTA): what the 1000 W cap left it
+        ceil_k = MMA_MACS_PER_CLK_SM[is_f32] * 2 * 148 * xt_mhz * 1e6 / 1e12
+        roofline["kernel_sm_mhz"] = xt_mhz
+        roofline["mma_ceiling_at_kernel_clock"] = ceil_k
+        roofline["frac_of_mma_ceiling_at_kernel_clock"] = achieved / ceil_k
     if ncu_xt and ncu_xt.get("sm_mhz"):
         # the same kernel under ncu: tensor-pipe activity and its own SM clock; the
         # tcgen05 issue ceiling at that clock is what the 1000 W cap allows

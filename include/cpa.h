@@ -270,6 +270,12 @@ enum { CPA_NUM_PHASES = 5 };
 CPA_API cpa_status cpa_phase_times(cpa_ctx *ctx, double ms[CPA_NUM_PHASES],
                                    int64_t launches[CPA_NUM_PHASES]);
 
+/* Average SM clock (MHz) of the last int8 cross-term launch, from the
+ * clock64 and %globaltimer readings its first CTA takes at its start and end
+ * (0 if none ran).  Synchronises the stream.  The roofline's issue-rate
+ * ceiling at the clock the power cap actually left the kernel.             */
+CPA_API cpa_status cpa_xterm_clock(cpa_ctx *ctx, double *mhz);
+
 /* Kernel launches issued by this context since creation (for bench
  * accounting).                                                              */
 CPA_API int64_t cpa_launch_count(const cpa_ctx *ctx);

@@ -27,7 +27,7 @@ FIELD_HW, FIELD_W, FIELD_W2, FIELD_H, FIELD_H2, FIELD_N = range(6)
 ABI_SYMBOLS = (
     "cpa_accum_words", "cpa_accum_bytes", "cpa_accum_offset", "cpa_init", "cpa_accumulate",
     "cpa_accumulate_host", "cpa_finalize", "cpa_finalize_async", "cpa_finalize_rows", "cpa_select",
-    "cpa_set_row_owners", "cpa_ipc_export", "cpa_ipc_open", "cpa_ipc_close", "cpa_reset", "cpa_sync", "cpa_destroy",
+    "cpa_set_row_owners", "cpa_ipc_export", "cpa_ipc_open", "cpa_ipc_close", "cpa_xterm_clock", "cpa_reset", "cpa_sync", "cpa_destroy",
     "cpa_set_offsets", "cpa_set_option", "cpa_phase_times", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
     "cpa_aes_expand_key", "cpa_aes_invert_key_schedule",
 )
@@ -67,6 +67,7 @@ def _load():
         "cpa_ipc_export": (ST, [P, P, C.POINTER(C.c_uint64)]),
         "cpa_ipc_open": (ST, [P, C.c_uint64, C.POINTER(P)]),
         "cpa_ipc_close": (ST, [P]),
+        "cpa_xterm_clock": (ST, [P, C.POINTER(C.c_double)]),
         "cpa_reset": (ST, [P]),
         "cpa_sync": (ST, [P]),
         "cpa_destroy": (ST, [P]),
@@ -157,6 +158,12 @@ def cpa_set_row_owners(ctx, owners):
         return
     arr = (C.c_void_p * 16)(*[int(o) or None for o in owners])
     _check(_lib.cpa_set_row_owners(ctx, arr), "cpa_set_row_owners")
+
+
+def cpa_xterm_clock(ctx) -> float:
+    mhz = C.c_double(0.0)
+    _check(_lib.cpa_xterm_clock(ctx, C.byref(mhz)), "cpa_xterm_clock")
+    return mhz.value
 
 
 def cpa_ipc_export(d_ptr) -> tuple[bytes, int]:

@@ -113,7 +113,8 @@ struct cpa_ctx {
     int fuse_hist = 0;
     // cpa_set_row_owners: fused multi-GPU combine (key byte b's sum_hw rows go to owners[b])
     int64_t *owners[16] = {};
-    bool owners_set = false;  // CPA_OPT_FUSE_HIST: a3 byte-pair histogram counted by the cross-term kernel (measured neutral)
+    bool owners_set = false;
+    unsigned long long *d_clk = nullptr;  // xterm clock probe (globaltimer, clock64 at CTA 0's start/end)  // CPA_OPT_FUSE_HIST: a3 byte-pair histogram counted by the cross-term kernel (measured neutral)
     int32_t *d_cs_cnt = nullptr, *d_cs_off = nullptr, *d_cs_cur = nullptr, *d_cs_perm = nullptr, *d_cs_S = nullptr;
     int64_t cs_perm_n = 0, cs_S_words = 0;
     // CPA_OPT_TIMING: CUDA events recorded on `stream` around every launch
@@ -240,6 +241,8 @@ cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, 
     if (e == cudaSuccess) e = cudaMalloc(&c->d_counter, 256);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_nonfinite, 256);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_hist, sizeof(uint32_t) * 16 * 65536);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_clk, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->d_clk, 0, 4 * sizeof(unsigned long long), c->stream);
     if (e == cudaSuccess) {
         int lo = 0, hi = 0;  // numerically greatest = lowest priority
         e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -531,7 +534,8 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                  return cpa::launch_xterm_i8(tmap, d_tx, c->d_vtab, acc, c->d_counter, M, n, kc, sgn, c->num_sms,
                                              c->stream, &launches, fused ? acc + cpa_accum_offset(M, 1) : nullptr,
                                              fused ? acc + cpa_accum_offset(M, 2) : nullptr,
-                                             fhist ? c->d_hist : nullptr, c->owners_set ? c->owners : nullptr);
+                                             fhist ? c->d_hist : nullptr, c->owners_set ? c->owners : nullptr,
+                                             c->d_clk);
              }),
              "xterm_i8");
     if (!fused && mode == 1) CUDA_TRY(moments(), "moments");
@@ -771,6 +775,16 @@ cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_
     return st;
 }
 
+cpa_status cpa_xterm_clock(cpa_ctx *c, double *mhz)
+{
+    if (!c || !mhz) return fail(CPA_E_INVALID_ARG, "null argument");
+    unsigned long long v[4];
+    CUDA_TRY(cudaMemcpyAsync(v, c->d_clk, sizeof v, cudaMemcpyDeviceToHost, c->stream), "D2H clock probe");
+    CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+    *mhz = (v[2] > v[0] && v[3] > v[1]) ? (double)(v[3] - v[1]) / (double)(v[2] - v[0]) * 1e3 : 0.0;
+    return CPA_OK;
+}
+
 cpa_status cpa_set_row_owners(cpa_ctx *c, void *const owners[16])
 {
     if (!c) return fail(CPA_E_INVALID_ARG, "null context");
@@ -944,6 +958,7 @@ cpa_status cpa_destroy(cpa_ctx *c)
     cudaFree(c->d_lo);
     cudaFree(c->d_nonfinite);
     cudaFree(c->d_hist);
+    cudaFree(c->d_clk);
     cudaFree(c->d_cs_cnt);
     cudaFree(c->d_cs_off);
     cudaFree(c->d_cs_cur);

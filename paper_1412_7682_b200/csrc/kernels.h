@@ -39,7 +39,7 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, c
                             int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
                             int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr,
                             int64_t *d_sum_w2 = nullptr, uint32_t *d_hist = nullptr,
-                            int64_t *const *owners = nullptr);
+                            int64_t *const *owners = nullptr, unsigned long long *d_clk = nullptr);
 
 // a6: float traces.  Split pre-pass: w' = w - offset[j] (fp32), hi = bf16(w'),
 // lo = bf16(w' - hi) into [n][ldh] bf16 planes; fp64 sum w', sum w'^2; sets

@@ -193,6 +193,12 @@ __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t m, uint32_t n)
 
 // ---- clusters / CTA pairs (cta_group::2) -------------------------------------
 namespace cpa {
+__device__ __forceinline__ unsigned long long globaltimer_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ uint32_t cluster_ctarank()
 {
     uint32_t r;

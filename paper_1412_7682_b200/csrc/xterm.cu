@@ -150,6 +150,9 @@ struct Params {
     // system-scope atomics, instead of to hw -- the reduce-scatter happens
     // inside the epilogue, overlapped with the MMAs
     int64_t *owners[16];
+    // clock probe (null = off): CTA 0 records (globaltimer ns, clock64) at its
+    // start and end, so the host can derive the SM clock the kernel ran at
+    unsigned long long *clk;
     int *unit_counter;       // zeroed before the launch
     int32_t M;
     int32_t n_tiles;         // tiles of NT*256 samples
@@ -369,6 +372,10 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (p.clk != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+        p.clk[0] = globaltimer_ns();
+        p.clk[1] = clock64();
+    }
 
     if (warp == 0) {
         // ================= scheduler (leader) + W TMA producer (both) =================
@@ -698,6 +705,10 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
     tc_fence_before();
     __syncthreads();
     cluster_sync_all();  // the peer's MMAs / remote arrivals are done with our smem and TMEM
+    if (p.clk != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+        p.clk[2] = globaltimer_ns();
+        p.clk[3] = clock64();
+    }
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc_pair<TMEM_COLS>(tmem_base);
@@ -708,7 +719,8 @@ template <bool F32>
 cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *d_texts, const uint8_t *d_vtab,
                    void *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, uint32_t idesc, int num_sms,
                    cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr, int64_t *d_sum_w2 = nullptr,
-                   bool w_signed = true, uint32_t *d_hist = nullptr, int64_t *const *owners = nullptr)
+                   bool w_signed = true, uint32_t *d_hist = nullptr, int64_t *const *owners = nullptr,
+                   unsigned long long *d_clk = nullptr)
 {
     using Cf = Cfg<F32>;
     Params p;
@@ -729,6 +741,7 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *
     p.w_signed = w_signed ? 1 : 0;
     p.hist = d_hist;
     for (int b = 0; b < 16; b++) p.owners[b] = owners ? owners[b] : nullptr;
+    p.clk = d_clk;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_xterm<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
@@ -796,12 +809,12 @@ int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms)
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
                             int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
                             int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w, int64_t *d_sum_w2,
-                            uint32_t *d_hist, int64_t *const *owners)
+                            uint32_t *d_hist, int64_t *const *owners, unsigned long long *d_clk)
 {
     static_assert(Cfg<false>::KB == 1, "owner routing assumes one key byte per unit");
     return launch<false>(tmap_w, tmap_w, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                          idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, d_sum_w, d_sum_w2, w_signed,
-                         d_hist, owners);
+                         d_hist, owners, d_clk);
 }
 
 cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,

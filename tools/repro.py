@@ -1,5 +1,7 @@
 """Run one accumulate+finalize on a synthetic config (debug / sanitizer aid).
-usage: python tools/repro.py C2 [n] [kchunk] [a]   (C3 runs the float path; a = leak amplitude)"""
+usage: python tools/repro.py C2 [n] [kchunk] [a]   (C3 runs the float path; a = leak amplitude)
+REPRO_CLASS_SUMS=1 with an HW workload (C2-HW) takes the class-sum cross term."""
+import os
 import sys
 sys.path.insert(0, ".")
 import numpy as np
@@ -17,7 +19,9 @@ texts, W = S.dataset(w)
 f32 = w.dtype == S.F32
 ld = (w.m + 3) // 4 * 4 if f32 else (w.m + 15) // 16 * 16
 Wp = np.zeros((w.n, ld), W.dtype); Wp[:, :w.m] = W
-eng = P.Engine(w.m, P.CPA_F32 if f32 else P.CPA_S8, P.CPA_HD_LAST, 0)
+eng = P.Engine(w.m, P.CPA_F32 if f32 else P.CPA_S8, w.leak_model, 0)
+if os.environ.get("REPRO_CLASS_SUMS") == "1":
+    eng.set_class_sums(True)
 if len(sys.argv) > 3 and int(sys.argv[3]):
     eng.set_kchunk(int(sys.argv[3]))
 eng.accumulate(torch.from_numpy(Wp).cuda()[:, :w.m], torch.from_numpy(texts).cuda())

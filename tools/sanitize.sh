@@ -3,9 +3,10 @@
 mkdir -p gpurun_out
 CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck racecheck synccheck initcheck; do
-  for cfg in "C1" "C2 2000 512" "C3 4000 0 0.02"; do
+  for cfg in "C1" "C2 2000 512" "C3 4000 0 0.02" "C2-HW 700"; do
     echo "== $tool $cfg" >> gpurun_out/sanitize.log
-    timeout -s KILL 900 $CS --tool $tool --error-exitcode 99 --print-limit 20 python tools/repro.py $cfg \
+    CS_ENV=""; case "$cfg" in C2-HW*) CS_ENV="REPRO_CLASS_SUMS=1";; esac
+    timeout -s KILL 900 env $CS_ENV $CS --tool $tool --error-exitcode 99 --print-limit 20 python tools/repro.py $cfg \
         > gpurun_out/san_tmp.log 2>&1
     echo "exit $?" >> gpurun_out/sanitize.log
     grep -E "ERROR SUMMARY|RACECHECK SUMMARY|========= (Invalid|Race|Barrier|Uninit)|key " gpurun_out/san_tmp.log | head -12 >> gpurun_out/sanitize.log
