@@ -399,7 +399,7 @@ def main():
         ceil_k = MMA_MACS_PER_CLK_SM[is_f32] * 2 * 148 * xt_mhz * 1e6 / 1e12
         roofline["kernel_sm_mhz"] = xt_mhz
         roofline["mma_ceiling_at_kernel_clock"] = ceil_k
-        roofline["frac_of_mma_ceiling_at_kernel_clock"] = achieved / ceil_k
+        roofline["frac_of_mma_ceiling_at_kernel_clock"] = (2 * achieved if is_f32 else achieved) / ceil_k
     if ncu_xt and ncu_xt.get("sm_mhz"):
         # the same kernel under ncu: tensor-pipe activity and its own SM clock; the
         # tcgen05 issue ceiling at that clock is what the 1000 W cap allows

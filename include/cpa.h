@@ -270,7 +270,7 @@ enum { CPA_NUM_PHASES = 5 };
 CPA_API cpa_status cpa_phase_times(cpa_ctx *ctx, double ms[CPA_NUM_PHASES],
                                    int64_t launches[CPA_NUM_PHASES]);
 
-/* Average SM clock (MHz) of the last int8 cross-term launch, from the
+/* Average SM clock (MHz) of the last cross-term launch, from the
  * clock64 and %globaltimer readings its first CTA takes at its start and end
  * (0 if none ran).  Synchronises the stream.  The roofline's issue-rate
  * ceiling at the clock the power cap actually left the kernel.             */

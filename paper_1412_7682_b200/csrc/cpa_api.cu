@@ -466,7 +466,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
             CUDA_TRY(c->timed(2, [&] {
                          return cpa::launch_xterm_bf16x2(mh, ml, d_tx + i0 * 16, c->d_vtab, acc, c->d_counter, M, m,
                                                          kc, c->num_sms, c->stream, &launches,
-                                                         fhist ? c->d_hist : nullptr);
+                                                         fhist ? c->d_hist : nullptr, c->d_clk);
                      }),
                      "xterm_bf16x2");
         }

@@ -52,7 +52,7 @@ int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms);
 cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
                                 const uint8_t *d_vtab, double *d_hw, int *d_counter, int32_t M, int64_t N,
                                 int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
-                                uint32_t *d_hist = nullptr);
+                                uint32_t *d_hist = nullptr, unsigned long long *d_clk = nullptr);
 
 // a5 for the single-byte models (HW_LAST / HW_FIRST), class sums (classsum.cu):
 // counting sort of n traces by text byte per byte (perm: 16 x n int32, off: 16 x

@@ -819,10 +819,11 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, c
 
 cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
                                 const uint8_t *d_vtab, double *d_hw, int *d_counter, int32_t M, int64_t N,
-                                int64_t kc_len, int num_sms, cudaStream_t stream, int *launches, uint32_t *d_hist)
+                                int64_t kc_len, int num_sms, cudaStream_t stream, int *launches, uint32_t *d_hist,
+                                unsigned long long *d_clk)
 {
     return launch<true>(tmap_hi, tmap_lo, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len, idesc_bf16(2 * BMC, BN),
-                        num_sms, stream, launches, nullptr, nullptr, true, d_hist);
+                        num_sms, stream, launches, nullptr, nullptr, true, d_hist, nullptr, d_clk);
 }
 
 }  // namespace cpa
