@@ -538,7 +538,13 @@ def run_stream(args, w, dev, world, rank, local):
     torch.cuda.synchronize()
     rk10 = P.cpa_aes_expand_key(w.key)[10]   # the known round key (library host helper)
     key_idx = torch.tensor([256 * b + rk10[b] for b in range(16)], device=dev)
-    st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, local)
+    fused = world > 1 and args.combine in ("auto", "fused") and 16 % world == 0
+    try:
+        st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, local, fused=fused)
+    except Exception as e:   # peers not mappable: NCCL reduce-scatter checkpoints
+        print(f"fused combine unavailable ({type(e).__name__}: {e}); reduce-scatter checkpoints", file=sys.stderr)
+        fused = False
+        st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, local)
     stream = st.eng.stream
 
     # non-final checkpoints run without blocking (one GPU): their ranks land in
@@ -606,7 +612,8 @@ def run_stream(args, w, dev, world, rank, local):
             "config": {"workload": f"{w.name}: {w.n} traces x {w.m} samples int8, streamed in {chunk}-trace chunks, "
                                    f"checkpoint finalize after every round of {world}, HD last-round model",
                        "n_traces": w.n, "n_samples": w.m, "chunk": chunk, "checkpoints": len(rounds),
-                       "parallelism": f"trace-chunk round-robin x{world}",
+                       "parallelism": f"trace-chunk round-robin x{world}"
+                                      + (", fused row combine" if fused else (", reduce-scatter checkpoints" if world > 1 else "")),
                        "l2": f"inputs {w.n * w.m / 1e9:.0f} GB > 126 MB L2, no flush needed"},
             "key_recovered": bytes(out["master_key"]) == w.key,
             "traces_to_key": curve.traces_to_key(),

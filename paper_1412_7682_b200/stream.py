@@ -8,11 +8,15 @@ and the rank of the known key byte among the 256 guesses is recorded per byte.
 The traces-to-key point is the first checkpoint from which every byte ranks 1.
 
 Multi-GPU [P:230]: global chunk c covers traces [c*chunk, (c+1)*chunk); round j
-gives chunk j*G + r to rank r.  Each rank keeps its own partial sums; a
-checkpoint reduce-scatters them (out of place) into a scratch accumulator, so
-the running partials are never double counted: each rank then finalizes its
+gives chunk j*G + r to rank r.  With the fused combine (fused=True) every rank's
+cross term adds each key byte's rows into the owner rank's running accumulator
+over NVLink (multigpu.FusedOwners), so a checkpoint only all-reduces the small
+fields into a scratch accumulator and copies the rank's own, already combined
+rows.  Otherwise each rank keeps its own partial sums and a checkpoint
+reduce-scatters them (out of place) into the scratch accumulator, so the running
+partials are never double counted.  Either way each rank then finalizes its
 4096/G hypothesis rows, the maxima are gathered and Phase 4 ranks them
-(multigpu.reduce_scatter_rows).
+(SURVEY §8e (ii)).
 
 Only index bookkeeping and orchestration live here; every sum, rho and rank is
 computed by libcpa through the C ABI."""
@@ -74,9 +78,11 @@ class StreamingAttack:
     multi-GPU) run.  `group` is a torch.distributed group (None = default when
     initialized; single process otherwise)."""
 
-    def __init__(self, M: int, dtype: int, model: int, device: int = 0, group=None):
+    def __init__(self, M: int, dtype: int, model: int, device: int = 0, group=None, fused: bool = False):
+        import torch
         import torch.distributed as dist
 
+        from . import multigpu as MG
         from .engine import Engine
         self.group = group
         self.world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
@@ -84,6 +90,11 @@ class StreamingAttack:
         # multi-GPU checkpoints finalize from an all-reduced copy of the partials
         self.view = Engine(M, dtype, model, device, stream=self.eng.stream) if self.world > 1 else None
         self.n_local = 0
+        # fused combine: every chunk's cross-term rows go straight to their owner
+        # rank's running accumulator (MG.FusedOwners); a checkpoint then only
+        # all-reduces the small fields
+        self.owners = MG.FusedOwners(self.eng, group) if (fused and self.world > 1) else None
+        self._bar = torch.zeros(1, dtype=torch.int32, device=self.eng.device)
 
     def add(self, traces, texts):
         self.eng.accumulate(traces, texts)
@@ -96,7 +107,19 @@ class StreamingAttack:
 
         from . import multigpu as MG
         with torch.cuda.stream(self.eng.stream):
-            h0, h1 = MG.reduce_scatter_rows(self.eng.accum, self.eng.M, self.group, out=self.view.accum)
+            if self.owners is not None:
+                # small fields: all-reduced copy (also the point after which every
+                # peer's atomics into this rank's rows are complete); then this
+                # rank's rows, already combined; then a barrier so that no peer
+                # starts the next round's atomics into them before the copy
+                M = self.eng.M
+                n_hw = 4096 * M
+                self.view.accum[n_hw:].copy_(self.eng.accum[n_hw:])
+                h0, h1 = MG.allreduce_small_fields(self.view.accum, M, self.group)
+                self.view.accum[h0 * M:h1 * M].copy_(self.eng.accum[h0 * M:h1 * M])
+                MG.device_barrier(self._bar, self.group)
+            else:
+                h0, h1 = MG.reduce_scatter_rows(self.eng.accum, self.eng.M, self.group, out=self.view.accum)
             mx, am, pk = (t[0] for t in self.view.maxima_buffers(1))
             rho = self.view.finalize_rows(h0, h1, mx, am, pk, want_rho)
             MG.gather_rows(mx, am, pk, h0, h1, self.group)
@@ -118,12 +141,20 @@ class StreamingAttack:
     def reset(self):
         self.eng.reset()
         self.n_local = 0
+        if self.owners is not None:   # every owner is zeroed before any peer adds into it
+            import torch
+
+            from . import multigpu as MG
+            with torch.cuda.stream(self.eng.stream):
+                MG.device_barrier(self._bar, self.group)
 
     @property
     def launches(self) -> int:
         return self.eng.launches + (self.view.launches if self.view is not None else 0)
 
     def close(self):
+        if self.owners is not None:
+            self.owners.close()
         if self.view is not None:
             self.view.close()
         self.eng.close()

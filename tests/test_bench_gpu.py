@@ -56,6 +56,7 @@ def test_bench_stream_two_ranks_one_gpu_gloo():
     assert d["n_gpus"] == 2 and d["key_recovered"] is True
     pts = d["rank_curve"]["points"]
     assert pts[-1][0] == 500 and d["config"]["checkpoints"] == len(pts)
+    assert "fused row combine" in d["config"]["parallelism"]   # rows routed to their owner by CUDA IPC
 
 
 @pytest.mark.gpu
