@@ -277,18 +277,10 @@ def main():
     if combine == "auto":
         combine = "fused" if (not is_f32 and not class_sums and 16 % world == 0) else "rows"
     owners = None
-    if combine == "fused":
-        try:   # map the peers' accumulators (CUDA IPC) and route the rows to their owners
-            owners = MG.FusedOwners(eng)
-        except Exception as e:  # no peer mapping on this box: NCCL reduce-scatter instead
-            fused_note = f"fused combine unavailable ({type(e).__name__}: {e}); rows"
-            combine = "rows"
-        ok = torch.tensor([0 if owners is None else 1], dtype=torch.int32, device=dev)
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)   # every rank or none
-        if owners is not None and int(ok.item()) == 0:
-            owners.close()
-            owners, combine = None, "rows"
-            fused_note = fused_note or "fused combine unavailable on a peer rank; rows"
+    if combine == "fused":   # map the peers' accumulators (CUDA IPC), route the rows to their owners
+        owners, why = MG.FusedOwners.try_create(eng)
+        if owners is None:      # no peer mapping on this box (every rank agrees): NCCL reduce-scatter
+            fused_note, combine = f"fused combine unavailable ({why}); rows", "rows"
     h0, h1 = MG.row_range(rank, world) if combine in ("rows", "fused") else (0, 4096)
     bar_t = torch.zeros(1, dtype=torch.int32, device=dev)
     rho = torch.empty((h1 - h0, m_local), dtype=torch.float64, device=dev)   # this rank's block of rho
@@ -539,12 +531,10 @@ def run_stream(args, w, dev, world, rank, local):
     rk10 = P.cpa_aes_expand_key(w.key)[10]   # the known round key (library host helper)
     key_idx = torch.tensor([256 * b + rk10[b] for b in range(16)], device=dev)
     fused = world > 1 and args.combine in ("auto", "fused") and 16 % world == 0
-    try:
-        st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, local, fused=fused)
-    except Exception as e:   # peers not mappable: NCCL reduce-scatter checkpoints
-        print(f"fused combine unavailable ({type(e).__name__}: {e}); reduce-scatter checkpoints", file=sys.stderr)
+    st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, local, fused=fused)
+    if fused and st.owners is None:   # peers not mappable: NCCL reduce-scatter checkpoints
+        print(f"fused combine unavailable ({st.fused_note}); reduce-scatter checkpoints", file=sys.stderr)
         fused = False
-        st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, local)
     stream = st.eng.stream
 
     # non-final checkpoints run without blocking (one GPU): their ranks land in

@@ -172,6 +172,10 @@ CPA_API cpa_status cpa_set_row_owners(cpa_ctx *ctx, void *const owners[16]);
  * another process (same or peer GPU, peer access enabled) and returns the
  * pointer at that offset; cpa_ipc_close unmaps the BASE (pointer - offset).   */
 CPA_API cpa_status cpa_ipc_export(const void *d_ptr, uint8_t handle[64], uint64_t *offset);
+/* *ok = 1 when device `dev` can access `peer`'s memory with native atomics
+ * (peer access + cudaDevP2PAttrNativeAtomicSupported; always 1 for dev == peer):
+ * the precondition of routing rows to a peer with cpa_set_row_owners.       */
+CPA_API cpa_status cpa_peer_atomics(int dev, int peer, int *ok);
 CPA_API cpa_status cpa_ipc_open(const uint8_t handle[64], uint64_t offset, void **d_ptr);
 CPA_API cpa_status cpa_ipc_close(void *d_base);
 

@@ -27,7 +27,7 @@ FIELD_HW, FIELD_W, FIELD_W2, FIELD_H, FIELD_H2, FIELD_N = range(6)
 ABI_SYMBOLS = (
     "cpa_accum_words", "cpa_accum_bytes", "cpa_accum_offset", "cpa_init", "cpa_accumulate",
     "cpa_accumulate_host", "cpa_finalize", "cpa_finalize_async", "cpa_finalize_rows", "cpa_select",
-    "cpa_set_row_owners", "cpa_ipc_export", "cpa_ipc_open", "cpa_ipc_close", "cpa_xterm_clock", "cpa_reset", "cpa_sync", "cpa_destroy",
+    "cpa_set_row_owners", "cpa_ipc_export", "cpa_ipc_open", "cpa_ipc_close", "cpa_xterm_clock", "cpa_peer_atomics", "cpa_reset", "cpa_sync", "cpa_destroy",
     "cpa_set_offsets", "cpa_set_option", "cpa_phase_times", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
     "cpa_aes_expand_key", "cpa_aes_invert_key_schedule",
 )
@@ -68,6 +68,7 @@ def _load():
         "cpa_ipc_open": (ST, [P, C.c_uint64, C.POINTER(P)]),
         "cpa_ipc_close": (ST, [P]),
         "cpa_xterm_clock": (ST, [P, C.POINTER(C.c_double)]),
+        "cpa_peer_atomics": (ST, [C.c_int, C.c_int, C.POINTER(C.c_int)]),
         "cpa_reset": (ST, [P]),
         "cpa_sync": (ST, [P]),
         "cpa_destroy": (ST, [P]),
@@ -164,6 +165,12 @@ def cpa_xterm_clock(ctx) -> float:
     mhz = C.c_double(0.0)
     _check(_lib.cpa_xterm_clock(ctx, C.byref(mhz)), "cpa_xterm_clock")
     return mhz.value
+
+
+def cpa_peer_atomics(dev: int, peer: int) -> bool:
+    ok = C.c_int(0)
+    _check(_lib.cpa_peer_atomics(dev, peer, C.byref(ok)), "cpa_peer_atomics")
+    return bool(ok.value)
 
 
 def cpa_ipc_export(d_ptr) -> tuple[bytes, int]:

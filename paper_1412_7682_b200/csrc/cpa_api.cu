@@ -803,6 +803,21 @@ cpa_status cpa_set_row_owners(cpa_ctx *c, void *const owners[16])
     return CPA_OK;
 }
 
+cpa_status cpa_peer_atomics(int dev, int peer, int *ok)
+{
+    if (!ok) return fail(CPA_E_INVALID_ARG, "null argument");
+    if (dev == peer) {
+        *ok = 1;
+        return CPA_OK;
+    }
+    int access = 0, atomics = 0;
+    CUDA_TRY(cudaDeviceCanAccessPeer(&access, dev, peer), "cudaDeviceCanAccessPeer");
+    CUDA_TRY(cudaDeviceGetP2PAttribute(&atomics, cudaDevP2PAttrNativeAtomicSupported, dev, peer),
+             "cudaDeviceGetP2PAttribute");
+    *ok = access && atomics;
+    return CPA_OK;
+}
+
 cpa_status cpa_ipc_export(const void *d_ptr, uint8_t handle[64], uint64_t *offset)
 {
     if (!d_ptr || !handle || !offset) return fail(CPA_E_INVALID_ARG, "null argument");

@@ -214,11 +214,15 @@ class FusedOwners:
         self.world, self.rank = _world(group)
         byte_owner(0, self.world)                  # validates world | 16
         h, off = B.cpa_ipc_export(eng.accum)
+        dev = eng.accum.device.index
         allh = [None] * self.world
-        dist.all_gather_object(allh, (h, off), group=group)
+        dist.all_gather_object(allh, (h, off, dev), group=group)
+        for r, (_, _, pdev) in enumerate(allh):   # system-scope atomics must work on every peer
+            if not B.cpa_peer_atomics(dev, pdev):
+                raise RuntimeError(f"no native peer atomics from device {dev} to rank {r}'s device {pdev}")
         self.mapped = []                           # (base, ptr) of opened peer buffers
         addrs = []
-        for r, (hr, offr) in enumerate(allh):
+        for r, (hr, offr, _) in enumerate(allh):
             if r == self.rank:
                 addrs.append(eng.accum.data_ptr())
                 continue
@@ -235,6 +239,27 @@ class FusedOwners:
         for base, _ in self.mapped:
             B.cpa_ipc_close(base)
         self.mapped = []
+
+    @classmethod
+    def try_create(cls, eng, group=None):
+        """Collective: every rank maps its peers, or (if any rank cannot: no peer
+        access, no native peer atomics, no IPC) none does.  Returns (owners or
+        None, reason or None)."""
+        import torch
+        import torch.distributed as dist
+        owners, why = None, None
+        try:
+            owners = cls(eng, group)
+        except Exception as e:  # noqa: BLE001 -- any failure means: use the NCCL combine
+            why = f"{type(e).__name__}: {e}"
+        ok = torch.tensor([0 if owners is None else 1], dtype=torch.int32, device=eng.accum.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            if owners is not None:
+                owners.close()
+                owners = None
+            why = why or "a peer rank cannot map the accumulators"
+        return owners, why
 
 
 def device_barrier(t, group=None):

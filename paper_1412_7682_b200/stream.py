@@ -93,7 +93,8 @@ class StreamingAttack:
         # fused combine: every chunk's cross-term rows go straight to their owner
         # rank's running accumulator (MG.FusedOwners); a checkpoint then only
         # all-reduces the small fields
-        self.owners = MG.FusedOwners(self.eng, group) if (fused and self.world > 1) else None
+        self.owners, self.fused_note = (MG.FusedOwners.try_create(self.eng, group) if (fused and self.world > 1)
+                                        else (None, None))
         self._bar = torch.zeros(1, dtype=torch.int32, device=self.eng.device)
 
     def add(self, traces, texts):

@@ -222,3 +222,56 @@ def test_byte_owner_table_matches_row_ranges():
     for G in (3, 5, 6):
         with pytest.raises(ValueError):
             MG.byte_owner(0, G)
+
+
+class _FakeEng:
+    def __init__(self):
+        self.accum = torch.zeros(8, dtype=torch.int64)
+        self.owner_calls = []
+
+    def set_row_owners(self, owners):
+        self.owner_calls.append(owners)
+
+
+class _Flaky(MG.FusedOwners):
+    """Rank 0 maps its peers; rank 1 cannot (as on a box without peer atomics)."""
+    closed = 0
+
+    def __init__(self, eng, group=None):
+        if dist.get_rank() == 1:
+            raise RuntimeError("no native peer atomics")
+        self.eng, self.mapped, self.owners = eng, [], [0] * 16
+        eng.set_row_owners(self.owners)
+
+    def close(self):
+        _Flaky.closed += 1
+        self.eng.set_row_owners(None)
+
+
+def _fused_consensus_worker(rank, world, port, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    eng = _FakeEng()
+    owners, why = _Flaky.try_create(eng)
+    ret.put((rank, owners is None, why, eng.owner_calls[-1] if eng.owner_calls else "none", _Flaky.closed))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_fused_combine_consensus_falls_back_on_every_rank():
+    """FusedOwners.try_create is collective: when one rank cannot map its peers,
+    every rank falls back to the NCCL combine (no rank is left routing rows)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_consensus_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, none0, why0, last0, closed0), (r1, none1, why1, last1, _) = res
+    assert none0 and none1                       # both fall back
+    assert last0 is None and closed0 == 1        # rank 0 undid its routing
+    assert "peer atomics" in why1 and why0       # the reason is reported on both
