@@ -56,7 +56,7 @@ typedef enum {
 typedef enum {
     CPA_S8 = 0,  /* signed 8-bit ADC samples (exact int path) */
     CPA_U8 = 1,  /* unsigned 8-bit ADC samples (exact int path) */
-    CPA_F32 = 2  /* float32 samples (bf16 hi/lo tensor-core path, fp64 sums) */
+    CPA_F32 = 2  /* float32 samples (fp16 hi + e4m3 lo tensor-core path, fp64 sums) */
 } cpa_dtype;
 
 /* Selection function H [P:67, P:75] (the paper never writes it out; see
@@ -216,11 +216,13 @@ CPA_API cpa_status cpa_select(cpa_ctx *ctx, int32_t G, double *d_maxabs, int32_t
                               double *d_peak, int32_t *d_rank, cpa_result *res);
 
 /* CPA_F32 only: per-sample offsets o_j (device pointer, M floats; NULL = 0)
- * subtracted from every sample before the bf16 hi/lo split.  rho is invariant
+ * subtracted from every sample before the fp16 hi / e4m3 lo split.  rho is invariant
  * to per-sample offsets [S:285]; centring keeps the split and the fp32 tensor-
  * core accumulation accurate.  Default: the first trace of the first
  * cpa_accumulate call.  Multi-GPU: every rank must use the same offsets (the
- * accumulated sums are of the offset samples).                               */
+ * accumulated sums are of the offset samples).  Setting offsets also re-derives
+ * the split's per-sample power-of-two scales (from the next accumulate's first
+ * <= 64 traces; a precision choice that never changes the sums' meaning).   */
 CPA_API cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets);
 
 CPA_API cpa_status cpa_reset(cpa_ctx *ctx);    /* zero the accumulator and the

@@ -100,10 +100,14 @@ struct cpa_ctx {
     int64_t stage_chunk_bytes = kStageBytes;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
-    // float path (a6): per-sample offsets, bf16 hi/lo planes, non-finite flag
+    // float path (a6): per-sample offsets and power-of-two scales ([M] scale |
+    // [M] 1/scale | range-repair scratch), fp16 hi and e4m3 lo planes, non-finite flag
     float *d_offset = nullptr;
     bool offset_set = false;
-    uint16_t *d_hi = nullptr, *d_lo = nullptr;
+    float *d_scale = nullptr;
+    bool scale_set = false;
+    uint16_t *d_hi = nullptr;
+    uint8_t *d_lo = nullptr;
     int64_t plane_rows = 0;
     int *d_nonfinite = nullptr;
     uint32_t *d_hist = nullptr;  // a3 byte-pair histogram scratch (16 x 65536)
@@ -252,6 +256,7 @@ cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, 
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
     }
     if (e == cudaSuccess) e = cudaMalloc(&c->d_offset, sizeof(float) * M);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_scale, 2 * sizeof(float) * M + 5 * (size_t)M + 16);
     if (e != cudaSuccess) {
         cpa_destroy(c);
         return fail(CPA_E_NO_MEMORY, "device scratch: %s", cudaGetErrorString(e));
@@ -279,6 +284,7 @@ cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets)
     else
         CUDA_TRY(cudaMemsetAsync(ctx->d_offset, 0, sizeof(float) * ctx->M, ctx->stream), "offsets");
     ctx->offset_set = true;
+    ctx->scale_set = false;  // the split scales follow the spread about the offsets
     return CPA_OK;
 }
 
@@ -419,7 +425,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                                           c->stream, &launches);
                      }),
                      "modelsums");
-        // per-sample offsets (centring keeps the bf16 hi/lo split and the fp32
+        // per-sample offsets (centring keeps the hi/lo split and the fp32
         // accumulation accurate; rho is invariant to them [S:285]): unless the
         // caller set them, take the first trace of the first accumulate call
         if (!c->offset_set) {
@@ -427,48 +433,61 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                      "offsets");
             c->offset_set = true;
         }
-        const int64_t ldh = (M + 7) / 8 * 8;
-        const int64_t max_rows = (1LL << 30) / (ldh * 2);  // <= 1 GiB per bf16 plane
+        // per-sample power-of-two scales of the split (exact; a precision choice,
+        // not a change of the sums): from the first <= 64 traces seen
+        if (!c->scale_set) {
+            CUDA_TRY(cpa::launch_scale_f32((const float *)d_w, ld, n < 64 ? n : 64, M, c->d_offset, c->d_scale,
+                                           c->d_scale + M, c->stream, &launches),
+                     "split scales");
+            c->scale_set = true;
+        }
+        const int64_t ldh = (M + 7) / 8 * 8;     // fp16 hi plane pitch (16-byte rows for TMA)
+        const int64_t ldl = (M + 15) / 16 * 16;  // e4m3 lo plane pitch
+        const int64_t max_rows = (1LL << 30) / (ldh * 2);  // <= 1 GiB per fp16 plane
         const int64_t chunk = n < max_rows ? n : max_rows;
         if (c->plane_rows < chunk) {
             CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
             cudaFree(c->d_hi);
             cudaFree(c->d_lo);
-            c->d_hi = c->d_lo = nullptr;
+            c->d_hi = nullptr;
+            c->d_lo = nullptr;
             c->plane_rows = 0;
-            if (cudaMalloc(&c->d_hi, chunk * ldh * 2) != cudaSuccess || cudaMalloc(&c->d_lo, chunk * ldh * 2) != cudaSuccess)
-                return fail(CPA_E_NO_MEMORY, "bf16 planes (%lld rows)", (long long)chunk);
+            if (cudaMalloc(&c->d_hi, chunk * ldh * 2) != cudaSuccess || cudaMalloc(&c->d_lo, chunk * ldl) != cudaSuccess)
+                return fail(CPA_E_NO_MEMORY, "hi/lo planes (%lld rows)", (long long)chunk);
             c->plane_rows = chunk;
         }
         for (int64_t i0 = 0; i0 < n; i0 += chunk) {
             const int64_t m = (n - i0) < chunk ? (n - i0) : chunk;
             const float *w = (const float *)d_w + i0 * ld;
             CUDA_TRY(c->timed(1, [&] {
-                         return cpa::launch_split_f32(w, ld, m, M, c->d_offset, c->d_hi, c->d_lo, ldh,
-                                                      acc + cpa_accum_offset(M, 1), acc + cpa_accum_offset(M, 2),
-                                                      c->d_nonfinite, c->stream, &launches);
+                         return cpa::launch_split_f32(w, ld, m, M, c->d_offset, c->d_scale, c->d_hi, c->d_lo, ldh,
+                                                      ldl, acc + cpa_accum_offset(M, 1), acc + cpa_accum_offset(M, 2),
+                                                      c->d_nonfinite, (uint8_t *)(c->d_scale + 2 * M), c->stream,
+                                                      &launches);
                      }),
                      "split_f32");
             CUtensorMap mh, ml;
             cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)m};
-            cuuint64_t strides[1] = {(cuuint64_t)(ldh * 2)};
-            cuuint32_t box[2] = {64, 64};  // 64 bf16 = the 128-byte swizzle span, x 64 traces
             cuuint32_t estr[2] = {1, 1};
             for (int k = 0; k < 2; k++) {
-                CUresult r = get_encode()(k ? &ml : &mh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, k ? c->d_lo : c->d_hi,
-                                          dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-                if (r != CUDA_SUCCESS) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled (bf16) failed (%d)", (int)r);
+                // hi: 64 fp16 = the 128-byte swizzle span; lo: 128 e4m3 bytes; x 64 traces
+                cuuint64_t strides[1] = {(cuuint64_t)(k ? ldl : ldh * 2)};
+                cuuint32_t box[2] = {k ? 128u : 64u, 64u};
+                CUresult r = get_encode()(k ? &ml : &mh,
+                                          k ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                                          k ? (void *)c->d_lo : (void *)c->d_hi, dims, strides, box, estr,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (r != CUDA_SUCCESS) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled (hi/lo) failed (%d)", (int)r);
             }
             const int64_t kc = c->kchunk ? (c->kchunk < 4096 ? c->kchunk : 4096)
                                          : cpa::xterm_f32_auto_kchunk(M, m, c->num_sms);
             CUDA_TRY(c->timed(2, [&] {
-                         return cpa::launch_xterm_bf16x2(mh, ml, d_tx + i0 * 16, c->d_vtab, acc, c->d_counter, M, m,
-                                                         kc, c->num_sms, c->stream, &launches,
-                                                         fhist ? c->d_hist : nullptr, c->d_clk);
+                         return cpa::launch_xterm_f32(mh, ml, d_tx + i0 * 16, c->d_vtab, acc, c->d_scale + M,
+                                                      c->d_counter, M, m, kc, c->num_sms, c->stream, &launches,
+                                                      fhist ? c->d_hist : nullptr, c->d_clk);
                      }),
-                     "xterm_bf16x2");
+                     "xterm_f32");
         }
         if (fhist)
             CUDA_TRY(c->timed(0, [&] {
@@ -969,6 +988,7 @@ cpa_status cpa_destroy(cpa_ctx *c)
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     cudaFree(c->d_offset);
+    cudaFree(c->d_scale);
     cudaFree(c->d_hi);
     cudaFree(c->d_lo);
     cudaFree(c->d_nonfinite);

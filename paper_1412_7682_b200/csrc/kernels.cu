@@ -4,6 +4,7 @@
 //   a8 finalize        Eq. (1) [P:69] in fp64 + max |rho| per (b,k) [P:83]
 //   a9 phase 4         per-byte ranking / best sub-key              [P:87]
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -611,7 +612,19 @@ cudaError_t launch_phase4(const FinalizeOut &o, cudaStream_t s, int *launches)
 }  // namespace cpa
 
 // ---------------------------------------------------------------------------
-// a6 pre-pass: float traces -> centred bf16 hi/lo planes + fp64 moments.
+// a6 pre-pass: float traces -> centred, per-sample scaled fp16 hi plane + e4m3
+// lo plane, and fp64 moments.  With c = w - o_j and s_j = 2^e_j (exact):
+//     hi = fp16(c s_j),  lo = e4m3_satfinite(512 (c s_j - hi))
+// so that c s_j ~= hi + lo / 512.  The cross term multiplies hi by fp16(H)
+// (kind::f16) and lo by the e4m3 value H / 512 (kind::f8f6f4), whose code is the
+// byte H itself (0..7 are the subnormals m 2^-9, 8 = 2^-6), into ONE fp32
+// accumulator; the spill multiplies column j by 1 / s_j (exact).  |lo / 512| is at
+// most half an fp16 ulp of c s_j (<= 2^-11 |c s_j|) and e4m3 keeps 4 significant
+// bits of it down to 2^-6 (steps of 2^-9 below), so the per-element error is at
+// most 2^-15 |c s_j| + 2^-19 (bf16 alone: 2^-9 |c s_j|; bf16 + e4m3: 2^-13, which
+// measured 1.4e-4 in rho at N = 65).  s_j puts the spread of the first traces in
+// [8, 16) (k_scale_f32): fp16 holds 4096x that, e4m3 lo saturates (448) only
+// above ~100x it, and then the element keeps fp16 precision.
 // Thread = 4 consecutive samples (one float4 per row) over SP_ROWS rows.
 // ---------------------------------------------------------------------------
 namespace cpa {
@@ -622,30 +635,43 @@ constexpr int SP_ROWS = 512;
 #define SP_U_ROWS 4
 #endif
 constexpr int SP_U = SP_U_ROWS;
+// |c s_j| from which the fp16 hi plane is not trusted (fp16 max 65504): the
+// column's scale is lowered and its planes rewritten (k_fix_scale, k_resplit_f32)
+constexpr float kF16Safe = 32768.0f;
 
-__device__ __forceinline__ uint16_t bf16_bits(float x)
+__device__ __forceinline__ uint16_t f16_bits(float x)
 {
-    __nv_bfloat16 h = __float2bfloat16_rn(x);
-    return *reinterpret_cast<uint16_t *>(&h);
+    return __half_as_ushort(__float2half_rn(x));
 }
-__device__ __forceinline__ float bf16_val(uint16_t b)
+__device__ __forceinline__ float f16_val(uint16_t b)
 {
-    return __uint_as_float((uint32_t)b << 16);
+    return __half2float(__ushort_as_half(b));
+}
+// two fp32 -> two e4m3 bytes (round to nearest even, saturating): x in the low byte
+__device__ __forceinline__ uint32_t e4m3x2(float x, float y)
+{
+    uint16_t d;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(d) : "f"(y), "f"(x));
+    return d;
 }
 
 __global__ void __launch_bounds__(SP_THREADS)
 k_split_f32(const float *__restrict__ w, int64_t ld, int64_t n, int32_t M, const float *__restrict__ offset,
-            uint16_t *__restrict__ hi, uint16_t *__restrict__ lo, int64_t ldh, double *sum_w, double *sum_w2,
-            int *nonfinite)
+            const float *__restrict__ scale, uint16_t *__restrict__ hi, uint8_t *__restrict__ lo, int64_t ldh,
+            int64_t ldl, double *sum_w, double *sum_w2, int *nonfinite, uint32_t *cmax, int *range)
 {
     const int g = blockIdx.x * SP_THREADS + threadIdx.x;
     const int j0 = g * 4;
     if (j0 >= M) return;
     const int cnt = min(4, M - j0);
-    float o[4];
+    float o[4], sc[4];
 #pragma unroll
-    for (int q = 0; q < 4; q++) o[q] = (q < cnt && offset) ? offset[j0 + q] : 0.0f;
+    for (int q = 0; q < 4; q++) {
+        o[q] = (q < cnt && offset) ? offset[j0 + q] : 0.0f;
+        sc[q] = q < cnt ? scale[j0 + q] : 1.0f;
+    }
     double s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+    float amax[4] = {0, 0, 0, 0};  // max |c| of this thread's rows (range repair)
     bool bad = false;
     const int64_t r0 = (int64_t)blockIdx.y * SP_ROWS;
     const int64_t r1 = min(n, r0 + SP_ROWS);
@@ -669,24 +695,29 @@ k_split_f32(const float *__restrict__ w, int64_t ld, int64_t n, int32_t M, const
         const int64_t r = rb + u;
         if (r >= r1) break;
         const float *x = xs[u];
-        uint16_t h[4], l[4];
+        uint16_t h[4];
+        float l[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) {
             bad |= !isfinite(x[q]);
             const float c = __fsub_rn(x[q], o[q]);
-            h[q] = bf16_bits(c);
-            l[q] = bf16_bits(__fsub_rn(c, bf16_val(h[q])));
+            const float cs = __fmul_rn(c, sc[q]);  // exact: power of two
+            amax[q] = fmaxf(amax[q], fabsf(c));      // (NaN is reported as non-finite)
+            h[q] = f16_bits(cs);
+            l[q] = __fmul_rn(__fsub_rn(cs, f16_val(h[q])), 512.0f);  // both exact
             s1[q] += (double)c;
             s2[q] += (double)c * (double)c;
         }
-        uint16_t *hp = hi + r * ldh + j0, *lp = lo + r * ldh + j0;
+        uint16_t *hp = hi + r * ldh + j0;
+        uint8_t *lp = lo + r * ldl + j0;
+        const uint32_t l8 = e4m3x2(l[0], l[1]) | (e4m3x2(l[2], l[3]) << 16);
         if (cnt == 4) {
             *(uint2 *)hp = make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
-            *(uint2 *)lp = make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
+            *(uint32_t *)lp = l8;
         } else {
             for (int q = 0; q < cnt; q++) {
                 hp[q] = h[q];
-                lp[q] = l[q];
+                lp[q] = (uint8_t)(l8 >> (8 * q));
             }
         }
     }
@@ -695,7 +726,76 @@ k_split_f32(const float *__restrict__ w, int64_t ld, int64_t n, int32_t M, const
         atomicAdd(&sum_w[j0 + q], s1[q]);
         atomicAdd(&sum_w2[j0 + q], s2[q]);
     }
+    bool over = false;
+    for (int q = 0; q < cnt; q++) {
+        atomicMax(&cmax[j0 + q], __float_as_uint(amax[q]));  // non-negative floats order as their bits
+        over |= amax[q] * sc[q] >= kF16Safe;
+    }
     if (bad) atomicOr(nonfinite, 1);
+    if (over) atomicOr(range, 1);
+}
+
+// Range repair (rare; both kernels exit at once unless *range is set): a column
+// whose |c s_j| reached kF16Safe in this chunk (an outlier far beyond the spread
+// the scale was chosen from) gets a smaller scale, from this chunk's max |c|, and
+// its hi/lo planes are rewritten before the cross term reads them.  The spill
+// uses the scale in force for the chunk, so later chunks keep the new one.
+__global__ void k_fix_scale(const int *range, const uint32_t *cmax, int32_t M, float *scale, float *inv_scale,
+                            uint8_t *colflag)
+{
+    if (*range == 0) return;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    const float r = __uint_as_float(cmax[j]);
+    uint8_t f = 0;
+    if (isfinite(r) && r * scale[j] >= kF16Safe) {
+        int E;
+        frexpf(r, &E);
+        const int e = min(64, max(-64, 4 - E));
+        scale[j] = ldexpf(1.0f, e);
+        inv_scale[j] = ldexpf(1.0f, -e);
+        f = 1;
+    }
+    colflag[j] = f;
+}
+
+__global__ void __launch_bounds__(SP_THREADS)
+k_resplit_f32(const int *range, const uint8_t *colflag, const float *__restrict__ w, int64_t ld, int64_t n, int32_t M,
+              const float *__restrict__ offset, const float *__restrict__ scale, uint16_t *__restrict__ hi,
+              uint8_t *__restrict__ lo, int64_t ldh, int64_t ldl)
+{
+    if (*range == 0) return;
+    const int j = blockIdx.x * SP_THREADS + threadIdx.x;
+    if (j >= M || !colflag[j]) return;
+    const float o = offset ? offset[j] : 0.0f, sc = scale[j];
+    const int64_t r0 = (int64_t)blockIdx.y * SP_ROWS, r1 = min(n, r0 + SP_ROWS);
+    for (int64_t r = r0; r < r1; r++) {
+        const float cs = __fmul_rn(__fsub_rn(w[r * ld + j], o), sc);
+        const uint16_t h = f16_bits(cs);
+        hi[r * ldh + j] = h;
+        lo[r * ldl + j] = (uint8_t)e4m3x2(__fmul_rn(__fsub_rn(cs, f16_val(h)), 512.0f), 0.0f);
+    }
+}
+
+// Per-sample scale s_j = 2^e_j for the split: the largest |w - o_j| over the
+// first n rows, r, is brought into [8, 16) (e_j clamped to [-64, 64]; 1 when r
+// is 0 or not finite).  inv_scale = 1 / s_j (exact).
+__global__ void k_scale_f32(const float *__restrict__ w, int64_t ld, int64_t n, int32_t M,
+                            const float *__restrict__ offset, float *scale, float *inv_scale)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    const float o = offset ? offset[j] : 0.0f;
+    float r = 0.0f;
+    for (int64_t i = 0; i < n; i++) r = fmaxf(r, fabsf(__fsub_rn(w[i * ld + j], o)));
+    int e = 0;
+    if (r > 0.0f && isfinite(r)) {
+        int E;
+        frexpf(r, &E);  // r in [2^(E-1), 2^E)
+        e = min(64, max(-64, 4 - E));
+    }
+    scale[j] = ldexpf(1.0f, e);
+    inv_scale[j] = ldexpf(1.0f, -e);
 }
 }  // namespace
 
@@ -741,12 +841,32 @@ cudaError_t launch_repack(const uint8_t *d_src, int64_t rb, uint8_t *d_dst, int6
 }
 
 cudaError_t launch_split_f32(const float *d_w, int64_t ld, int64_t n, int32_t M, const float *d_offset,
-                             uint16_t *d_hi, uint16_t *d_lo, int64_t ldh, double *d_sum_w, double *d_sum_w2,
-                             int *d_nonfinite, cudaStream_t s, int *launches)
+                             const float *d_scale, uint16_t *d_hi, uint8_t *d_lo, int64_t ldh, int64_t ldl,
+                             double *d_sum_w, double *d_sum_w2, int *d_nonfinite, uint8_t *d_scratch, cudaStream_t s,
+                             int *launches)
 {
     const int groups = (M + 3) / 4;
     dim3 grid((groups + SP_THREADS - 1) / SP_THREADS, (unsigned)((n + SP_ROWS - 1) / SP_ROWS));
-    k_split_f32<<<grid, SP_THREADS, 0, s>>>(d_w, ld, n, M, d_offset, d_hi, d_lo, ldh, d_sum_w, d_sum_w2, d_nonfinite);
+    // per chunk: column maxima and the range flag start at zero
+    uint32_t *cmax = reinterpret_cast<uint32_t *>(d_scratch);
+    int *range = reinterpret_cast<int *>(d_scratch + 4 * (size_t)M);
+    uint8_t *colflag = d_scratch + 4 * (size_t)M + 16;
+    cudaError_t e = cudaMemsetAsync(d_scratch, 0, 4 * (size_t)M + 16, s);
+    if (e != cudaSuccess) return e;
+    float *scale = const_cast<float *>(d_scale);
+    k_split_f32<<<grid, SP_THREADS, 0, s>>>(d_w, ld, n, M, d_offset, d_scale, d_hi, d_lo, ldh, ldl, d_sum_w, d_sum_w2,
+                                            d_nonfinite, cmax, range);
+    k_fix_scale<<<(M + 127) / 128, 128, 0, s>>>(range, cmax, M, scale, scale + M, colflag);
+    dim3 grid1((M + SP_THREADS - 1) / SP_THREADS, grid.y);
+    k_resplit_f32<<<grid1, SP_THREADS, 0, s>>>(range, colflag, d_w, ld, n, M, d_offset, d_scale, d_hi, d_lo, ldh, ldl);
+    if (launches) (*launches) += 3;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scale_f32(const float *d_w, int64_t ld, int64_t n, int32_t M, const float *d_offset,
+                             float *d_scale, float *d_inv_scale, cudaStream_t s, int *launches)
+{
+    k_scale_f32<<<(M + 127) / 128, 128, 0, s>>>(d_w, ld, n, M, d_offset, d_scale, d_inv_scale);
     if (launches) (*launches)++;
     return cudaGetLastError();
 }

@@ -41,18 +41,25 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, c
                             int64_t *d_sum_w2 = nullptr, uint32_t *d_hist = nullptr,
                             int64_t *const *owners = nullptr, unsigned long long *d_clk = nullptr);
 
-// a6: float traces.  Split pre-pass: w' = w - offset[j] (fp32), hi = bf16(w'),
-// lo = bf16(w' - hi) into [n][ldh] bf16 planes; fp64 sum w', sum w'^2; sets
-// *nonfinite on NaN/Inf [S:140].  Cross term: kind::f16 on hi and lo, fp32 TMEM
-// accumulation per <= 4096-trace unit, fp64 atomic spill.
+// a6: float traces.  Split pre-pass: c = w - offset[j], hi = fp16(c s_j),
+// lo = e4m3(512 (c s_j - hi)) into [n][ldh] fp16 / [n][ldl] byte planes (s_j =
+// scale[j], a power of two from launch_scale_f32 over the first traces); fp64
+// sum c, sum c^2; sets *nonfinite on NaN/Inf [S:140].  Cross term: kind::f16 on
+// hi and kind::f8f6f4 on lo into one fp32 TMEM accumulator per <= 4096-trace
+// unit, spilled to fp64 times inv_scale[j].  d_scale = [M] scale | [M] inv_scale;
+// a column whose |c s_j| reaches 2^15 in a chunk gets a smaller scale and its
+// planes rewritten before the cross term (d_scratch: 5 M + 16 bytes).
+cudaError_t launch_scale_f32(const float *d_w, int64_t ld, int64_t n, int32_t M, const float *d_offset,
+                             float *d_scale, float *d_inv_scale, cudaStream_t s, int *launches);
 cudaError_t launch_split_f32(const float *d_w, int64_t ld, int64_t n, int32_t M, const float *d_offset,
-                             uint16_t *d_hi, uint16_t *d_lo, int64_t ldh, double *d_sum_w, double *d_sum_w2,
-                             int *d_nonfinite, cudaStream_t s, int *launches);
+                             const float *d_scale, uint16_t *d_hi, uint8_t *d_lo, int64_t ldh, int64_t ldl,
+                             double *d_sum_w, double *d_sum_w2, int *d_nonfinite, uint8_t *d_scratch, cudaStream_t s,
+                             int *launches);
 int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms);
-cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
-                                const uint8_t *d_vtab, double *d_hw, int *d_counter, int32_t M, int64_t N,
-                                int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
-                                uint32_t *d_hist = nullptr, unsigned long long *d_clk = nullptr);
+cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
+                             const uint8_t *d_vtab, double *d_hw, const float *d_inv_scale, int *d_counter, int32_t M,
+                             int64_t N, int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
+                             uint32_t *d_hist = nullptr, unsigned long long *d_clk = nullptr);
 
 // a5 for the single-byte models (HW_LAST / HW_FIRST), class sums (classsum.cu):
 // counting sort of n traces by text byte per byte (perm: 16 x n int32, off: 16 x

@@ -188,6 +188,14 @@ __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t m, uint32_t n)
            | (1u << 10)   // b_format = BF16
            | (1u << 15) | (1u << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
+// kind::f16 with fp16 inputs (format code 0), fp32 accumulate, both operands MN-major
+__host__ __device__ constexpr uint32_t idesc_f16(uint32_t m, uint32_t n)
+{
+    return (1u << 4)      // c_format = F32
+           | (0u << 7)    // a_format = F16
+           | (0u << 10)   // b_format = F16
+           | (1u << 15) | (1u << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
 
 }  // namespace cpa
 
@@ -287,8 +295,8 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar, uint16_t mask)
 }  // namespace cpa
 
 namespace cpa {
-// D[tmem of both CTAs] (+)= A . B, kind::f16 (bf16 inputs, fp32 accumulate), CTA pair
-__device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+// D[tmem of both CTAs] (+)= A . B, kind::f16 (fp16 or bf16 inputs per idesc, fp32 accumulate), CTA pair
+__device__ __forceinline__ void mma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                               uint32_t accumulate)
 {
     asm volatile(
@@ -297,5 +305,24 @@ __device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t adesc, u
         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
+}
+// D[tmem of both CTAs] (+)= A . B, kind::f8f6f4 (e4m3 inputs, fp32 accumulate), CTA pair
+__device__ __forceinline__ void mma_f8_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// kind::f8f6f4 with e4m3 inputs (format code 0), fp32 accumulate, both operands MN-major
+__host__ __device__ constexpr uint32_t idesc_e4m3(uint32_t m, uint32_t n)
+{
+    return (1u << 4)      // c_format = F32
+           | (0u << 7)    // a_format = E4M3
+           | (0u << 10)   // b_format = E4M3
+           | (1u << 15) | (1u << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
 }  // namespace cpa

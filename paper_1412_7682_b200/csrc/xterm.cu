@@ -4,9 +4,12 @@
 // template, two instantiations:
 //   I8  (a5): W int8 (s8/u8), tcgen05.mma kind::i8, exact int32 accumulation in
 //        TMEM, spilled to int64 with red.add (bit-exact for any schedule);
-//   F32 (a6): W float32 pre-split into bf16 hi + lo planes (k_split_f32), two
-//        kind::f16 MMAs per K step (H.hi + H.lo), fp32 TMEM accumulation over
-//        <= 4096 traces per work unit, spilled to fp64 with atomicAdd [P:201-217].
+//   F32 (a6): W float32 pre-split (k_split_f32) into an fp16 hi plane and an e4m3
+//        lo plane (per-sample power-of-two scale s_j): per 64-trace stage 4
+//        kind::f16 MMAs (fp16(H) . hi, K = 16) and 2 kind::f8f6f4 MMAs (H/512 .
+//        512 lo, K = 32; the e4m3 code of H/512 is the byte H) into ONE fp32 TMEM
+//        accumulator over <= 4096 traces per work unit -- 3/4 of the tensor time
+//        of two 16-bit MMAs -- spilled to fp64 x 1/s_j with atomicAdd [P:201-217].
 //
 // The paper computed this serially per (k, b, j) thread [P:121]; here a CTA
 // PAIR (cluster of 2, tcgen05 cta_group::2) owns one key byte b (M = 256
@@ -32,7 +35,7 @@
 // ciphertext producer, w4-7 epilogue (TMEM lanes 32*(w%4)...) + fused moments,
 // w8-15 H generators (8: measured ~1% faster than 16 once NT = 2 halved the generation).
 #include <cuda.h>
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -74,18 +77,19 @@ template <bool F32>
 struct Cfg {
     static constexpr int ESZ = F32 ? 2 : 1;         // bytes per operand element
     static constexpr int KMMA = F32 ? 16 : 32;      // K per MMA instruction
-    static constexpr int NB = F32 ? 2 : 1;          // B operands (hi, lo)
     static constexpr int KB = F32 ? 1 : XT_KB_I8;   // key bytes per unit (A tiles sharing one W tile)
     static constexpr int NT = F32 ? 1 : XT_NT_I8;   // N=256 sample tiles per unit (W tiles sharing one A tile)
     static constexpr int NBUF = F32 ? 2 : 1;        // TMEM accumulator buffers
     static constexpr int NACC = KB * NT;            // N=256 accumulators per unit
     static constexpr int BK = F32 ? 64 : 128;       // traces per pipeline stage
     static constexpr int BOX_X = 128 / ESZ;         // samples per TMA box (128-byte swizzle span)
-    static constexpr int BH_BYTES = BK * 128 * ESZ; // one CTA's half (128 samples) of one N tile, one operand
-    static constexpr int A_BYTES = BK * 128 * ESZ;  // 128 keys x BK traces
+    static constexpr int BH_BYTES = BK * 128 * ESZ; // one CTA's half (128 samples) of one N tile: W (I8) / hi (F32)
+    static constexpr int BL_BYTES = F32 ? BK * 128 : 0;  // F32: the same half of the e4m3 lo plane
+    static constexpr int A_BYTES = BK * 128 * ESZ;  // 128 keys x BK traces: H (I8) / fp16(H) (F32)
+    static constexpr int A8_BYTES = F32 ? BK * 128 : 0;  // F32: the e4m3 tile of H/512 (= the bytes H)
     static constexpr int A_ATOM = BK * 128;         // bytes between 128-byte MN groups (A and B)
-    static constexpr int A_STAGE = KB * A_BYTES;    // generated H tiles of one stage
-    static constexpr int B_STAGE = NT * NB * BH_BYTES;  // TMA-loaded W tiles of one stage
+    static constexpr int A_STAGE = KB * A_BYTES + A8_BYTES;        // generated H tiles of one stage
+    static constexpr int B_STAGE = NT * (BH_BYTES + BL_BYTES);     // TMA-loaded W tiles of one stage
     // separate rings: W (TMA, long latency) runs deeper than H (generated on chip)
     static constexpr int A_STAGES = F32 ? XT_A_STAGES_F32 : XT_A_STAGES_I8;
     static constexpr int B_STAGES = F32 ? XT_B_STAGES_F32 : XT_B_STAGES_I8;
@@ -162,6 +166,8 @@ struct Params {
     int64_t N;
     int64_t kc_len;
     uint32_t idesc;
+    uint32_t idesc8;         // F32: kind::f8f6f4 (e4m3) descriptor of the lo MMAs
+    const float *inv_scale;  // F32: [M] 1 / s_j, applied at the fp64 spill
     // fused a4 (I8 only; null = off): the epilogue warps add sum W, sum W^2 of
     // 1/8 of the rows of every W tile they stage (moments_pass)
     int64_t *sum_w;
@@ -188,14 +194,14 @@ __device__ __forceinline__ void unit_coords(const Params &p, int u, int &b, int 
 
 __device__ __forceinline__ int shiftrows_src(int b) { return (b & 3) + 4 * (((b >> 2) + (b & 3)) & 3); }
 
-// bf16(x) for two bytes x0 (byte sel0) and x1 of w, x in 0..255: the bf16 bit
-// pattern of 128 + x is 0x4300 | x (exact: spacing 1 in [128, 256)); subtract
-// 128 in packed bf16 arithmetic (exact).
-__device__ __forceinline__ uint32_t bf16x2_of_bytes(uint32_t w, uint32_t sel)
+// fp16(x) for two bytes x0 (byte sel0) and x1 of w, x in 0..255: the fp16 bit
+// pattern of 1024 + x is 0x6400 | x (exact: spacing 1 in [1024, 2048)); subtract
+// 1024 in packed fp16 arithmetic (exact).
+__device__ __forceinline__ uint32_t f16x2_of_bytes(uint32_t w, uint32_t sel)
 {
-    const uint32_t biased = __byte_perm(w, 0x43434343u, sel);
-    __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162 *>(&biased);
-    const __nv_bfloat162 off = __floats2bfloat162_rn(128.0f, 128.0f);
+    const uint32_t biased = __byte_perm(w, 0x64646464u, sel);
+    __half2 v = *reinterpret_cast<const __half2 *>(&biased);
+    const __half2 off = __floats2half2_rn(1024.0f, 1024.0f);
     v = __hsub2(v, off);
     return *reinterpret_cast<const uint32_t *>(&v);
 }
@@ -227,7 +233,7 @@ __device__ __forceinline__ void moments_pass(const Params &p, uint32_t bring, ui
                                              uint32_t mdone0)
 {
     using C = Cfg<false>;
-    static_assert(C::KB * C::NT == 2 && C::NB == 1 && C::ESZ == 1 && C::BK == 128, "moments_pass thread map");
+    static_assert(C::KB * C::NT == 2 && C::BL_BYTES == 0 && C::ESZ == 1 && C::BK == 128, "moments_pass thread map");
     constexpr int BS = C::B_STAGES;
     uint32_t s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
     const int n = q % C::NT;
@@ -424,22 +430,24 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     }
                     if (leader) mbar_arrive_expect_tx(bfull_bar(s), 2 * C::B_STAGE);
                     uint32_t bdst = sbase + smem_b<F32>() + s * C::B_STAGE;
+                    const int32_t trow = (XT_EXP & 1) ? (int32_t)(tb & 8191) : (int32_t)tb;
 #pragma unroll
-                    for (int n = 0; n < C::NT; n++)
+                    for (int n = 0; n < C::NT; n++) {
 #pragma unroll
-                        for (int op = 0; op < C::NB; op++)
-#pragma unroll
-                            for (int at = 0; at < C::ESZ; at++) {  // 128-byte MN atoms of this half
-                                tma_load_2d_pair(bdst, op == 0 ? &tmap_b0 : &tmap_b1, x0 + n * BN + at * C::BOX_X,
-                                                 (XT_EXP & 1) ? (int32_t)(tb & 8191) : (int32_t)tb, lbar);
-                                bdst += C::A_ATOM;
-                                // the load latency (L2 miss -> HBM) exceeds the ring's
-                                // slack: pull the box PREFETCH_STAGES ahead into L2
-                                const int64_t tp = tb + PREFETCH_STAGES * C::BK;
-                                if (PREFETCH_STAGES > 0 && tp < t1)
-                                    tma_prefetch_2d(op == 0 ? &tmap_b0 : &tmap_b1, x0 + n * BN + at * C::BOX_X,
-                                                    (int32_t)tp);
-                            }
+                        for (int at = 0; at < C::ESZ; at++) {  // 128-byte MN atoms of this half
+                            tma_load_2d_pair(bdst, &tmap_b0, x0 + n * BN + at * C::BOX_X, trow, lbar);
+                            bdst += C::A_ATOM;
+                            // the load latency (L2 miss -> HBM) exceeds the ring's
+                            // slack: pull the box PREFETCH_STAGES ahead into L2
+                            const int64_t tp = tb + PREFETCH_STAGES * C::BK;
+                            if (PREFETCH_STAGES > 0 && tp < t1)
+                                tma_prefetch_2d(&tmap_b0, x0 + n * BN + at * C::BOX_X, (int32_t)tp);
+                        }
+                        if constexpr (F32) {  // the e4m3 lo half: one 128-byte atom
+                            tma_load_2d_pair(bdst, &tmap_b1, x0 + n * BN, trow, lbar);
+                            bdst += C::BL_BYTES;
+                        }
+                    }
                 }
             }
         }
@@ -496,16 +504,24 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
 #pragma unroll
                         for (int n = 0; n < C::NT; n++)
 #pragma unroll
-                            for (int kb = 0; kb < C::KB; kb++)
-#pragma unroll
-                                for (int op = 0; op < C::NB; op++) {
-                                    const uint64_t a = adk + (uint64_t)((kb * C::A_BYTES) >> 4);
-                                    const uint64_t bd = bdk + (uint64_t)(((n * C::NB + op) * C::BH_BYTES) >> 4);
-                                    const uint32_t d = dbase + (kb * C::NT + n) * BN;
-                                    if (F32) mma_bf16_pair(d, a, bd, p.idesc, op == 0 ? accum : 1u);
-                                    else mma_i8_pair(d, a, bd, p.idesc, accum);
-                                }
+                            for (int kb = 0; kb < C::KB; kb++) {
+                                const uint64_t a = adk + (uint64_t)((kb * C::A_BYTES) >> 4);
+                                const uint64_t bd = bdk + (uint64_t)((n * (C::BH_BYTES + C::BL_BYTES)) >> 4);
+                                const uint32_t d = dbase + (kb * C::NT + n) * BN;
+                                if (F32) mma_f16_pair(d, a, bd, p.idesc, accum);
+                                else mma_i8_pair(d, a, bd, p.idesc, accum);
+                            }
                         accum = 1;
+                    }
+                    if constexpr (F32) {
+                        // lo: (H/512) . (512 lo), e4m3, K = 32 rows of 128 bytes per MMA
+                        static_assert(C::KB == 1 && C::NT == 1, "F32 lo MMAs: one accumulator");
+                        const uint64_t a8 = ad + (uint64_t)(C::A_BYTES >> 4);
+                        const uint64_t b8 = bdd + (uint64_t)(C::BH_BYTES >> 4);
+#pragma unroll
+                        for (int k8 = 0; k8 < C::BK / 32; k8++)
+                            mma_f8_pair(dbase, a8 + (uint64_t)((k8 * 32 * 128) >> 4),
+                                        b8 + (uint64_t)((k8 * 32 * 128) >> 4), p.idesc8, 1u);
                     }
                     mma_commit_pair(aempty_bar(sa), 0x3);  // frees the slots in both CTAs when done
                     mma_commit_pair(bempty_bar(sb), 0x3);
@@ -569,11 +585,12 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 const int j = nt * (C::NT * BN) + cc * 8 + csub;  // accumulator column = sample
                 if (!(XT_EXP & 4) && j < p.M) {
                     const int64_t off = (int64_t)(hrow0 + rsub) * p.M + j;
+                    const double inv = F32 ? (double)p.inv_scale[j] : 1.0;
 #pragma unroll
                     for (int rr = 0; rr < 8; rr++) {
                         const uint32_t bits = tbuf[(4 * rr + rsub) * TB_LD + csub];
                         if (F32) {
-                            atomicAdd((double *)p.hw + off + (int64_t)(4 * rr) * p.M, (double)__uint_as_float(bits));
+                            atomicAdd((double *)p.hw + off + (int64_t)(4 * rr) * p.M, (double)__uint_as_float(bits) * inv);
                         } else if (own != nullptr) {  // peer (or own) accumulator of the row owner
                             atomicAdd_system((unsigned long long *)own + off + (int64_t)(4 * rr) * p.M,
                                              (unsigned long long)(long long)(int32_t)bits);
@@ -679,16 +696,18 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     if (!F32) {
                         *(uint4 *)(abase + row * 128 + ((ql ^ (row & 7)) << 4)) = outv;  // 128B swizzle
                     } else {
-                        // 16 keys -> 32 bytes of bf16: keys 16ql.. live in MN atom ql/4,
+                        // 16 keys -> 32 bytes of fp16: keys 16ql.. live in MN atom ql/4,
                         // 16-byte chunks 2(ql%4) and 2(ql%4)+1 of the row (swizzled)
-                        const uint4 lo4 = make_uint4(bf16x2_of_bytes(outv.x, 0x7170), bf16x2_of_bytes(outv.x, 0x7372),
-                                                     bf16x2_of_bytes(outv.y, 0x7170), bf16x2_of_bytes(outv.y, 0x7372));
-                        const uint4 hi4 = make_uint4(bf16x2_of_bytes(outv.z, 0x7170), bf16x2_of_bytes(outv.z, 0x7372),
-                                                     bf16x2_of_bytes(outv.w, 0x7170), bf16x2_of_bytes(outv.w, 0x7372));
+                        const uint4 lo4 = make_uint4(f16x2_of_bytes(outv.x, 0x7170), f16x2_of_bytes(outv.x, 0x7372),
+                                                     f16x2_of_bytes(outv.y, 0x7170), f16x2_of_bytes(outv.y, 0x7372));
+                        const uint4 hi4 = make_uint4(f16x2_of_bytes(outv.z, 0x7170), f16x2_of_bytes(outv.z, 0x7372),
+                                                     f16x2_of_bytes(outv.w, 0x7170), f16x2_of_bytes(outv.w, 0x7372));
                         uint8_t *rowp = abase + (ql >> 2) * C::A_ATOM + row * 128;
                         const int c0i = 2 * (ql & 3);
                         *(uint4 *)(rowp + (((c0i) ^ (row & 7)) << 4)) = lo4;
                         *(uint4 *)(rowp + (((c0i + 1) ^ (row & 7)) << 4)) = hi4;
+                        // and the e4m3 tile of H/512: the same bytes as the I8 tile
+                        *(uint4 *)(abase + C::A_BYTES + row * 128 + ((ql ^ (row & 7)) << 4)) = outv;
                     }
                 }
                 fence_proxy_async_smem();
@@ -720,7 +739,7 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *
                    void *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, uint32_t idesc, int num_sms,
                    cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr, int64_t *d_sum_w2 = nullptr,
                    bool w_signed = true, uint32_t *d_hist = nullptr, int64_t *const *owners = nullptr,
-                   unsigned long long *d_clk = nullptr)
+                   unsigned long long *d_clk = nullptr, uint32_t idesc8 = 0, const float *d_inv_scale = nullptr)
 {
     using Cf = Cfg<F32>;
     Params p;
@@ -736,6 +755,8 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *
     p.kc_count = (int32_t)((N + kc_len - 1) / kc_len);
     p.units = p.groups * p.n_tiles * p.kc_count;
     p.idesc = idesc;
+    p.idesc8 = idesc8;
+    p.inv_scale = d_inv_scale;
     p.sum_w = d_sum_w;
     p.sum_w2 = d_sum_w2;
     p.w_signed = w_signed ? 1 : 0;
@@ -817,13 +838,14 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, c
                          d_hist, owners, d_clk);
 }
 
-cudaError_t launch_xterm_bf16x2(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
-                                const uint8_t *d_vtab, double *d_hw, int *d_counter, int32_t M, int64_t N,
-                                int64_t kc_len, int num_sms, cudaStream_t stream, int *launches, uint32_t *d_hist,
-                                unsigned long long *d_clk)
+cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
+                             const uint8_t *d_vtab, double *d_hw, const float *d_inv_scale, int *d_counter, int32_t M,
+                             int64_t N, int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
+                             uint32_t *d_hist, unsigned long long *d_clk)
 {
-    return launch<true>(tmap_hi, tmap_lo, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len, idesc_bf16(2 * BMC, BN),
-                        num_sms, stream, launches, nullptr, nullptr, true, d_hist, nullptr, d_clk);
+    return launch<true>(tmap_hi, tmap_lo, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len, idesc_f16(2 * BMC, BN),
+                        num_sms, stream, launches, nullptr, nullptr, true, d_hist, nullptr, d_clk,
+                        idesc_e4m3(2 * BMC, BN), d_inv_scale);
 }
 
 }  // namespace cpa

@@ -1,5 +1,5 @@
-"""GPU parity of the float-trace variant (a6, [P:201-217]): bf16 hi/lo tensor-core
-path vs the fp64 oracle.  Bar (north_star): |rho_gpu - rho_oracle| <= 1e-4 on
+"""GPU parity of the float-trace variant (a6, [P:201-217]): fp16 hi + e4m3 lo
+tensor-core path vs the fp64 oracle.  Bar (north_star): |rho_gpu - rho_oracle| <= 1e-4 on
 every cell [S:461], identical recovered key."""
 import numpy as np
 import pytest
@@ -88,3 +88,46 @@ def test_c3_fullsize_sampled(P):
     assert out["master_key"] == w.key
     assert out["peak_sample"] == w.leak_positions()
     eng.close()
+
+
+# The split is fp16 hi + e4m3 lo (per-sample power-of-two scale): per element
+# |error| <= 2^-15 |c s_j| + 2^-19 in scaled units, so rho sits far inside the
+# north-star bar (measured <= 2e-6 here).  A swapped e4m3 byte pair or a lost lo
+# term (fp16 alone ~4e-5, bf16 alone ~3e-4 on these inputs) fails this bar.
+TIGHT = 1e-5
+
+
+def _max_err(P, texts, W):
+    out, n = gpu_rho(P, texts, W)
+    shw, sw, sw2 = O.sums_f32(O.HD_LAST, texts, W)
+    sh, sh2 = O.model_sums(O.HD_LAST, texts)
+    ref = O.rho_eq1_f64_grid(W.shape[0], shw, sh, sh2, sw, sw2)
+    return float(np.max(np.abs(out["rho"].cpu().numpy() - ref))), out
+
+
+@pytest.mark.parametrize("scale", [1.0, 2.0 ** 40, 2.0 ** -40])
+def test_float_split_precision_any_magnitude(P, scale):
+    w = S.CONFIGS["C3"].replace(n=3000, m=160, a=0.02)
+    texts, W = S.dataset(w)
+    Ws = (W.astype(np.float64) * scale).astype(np.float32)  # exact: power of two
+    err, out = _max_err(P, texts, Ws)
+    print(f"scale {scale:g}: max |drho| = {err:.3g}")
+    assert err <= TIGHT
+
+
+@pytest.mark.parametrize("amp", [50.0, 1e4])
+def test_float_split_outliers(P, amp):
+    """Values far above the spread the per-sample scales were chosen from (the
+    first 64 traces, spread ~0.1): amp 50 saturates the e4m3 lo term (the element
+    keeps fp16 precision); amp 1e4 would overflow fp16, so the column's scale is
+    lowered and its planes rewritten (range repair).  Both within the bar."""
+    w = S.CONFIGS["C3"].replace(n=3000, m=96, a=0.02)
+    texts, W = S.dataset(w)
+    W = W.copy()
+    rng = np.random.default_rng(7)
+    rows = rng.integers(64, w.n, 40)
+    cols = rng.integers(0, w.m, 40)
+    W[rows, cols] += np.float32(amp) * rng.standard_normal(40).astype(np.float32)
+    err, _ = _max_err(P, texts, W)
+    print(f"outliers x{amp:g}: max |drho| = {err:.3g}")
+    assert err <= TOL
