@@ -72,6 +72,9 @@ def parse():
                          "(C4-HW); default: the tensor-core contraction (faster on B200, DESIGN.md)")
     ap.add_argument("--fuse-hist", choices=["0", "1"], default="0",
                     help="CPA_OPT_FUSE_HIST: a3's byte-pair histogram counted inside the cross-term kernel")
+    ap.add_argument("--xt-tiles", type=int, default=0, choices=[0, 1, 2],
+                    help="CPA_OPT_XT_TILES: int8 cross-term variant (0 = the library's cost model, 1 = two "
+                         "sample tiles per unit, 2 = one tile with the spill overlapped)")
     ap.add_argument("--chunk", type=int, default=0,
                     help="stream the traces in chunks of this many, finalizing after every round "
                          "(key-rank curve); default for C5: 65536")
@@ -272,6 +275,8 @@ def main():
     if class_sums:
         eng.set_class_sums(True)
     eng.set_fuse_hist(args.fuse_hist == "1")
+    if not is_f32:
+        eng.set_xt_tiles(args.xt_tiles)
     eng.set_col0(j0)
     ovl_mode = 0 if args.no_overlap else (args.overlap_mode if args.overlap_mode is not None else OVERLAP_DEFAULT)
     eng.set_overlap(ovl_mode)
@@ -415,7 +420,8 @@ def main():
     tot = sum(step_phase_ms.values()) or 1.0
     # HBM-bound kernels: achieved GB/s on their algorithmic bytes
     mo_launch_ms = phase_ms["moments"] / max(1, phase_n["moments"])
-    fused = ovl_mode == 3 and not is_f32 and not class_sums
+    # (the NT = 1 cross-term variant, CPA_OPT_XT_TILES, runs a4 as its own pass)
+    fused = ovl_mode == 3 and not is_f32 and not class_sums and not phase_n["moments"]
     mo_solo = solo or mo_launch_ms
     mo_bytes = n_local * m_local * (7 if is_f32 else 1)  # f32: k_split_f32 reads 4 B, writes 2 B (fp16) + 1 B (e4m3)
     hbm = {"moments_GBps": mo_bytes / (mo_solo * 1e-3) / 1e9 if mo_solo else None,

@@ -263,9 +263,17 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *                   sum H^2 are contracted from [P:75] as it generates H (no
  *                   separate histogram pass); 0 (default) = separate pass
  *                   (the fused counting cost the cross term what the pass
- *                   cost).  Same exact sums either way.           */
+ *                   cost).  Same exact sums either way.
+ *   CPA_OPT_XT_TILES: int8 cross-term variant: 0 (default) = 1; 1 = two
+ *                   256-sample tiles per work unit
+ *                   (one generated H tile feeds both; a4 fused per OVERLAP;
+ *                   the unit's spill waits for its MMAs); 2 = one tile per
+ *                   unit with double-buffered TMEM accumulators (the spill
+ *                   overlaps the next unit's MMAs: short units, i.e. wide or
+ *                   few traces; a4 then runs as a separate pass; measured
+ *                   slower on B200).  Same exact sums either way.  */
 enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2, CPA_OPT_OVERLAP = 3, CPA_OPT_STAGE_BYTES = 4,
-       CPA_OPT_COL0 = 5, CPA_OPT_CLASS_SUMS = 6, CPA_OPT_FUSE_HIST = 7 };
+       CPA_OPT_COL0 = 5, CPA_OPT_CLASS_SUMS = 6, CPA_OPT_FUSE_HIST = 7, CPA_OPT_XT_TILES = 8 };
 CPA_API cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value);
 
 /* Per-phase device time (ms) and launch count since the last call, from the

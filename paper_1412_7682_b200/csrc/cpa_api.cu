@@ -115,6 +115,7 @@ struct cpa_ctx {
     // (classsum.cu); scratch allocated on first use
     int class_sums = 0;
     int fuse_hist = 0;
+    int xt_tiles = 0;  // CPA_OPT_XT_TILES: 0 model, 1 NT = 2, 2 NT = 1 overlapped
     // cpa_set_row_owners: fused multi-GPU combine (key byte b's sum_hw rows go to owners[b])
     int64_t *owners[16] = {};
     bool owners_set = false;
@@ -315,6 +316,11 @@ cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
         if (value < 0 || value % 128 || value > (1 << 20))
             return fail(CPA_E_INVALID_ARG, "KCHUNK=%lld must be a multiple of 128 in [0, 2^20]", (long long)value);
         ctx->kchunk = value;
+        return CPA_OK;
+    }
+    if (option == CPA_OPT_XT_TILES) {
+        if (value < 0 || value > 2) return fail(CPA_E_INVALID_ARG, "XT_TILES=%lld outside [0, 2]", (long long)value);
+        ctx->xt_tiles = (int)value;
         return CPA_OK;
     }
     if (option == CPA_OPT_FUSE_HIST) {
@@ -525,8 +531,11 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     //              per SM, so both kernels are co-resident from the start.
     //   overlap 3: no separate pass: the cross-term kernel's epilogue warps sum
     //              the W tiles it loads anyway (no extra HBM traffic).
-    const bool fused = c->overlap == 3;
-    const int mode = (c->side && !fused) ? c->overlap : 0;
+    // cross-term variant (CPA_OPT_XT_TILES): the NT = 1 overlapped one cannot
+    // fuse a4, which then runs serialised before it (mode 0)
+    const cpa::XtermI8Plan plan = cpa::xterm_i8_plan(M, n, c->num_sms, c->owners_set, c->xt_tiles);
+    const bool fused = c->overlap == 3 && !plan.overlapped;
+    const int mode = (c->side && !fused && c->overlap != 3) ? c->overlap : 0;
     cudaStream_t mst = mode == 2 ? c->side_hi : (mode == 1 ? c->side : c->stream);
     if (mode) {
         CUDA_TRY(cudaEventRecord(c->ev_fork, c->stream), "fork");
@@ -548,13 +557,13 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    const int64_t kc = c->kchunk ? c->kchunk : cpa::xterm_i8_auto_kchunk(M, n, c->num_sms, c->owners_set);
+    const int64_t kc = c->kchunk ? c->kchunk : plan.kc_len;
     CUDA_TRY(c->timed(2, [&] {
                  return cpa::launch_xterm_i8(tmap, d_tx, c->d_vtab, acc, c->d_counter, M, n, kc, sgn, c->num_sms,
                                              c->stream, &launches, fused ? acc + cpa_accum_offset(M, 1) : nullptr,
                                              fused ? acc + cpa_accum_offset(M, 2) : nullptr,
                                              fhist ? c->d_hist : nullptr, c->owners_set ? c->owners : nullptr,
-                                             c->d_clk);
+                                             c->d_clk, plan.overlapped);
              }),
              "xterm_i8");
     if (!fused && mode == 1) CUDA_TRY(moments(), "moments");

@@ -35,11 +35,22 @@ cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M,
 // the kernel also adds a4's sum W, sum W^2 (fused moments).
 int xterm_smem_bytes();
 int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms, bool remote_epilogue = false);
+// Variant choice: NT = 2 sample tiles per unit (A tile reused twice, a4 fused,
+// epilogue serialised with the unit's MMAs) or NT = 1 with double-buffered TMEM
+// accumulators (the epilogue overlaps the next unit; a4 as a separate pass) --
+// the latter was meant for short units (wide / few traces) but measured slower
+// (xterm.cu), so force: 0 or 1 = NT = 2, 2 = NT = 1 overlapped.
+struct XtermI8Plan {
+    bool overlapped = false;
+    int64_t kc_len = 0;
+};
+XtermI8Plan xterm_i8_plan(int32_t M, int64_t N, int num_sms, bool remote_epilogue, int force);
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
                             int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
                             int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr,
                             int64_t *d_sum_w2 = nullptr, uint32_t *d_hist = nullptr,
-                            int64_t *const *owners = nullptr, unsigned long long *d_clk = nullptr);
+                            int64_t *const *owners = nullptr, unsigned long long *d_clk = nullptr,
+                            bool overlapped = false);
 
 // a6: float traces.  Split pre-pass: c = w - offset[j], hi = fp16(c s_j),
 // lo = e4m3(512 (c s_j - hi)) into [n][ldh] fp16 / [n][ldl] byte planes (s_j =

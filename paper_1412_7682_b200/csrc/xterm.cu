@@ -73,13 +73,19 @@
 namespace cpa {
 namespace {
 
-template <bool F32>
+// Kernel variants: V_I8 (NT = 2 sample tiles per unit, one accumulator set, fused
+// a4), V_F32 (a6), V_I8O (int8 with NT = 1 and double-buffered accumulators: the
+// epilogue overlaps the next unit's MMAs; for short units, where the spill of a
+// unit would otherwise stall the tensor pipe -- wide traces, few traces).
+constexpr int V_I8 = 0, V_F32 = 1, V_I8O = 2;
+template <int V>
 struct Cfg {
+    static constexpr bool F32 = V == V_F32;
     static constexpr int ESZ = F32 ? 2 : 1;         // bytes per operand element
     static constexpr int KMMA = F32 ? 16 : 32;      // K per MMA instruction
     static constexpr int KB = F32 ? 1 : XT_KB_I8;   // key bytes per unit (A tiles sharing one W tile)
-    static constexpr int NT = F32 ? 1 : XT_NT_I8;   // N=256 sample tiles per unit (W tiles sharing one A tile)
-    static constexpr int NBUF = F32 ? 2 : 1;        // TMEM accumulator buffers
+    static constexpr int NT = V == V_I8 ? XT_NT_I8 : 1;  // N=256 sample tiles per unit (W tiles sharing one A tile)
+    static constexpr int NBUF = V == V_I8 ? 1 : 2;      // TMEM accumulator buffers
     static constexpr int NACC = KB * NT;            // N=256 accumulators per unit
     static constexpr int BK = F32 ? 64 : 128;       // traces per pipeline stage
     static constexpr int BOX_X = 128 / ESZ;         // samples per TMA box (128-byte swizzle span)
@@ -135,15 +141,17 @@ constexpr int SMEM_TOTAL = SMEM_SCHED + SCHED_Q * 4 + 16;
 constexpr int SMEM_ALLOC = SMEM_TOTAL;
 constexpr int THREADS = 32 * (8 + GEN_WARPS);
 constexpr uint32_t TMEM_COLS = 512;
-template <bool F32>
-__host__ __device__ constexpr int smem_b() { return SMEM_A + Cfg<F32>::A_STAGES * Cfg<F32>::A_STAGE; }
-static_assert(Cfg<false>::A_STAGES * Cfg<false>::A_STAGE + Cfg<false>::B_STAGES * Cfg<false>::B_STAGE <= RINGS_BYTES, "");
-static_assert(Cfg<true>::A_STAGES * Cfg<true>::A_STAGE + Cfg<true>::B_STAGES * Cfg<true>::B_STAGE <= RINGS_BYTES, "");
-static_assert(Cfg<false>::A_STAGES <= MAX_RING && Cfg<false>::B_STAGES <= MAX_RING, "");
-static_assert(Cfg<true>::A_STAGES <= MAX_RING && Cfg<true>::B_STAGES <= MAX_RING, "");
+template <int V>
+__host__ __device__ constexpr int smem_b() { return SMEM_A + Cfg<V>::A_STAGES * Cfg<V>::A_STAGE; }
+template <int V>
+constexpr bool cfg_ok()
+{
+    using C = Cfg<V>;
+    return C::A_STAGES * C::A_STAGE + C::B_STAGES * C::B_STAGE <= RINGS_BYTES && C::A_STAGES <= MAX_RING &&
+           C::B_STAGES <= MAX_RING && C::NACC * C::NBUF * BN == (int)TMEM_COLS;
+}
+static_assert(cfg_ok<V_I8>() && cfg_ok<V_F32>() && cfg_ok<V_I8O>(), "rings, barriers, TMEM columns");
 static_assert(SMEM_ALLOC <= 232448, "shared memory");
-static_assert(Cfg<false>::NACC * Cfg<false>::NBUF * BN == TMEM_COLS, "");
-static_assert(Cfg<true>::NACC * Cfg<true>::NBUF * BN == TMEM_COLS, "");
 
 struct Params {
     const uint8_t *texts;    // N x 16
@@ -179,11 +187,11 @@ struct Params {
     uint32_t *hist;
 };
 
-template <bool F32>
+template <int V>
 __device__ __forceinline__ void unit_coords(const Params &p, int u, int &b, int &n_tile, int64_t &t0, int64_t &t1)
 {
     // b = first key byte of the unit's group (bytes b .. b+KB-1)
-    b = (u % p.groups) * Cfg<F32>::KB;
+    b = (u % p.groups) * Cfg<V>::KB;
     const int r = u / p.groups;
     const int kc = r % p.kc_count;
     n_tile = r / p.kc_count;
@@ -232,7 +240,7 @@ __device__ __forceinline__ void moments_pass(const Params &p, uint32_t bring, ui
                                              int g, int q, int lane, int j0, uint32_t bfull0, uint32_t mready0,
                                              uint32_t mdone0)
 {
-    using C = Cfg<false>;
+    using C = Cfg<V_I8>;
     static_assert(C::KB * C::NT == 2 && C::BL_BYTES == 0 && C::ESZ == 1 && C::BK == 128, "moments_pass thread map");
     constexpr int BS = C::B_STAGES;
     uint32_t s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
@@ -254,7 +262,7 @@ __device__ __forceinline__ void moments_pass(const Params &p, uint32_t bring, ui
         } else {
             mbar_wait(mready0 + 8 * s, ph);  // relayed by the leader
         }
-        const uint32_t tile = bring + s * Cfg<false>::B_STAGE + off0;
+        const uint32_t tile = bring + s * C::B_STAGE + off0;
         uint32_t x[4];
 #pragma unroll
         for (int r = 0; r < 4; r++) {
@@ -284,11 +292,12 @@ __device__ __forceinline__ void moments_pass(const Params &p, uint32_t bring, ui
     }
 }
 
-template <bool F32>
+template <int V>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUtensorMap tmap_b1, const Params p)
 {
-    using C = Cfg<F32>;
+    using C = Cfg<V>;
+    constexpr bool F32 = C::F32;
     extern __shared__ __align__(1024) uint8_t smem[];  // keeps shared provenance (LDS/STS)
     const uint32_t sbase = smem_u32(smem);
     if (threadIdx.x == 0 && (sbase & 1023)) __trap();  // 128B-swizzle atoms need 1 KB alignment
@@ -408,7 +417,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 if (u < 0) break;
                 int b, nt;
                 int64_t t0, t1;
-                unit_coords<F32>(p, u, b, nt, t0, t1);
+                unit_coords<V>(p, u, b, nt, t0, t1);
                 const int x0 = nt * (C::NT * BN) + (int)rank * (BN / 2);  // this CTA's half of N tile 0
                 const bool mom = !F32 && p.sum_w != nullptr;
                 for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
@@ -429,7 +438,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                         continue;
                     }
                     if (leader) mbar_arrive_expect_tx(bfull_bar(s), 2 * C::B_STAGE);
-                    uint32_t bdst = sbase + smem_b<F32>() + s * C::B_STAGE;
+                    uint32_t bdst = sbase + smem_b<V>() + s * C::B_STAGE;
                     const int32_t trow = (XT_EXP & 1) ? (int32_t)(tb & 8191) : (int32_t)tb;
 #pragma unroll
                     for (int n = 0; n < C::NT; n++) {
@@ -460,7 +469,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 if (u < 0) break;
                 int b, nt;
                 int64_t t0, t1;
-                unit_coords<F32>(p, u, b, nt, t0, t1);
+                unit_coords<V>(p, u, b, nt, t0, t1);
                 for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
                     const int x = it % TX_STAGES;
                     mbar_wait(txempty_bar(x), ((it / TX_STAGES) & 1) ^ 1);
@@ -477,14 +486,14 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             // 16-byte units to their start-address field; the full barrier is waited
             // on at CTA scope (tools/pair_bench: 65% -> 100% of the pair MMA rate).
             const uint64_t adesc0 = smem_desc_sw128(sbase + SMEM_A, C::A_ATOM, 1024);
-            const uint64_t bdesc0 = smem_desc_sw128(sbase + smem_b<F32>(), C::A_ATOM, 1024);
+            const uint64_t bdesc0 = smem_desc_sw128(sbase + smem_b<V>(), C::A_ATOM, 1024);
             uint32_t sa = 0, pa = 0, sb = 0, pb = 0;
             for (uint32_t t = 0;; t++) {
                 const int u = next_unit(t, true);
                 if (u < 0) break;
                 int b, nt;
                 int64_t t0, t1;
-                unit_coords<F32>(p, u, b, nt, t0, t1);
+                unit_coords<V>(p, u, b, nt, t0, t1);
                 const uint32_t acc = t % C::NBUF;
                 mbar_wait_cluster(tempty_bar(acc), ((t / C::NBUF) & 1) ^ 1);  // both epilogues drained it
                 tc_fence_after();
@@ -548,14 +557,14 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             if (u < 0) break;
             int b, nt;
             int64_t t0, t1;
-            unit_coords<F32>(p, u, b, nt, t0, t1);
+            unit_coords<V>(p, u, b, nt, t0, t1);
             const uint32_t nst = (uint32_t)((t1 - t0 + C::BK - 1) / C::BK);
-            if constexpr (!F32) {
+            if constexpr (V == V_I8) {
                 if (p.sum_w != nullptr) {
                     const int j0 = nt * (C::NT * BN) + (int)rank * (BN / 2);  // this CTA's half of N tile 0
-                    if (p.w_signed) moments_pass<true>(p, sbase + smem_b<F32>(), eit, nst, leader, b / C::KB, q, lane,
+                    if (p.w_signed) moments_pass<true>(p, sbase + smem_b<V>(), eit, nst, leader, b / C::KB, q, lane,
                                                        j0, bfull_bar(0), mready_bar(0), mdone_bar(0));
-                    else moments_pass<false>(p, sbase + smem_b<F32>(), eit, nst, leader, b / C::KB, q, lane, j0,
+                    else moments_pass<false>(p, sbase + smem_b<V>(), eit, nst, leader, b / C::KB, q, lane, j0,
                                              bfull_bar(0), mready_bar(0), mdone_bar(0));
                 }
             }
@@ -636,7 +645,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             if (u < 0) break;
             int b, nt;
             int64_t t0, t1;
-            unit_coords<F32>(p, u, b, nt, t0, t1);
+            unit_coords<V>(p, u, b, nt, t0, t1);
             // this lane's descriptor slot: row ROWS*g + lane%ROWS, key byte b + lane/ROWS
             const int drow = ROWS * g + lane % ROWS, dkb = lane / ROWS;
             const int dsrc = shiftrows_src(b + dkb);
@@ -734,14 +743,14 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
     }
 }
 
-template <bool F32>
+template <int V>
 cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *d_texts, const uint8_t *d_vtab,
                    void *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, uint32_t idesc, int num_sms,
                    cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr, int64_t *d_sum_w2 = nullptr,
                    bool w_signed = true, uint32_t *d_hist = nullptr, int64_t *const *owners = nullptr,
                    unsigned long long *d_clk = nullptr, uint32_t idesc8 = 0, const float *d_inv_scale = nullptr)
 {
-    using Cf = Cfg<F32>;
+    using Cf = Cfg<V>;
     Params p;
     p.texts = d_texts;
     p.vtab = d_vtab;
@@ -765,14 +774,14 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *
     p.clk = d_clk;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_xterm<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
+        cudaError_t e = cudaFuncSetAttribute(k_xterm<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(int), stream);
     if (e != cudaSuccess) return e;
     const int pairs = (p.units < num_sms / 2 ? p.units : num_sms / 2);
-    k_xterm<F32><<<2 * pairs, THREADS, SMEM_ALLOC, stream>>>(m0, m1, p);
+    k_xterm<V><<<2 * pairs, THREADS, SMEM_ALLOC, stream>>>(m0, m1, p);
     if (launches) (*launches)++;
     return cudaGetLastError();
 }
@@ -818,24 +827,44 @@ int xterm_smem_bytes() { return SMEM_ALLOC; }
 
 int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms, bool remote_epilogue)
 {
-    return auto_kchunk(M, N, num_sms, Cfg<false>::KB, Cfg<false>::NT, Cfg<false>::BK, 1 << 20, false,
+    return auto_kchunk(M, N, num_sms, Cfg<V_I8>::KB, Cfg<V_I8>::NT, Cfg<V_I8>::BK, 1 << 20, false,
                        remote_epilogue ? 75000.0 : 25000.0);
 }
 
 int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms)
 {
-    return auto_kchunk(M, N, num_sms, Cfg<true>::KB, Cfg<true>::NT, Cfg<true>::BK, 4096, true);
+    return auto_kchunk(M, N, num_sms, Cfg<V_F32>::KB, Cfg<V_F32>::NT, Cfg<V_F32>::BK, 4096, true);
+}
+
+XtermI8Plan xterm_i8_plan(int32_t M, int64_t N, int num_sms, bool remote_epilogue, int force)
+{
+    // NT = 1 with the overlapped spill measured SLOWER everywhere it was meant to
+    // help (W48 cross term 1.75 vs 1.18 ms, C2 0.148 vs 0.110, C4 27.8 vs 18.3 ms:
+    // generating an A tile per 4 MMAs instead of 8 starves the tensor pipe), so
+    // the default is NT = 2; variant 2 stays an exact, tested option.
+    XtermI8Plan pl;
+    pl.overlapped = force == 2;
+    pl.kc_len = pl.overlapped
+                    ? auto_kchunk(M, N, num_sms, Cfg<V_I8O>::KB, Cfg<V_I8O>::NT, Cfg<V_I8O>::BK, 1 << 20, true)
+                    : xterm_i8_auto_kchunk(M, N, num_sms, remote_epilogue);
+    return pl;
 }
 
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
                             int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
                             int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w, int64_t *d_sum_w2,
-                            uint32_t *d_hist, int64_t *const *owners, unsigned long long *d_clk)
+                            uint32_t *d_hist, int64_t *const *owners, unsigned long long *d_clk, bool overlapped)
 {
-    static_assert(Cfg<false>::KB == 1, "owner routing assumes one key byte per unit");
-    return launch<false>(tmap_w, tmap_w, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
-                         idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, d_sum_w, d_sum_w2, w_signed,
-                         d_hist, owners, d_clk);
+    static_assert(Cfg<V_I8>::KB == 1 && Cfg<V_I8O>::KB == 1, "owner routing assumes one key byte per unit");
+    if (overlapped) {
+        if (d_sum_w != nullptr) return cudaErrorInvalidValue;  // a4 is fused into the NT = 2 variant only
+        return launch<V_I8O>(tmap_w, tmap_w, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
+                             idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, nullptr, nullptr, w_signed,
+                             d_hist, owners, d_clk);
+    }
+    return launch<V_I8>(tmap_w, tmap_w, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
+                        idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, d_sum_w, d_sum_w2, w_signed,
+                        d_hist, owners, d_clk);
 }
 
 cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
@@ -843,7 +872,7 @@ cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap
                              int64_t N, int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
                              uint32_t *d_hist, unsigned long long *d_clk)
 {
-    return launch<true>(tmap_hi, tmap_lo, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len, idesc_f16(2 * BMC, BN),
+    return launch<V_F32>(tmap_hi, tmap_lo, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len, idesc_f16(2 * BMC, BN),
                         num_sms, stream, launches, nullptr, nullptr, true, d_hist, nullptr, d_clk,
                         idesc_e4m3(2 * BMC, BN), d_inv_scale);
 }

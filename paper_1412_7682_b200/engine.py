@@ -73,6 +73,10 @@ class Engine:
         """CPA_OPT_FUSE_HIST: a3's byte-pair histogram counted inside the cross-term kernel (default off)."""
         B.cpa_set_option(self.ctx, B.CPA_OPT_FUSE_HIST, int(bool(on)))
 
+    def set_xt_tiles(self, v: int):
+        """CPA_OPT_XT_TILES: int8 cross-term variant (0 model, 1 two sample tiles per unit, 2 one tile, overlapped spill)."""
+        B.cpa_set_option(self.ctx, B.CPA_OPT_XT_TILES, v)
+
     def set_row_owners(self, owners):
         """cpa_set_row_owners: 16 device addresses (0 = own accumulator) or None."""
         B.cpa_set_row_owners(self.ctx, owners)

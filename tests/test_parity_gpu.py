@@ -23,9 +23,12 @@ def P():
 MODEL = {O.HD_LAST: 0, O.HW_LAST: 1, O.HW_FIRST: 2}
 
 
-def run_gpu(P, texts, W, model=0, kchunk=0, chunks=None, want_rho=True, overlap=True, mode=None, fuse_hist=None):
+def run_gpu(P, texts, W, model=0, kchunk=0, chunks=None, want_rho=True, overlap=True, mode=None, fuse_hist=None,
+            xt=None):
     dtype = {np.int8: P.CPA_S8, np.uint8: P.CPA_U8}[W.dtype.type]
     eng = P.Engine(W.shape[1], dtype, model, 0)
+    if xt is not None:
+        eng.set_xt_tiles(xt)
     if kchunk:
         eng.set_kchunk(kchunk)
     if not overlap:
@@ -94,26 +97,28 @@ def test_c1_noiseless_rho_one(P):
     assert out["master_key"] == w.key
 
 
+@pytest.mark.parametrize("xt", [1, 2])
 @pytest.mark.parametrize("model", [O.HD_LAST, O.HW_LAST, O.HW_FIRST])
 @pytest.mark.parametrize("dtype", [np.int8, np.uint8])
-def test_models_dtypes_ragged(P, model, dtype):
+def test_models_dtypes_ragged(P, model, dtype, xt):
     rng = np.random.default_rng(100 + model)
     n, m = 333, 300                     # ragged: 333 = 5*64+13 traces, 300 = 256+44 samples
     texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
     lo, hi = (-128, 128) if dtype == np.int8 else (0, 256)
     W = rng.integers(lo, hi, (n, m)).astype(dtype)
     ref = O.attack_i8(model, texts, W)
-    sums, out = run_gpu(P, texts, W, model=MODEL[model])
+    sums, out = run_gpu(P, texts, W, model=MODEL[model], xt=xt)
     assert_parity(sums, out, ref)
 
 
+@pytest.mark.parametrize("xt", [1, 2])
 @pytest.mark.parametrize("n,m", [(2, 1), (3, 17), (64, 256), (65, 257), (130, 513), (1000, 16)])
-def test_edge_shapes(P, n, m):
+def test_edge_shapes(P, n, m, xt):
     rng = np.random.default_rng(n * 1000 + m)
     texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
     W = rng.integers(-128, 128, (n, m)).astype(np.int8)
     ref = O.attack_i8(O.HD_LAST, texts, W)
-    sums, out = run_gpu(P, texts, W)
+    sums, out = run_gpu(P, texts, W, xt=xt)
     assert_parity(sums, out, ref)
 
 
@@ -140,7 +145,9 @@ def test_split_k_chunks_and_permutation_bit_identical(P):
     W = rng.integers(-128, 128, (n, m)).astype(np.int8)
     base, out0 = run_gpu(P, texts, W)
     for kw in (dict(kchunk=128), dict(kchunk=1024), dict(chunks=[0, 1, 700, 4097, 9000]),
-               dict(overlap=False), dict(overlap=False, chunks=[0, 5000, 9000])):
+               dict(overlap=False), dict(overlap=False, chunks=[0, 5000, 9000]),
+               dict(xt=1), dict(xt=2), dict(xt=1, kchunk=256), dict(xt=2, kchunk=256),
+               dict(xt=2, chunks=[0, 1, 700, 4097, 9000])):
         s, o = run_gpu(P, texts, W, **kw)
         for k in base:
             assert np.array_equal(base[k], s[k]), (kw, k)
@@ -287,8 +294,9 @@ def test_moment_modes_exact(P, dt):
     sw, sw2 = O.trace_sums_i8(W)
     ref_hw = O.cross_sums_i8(O.HD_LAST, texts, W, np.array([0, 7, 11, 255, 256, 299], np.int32))
     for mode in (0, 1, 2, 3):
-        for kw in (dict(), dict(kchunk=128), dict(chunks=[0, 3, 400, n])):
-            s, _ = run_gpu(P, texts, W, mode=mode, want_rho=False, **kw)
+        for kw in (dict(), dict(kchunk=128), dict(chunks=[0, 3, 400, n]), dict(xt=2), dict(xt=2, kchunk=128)):
+            # xt = 1 forces the NT = 2 kernel, the one that fuses a4 (mode 3)
+            s, _ = run_gpu(P, texts, W, mode=mode, want_rho=False, **dict(dict(xt=1), **kw))
             assert np.array_equal(s["sum_w"], sw), (mode, kw)
             assert np.array_equal(s["sum_w2"], sw2), (mode, kw)
             assert np.array_equal(s["sum_hw"][:, [0, 7, 11, 255, 256, 299]], ref_hw), (mode, kw)
@@ -303,7 +311,7 @@ def test_fused_moments_32bit_bound(P, dt, v):
     n, m = (1 << 20) + 5, 16
     texts = np.random.default_rng(3).integers(0, 256, (n, 16), dtype=np.uint8)
     W = np.full((n, m), v, dt)
-    s, _ = run_gpu(P, texts, W, kchunk=1 << 20, mode=3, want_rho=False)
+    s, _ = run_gpu(P, texts, W, kchunk=1 << 20, mode=3, want_rho=False, xt=1)
     assert np.all(s["sum_w"] == n * v) and np.all(s["sum_w2"] == n * v * v)
     hw = s["sum_hw"].reshape(16, 256, m).sum(axis=1)
     assert np.all(hw == 1024 * n * v)

@@ -15,4 +15,11 @@ timeout -s KILL 600 python bench.py --config C4-HW --class-sums 1 --no-e2e --no-
 timeout -s KILL 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log | cut -c1-300
 bash profiles/run_ncu.sh $TAG > /dev/null 2>&1
 timeout -s KILL 300 ncu --set full --import-source on --clock-control none -k regex:k_cs_sum -s 1 -c 1 -o gpurun_out/k_cs_sum_$TAG -f python bench.py --config C4-HW --class-sums 1 --no-e2e --no-cpu-baseline --no-clocks --steps 1 --warmup 1 > /dev/null 2>&1
+
+# float path (C3): full captures of the cross term and the split pre-pass
+BC3="python bench.py --config C3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-clocks"
+timeout -s KILL 300 ncu --set full --clock-control none --import-source on -k regex:k_xterm -s 1 -c 1 -o gpurun_out/k_xterm_c3_$TAG -f $BC3 > /dev/null 2>&1
+timeout -s KILL 300 ncu --set full --clock-control none --import-source on -k regex:k_split_f32 -s 1 -c 1 -o gpurun_out/k_split_f32_c3_$TAG -f $BC3 > /dev/null 2>&1
+timeout -s KILL 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3_$TAG.csv python bench.py --config C3 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-clocks > /dev/null 2>&1
+
 ls gpurun_out
