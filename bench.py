@@ -380,7 +380,7 @@ def main():
     peak = peaks["bf16_tflops"] * ratio
     traffic = None
     ncu_xt = None
-    tp = os.path.join(ROOT, "profiles", "xterm_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "xterm_traffic.json" if w.name == "C4" else f"xterm_traffic_{w.name}.json")
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)

@@ -14,6 +14,7 @@ from collections import defaultdict
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 KERNELS = ["k_xterm", "k_moments_i8", "k_texthist", "k_hist_contract", "k_finalize_i8"]
+KERNELS_C3 = ["k_xterm_c3", "k_split_f32_c3"]  # float path (C3 bench step), tools/gpu_full.sh
 METRICS = {
     "duration_ms": ("gpu__time_duration.sum", 1e-3),  # reported in us by default -> ms below
     "dram_read_bytes": ("dram__bytes_read.sum", None),
@@ -21,6 +22,7 @@ METRICS = {
     "dram_pct_peak": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", None),
     "tensor_active_pct": ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", None),
     "imma_active_pct": ("sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active", None),
+    "hmma_active_pct": ("sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active", None),
     "issue_active_pct": ("smsp__issue_active.avg.pct_of_peak_sustained_active", None),
     "smem_lsu_wavefronts": ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", None),
     "smem_tc_wavefronts": ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum", None),
@@ -69,8 +71,8 @@ def kernel_summary(rep):
     return out
 
 
-def launches(tag):
-    p = os.path.join(OUT, f"launches_{tag}.csv")
+def launches(tag, prefix="launches"):
+    p = os.path.join(OUT, f"{prefix}_{tag}.csv")
     if not os.path.exists(p):
         return {}
     txt = open(p).read()
@@ -91,10 +93,11 @@ def launches(tag):
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     res = {"tag": tag, "launch_list": launches(tag), "kernels": {}}
-    for k in KERNELS:
+    for k in KERNELS + KERNELS_C3:
         rep = os.path.join(OUT, f"{k}_{tag}.ncu-rep")
         if os.path.exists(rep):
             res["kernels"][k] = kernel_summary(rep)
+    res["launch_list_c3"] = launches(tag, "launches_c3")
     with open(os.path.join(ROOT, "profiles", f"ncu_{tag}.json"), "w") as f:
         json.dump(res, f, indent=1)
     lines = [f"# ncu summary, {tag} (C4: 1.5M x 5000 int8, one bench step)", "",
@@ -112,21 +115,28 @@ def main():
                      f"{g('issue_active_pct', 1, '{:.1f}')} | {g('smem_lsu_wavefronts', 1, '{:.3g}')} | "
                      f"{g('smem_tc_wavefronts', 1, '{:.3g}')} | {g('l2_to_sm_bytes', 1e-9)} | "
                      f"{g('l2_pct_peak', 1, '{:.1f}')} | {g('registers', 1, '{:.0f}')} |")
+    if res["launch_list_c3"]:
+        lines += ["", "C3 (100K x 5000 float32) launch list:", "", "| kernel | launches | ms (sum) | share |",
+                  "|---|---|---|---|"]
+        for k, v in res["launch_list_c3"].items():
+            lines.append(f"| {k} | {v['launches']} | {v['ms_total']:.3f} | {v['share'] * 100:.1f}% |")
     with open(os.path.join(ROOT, "profiles", f"ncu_{tag}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    x = res["kernels"].get("k_xterm")
-    if x and "dram_read_bytes" in x:
-        with open(os.path.join(ROOT, "profiles", "xterm_traffic.json"), "w") as f:
+    for kname, cfg, fname in (("k_xterm", "C4", "xterm_traffic.json"), ("k_xterm_c3", "C3", "xterm_traffic_C3.json")):
+        x = res["kernels"].get(kname)
+        if not (x and "dram_read_bytes" in x):
+            continue
+        with open(os.path.join(ROOT, "profiles", fname), "w") as f:
             ms = x.get("duration_ms")
             cyc = x.get("sm_cycles")
-            json.dump({"config": "C4", "n_gpus": 1, "tag": tag,
+            json.dump({"config": cfg, "n_gpus": 1, "tag": tag,
                        "dram_bytes_per_launch": x["dram_read_bytes"] + x.get("dram_write_bytes", 0.0),
                        "tensor_active_pct": x.get("tensor_active_pct"),
                        "duration_ms": ms,
                        # the kernel's own average SM clock (cycles / duration): nvidia-smi's
                        # coarse samples overstate it under the power cap
                        "sm_mhz": (cyc / (ms * 1e-3) / 1e6) if (cyc and ms) else None,
-                       "source": f"ncu --set full capture gpurun_out/k_xterm_{tag}.ncu-rep (profiles/ncu_{tag}.md)"}, f, indent=1)
+                       "source": f"ncu --set full capture gpurun_out/{kname}_{tag}.ncu-rep (profiles/ncu_{tag}.md)"}, f, indent=1)
     print("\n".join(lines))
 
 
