@@ -180,6 +180,71 @@ def cpu_baseline(w, sample_traces=CPU_SAMPLE_TRACES, ncols=CPU_SAMPLE_COLS):
             "seconds": t, "key_bytes_ranked_first": int(sum(a["best"] == O.expand_key(w.key)[10]))}
 
 
+def host_cpu_info():
+    """CPU model and socket count of this host (for the all-cores baseline)."""
+    info = {"model": None, "sockets": None, "logical_cpus": os.cpu_count()}
+    try:
+        txt = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in txt.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() == "Model name":
+                info["model"] = v.strip()
+            elif k.strip() == "Socket(s)":
+                info["sockets"] = int(v.strip()) if v.strip().isdigit() else v.strip()
+    except Exception:  # noqa: BLE001
+        pass
+    return info
+
+
+def cpu_baseline_all_cores(w, sample_traces=65536, cols_per_thread=2):
+    """SURVEY 8d's all-cores CPU baseline (the paper's multi-threaded server
+    comparison [P:164]): the oracle's own functions, Phase 1 once, then its
+    Phase 2 loops (trace and cross sums, single-threaded C that releases the
+    GIL) over one column block per host thread, then Phases 3-4 over all
+    columns.  No other change to the oracle."""
+    import concurrent.futures as cf
+    import numpy as np
+    from oracle import oracle as O
+    from synth import synth as S
+    threads = max(1, min(len(os.sched_getaffinity(0)), 128))
+    n = min(sample_traces, w.n)
+    texts, lv = S.texts(w, 0, n)
+    lp = list(w.leak_positions())
+    extra = np.linspace(0, w.m - 1, threads * cols_per_thread, dtype=np.int64).tolist()
+    cols = np.array(sorted(set(lp + extra))[:threads * cols_per_thread], np.int32)
+    Ws = S.traces(w, lv, 0, cols)
+    is_f32 = Ws.dtype == np.float32
+    blocks = [np.arange(i, len(cols), threads) for i in range(threads)]
+    blocks = [c for c in blocks if len(c)]
+    Wb = [np.ascontiguousarray(Ws[:, c]) for c in blocks]
+
+    def phase2(Wk):
+        if is_f32:
+            return O.sums_f32(w.leak_model, texts, Wk)
+        sw, sw2 = O.trace_sums_i8(Wk)
+        return O.cross_sums_i8(w.leak_model, texts, Wk), sw, sw2
+
+    t0 = time.perf_counter()
+    sh, sh2 = O.model_sums(w.leak_model, texts)
+    with cf.ThreadPoolExecutor(max_workers=len(Wb)) as ex:
+        parts = list(ex.map(phase2, Wb))
+    shw = np.zeros((4096, len(cols)), parts[0][0].dtype)
+    sw = np.zeros(len(cols), parts[0][1].dtype)
+    sw2 = np.zeros(len(cols), parts[0][2].dtype)
+    for c, (a, b1, b2) in zip(blocks, parts):
+        shw[:, c], sw[c], sw2[c] = a, b1, b2
+    rho = (O.rho_eq1_f64_grid if is_f32 else O.rho_eq1_grid)(n, shw, sh, sh2, sw, sw2)
+    mx, _, _ = O.phase3(rho)
+    best, _ = O.phase4(mx)
+    t = time.perf_counter() - t0
+    t_full = t * (w.n / n)
+    return {"value": 4096 * len(cols) / t_full, "unit": "correlations/s", "cores": len(Wb),
+            "kind": "oracle, Phase 2 over one column block per host thread",
+            "sample": f"{len(cols)} sample columns x first {n} traces of {w.name}; time x{w.n / n:.2f} to N={w.n}",
+            "seconds": t, "host": host_cpu_info(),
+            "key_bytes_ranked_first": int(sum(np.asarray(best) == O.expand_key(w.key)[10]))}
+
+
 def run_reference(args, w):
     """--impl reference: the oracle on the host cores, one bounded sample of the
     workload per step."""
@@ -468,6 +533,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w)
+        try:
+            cpu["all_cores"] = cpu_baseline_all_cores(w)
+        except Exception as ex:  # noqa: BLE001
+            cpu["all_cores"] = {"error": f"{type(ex).__name__}: {ex}"}
 
     if rank == 0:
         line = {
