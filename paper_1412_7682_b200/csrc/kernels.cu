@@ -214,7 +214,10 @@ __device__ __forceinline__ Best warp_best(Best x)
 }
 
 constexpr int FIN_THREADS = 256;
-constexpr int FIN_UNROLL = 4;
+#ifndef FIN_UNROLL_ROWS
+#define FIN_UNROLL_ROWS 4
+#endif
+constexpr int FIN_UNROLL = FIN_UNROLL_ROWS;
 
 __device__ __forceinline__ void block_best_store(Best best, int h, const FinalizeOut &o)
 {
