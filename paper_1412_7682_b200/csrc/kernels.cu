@@ -617,17 +617,17 @@ cudaError_t launch_phase4(const FinalizeOut &o, cudaStream_t s, int *launches)
 // ---------------------------------------------------------------------------
 // a6 pre-pass: float traces -> centred, per-sample scaled fp16 hi plane + e4m3
 // lo plane, and fp64 moments.  With c = w - o_j and s_j = 2^e_j (exact):
-//     hi = fp16(c s_j),  lo = e4m3_satfinite(512 (c s_j - hi))
-// so that c s_j ~= hi + lo / 512.  The cross term multiplies hi by fp16(H)
-// (kind::f16) and lo by the e4m3 value H / 512 (kind::f8f6f4), whose code is the
-// byte H itself (0..7 are the subnormals m 2^-9, 8 = 2^-6), into ONE fp32
-// accumulator; the spill multiplies column j by 1 / s_j (exact).  |lo / 512| is at
-// most half an fp16 ulp of c s_j (<= 2^-11 |c s_j|) and e4m3 keeps 4 significant
-// bits of it down to 2^-6 (steps of 2^-9 below), so the per-element error is at
-// most 2^-15 |c s_j| + 2^-19 (bf16 alone: 2^-9 |c s_j|; bf16 + e4m3: 2^-13, which
-// measured 1.4e-4 in rho at N = 65).  s_j puts the spread of the first traces in
-// [8, 16) (k_scale_f32): fp16 holds 4096x that, e4m3 lo saturates (448) only
-// above ~100x it, and then the element keeps fp16 precision.
+//     hi = fp16(c s_j),  lo = e4m3_satfinite(c s_j - hi)
+// so that c s_j ~= hi + lo.  The cross term multiplies both by H 2^-16 -- as
+// fp16 (kind::f16; its bit pattern is H << 8) for hi and as e5m2 (kind::f8f6f4;
+// its code is the byte H itself) for lo -- into ONE fp32 accumulator, so the
+// generator needs no conversion arithmetic; the spill multiplies column j by
+// 2^16 / s_j (exact).  |lo| is at most half an fp16 ulp of c s_j (<= 2^-11
+// |c s_j|) and e4m3 keeps 4 significant bits of it down to 2^-6 (steps of 2^-9
+// below), so the per-element error is at most 2^-15 |c s_j| + 2^-10 against a
+// spread of 2^7..2^8 (k_scale_f32): the same relative budget as fp16 + 4 bits.
+// fp16 holds 2^15 (the range-repair threshold), 128x that spread; beyond it the
+// column's scale is lowered and its planes rewritten (k_fix_scale, k_resplit_f32).
 // Thread = 4 consecutive samples (one float4 per row) over SP_ROWS rows.
 // ---------------------------------------------------------------------------
 namespace cpa {
@@ -707,7 +707,7 @@ k_split_f32(const float *__restrict__ w, int64_t ld, int64_t n, int32_t M, const
             const float cs = __fmul_rn(c, sc[q]);  // exact: power of two
             amax[q] = fmaxf(amax[q], fabsf(c));      // (NaN is reported as non-finite)
             h[q] = f16_bits(cs);
-            l[q] = __fmul_rn(__fsub_rn(cs, f16_val(h[q])), 512.0f);  // both exact
+            l[q] = __fsub_rn(cs, f16_val(h[q]));  // exact
             s1[q] += (double)c;
             s2[q] += (double)c * (double)c;
         }
@@ -754,9 +754,9 @@ __global__ void k_fix_scale(const int *range, const uint32_t *cmax, int32_t M, f
     if (isfinite(r) && r * scale[j] >= kF16Safe) {
         int E;
         frexpf(r, &E);
-        const int e = min(64, max(-64, 4 - E));
+        const int e = min(64, max(-64, 8 - E));
         scale[j] = ldexpf(1.0f, e);
-        inv_scale[j] = ldexpf(1.0f, -e);
+        inv_scale[j] = ldexpf(1.0f, 16 - e);  // also undoes the 2^-16 of the A operands
         f = 1;
     }
     colflag[j] = f;
@@ -776,13 +776,14 @@ k_resplit_f32(const int *range, const uint8_t *colflag, const float *__restrict_
         const float cs = __fmul_rn(__fsub_rn(w[r * ld + j], o), sc);
         const uint16_t h = f16_bits(cs);
         hi[r * ldh + j] = h;
-        lo[r * ldl + j] = (uint8_t)e4m3x2(__fmul_rn(__fsub_rn(cs, f16_val(h)), 512.0f), 0.0f);
+        lo[r * ldl + j] = (uint8_t)e4m3x2(__fsub_rn(cs, f16_val(h)), 0.0f);
     }
 }
 
 // Per-sample scale s_j = 2^e_j for the split: the largest |w - o_j| over the
-// first n rows, r, is brought into [8, 16) (e_j clamped to [-64, 64]; 1 when r
-// is 0 or not finite).  inv_scale = 1 / s_j (exact).
+// first n rows, r, is brought into [2^7, 2^8) (e_j clamped to [-64, 64]; 1 when
+// r is 0 or not finite).  inv_scale = 2^16 / s_j (exact; the 2^16 undoes the
+// H 2^-16 of the cross term's A operands).
 __global__ void k_scale_f32(const float *__restrict__ w, int64_t ld, int64_t n, int32_t M,
                             const float *__restrict__ offset, float *scale, float *inv_scale)
 {
@@ -795,10 +796,10 @@ __global__ void k_scale_f32(const float *__restrict__ w, int64_t ld, int64_t n, 
     if (r > 0.0f && isfinite(r)) {
         int E;
         frexpf(r, &E);  // r in [2^(E-1), 2^E)
-        e = min(64, max(-64, 4 - E));
+        e = min(64, max(-64, 8 - E));
     }
     scale[j] = ldexpf(1.0f, e);
-    inv_scale[j] = ldexpf(1.0f, -e);
+    inv_scale[j] = ldexpf(1.0f, 16 - e);
 }
 }  // namespace
 

@@ -53,11 +53,11 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, c
                             bool overlapped = false);
 
 // a6: float traces.  Split pre-pass: c = w - offset[j], hi = fp16(c s_j),
-// lo = e4m3(512 (c s_j - hi)) into [n][ldh] fp16 / [n][ldl] byte planes (s_j =
+// lo = e4m3(c s_j - hi) into [n][ldh] fp16 / [n][ldl] byte planes (s_j =
 // scale[j], a power of two from launch_scale_f32 over the first traces); fp64
 // sum c, sum c^2; sets *nonfinite on NaN/Inf [S:140].  Cross term: kind::f16 on
 // hi and kind::f8f6f4 on lo into one fp32 TMEM accumulator per <= 4096-trace
-// unit, spilled to fp64 times inv_scale[j].  d_scale = [M] scale | [M] inv_scale;
+// unit (A operands H 2^-16), spilled to fp64 times inv_scale[j] = 2^16 / s_j.  d_scale = [M] scale | [M] inv_scale;
 // a column whose |c s_j| reaches 2^15 in a chunk gets a smaller scale and its
 // planes rewritten before the cross term (d_scratch: 5 M + 16 bytes).
 cudaError_t launch_scale_f32(const float *d_w, int64_t ld, int64_t n, int32_t M, const float *d_offset,

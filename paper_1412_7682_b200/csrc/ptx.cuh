@@ -317,6 +317,14 @@ __device__ __forceinline__ void mma_f8_pair(uint32_t d_tmem, uint64_t adesc, uin
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// kind::f8f6f4 with A e5m2 (format code 1), B e4m3 (code 0), fp32 accumulate, both MN-major
+__host__ __device__ constexpr uint32_t idesc_e5m2_e4m3(uint32_t m, uint32_t n)
+{
+    return (1u << 4)      // c_format = F32
+           | (1u << 7)    // a_format = E5M2
+           | (0u << 10)   // b_format = E4M3
+           | (1u << 15) | (1u << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
 // kind::f8f6f4 with e4m3 inputs (format code 0), fp32 accumulate, both operands MN-major
 __host__ __device__ constexpr uint32_t idesc_e4m3(uint32_t m, uint32_t n)
 {

@@ -6,8 +6,9 @@
 //        TMEM, spilled to int64 with red.add (bit-exact for any schedule);
 //   F32 (a6): W float32 pre-split (k_split_f32) into an fp16 hi plane and an e4m3
 //        lo plane (per-sample power-of-two scale s_j): per 64-trace stage 4
-//        kind::f16 MMAs (fp16(H) . hi, K = 16) and 2 kind::f8f6f4 MMAs (H/512 .
-//        512 lo, K = 32; the e4m3 code of H/512 is the byte H) into ONE fp32 TMEM
+//        kind::f16 MMAs (H 2^-16 . hi, K = 16; the fp16 bits of H 2^-16 are H << 8)
+//        and 2 kind::f8f6f4 MMAs (H 2^-16 . lo, K = 32; the e5m2 code of H 2^-16
+//        is the byte H, lo is e4m3) into ONE fp32 TMEM
 //        accumulator over <= 4096 traces per work unit -- 3/4 of the tensor time
 //        of two 16-bit MMAs -- spilled to fp64 x 1/s_j with atomicAdd [P:201-217].
 //
@@ -92,7 +93,7 @@ struct Cfg {
     static constexpr int BH_BYTES = BK * 128 * ESZ; // one CTA's half (128 samples) of one N tile: W (I8) / hi (F32)
     static constexpr int BL_BYTES = F32 ? BK * 128 : 0;  // F32: the same half of the e4m3 lo plane
     static constexpr int A_BYTES = BK * 128 * ESZ;  // 128 keys x BK traces: H (I8) / fp16(H) (F32)
-    static constexpr int A8_BYTES = F32 ? BK * 128 : 0;  // F32: the e4m3 tile of H/512 (= the bytes H)
+    static constexpr int A8_BYTES = F32 ? BK * 128 : 0;  // F32: the e5m2 tile of H 2^-16 (= the bytes H)
     static constexpr int A_ATOM = BK * 128;         // bytes between 128-byte MN groups (A and B)
     static constexpr int A_STAGE = KB * A_BYTES + A8_BYTES;        // generated H tiles of one stage
     static constexpr int B_STAGE = NT * (BH_BYTES + BL_BYTES);     // TMA-loaded W tiles of one stage
@@ -202,16 +203,13 @@ __device__ __forceinline__ void unit_coords(const Params &p, int u, int &b, int 
 
 __device__ __forceinline__ int shiftrows_src(int b) { return (b & 3) + 4 * (((b >> 2) + (b & 3)) & 3); }
 
-// fp16(x) for two bytes x0 (byte sel0) and x1 of w, x in 0..255: the fp16 bit
-// pattern of 1024 + x is 0x6400 | x (exact: spacing 1 in [1024, 2048)); subtract
-// 1024 in packed fp16 arithmetic (exact).
-__device__ __forceinline__ uint32_t f16x2_of_bytes(uint32_t w, uint32_t sel)
+// The fp16 value H 2^-16 for two bytes H0 (byte sel0) and H1 of w, H in 0..8: its
+// bit pattern is H << 8 (0x0100..0x0300 are the subnormals m 2^-24 with m = 256 H,
+// 0x0400 = 2^-14, 0x0500..0x0700 = (1 + m/1024) 2^-14, 0x0800 = 2^-13: all H 2^-16),
+// so one PRMT places H0, H1 in bytes 1 and 3 -- no conversion arithmetic.
+__device__ __forceinline__ uint32_t f16x2_h16_of_bytes(uint32_t w, uint32_t sel)
 {
-    const uint32_t biased = __byte_perm(w, 0x64646464u, sel);
-    __half2 v = *reinterpret_cast<const __half2 *>(&biased);
-    const __half2 off = __floats2half2_rn(1024.0f, 1024.0f);
-    v = __hsub2(v, off);
-    return *reinterpret_cast<const uint32_t *>(&v);
+    return __byte_perm(w, 0u, sel);
 }
 
 // Fused a4 [P:79]: sum W_ij and sum W_ij^2, read from the W ring while the MMAs
@@ -523,7 +521,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                         accum = 1;
                     }
                     if constexpr (F32) {
-                        // lo: (H/512) . (512 lo), e4m3, K = 32 rows of 128 bytes per MMA
+                        // lo: (H 2^-16, e5m2) . (lo, e4m3), K = 32 rows of 128 bytes per MMA
                         static_assert(C::KB == 1 && C::NT == 1, "F32 lo MMAs: one accumulator");
                         const uint64_t a8 = ad + (uint64_t)(C::A_BYTES >> 4);
                         const uint64_t b8 = bdd + (uint64_t)(C::BH_BYTES >> 4);
@@ -707,15 +705,15 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     } else {
                         // 16 keys -> 32 bytes of fp16: keys 16ql.. live in MN atom ql/4,
                         // 16-byte chunks 2(ql%4) and 2(ql%4)+1 of the row (swizzled)
-                        const uint4 lo4 = make_uint4(f16x2_of_bytes(outv.x, 0x7170), f16x2_of_bytes(outv.x, 0x7372),
-                                                     f16x2_of_bytes(outv.y, 0x7170), f16x2_of_bytes(outv.y, 0x7372));
-                        const uint4 hi4 = make_uint4(f16x2_of_bytes(outv.z, 0x7170), f16x2_of_bytes(outv.z, 0x7372),
-                                                     f16x2_of_bytes(outv.w, 0x7170), f16x2_of_bytes(outv.w, 0x7372));
+                        const uint4 lo4 = make_uint4(f16x2_h16_of_bytes(outv.x, 0x1404), f16x2_h16_of_bytes(outv.x, 0x3424),
+                                                     f16x2_h16_of_bytes(outv.y, 0x1404), f16x2_h16_of_bytes(outv.y, 0x3424));
+                        const uint4 hi4 = make_uint4(f16x2_h16_of_bytes(outv.z, 0x1404), f16x2_h16_of_bytes(outv.z, 0x3424),
+                                                     f16x2_h16_of_bytes(outv.w, 0x1404), f16x2_h16_of_bytes(outv.w, 0x3424));
                         uint8_t *rowp = abase + (ql >> 2) * C::A_ATOM + row * 128;
                         const int c0i = 2 * (ql & 3);
                         *(uint4 *)(rowp + (((c0i) ^ (row & 7)) << 4)) = lo4;
                         *(uint4 *)(rowp + (((c0i + 1) ^ (row & 7)) << 4)) = hi4;
-                        // and the e4m3 tile of H/512: the same bytes as the I8 tile
+                        // and the e5m2 tile of H 2^-16: the same bytes as the I8 tile
                         *(uint4 *)(abase + C::A_BYTES + row * 128 + ((ql ^ (row & 7)) << 4)) = outv;
                     }
                 }
@@ -874,7 +872,7 @@ cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap
 {
     return launch<V_F32>(tmap_hi, tmap_lo, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len, idesc_f16(2 * BMC, BN),
                         num_sms, stream, launches, nullptr, nullptr, true, d_hist, nullptr, d_clk,
-                        idesc_e4m3(2 * BMC, BN), d_inv_scale);
+                        idesc_e5m2_e4m3(2 * BMC, BN), d_inv_scale);
 }
 
 }  // namespace cpa

@@ -91,7 +91,7 @@ def test_c3_fullsize_sampled(P):
 
 
 # The split is fp16 hi + e4m3 lo (per-sample power-of-two scale): per element
-# |error| <= 2^-15 |c s_j| + 2^-19 in scaled units, so rho sits far inside the
+# |error| <= 2^-15 |c s_j| + 2^-10 against a spread of 2^7..2^8, so rho sits far inside the
 # north-star bar (measured <= 2e-6 here).  A swapped e4m3 byte pair or a lost lo
 # term (fp16 alone ~4e-5, bf16 alone ~3e-4 on these inputs) fails this bar.
 TIGHT = 1e-5
@@ -118,8 +118,8 @@ def test_float_split_precision_any_magnitude(P, scale):
 @pytest.mark.parametrize("amp", [50.0, 1e4])
 def test_float_split_outliers(P, amp):
     """Values far above the spread the per-sample scales were chosen from (the
-    first 64 traces, spread ~0.1): amp 50 saturates the e4m3 lo term (the element
-    keeps fp16 precision); amp 1e4 would overflow fp16, so the column's scale is
+    first 64 traces, spread ~0.1): at amp 50 and 1e4 (500x, 1e5x the spread) the
+    fp16 hi plane would pass the 2^15 repair threshold, so the column's scale is
     lowered and its planes rewritten (range repair).  Both within the bar."""
     w = S.CONFIGS["C3"].replace(n=3000, m=96, a=0.02)
     texts, W = S.dataset(w)
