@@ -131,3 +131,28 @@ def test_float_split_outliers(P, amp):
     err, _ = _max_err(P, texts, W)
     print(f"outliers x{amp:g}: max |drho| = {err:.3g}")
     assert err <= TOL
+
+
+def test_float_range_repair_in_a_later_chunk(P):
+    """Outliers only after the first 45000 traces: the scales chosen from the
+    first 64 traces hold until then, and the repair lowers some columns' scales
+    part-way through the call.  Against the oracle, and against several
+    accumulate calls (the repair persisting across calls)."""
+    w = S.CONFIGS["C3"].replace(n=66000, m=48, a=0.02)
+    texts, W = S.dataset(w)
+    W = W.copy()
+    rng = np.random.default_rng(11)
+    rows = rng.integers(45000, w.n, 30)
+    cols = rng.integers(0, w.m, 30)
+    W[rows, cols] += np.float32(1e4) * rng.standard_normal(30).astype(np.float32)
+    err, out = _max_err(P, texts, W)
+    print(f"repair in a later chunk: max |drho| = {err:.3g}")
+    assert err <= TOL
+    eng = P.Engine(w.m, P.CPA_F32, P.CPA_HD_LAST, 0)
+    dW = torch.from_numpy(np.ascontiguousarray(W)).cuda()
+    dT = torch.from_numpy(texts).cuda()
+    for a, b in ((0, 30000), (30000, 50000), (50000, w.n)):
+        eng.accumulate(dW[a:b], dT[a:b])
+    ch = eng.finalize(want_rho=True)
+    eng.close()
+    assert np.max(np.abs(ch["rho"].cpu().numpy() - out["rho"].cpu().numpy())) <= TOL
