@@ -476,9 +476,9 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
             cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)m};
             cuuint32_t estr[2] = {1, 1};
             for (int k = 0; k < 2; k++) {
-                // hi: 64 fp16 = the 128-byte swizzle span; lo: 128 e4m3 bytes; x 64 traces
+                // hi: 64 fp16 = the 128-byte swizzle span; lo: 128 e4m3 bytes; x one stage of traces
                 cuuint64_t strides[1] = {(cuuint64_t)(k ? ldl : ldh * 2)};
-                cuuint32_t box[2] = {k ? 128u : 64u, 64u};
+                cuuint32_t box[2] = {k ? 128u : 64u, (cuuint32_t)cpa::xterm_f32_bk()};
                 CUresult r = get_encode()(k ? &ml : &mh,
                                           k ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
                                           k ? (void *)c->d_lo : (void *)c->d_hi, dims, strides, box, estr,

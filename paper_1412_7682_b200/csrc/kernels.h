@@ -34,6 +34,7 @@ cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M,
 // a5: cross term (tcgen05 kind::i8, CTA pairs).  With d_sum_w / d_sum_w2 set,
 // the kernel also adds a4's sum W, sum W^2 (fused moments).
 int xterm_smem_bytes();
+int xterm_f32_bk();  // traces per stage of the float cross term (the TMA box height of its planes)
 int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms, bool remote_epilogue = false);
 // Variant choice: NT = 2 sample tiles per unit (A tile reused twice, a4 fused,
 // epilogue serialised with the unit's MMAs) or NT = 1 with double-buffered TMEM

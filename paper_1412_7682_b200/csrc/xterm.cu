@@ -49,6 +49,7 @@
 //   bit 1: generators skip the H generation (barrier traffic only)
 //   bit 2: the epilogue skips its global atomics (TMEM reads only)
 //   bit 4: no W loads (the leader's producer arrives without tx bytes)
+//   bit 32: F32 skips the e4m3 lo MMAs; bit 64: F32 skips the fp16 hi MMAs
 #ifndef XT_EXP
 #define XT_EXP 0
 #endif
@@ -63,6 +64,9 @@
 #endif
 #ifndef XT_B_STAGES_I8
 #define XT_B_STAGES_I8 4
+#endif
+#ifndef XT_BK_F32
+#define XT_BK_F32 64
 #endif
 #ifndef XT_A_STAGES_F32
 #define XT_A_STAGES_F32 4  // (4, 3): C3 cross term 5.00 vs 5.12 ms for (3, 4), 5.25 for (2, 5)
@@ -88,7 +92,7 @@ struct Cfg {
     static constexpr int NT = V == V_I8 ? XT_NT_I8 : 1;  // N=256 sample tiles per unit (W tiles sharing one A tile)
     static constexpr int NBUF = V == V_I8 ? 1 : 2;      // TMEM accumulator buffers
     static constexpr int NACC = KB * NT;            // N=256 accumulators per unit
-    static constexpr int BK = F32 ? 64 : 128;       // traces per pipeline stage
+    static constexpr int BK = F32 ? XT_BK_F32 : 128;  // traces per pipeline stage
     static constexpr int BOX_X = 128 / ESZ;         // samples per TMA box (128-byte swizzle span)
     static constexpr int BH_BYTES = BK * 128 * ESZ; // one CTA's half (128 samples) of one N tile: W (I8) / hi (F32)
     static constexpr int BL_BYTES = F32 ? BK * 128 : 0;  // F32: the same half of the e4m3 lo plane
@@ -515,7 +519,9 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                                 const uint64_t a = adk + (uint64_t)((kb * C::A_BYTES) >> 4);
                                 const uint64_t bd = bdk + (uint64_t)((n * (C::BH_BYTES + C::BL_BYTES)) >> 4);
                                 const uint32_t d = dbase + (kb * C::NT + n) * BN;
-                                if (F32) mma_f16_pair(d, a, bd, p.idesc, accum);
+                                if (F32) {
+                                    if (!(XT_EXP & 64)) mma_f16_pair(d, a, bd, p.idesc, accum);
+                                }
                                 else mma_i8_pair(d, a, bd, p.idesc, accum);
                             }
                         accum = 1;
@@ -526,7 +532,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                         const uint64_t a8 = ad + (uint64_t)(C::A_BYTES >> 4);
                         const uint64_t b8 = bdd + (uint64_t)(C::BH_BYTES >> 4);
 #pragma unroll
-                        for (int k8 = 0; k8 < C::BK / 32; k8++)
+                        for (int k8 = 0; k8 < ((XT_EXP & 32) ? 0 : C::BK / 32); k8++)
                             mma_f8_pair(dbase, a8 + (uint64_t)((k8 * 32 * 128) >> 4),
                                         b8 + (uint64_t)((k8 * 32 * 128) >> 4), p.idesc8, 1u);
                     }
@@ -822,6 +828,7 @@ int64_t auto_kchunk(int32_t M, int64_t N, int num_sms, int kb, int nt, int bk, i
 }  // namespace
 
 int xterm_smem_bytes() { return SMEM_ALLOC; }
+int xterm_f32_bk() { return Cfg<V_F32>::BK; }
 
 int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms, bool remote_epilogue)
 {
