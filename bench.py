@@ -345,6 +345,10 @@ def main():
     eng.set_col0(j0)
     ovl_mode = 0 if args.no_overlap else (args.overlap_mode if args.overlap_mode is not None else OVERLAP_DEFAULT)
     eng.set_overlap(ovl_mode)
+    if is_f32 and world > 1:
+        # float sums are centred per sample: every rank must use the same offsets
+        # (rank 0's first trace), or the combined sums mix differently-shifted data
+        MG.share_offsets(eng, dWv if rank == 0 else None)
     combine = ("columns" if shard == "samples" else args.combine) if world > 1 else "none"
     fused_note = None
     if combine == "auto":
@@ -385,7 +389,7 @@ def main():
             P.cpa_finalize_rows(eng.ctx, 0, 4096, rho, maxabs, argmax, peak)
             return P.cpa_select(eng.ctx, world, *MG.gather_shards(maxabs, argmax, peak), rank_t)
         if combine == "allreduce":
-            eng.allreduce()
+            eng.allreduce(check_offsets=False)   # float: checked once before the timed steps
         return P.cpa_finalize(eng.ctx, rho, maxabs, argmax, rank_t)
 
     def barrier():
@@ -395,6 +399,8 @@ def main():
 
     for _ in range(args.warmup):
         res = step()
+    if is_f32 and world > 1 and shard == "traces":
+        MG.check_same_offsets(eng)   # every rank's sums centred on the same offsets
     eng.set_timing(True)
     eng.phase_times()  # clear
     barrier()

@@ -145,8 +145,12 @@ CPA_API cpa_status cpa_finalize(cpa_ctx *ctx, double *d_rho, double *d_maxabs,
  *             scratch for maxabs/argmax/rank);
  *   d_best    optional [32] int32: best sub-key per byte [0..15] and its peak
  *             sample [16..31].
- * No host-side checks: N < 2 gives rho = 0 (zero variance), and the
- * non-finite flag (f32) is reported only by the blocking cpa_finalize.      */
+ * Checks without blocking: CPA_E_TOO_FEW_TRACES / CPA_E_OVERFLOW from the
+ * traces this context accumulated since its last reset (N = 1, or > 2^23 for
+ * int traces; cpa_accumulate also refuses a running total past 2^23); not
+ * checked when none were accumulated here (an externally combined
+ * accumulator).  The non-finite flag (f32) is only reported by the blocking
+ * calls (cpa_finalize, cpa_finalize_rows): end a stream with one of them.   */
 CPA_API cpa_status cpa_finalize_async(cpa_ctx *ctx, double *d_rho, double *d_maxabs, int32_t *d_argmax,
                                       int32_t *d_rank, int32_t *d_best);
 
@@ -220,10 +224,20 @@ CPA_API cpa_status cpa_select(cpa_ctx *ctx, int32_t G, double *d_maxabs, int32_t
  * to per-sample offsets [S:285]; centring keeps the split and the fp32 tensor-
  * core accumulation accurate.  Default: the first trace of the first
  * cpa_accumulate call.  Multi-GPU: every rank must use the same offsets (the
- * accumulated sums are of the offset samples).  Setting offsets also re-derives
+ * accumulated sums are of the offset samples; a caller combining ranks sets
+ * them explicitly, e.g. rank 0's first trace broadcast to every rank).  The
+ * finalize also reads them: SPEC's degenerate-column rule compares dw with the
+ * RAW second moment [S:293], rebuilt from the centred sums and o_j.  Setting offsets also re-derives
  * the split's per-sample power-of-two scales (from the next accumulate's first
  * <= 64 traces; a precision choice that never changes the sums' meaning).   */
 CPA_API cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets);
+/* CPA_F32 only: copy the offsets in force (M floats; 0 until set) to d_out
+ * (device, may be NULL; asynchronous on the context's stream) and report in
+ * *is_set (may be NULL) whether they were set -- by cpa_set_offsets or by the
+ * first cpa_accumulate.  Lets a multi-GPU caller verify that every rank's sums
+ * are centred on the same offsets before it adds them (paper_1412_7682_b200.
+ * multigpu.check_same_offsets).  CPA_E_INVALID_ARG for an int context.       */
+CPA_API cpa_status cpa_get_offsets(cpa_ctx *ctx, float *d_out, int *is_set);
 
 CPA_API cpa_status cpa_reset(cpa_ctx *ctx);    /* zero the accumulator and the
                                                   non-finite flag (async) */

@@ -44,6 +44,8 @@ def run_attack(traces: np.ndarray, texts: np.ndarray, model: int = 0, device: in
     kind = {np.dtype(np.int8): B.CPA_S8, np.dtype(np.uint8): B.CPA_U8, np.dtype(np.float32): B.CPA_F32}
     if traces.dtype == np.float64:
         print("note: float64 traces are narrowed to float32 (the float path's input type)", file=sys.stderr)
+    if traces.dtype not in kind and traces.dtype != np.float64:
+        raise TypeError(f"unsupported trace dtype {traces.dtype} (int8, uint8, float32 or float64)")
     dt = kind.get(traces.dtype, B.CPA_F32)
     eng = Engine(m, dt, model, device)
     rows = max(1, chunk_bytes // (m * traces.dtype.itemsize))

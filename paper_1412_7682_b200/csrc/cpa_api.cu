@@ -89,6 +89,7 @@ struct cpa_ctx {
     int32_t *d_argmax = nullptr, *d_rank = nullptr, *d_best = nullptr;
     int *d_counter = nullptr;  // work-unit counter of the cross-term scheduler
     int64_t kchunk = 0;
+    int64_t n_since_reset = 0;  // traces accumulated through this context since init / cpa_reset
     int32_t col0 = 0;  // CPA_OPT_COL0: global index of sample 0 (sample-axis sharding)
     int64_t launches = 0;
     // cpa_accumulate_host staging
@@ -119,7 +120,7 @@ struct cpa_ctx {
     // cpa_set_row_owners: fused multi-GPU combine (key byte b's sum_hw rows go to owners[b])
     int64_t *owners[16] = {};
     bool owners_set = false;
-    unsigned long long *d_clk = nullptr;  // xterm clock probe (globaltimer, clock64 at CTA 0's start/end)  // CPA_OPT_FUSE_HIST: a3 byte-pair histogram counted by the cross-term kernel (measured neutral)
+    unsigned long long *d_clk = nullptr;  // xterm clock probe (globaltimer, clock64 at CTA 0's start/end)
     int32_t *d_cs_cnt = nullptr, *d_cs_off = nullptr, *d_cs_cur = nullptr, *d_cs_perm = nullptr, *d_cs_S = nullptr;
     int64_t cs_perm_n = 0, cs_S_words = 0;
     // CPA_OPT_TIMING: CUDA events recorded on `stream` around every launch
@@ -199,6 +200,7 @@ cpa_status cpa_reset(cpa_ctx *ctx)
     CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
     CUDA_TRY(cudaMemsetAsync(ctx->accum, 0, cpa_accum_bytes(ctx->M), ctx->stream), "reset accumulator");
     CUDA_TRY(cudaMemsetAsync(ctx->d_nonfinite, 0, sizeof(int), ctx->stream), "reset flag");
+    ctx->n_since_reset = 0;
     return CPA_OK;
 }
 
@@ -264,6 +266,7 @@ cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, 
     }
     e = cudaMemcpyAsync(c->d_vtab, vt, 65536, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_accum, 0, cpa_accum_bytes(M), c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->d_offset, 0, sizeof(float) * M, c->stream);  // until set
     if (e == cudaSuccess) e = cudaMemsetAsync(c->d_nonfinite, 0, sizeof(int), c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
@@ -286,6 +289,18 @@ cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets)
         CUDA_TRY(cudaMemsetAsync(ctx->d_offset, 0, sizeof(float) * ctx->M, ctx->stream), "offsets");
     ctx->offset_set = true;
     ctx->scale_set = false;  // the split scales follow the spread about the offsets
+    return CPA_OK;
+}
+
+cpa_status cpa_get_offsets(cpa_ctx *ctx, float *d_out, int *is_set)
+{
+    if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
+    if (ctx->dtype != CPA_F32) return fail(CPA_E_INVALID_ARG, "offsets apply to CPA_F32 contexts only");
+    CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (d_out)
+        CUDA_TRY(cudaMemcpyAsync(d_out, ctx->d_offset, sizeof(float) * ctx->M, cudaMemcpyDeviceToDevice, ctx->stream),
+                 "offsets");
+    if (is_set) *is_set = ctx->offset_set ? 1 : 0;
     return CPA_OK;
 }
 
@@ -582,18 +597,17 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     return CPA_OK;
 }
 
-static cpa_status check_accumulate_args(cpa_ctx *c, const void *w, int64_t ld, const uint8_t *tx, int64_t n,
-                                        bool device)
+static cpa_status check_accumulate_args(cpa_ctx *c, const void *w, int64_t ld, const uint8_t *tx, int64_t n)
 {
     if (!c) return fail(CPA_E_INVALID_ARG, "null context");
     if (n < 0) return fail(CPA_E_INVALID_ARG, "N=%lld < 0", (long long)n);
     if (n == 0) return CPA_OK;
     if (!w || !tx) return fail(CPA_E_INVALID_ARG, "null traces or texts");
     if (n > kMaxTraces) return fail(CPA_E_OVERFLOW, "N=%lld per call exceeds 2^23", (long long)n);
+    if (c->dtype != CPA_F32 && c->n_since_reset + n > kMaxTraces)
+        return fail(CPA_E_OVERFLOW, "%lld + %lld traces since the last reset exceed 2^23 (exact-int64 bound of Eq. (1))",
+                    (long long)c->n_since_reset, (long long)n);
     if (ld < c->M) return fail(CPA_E_INVALID_ARG, "ld=%lld < M=%d", (long long)ld, c->M);
-    const int64_t esz = c->dtype == CPA_F32 ? 4 : 1;
-    (void)device;
-    (void)esz;
     return CPA_OK;
 }
 
@@ -601,13 +615,16 @@ static cpa_status accumulate_staged(cpa_ctx *c, const void *src, int64_t ld, con
 
 cpa_status cpa_accumulate(cpa_ctx *c, const void *d_traces, int64_t ld, const uint8_t *d_texts, int64_t N)
 {
-    cpa_status st = check_accumulate_args(c, d_traces, ld, d_texts, N, false);
+    cpa_status st = check_accumulate_args(c, d_traces, ld, d_texts, N);
     if (st != CPA_OK || N == 0) return st;
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
     const int64_t esz = c->dtype == CPA_F32 ? 4 : 1;
     if (((uintptr_t)d_traces & 15) || ((ld * esz) & 15) || ((uintptr_t)d_texts & 15))
-        return accumulate_staged(c, d_traces, ld, d_texts, N);  // TMA needs 16-byte strides
-    return accumulate_device(c, d_traces, ld, d_texts, N);
+        st = accumulate_staged(c, d_traces, ld, d_texts, N);  // TMA needs 16-byte strides
+    else
+        st = accumulate_device(c, d_traces, ld, d_texts, N);
+    if (st == CPA_OK) c->n_since_reset += N;
+    return st;
 }
 
 // Stream (host or unaligned device) traces through the library's staging
@@ -691,11 +708,12 @@ static cpa_status accumulate_staged(cpa_ctx *c, const void *src, int64_t ld, con
 
 cpa_status cpa_accumulate_host(cpa_ctx *c, const void *h_traces, int64_t ld, const uint8_t *h_texts, int64_t N)
 {
-    cpa_status st = check_accumulate_args(c, h_traces, ld, h_texts, N, false);
+    cpa_status st = check_accumulate_args(c, h_traces, ld, h_texts, N);
     if (st != CPA_OK || N == 0) return st;
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
     st = accumulate_staged(c, h_traces, ld, h_texts, N);
     if (st != CPA_OK) return st;
+    c->n_since_reset += N;
     CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
     return CPA_OK;
 }
@@ -739,8 +757,8 @@ static cpa_status phase3(cpa_ctx *c, const cpa::FinalizeOut &o, int *launches)
     if (o.h1 <= o.h0) return CPA_OK;
     CUDA_TRY(c->timed(3, [&] {
                  return c->dtype == CPA_F32
-                            ? cpa::launch_finalize_f64((const double *)c->accum, c->M, c->d_sqrt_dw, o, c->stream,
-                                                       launches)
+                            ? cpa::launch_finalize_f64((const double *)c->accum, c->M, c->d_offset, c->d_sqrt_dw, o,
+                                                       c->stream, launches)
                             : cpa::launch_finalize_i8((const int64_t *)c->accum, c->M, c->d_sqrt_dw, o, c->stream,
                                                       launches);
              }),
@@ -884,6 +902,13 @@ cpa_status cpa_finalize_async(cpa_ctx *c, double *d_rho, double *d_maxabs, int32
                               int32_t *d_best)
 {
     if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    // host-side checks on the traces this context accumulated since its last
+    // reset (no device read: the call must not block); a context whose
+    // accumulator was filled from outside (none accumulated here) is not checked
+    if (c->n_since_reset == 1)
+        return fail(CPA_E_TOO_FEW_TRACES, "N=1 < 2: Eq. (1) undefined");
+    if (c->dtype != CPA_F32 && c->n_since_reset > kMaxTraces)
+        return fail(CPA_E_OVERFLOW, "N=%lld > 2^23", (long long)c->n_since_reset);
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
     cpa::FinalizeOut o = outputs(c, d_rho, d_maxabs, d_argmax, nullptr, d_rank);
     if (d_best) o.best = d_best;

@@ -302,15 +302,22 @@ k_finalize_i8(const int64_t *__restrict__ hw, const int64_t *__restrict__ sw,
 }
 
 // float path: all sums fp64 (same shape as the int accumulator)
+// The float sums are of the centred samples c = w - o_j (cpa_set_offsets).  dw
+// is offset-invariant, but SPEC's degenerate-column rule [S:293] compares it
+// with the RAW second moment: dw <= 1e-12 * N * sum w^2 -> rho = 0 (marked by a
+// 0 here), with sum w^2 = sum c^2 + 2 o_j sum c + N o_j^2 rebuilt from the
+// centred sums (the same decision as the oracle's raw-sum test, or_rho_eq1_f64_grid)
 __global__ void k_sqrt_dw_f64(const double *__restrict__ sw, const double *__restrict__ sw2,
-                              const double *__restrict__ count, int32_t M, double *out)
+                              const double *__restrict__ count, const float *__restrict__ offset, int32_t M,
+                              double *out)
 {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= M) return;
     const double n = *count;
     const double dw = __dsub_rn(__dmul_rn(n, sw2[j]), __dmul_rn(sw[j], sw[j]));
-    // degenerate column [S:293]: dw <= 1e-12 * N * S_w2 -> rho = 0 (marked by 0)
-    out[j] = (dw > __dmul_rn(1e-12, __dmul_rn(n, sw2[j]))) ? __dsqrt_rn(dw) : 0.0;
+    const double o = offset ? (double)offset[j] : 0.0;
+    const double raw2 = sw2[j] + o * (2.0 * sw[j] + n * o);
+    out[j] = (dw > 1e-12 * n * raw2) ? __dsqrt_rn(dw) : 0.0;
 }
 
 __global__ void __launch_bounds__(FIN_THREADS)
@@ -453,13 +460,9 @@ template <typename Acc>
 cudaError_t hist_contract(const uint32_t *d_hist, int64_t n, const uint8_t *d_vtab, Acc *d_sum_h, Acc *d_sum_h2,
                           Acc *d_count, cudaStream_t s, int *launches)
 {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_hist_contract<Acc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             65536 + HC_X * 256 * 4);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    cudaError_t e = smem_attr_once((const void *)k_hist_contract<Acc>, 65536 + HC_X * 256 * 4, attr);
+    if (e != cudaSuccess) return e;
     k_hist_contract<Acc><<<dim3(256 / HC_X, 16), 256, 65536 + HC_X * 256 * 4, s>>>(d_hist, d_vtab, d_sum_h, d_sum_h2,
                                                                                    d_count, n);
     if (launches) (*launches)++;
@@ -470,16 +473,10 @@ template <typename Acc>
 cudaError_t modelsums(const uint8_t *d_texts, int64_t n, const uint8_t *d_vtab, uint32_t *d_hist, Acc *d_sum_h,
                       Acc *d_sum_h2, Acc *d_count, cudaStream_t s, int *launches)
 {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_modelsums<Acc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             65536 + MS_STAGE * 16);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_hist_contract<Acc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     65536 + HC_X * 256 * 4);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr_ms{0}, attr_hc{0};
+    cudaError_t e0 = smem_attr_once((const void *)k_modelsums<Acc>, 65536 + MS_STAGE * 16, attr_ms);
+    if (e0 == cudaSuccess) e0 = smem_attr_once((const void *)k_hist_contract<Acc>, 65536 + HC_X * 256 * 4, attr_hc);
+    if (e0 != cudaSuccess) return e0;
     if (d_hist && n >= kHistMinTraces) {
         cudaError_t e = cudaMemsetAsync(d_hist, 0, sizeof(uint32_t) * 16 * 65536, s);
         if (e != cudaSuccess) return e;
@@ -536,14 +533,12 @@ cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M,
     // one resident wave: rows per item so that (groups x chunks) fills the
     // GPU's resident threads exactly once (no wave-quantisation tail);
     // blocks_per_sm > 0 caps the wave (room for a concurrent cross term)
-    static int sms = 0, per_sm = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_moments_i8<true>, MO_THREADS, 0);
-        if (per_sm < 1) per_sm = 1;
-    }
+    int dev = 0, sms = 0, per_sm = 0;  // per device: a process may drive several GPUs
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_moments_i8<true>, MO_THREADS, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
     const int bps = (blocks_per_sm > 0 && blocks_per_sm < per_sm) ? blocks_per_sm : per_sm;
     const int64_t resident = (int64_t)sms * bps * MO_THREADS;
     const int64_t groups = (M + 15) / 16;
@@ -582,8 +577,8 @@ cudaError_t launch_finalize_i8(const int64_t *d_accum, int32_t M, double *d_sqrt
     return cudaGetLastError();
 }
 
-cudaError_t launch_finalize_f64(const double *d_accum, int32_t M, double *d_sqrt_dw, const FinalizeOut &o,
-                                cudaStream_t s, int *launches)
+cudaError_t launch_finalize_f64(const double *d_accum, int32_t M, const float *d_offset, double *d_sqrt_dw,
+                                const FinalizeOut &o, cudaStream_t s, int *launches)
 {
     const double *hw = d_accum;
     const double *sw = d_accum + 4096LL * M;
@@ -591,7 +586,7 @@ cudaError_t launch_finalize_f64(const double *d_accum, int32_t M, double *d_sqrt
     const double *sh = sw2 + M;
     const double *sh2 = sh + 4096;
     const double *cnt = sh2 + 4096;
-    k_sqrt_dw_f64<<<(M + 255) / 256, 256, 0, s>>>(sw, sw2, cnt, M, d_sqrt_dw);
+    k_sqrt_dw_f64<<<(M + 255) / 256, 256, 0, s>>>(sw, sw2, cnt, d_offset, M, d_sqrt_dw);
     k_finalize_f64<<<o.h1 - o.h0, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o);
     if (launches) (*launches) += 2;
     return cudaGetLastError();

@@ -3,9 +3,26 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 namespace cpa {
+
+// Opt-in dynamic shared memory beyond 48 KB is a per-device-context attribute of
+// a kernel: remember it per device ordinal (bit d of `done`), so that a process
+// driving several GPUs sets it on each; setting it twice is harmless, so a race
+// between host threads costs nothing but a repeated call.
+inline cudaError_t smem_attr_once(const void *fn, int bytes, std::atomic<unsigned long long> &done)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
+    if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
 
 // a3: Phase 1 model sums [P:75]; also adds n to the trace count word.  With a
 // 16 x 65536 uint32 scratch (d_hist) and n >= kHistMinTraces the byte-pair
@@ -107,7 +124,9 @@ struct FinalizeOut {
 };
 cudaError_t launch_finalize_i8(const int64_t *d_accum, int32_t M, double *d_sqrt_dw,
                                const FinalizeOut &o, cudaStream_t s, int *launches);
-cudaError_t launch_finalize_f64(const double *d_accum, int32_t M, double *d_sqrt_dw,
+// float path: d_offset = the context's per-sample offsets (the sums are centred
+// on them; the degenerate-column rule needs the raw second moment)
+cudaError_t launch_finalize_f64(const double *d_accum, int32_t M, const float *d_offset, double *d_sqrt_dw,
                                 const FinalizeOut &o, cudaStream_t s, int *launches);
 cudaError_t launch_phase4(const FinalizeOut &o, cudaStream_t s, int *launches);
 // Phase-3 merge of G shards' per-hypothesis maxima (stacked [G][4096]) into

@@ -776,13 +776,10 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *
     p.hist = d_hist;
     for (int b = 0; b < 16; b++) p.owners[b] = owners ? owners[b] : nullptr;
     p.clk = d_clk;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_xterm<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
-    cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(int), stream);
+    static std::atomic<unsigned long long> attr_set{0};
+    cudaError_t e = smem_attr_once((const void *)k_xterm<V>, SMEM_ALLOC, attr_set);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(d_counter, 0, sizeof(int), stream);
     if (e != cudaSuccess) return e;
     const int pairs = (p.units < num_sms / 2 ? p.units : num_sms / 2);
     k_xterm<V><<<2 * pairs, THREADS, SMEM_ALLOC, stream>>>(m0, m1, p);

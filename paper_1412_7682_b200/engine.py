@@ -102,14 +102,53 @@ class Engine:
         B.cpa_accumulate(self.ctx, traces, traces.stride(0), texts, traces.shape[0])
 
     def accumulate_host(self, traces: np.ndarray | torch.Tensor, texts: np.ndarray | torch.Tensor):
+        """Host (ideally pinned) buffers: the library stages them (cpa_accumulate_host).
+        The element type must be the context's: raw bytes are passed through."""
+        want = _TORCH_DTYPE[self.dtype]
+        if isinstance(traces, np.ndarray):
+            ok = traces.dtype == np.dtype(str(want).replace("torch.", ""))
+            row_ok = traces.ndim == 2 and traces.strides[1] == traces.itemsize
+            ld = traces.strides[0] // traces.itemsize if traces.ndim == 2 else 0
+        else:
+            ok = traces.dtype == want and traces.device.type == "cpu"
+            row_ok = traces.dim() == 2 and traces.stride(1) == 1
+            ld = traces.stride(0) if traces.dim() == 2 else 0
+        if not ok:
+            raise TypeError(f"traces dtype {traces.dtype} does not match the context's {want} (host buffer)")
+        if not row_ok or traces.shape[1] != self.M:
+            raise ValueError(f"traces must be [N][{self.M}] with unit column stride")
         n = traces.shape[0]
-        ld = traces.strides[0] // traces.itemsize if isinstance(traces, np.ndarray) else traces.stride(0)
+        tx_dtype = texts.dtype == (np.uint8 if isinstance(texts, np.ndarray) else torch.uint8)
+        tx_contig = texts.flags["C_CONTIGUOUS"] if isinstance(texts, np.ndarray) else texts.is_contiguous()
+        if not tx_dtype or tuple(texts.shape) != (n, 16) or not tx_contig:
+            raise ValueError("texts must be a contiguous uint8 [N][16] host buffer")
         B.cpa_accumulate_host(self.ctx, traces, ld, texts, n)
 
-    def allreduce(self, group=None):
+    # ---- float path: per-sample offsets (include/cpa.h cpa_set_offsets) ----
+    def set_offsets(self, offsets: torch.Tensor | None):
+        """CPA_F32: centre every sample on offsets[j] (device float32 [M]; None =
+        0).  Multi-GPU: every rank must use the SAME offsets, see
+        multigpu.share_offsets."""
+        if offsets is not None:
+            assert offsets.device == self.device and offsets.dtype == torch.float32
+            assert offsets.is_contiguous() and offsets.numel() == self.M
+        B.cpa_set_offsets(self.ctx, offsets)
+
+    def offsets(self) -> tuple[torch.Tensor, bool]:
+        """(the offsets in force [M] float32, whether they were set)."""
+        out = torch.empty(self.M, dtype=torch.float32, device=self.device)
+        ok = B.cpa_get_offsets(self.ctx, out)
+        self.sync()
+        return out, ok
+
+    def allreduce(self, group=None, check_offsets: bool = True):
         """Combine partial sums over ranks: one all-reduce(SUM) [a7].  Exact
-        for the int64 accumulator under any reduction order."""
-        from .multigpu import allreduce_accumulator
+        for the int64 accumulator under any reduction order.  Float contexts:
+        the ranks' sums must be centred on the same offsets (checked first
+        unless the caller already did, check_offsets=False)."""
+        from .multigpu import allreduce_accumulator, check_same_offsets
+        if self.dtype == B.CPA_F32 and check_offsets:
+            check_same_offsets(self, group)
         with torch.cuda.stream(self.stream):
             allreduce_accumulator(self.accum, group)
 

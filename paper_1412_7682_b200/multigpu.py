@@ -59,6 +59,60 @@ def allreduce_accumulator(acc, group=None):
     return acc
 
 
+# ---- float traces: one set of per-sample offsets for every rank ---------------
+# The CPA_F32 sums are of centred samples w - o_j (include/cpa.h cpa_set_offsets);
+# partial sums of different ranks add up to the sums of ONE data set only if
+# every rank centred on the same o_j.  The library's default (each context's own
+# first trace) differs per rank, so a float multi-GPU run shares rank 0's.
+
+def broadcast_offsets(first_trace, M: int, device, group=None, src: int = 0):
+    """Collective: rank `src` passes its first trace ([M] float32, any device),
+    the others anything (ignored); every rank returns the same [M] float32
+    tensor on `device`."""
+    import torch
+    import torch.distributed as dist
+    world, rank = _world(group)
+    buf = torch.empty(M, dtype=torch.float32, device=device)
+    if rank == src:
+        buf.copy_(first_trace.reshape(-1)[:M])
+    if world > 1:
+        dist.broadcast(buf, src=src, group=group)
+    return buf
+
+
+def share_offsets(engine, traces=None, group=None, src: int = 0):
+    """Set rank `src`'s first trace (traces[0], its shard's) as the offsets of
+    `engine` on every rank, before the first accumulate.  Returns them."""
+    t0 = traces[0] if traces is not None else None
+    o = broadcast_offsets(t0, engine.M, engine.device, group, src)
+    engine.set_offsets(o)
+    return o
+
+
+def check_same_offsets(engine, group=None):
+    """Raise unless every rank's float engine has its offsets set and equal."""
+    o, ok = engine.offsets()
+    assert_same_offsets(o, ok, group)
+
+
+def assert_same_offsets(o, ok: bool = True, group=None):
+    """Collective: raise on every rank unless all ranks' offsets `o` ([M]) are
+    equal and set (all-reduce of MIN/MAX of `o` and of the 'set' flag)."""
+    import torch
+    import torch.distributed as dist
+    world, _ = _world(group)
+    if world == 1:
+        return
+    lo, hi = o.clone(), o.clone()
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=o.device)
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    if int(flag.item()) == 0 or not torch.equal(lo, hi):
+        raise RuntimeError("float ranks centred their sums on different offsets: call "
+                           "multigpu.share_offsets(engine, traces) on every rank before the first accumulate")
+
+
 # ---- sharded Phase 3/4 (SURVEY §8e; include/cpa.h "sharded Phase 3/4") -------
 # The engine protocol used below (paper_1412_7682_b200.Engine implements it):
 #   .accum, .M, .maxima_buffers(G), .finalize_rows(h0, h1, mx, am, pk, want_rho),
@@ -163,6 +217,9 @@ def finalize_rows_sharded(engine, group=None, want_rho: bool = False) -> dict:
     the sums, Phase 3 on this rank's hypothesis rows, gather of the maxima,
     Phase 4.  Every rank returns the same key; rho (if wanted) covers only
     this rank's rows (`rows`)."""
+    from . import _binding as B
+    if getattr(engine, "dtype", None) == B.CPA_F32:
+        check_same_offsets(engine, group)
     h0, h1 = reduce_scatter_rows(engine.accum, engine.M, group)
     mx, am, pk = (t[0] for t in engine.maxima_buffers(1))
     rho = engine.finalize_rows(h0, h1, mx, am, pk, want_rho)

@@ -97,7 +97,21 @@ class StreamingAttack:
                                         else (None, None))
         self._bar = torch.zeros(1, dtype=torch.int32, device=self.eng.device)
 
+    def share_offsets(self, traces=None, src: int = 0):
+        """Float traces, multi-GPU (collective, before the first add): centre
+        every rank's sums on rank `src`'s first trace (multigpu.share_offsets);
+        the checkpoint view finalizes with the same offsets."""
+        from . import multigpu as MG
+        o = MG.share_offsets(self.eng, traces, self.group, src)
+        if self.view is not None:
+            self.view.set_offsets(o)
+        self._offsets_shared = True
+
     def add(self, traces, texts):
+        from . import _binding as B
+        if self.view is not None and self.eng.dtype == B.CPA_F32 and not getattr(self, "_offsets_shared", False):
+            raise RuntimeError("float multi-GPU stream: call share_offsets() on every rank before the first add "
+                               "(each rank's sums must be centred on the same offsets)")
         self.eng.accumulate(traces, texts)
         self.n_local += traces.shape[0]
 

@@ -68,3 +68,17 @@ def test_bench_sample_shards_two_ranks_one_gpu_gloo(config, port):
              env={"CPA_BENCH_SAME_DEVICE": "1", "CPA_BENCH_BACKEND": "gloo"})
     assert d["n_gpus"] == 2 and d["key_recovered"] is True
     assert d["config"]["parallelism"].startswith("sample-shard x2")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("combine,port", [("rows", 29541), ("allreduce", 29542)])
+def test_bench_float_two_ranks_one_gpu_gloo(combine, port):
+    """north_star config 3 at 2 GPUs (C3, float traces): rank 0's offsets are
+    shared before the first accumulate (multigpu.share_offsets), the combined
+    sums recover the key; the line says float."""
+    d = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+              "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--config", "C3",
+              "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--combine", combine],
+             env={"CPA_BENCH_SAME_DEVICE": "1", "CPA_BENCH_BACKEND": "gloo"})
+    assert d["n_gpus"] == 2 and d["key_recovered"] is True
+    assert combine in d["config"]["parallelism"] and "float32" in d["config"]["workload"]

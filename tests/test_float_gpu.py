@@ -156,3 +156,72 @@ def test_float_range_repair_in_a_later_chunk(P):
     ch = eng.finalize(want_rho=True)
     eng.close()
     assert np.max(np.abs(ch["rho"].cpu().numpy() - out["rho"].cpu().numpy())) <= TOL
+
+
+def _oracle_rho_f32(texts, W):
+    shw, sw, sw2 = O.sums_f32(O.HD_LAST, texts, W)
+    sh, sh2 = O.model_sums(O.HD_LAST, texts)
+    return O.rho_eq1_f64_grid(W.shape[0], shw, sh, sh2, sw, sw2)
+
+
+@pytest.mark.parametrize("parts", [2, 3])
+def test_float_contexts_over_trace_shards_sum_exactly(P, parts):
+    """north_star config 3 at 2 GPUs [P:201-217, P:230], emulated on one GPU:
+    `parts` contexts accumulate disjoint trace ranges of C3-style float data,
+    all centred on ONE set of offsets (trace 0, what multigpu.share_offsets
+    broadcasts), their fp64 accumulators are summed (what the all-reduce /
+    reduce-scatter does) and Eq. (1) runs on the sum: every cell within 1e-4
+    of the oracle.  The library's per-context default offsets differ."""
+    from paper_1412_7682_b200 import multigpu as MG
+    w = S.CONFIGS["C3"].replace(n=6000, m=200, a=0.02)
+    texts, W = S.dataset(w)
+    dW = torch.from_numpy(W).cuda()
+    dT = torch.from_numpy(texts).cuda()
+    o = dW[0].clone()
+    engs = [P.Engine(w.m, P.CPA_F32, P.CPA_HD_LAST, 0) for _ in range(parts)]
+    for r, e in enumerate(engs):
+        i0, i1 = MG.shard_range(w.n, r, parts)
+        e.set_offsets(o)
+        e.accumulate(dW[i0:i1], dT[i0:i1])
+        e.sync()
+    offs = [e.offsets() for e in engs]
+    assert all(ok and torch.equal(x, o) for x, ok in offs)
+    for e in engs[1:]:
+        engs[0].accum += e.accum
+    out = engs[0].finalize(want_rho=True)
+    ref = _oracle_rho_f32(texts, W)
+    err = float(np.max(np.abs(out["rho"].cpu().numpy() - ref)))
+    print(f"{parts} float shards: max |drho| = {err:.3g}")
+    assert err <= TOL
+    assert out["master_key"] == w.key
+    # the library default: each context's own first trace -> different offsets
+    d = [P.Engine(w.m, P.CPA_F32, P.CPA_HD_LAST, 0) for _ in range(2)]
+    for r, e in enumerate(d):
+        i0, i1 = MG.shard_range(w.n, r, 2)
+        e.accumulate(dW[i0:i1], dT[i0:i1])
+    (a, oka), (b, okb) = d[0].offsets(), d[1].offsets()
+    assert oka and okb and not torch.equal(a, b)
+    for e in engs + d:
+        e.close()
+
+
+def test_float_degenerate_columns_match_oracle(P):
+    """SPEC's degenerate-variance rule [S:293] on the RAW second moment: a DC
+    level far above the noise gives rho = 0 on the GPU exactly where the oracle
+    gives 0 (tests/test_oracle_rho.degenerate_columns pins the oracle), the
+    other columns within the bar -- with the default offsets (the sums are
+    centred, the rule rebuilds the raw moment) and with zero offsets."""
+    from tests.test_oracle_rho import degenerate_columns
+    W, flags = degenerate_columns()
+    rng = np.random.default_rng(32)
+    texts = rng.integers(0, 256, (W.shape[0], 16), dtype=np.uint8)
+    ref = _oracle_rho_f32(texts, W)
+    for offsets in ("default", None):
+        out, _ = gpu_rho(P, texts, W, offsets=offsets)
+        rho = out["rho"].cpu().numpy()
+        for j, deg in enumerate(flags):
+            if deg:
+                assert np.all(rho[:, j] == 0.0) and np.all(ref[:, j] == 0.0), (offsets, j)
+            else:
+                assert np.max(np.abs(rho[:, j] - ref[:, j])) <= TOL, (offsets, j)
+                assert np.any(rho[:, j] != 0.0)

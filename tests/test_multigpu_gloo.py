@@ -275,3 +275,80 @@ def test_fused_combine_consensus_falls_back_on_every_rank():
     assert none0 and none1                       # both fall back
     assert last0 is None and closed0 == 1        # rank 0 undid its routing
     assert "peer atomics" in why1 and why0       # the reason is reported on both
+
+
+def _float_worker(rank, world, port, shared, ret):
+    """Float traces (a6) on a trace shard: the sums are of the CENTRED samples
+    fl32(w - o_j), as the library computes them (k_split_f32), packed in the
+    fp64 accumulator layout and combined by the production reduce-scatter.
+    shared=True: o = rank 0's first trace, broadcast (multigpu.broadcast_offsets,
+    what bench.py / share_offsets do); False: each rank's own first trace (the
+    library default, wrong across ranks)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import oracle as O
+    from synth import synth as S
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = S.CONFIGS["C3"].replace(n=3000, m=24, a=0.02)
+    i0, i1 = MG.shard_range(w.n, rank, world)
+    texts, lv = S.texts(w, i0, i1 - i0)
+    W = S.traces(w, lv, i0)
+    if shared:
+        o = MG.broadcast_offsets(torch.from_numpy(W[0]), w.m, "cpu").numpy()
+        MG.assert_same_offsets(torch.from_numpy(o))
+    else:
+        o = W[0].copy()
+        try:
+            MG.assert_same_offsets(torch.from_numpy(o))
+            raised = False
+        except RuntimeError:
+            raised = True
+        assert raised, "differing offsets must be rejected"
+    C = (W - o[None, :]).astype(np.float32)        # fp32 subtraction, as on the GPU
+    sh, sh2 = O.model_sums(O.HD_LAST, texts)
+    shw, sw, sw2 = O.sums_f32(O.HD_LAST, texts, C)
+    acc = MG.pack(w.m, dict(sum_hw=shw, sum_w=sw, sum_w2=sw2, sum_h=sh, sum_h2=sh2, n=[i1 - i0]),
+                  torch.zeros(1, dtype=torch.float64))
+    h0, h1 = MG.reduce_scatter_rows(acc, w.m)
+    ret.put((rank, h0, h1, acc.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shared", [True, False])
+def test_gloo_float_combine_needs_shared_offsets(shared):
+    """World 2, float traces [P:201-217, P:230]: with one set of offsets the
+    combined rows give rho within 1e-9 of the single-process oracle on the raw
+    traces; with per-rank offsets (the library default) they do not (>1e-3)."""
+    from oracle import oracle as O
+    from synth import synth as S
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_float_worker, args=(r, world, port, shared, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = _collect(q, procs, world)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    w = S.CONFIGS["C3"].replace(n=3000, m=24, a=0.02)
+    texts, W = S.dataset(w)
+    shw, sw, sw2 = O.sums_f32(O.HD_LAST, texts, W)
+    sh, sh2 = O.model_sums(O.HD_LAST, texts)
+    ref = O.rho_eq1_f64_grid(w.n, shw, sh, sh2, sw, sw2)
+    err = 0.0
+    for rank, h0, h1, acc in res:
+        got = MG.unpack(w.m, torch.from_numpy(acc))
+        assert int(got["n"][0]) == w.n
+        rho = O.rho_eq1_f64_grid(w.n, got["sum_hw"].numpy(), got["sum_h"].numpy().astype(np.int64),
+                                 got["sum_h2"].numpy().astype(np.int64), got["sum_w"].numpy(),
+                                 got["sum_w2"].numpy())
+        err = max(err, float(np.max(np.abs(rho[h0:h1] - ref[h0:h1]))))
+    if shared:
+        assert err <= 1e-9, err
+    else:
+        assert err > 1e-3, err

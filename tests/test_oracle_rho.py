@@ -130,3 +130,53 @@ def test_float_oracle_pins():
     ri = O.rho_two_pass_i8(O.HD_LAST, t, Wi)
     rf = O.rho_two_pass_f32(O.HD_LAST, t, Wi.astype(np.float32))
     assert np.array_equal(ri, rf)
+
+
+def degenerate_columns(n=400, seed=31):
+    """Float columns on both sides of SPEC's degenerate-variance rule [S:293]
+    (rho = 0 iff n*sum w^2 - (sum w)^2 <= 1e-12 * n * sum w^2, RAW sums), each
+    >= 4x away from the boundary: a DC level far above the noise makes a column
+    degenerate although its variance is not 0.  Returns (W [n][6] f32, expected
+    degenerate flags decided in exact rational arithmetic on the f32 values)."""
+    from fractions import Fraction
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal((n, 6))
+    dc = np.array([1000.0, 1000.0, 1.0, 1.0, 0.0, 3.0])
+    sd = np.array([0.0, 0.05, 3e-7, 4e-6, 1.0, 1e-3])
+    W = (dc + sd * z).astype(np.float32)
+    W[::7, 0] = np.nextafter(np.float32(1000.0), np.float32(2000.0))  # var > 0, 1 ulp steps
+    flags = []
+    for j in range(6):
+        v = [Fraction(float(x)) for x in W[:, j]]
+        s1, s2 = sum(v), sum(x * x for x in v)
+        dw = n * s2 - s1 * s1
+        ratio = dw / (n * s2)
+        eps = Fraction(1, 10**12)
+        assert ratio <= eps / 4 or ratio >= 4 * eps, (j, float(ratio))
+        flags.append(ratio <= eps)
+    assert flags == [True, False, True, False, False, False]
+    return W, flags
+
+
+def test_float_degenerate_rule_pinned():
+    """The eps branch of both float oracle functions [S:293]: columns whose
+    variance is below 1e-12 of their raw second moment give rho = 0 exactly,
+    the others the textbook Pearson value (numpy.corrcoef)."""
+    W, flags = degenerate_columns()
+    rng = np.random.default_rng(32)
+    t = rng.integers(0, 256, (W.shape[0], 16), dtype=np.uint8)
+    H = h_matrix(O.HD_LAST, t).astype(np.float64)
+    shw, sw, sw2 = O.sums_f32(O.HD_LAST, t, W)
+    sh, sh2 = O.model_sums(O.HD_LAST, t)
+    rb = O.rho_eq1_f64_grid(W.shape[0], shw, sh, sh2, sw, sw2)
+    hyps = np.array([0, 77, 1000, 4095], np.int32)
+    ra = O.rho_two_pass_f32(O.HD_LAST, t, W, hyps=hyps)
+    for j, deg in enumerate(flags):
+        if deg:
+            assert np.all(rb[:, j] == 0.0) and np.all(ra[:, j] == 0.0), j
+        else:
+            for a, h in enumerate(hyps):
+                ref = np.corrcoef(H[:, h], W[:, j].astype(np.float64))[0, 1]
+                assert abs(ra[a, j] - ref) <= 1e-9, (j, h)
+                assert abs(rb[h, j] - ref) <= 1e-4, (j, h)
+                assert ref != 0.0

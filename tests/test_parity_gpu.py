@@ -241,6 +241,29 @@ def test_errors(P):
         P.cpa_accumulate(eng.ctx, W, 99, T, 10)           # ld < M
     with pytest.raises(P.CpaError, match="TOO_FEW"):
         eng.finalize()                                     # N = 0 < 2
+    eng.accumulate(W[:1], T[:1])
+    rk = torch.empty(4096, dtype=torch.int32, device="cuda")
+    with pytest.raises(P.CpaError, match="TOO_FEW"):
+        eng.finalize_async(rk)                             # N = 1, checked without blocking
+    eng.close()
+    # the exact-int64 bound of Eq. (1) on the running total (not only per call)
+    eng = P.Engine(16, P.CPA_S8, P.CPA_HD_LAST, 0)
+    n = 1 << 23
+    W = torch.zeros((n, 16), dtype=torch.int8, device="cuda")
+    T = torch.zeros((n, 16), dtype=torch.uint8, device="cuda")
+    eng.accumulate(W[: n // 2], T[: n // 2])
+    eng.accumulate(W[n // 2:], T[n // 2:])                # exactly 2^23: allowed
+    with pytest.raises(P.CpaError, match="OVERFLOW"):
+        eng.accumulate(W[:1], T[:1])
+    eng.reset()
+    eng.accumulate(W[:1], T[:1])                          # the reset restarts the count
+    eng.close()
+    # host buffers: the element type must match the context's
+    eng = P.Engine(100, P.CPA_S8, P.CPA_HD_LAST, 0)
+    with pytest.raises(TypeError):
+        eng.accumulate_host(np.zeros((10, 100), np.float64), np.zeros((10, 16), np.uint8))
+    with pytest.raises(ValueError):
+        eng.accumulate_host(np.zeros((10, 100), np.int8), np.zeros((10, 15), np.uint8))
     eng.close()
 
 

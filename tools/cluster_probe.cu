@@ -1,7 +1,7 @@
 // probe: shared-address encodings in a 2-CTA cluster (debug aid)
 #include <cstdio>
 #include <cstdint>
-#include "../paper_1412_7682_b200/csrc/ptx.cuh"
+#include "ptx_tools.cuh"
 using namespace cpa;
 __global__ void __cluster_dims__(2, 1, 1) k(unsigned *out)
 {

@@ -8,7 +8,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#include "../paper_1412_7682_b200/csrc/ptx.cuh"
+#include "ptx_tools.cuh"
 
 using namespace cpa;
 
