@@ -33,8 +33,31 @@ def test_c4_fullsize_sampled_parity():
     assert torch.equal(eng.sum_h.view(16, 256).sum(1), torch.full((16,), 1024 * w.n, device="cuda", dtype=torch.int64))
     assert torch.equal(eng.sum_h2.view(16, 256).sum(1), torch.full((16,), 4608 * w.n, device="cuda", dtype=torch.int64))
 
-    # sampled outputs against the oracle: 6 columns x 48 hypotheses, all traces
-    cols = np.array(sorted([0, w.leak_positions()[0], w.leak_positions()[7], 2047, 4097, w.m - 1]), np.int32)
+    # sum W, sum W^2 of EVERY column against the oracle (host generator, column
+    # blocks over the host's cores): with them the closed form above pins
+    # sum_k sum_hw[b][k][j] for every (b, j) independently of the kernel's fused a4,
+    # so a lost (trace chunk, tile group) unit anywhere fails
+    import concurrent.futures as cf
+    import os
+
+    def block_sums(j0):
+        cb = np.arange(j0, min(w.m, j0 + 50), dtype=np.int32)
+        return j0, O.trace_sums_i8(S.traces(w, lv, 0, cb))
+    ref_w = np.zeros(w.m, np.int64)
+    ref_w2 = np.zeros(w.m, np.int64)
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(32, os.cpu_count() or 1))) as ex:
+        for j0, (a1, a2) in ex.map(block_sums, range(0, w.m, 50)):
+            ref_w[j0:j0 + len(a1)], ref_w2[j0:j0 + len(a2)] = a1, a2
+    assert np.array_equal(eng.sum_w.cpu().numpy(), ref_w)
+    assert np.array_equal(eng.sum_w2.cpu().numpy(), ref_w2)
+
+    # sampled outputs against the oracle: 48 hypotheses (the true key of every
+    # byte + 32 random) x a column in every 512-sample tile group of the
+    # cross-term schedule, the planted samples of bytes 0 and 7, the last column
+    groups = [g * 512 + (g * 97) % 512 for g in range((w.m + 511) // 512)]
+    cols = np.array(sorted(set([c for c in groups if c < w.m] + [w.leak_positions()[0], w.leak_positions()[7],
+                                                                  w.m - 1])), np.int32)
+    assert set(int(c) // 512 for c in cols) == set(range((w.m + 511) // 512))
     rng = np.random.default_rng(0)
     hyps = np.array(sorted(set([256 * b + rk[b] for b in range(16)]) | set(rng.integers(0, 4096, 32).tolist())),
                     np.int32)
