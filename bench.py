@@ -29,8 +29,6 @@ sys.path.insert(0, ROOT)
 
 PEAK_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 INT8_PER_BF16 = 4.5 / 2.25  # nominal dense int8 : bf16 ratio (B200_PROFILING.md)
-CPU_SAMPLE_TRACES = 131072
-CPU_SAMPLE_COLS = 4
 MODEL_NAMES = ("HD last-round", "HW last-round", "HW first-round")
 # tcgen05 MAC/clk/SM (tools/pair_bench: kind::i8 8192, kind::f16 4096, both measured 100% reachable)
 MMA_MACS_PER_CLK_SM = {False: 8192, True: 4096}
@@ -57,8 +55,10 @@ def parse():
                          "an all-reduce of the small fields, row-sharded finalize, gather of the "
                          "maxima; 'rows' = the same with an NCCL reduce-scatter of the rows after "
                          "the kernel; 'allreduce' = one all-reduce of the whole accumulator, "
-                         "finalize on every rank; 'auto' = fused when possible (int8, G | 16), "
-                         "else rows")
+                         "finalize on every rank; 'auto' = rows (north_star's NCCL combine); the "
+                         "others are timed after it in the same run (combine_ms_per_step)")
+    ap.add_argument("--no-combine-sweep", action="store_true",
+                    help="N>1 trace shards: skip timing the other combines after the headline one")
     ap.add_argument("--shard", choices=["auto", "traces", "samples"], default="auto",
                     help="N>1: split the traces (partial sums combined per --combine) or the sample "
                          "columns (every rank all traces of M/G columns; only the per-hypothesis maxima "
@@ -86,6 +86,37 @@ def metric_name(w) -> str:
     configs state their own N."""
     at = "1.5M" if w.n == 1_500_000 else f"{w.n}"
     return f"hypothesis x sample correlations/s at {at} traces"
+
+
+DATASHEET_TOPS = {False: 4500.0, True: 2250.0}   # B200 dense int8 / fp16-bf16 (B200_PROFILING.md)
+
+
+def cublaslt_peak_tops(dev, int8: bool = True, n: int = 8192, reps: int = 5) -> float:
+    """The library GEMM on this GPU, measured in this run: cuBLASLt int8
+    (torch._int_mm, int32 out) or bf16 (torch.matmul) at n^3, best of `reps`
+    after a warm-up (2 n^3 ops each).  A reference point for the roofline of
+    the cross term, not part of the path."""
+    import torch
+    if int8:
+        a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=dev)
+        b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=dev).t()
+        fn = lambda: torch._int_mm(a, b)  # noqa: E731
+    else:
+        a = torch.randn(n, n, dtype=torch.bfloat16, device=dev)
+        fn = lambda: torch.matmul(a, a)  # noqa: E731
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = float("inf")
+    for _ in range(reps):
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
 
 
 def load_peaks():
@@ -148,6 +179,27 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- cpu baseline ----
+# SURVEY 8d's CPU protocol: the oracle as it stands, single-threaded, on the 16
+# leak samples + 48 seeded random columns of the workload (all columns for the
+# small configs C1/C2), on the first CPU_SAMPLE_TRACES traces (bounded: ~5 s
+# per run on a Xeon core).  Its cost is t(c) = a + b c per run (a: the per-trace
+# Phase-1 / selection work, shared by all columns; b: per column), so it is also
+# timed on the 16 leak columns alone, and the time of the FULL workload (all M
+# columns, all N traces) is extrapolated as (a + b M) N / n -- stated as such.
+CPU_SAMPLE_TRACES = 16384
+CPU_COLS_RANDOM = 48
+CPU_FULL_MAX_CELLS = 2000 * 5000   # C1, C2: the oracle runs on the whole workload
+
+
+def oracle_columns(w, n_random=CPU_COLS_RANDOM, seed=1412):
+    """The 16 leak samples + n_random seeded distinct other columns (sorted)."""
+    import numpy as np
+    lp = sorted(set(w.leak_positions()))
+    rest = np.setdiff1d(np.arange(w.m), lp)
+    rnd = np.random.default_rng(seed).choice(rest, min(n_random, len(rest)), replace=False)
+    return np.array(sorted(lp + rnd.tolist()), np.int32), np.array(lp, np.int32)
+
+
 def oracle_attack(O, texts, Ws, model=0):
     """The oracle's Phases 1-4 on the sampled columns (int or float traces)."""
     import numpy as np
@@ -157,27 +209,71 @@ def oracle_attack(O, texts, Ws, model=0):
         rho = O.rho_eq1_f64_grid(Ws.shape[0], shw, sh, sh2, sw, sw2)
         mx, am, pk = O.phase3(rho)
         best, rank = O.phase4(mx)
-        return {"best": best}
+        return {"best": best, "argmax": am}
     return O.attack_i8(model, texts, Ws, np.arange(Ws.shape[1], dtype=np.int32))
 
 
-def cpu_baseline(w, sample_traces=CPU_SAMPLE_TRACES, ncols=CPU_SAMPLE_COLS):
-    """The oracle as it stands (single-threaded C, oracle/oracle.c), timed on a
-    bounded sample of the same workload; rate scaled linearly to N = w.n."""
-    import numpy as np
-    from oracle import oracle as O
-    from synth import synth as S
-    n = min(sample_traces, w.n)
-    texts, lv = S.texts(w, 0, n)
-    cols = np.array(sorted(w.leak_positions()[:2] + [w.m // 5, (3 * w.m) // 5]), np.int32)[:ncols]
-    Ws = S.traces(w, lv, 0, cols)
-    t0 = time.perf_counter()
-    a = oracle_attack(O, texts, Ws, w.leak_model)
-    t = time.perf_counter() - t0
-    t_full = t * (w.n / n)
-    return {"value": 4096 * len(cols) / t_full, "unit": "correlations/s", "cores": 1, "kind": "oracle",
-            "sample": f"{len(cols)} sample columns x first {n} traces of {w.name}; time x{w.n / n:.2f} to N={w.n}",
-            "seconds": t, "key_bytes_ranked_first": int(sum(a["best"] == O.expand_key(w.key)[10]))}
+class OracleSample:
+    """A bounded sample of workload w for the oracle: texts + the chosen
+    columns of the first n traces (host generator), and the timing model."""
+
+    def __init__(self, w, n_traces=CPU_SAMPLE_TRACES):
+        import numpy as np
+        from synth import synth as S
+        self.w = w
+        self.full = w.n * w.m <= CPU_FULL_MAX_CELLS
+        self.n = w.n if self.full else min(n_traces, w.n)
+        self.texts, lv = S.texts(w, 0, self.n)
+        if self.full:
+            self.cols, self.leak = np.arange(w.m, dtype=np.int32), np.array(w.leak_positions(), np.int32)
+        else:
+            self.cols, self.leak = oracle_columns(w)
+        self.W = S.traces(w, lv, 0, self.cols)
+        lidx = np.searchsorted(self.cols, self.leak)
+        self.W16 = np.ascontiguousarray(self.W[:, lidx])
+        self.describe = (f"all {w.m} columns x all {w.n} traces of {w.name} (measured, no extrapolation)"
+                         if self.full else
+                         f"{len(self.cols)} columns (the 16 leak samples + {len(self.cols) - 16} seeded random) x "
+                         f"first {self.n} traces of {w.name}; also timed on the 16 leak columns alone to split "
+                         f"the per-trace cost a from the per-column cost b; full step (all {w.m} columns, "
+                         f"{w.n} traces) extrapolated as (a + b*{w.m}) x {w.n / self.n:.2f}")
+
+    def run(self, leak_only=False):
+        """(seconds, key bytes ranked first) of one oracle pass over the sample."""
+        from oracle import oracle as O
+        W = self.W16 if leak_only else self.W
+        t0 = time.perf_counter()
+        a = oracle_attack(O, self.texts, W, self.w.leak_model)
+        t = time.perf_counter() - t0
+        return t, int(sum(a["best"] == O.expand_key(self.w.key)[10]))
+
+    def full_step_seconds(self, t_all, t_leak):
+        """Extrapolated seconds of one oracle pass over the whole workload."""
+        if self.full:
+            return t_all
+        c = len(self.cols)
+        b = max(0.0, (t_all - t_leak) / (c - 16))
+        a = max(0.0, t_all - b * c)
+        return (a + b * self.w.m) * (self.w.n / self.n)
+
+
+def cpu_baseline(w, repeats=None):
+    """The oracle as it stands (single-threaded C, oracle/oracle.c) on the
+    bounded sample; rate = 4096 M / (extrapolated full-step time)."""
+    smp = OracleSample(w)
+    reps = repeats or (3 if smp.full and w.n * w.m <= 500 * 500 else 1)
+    ts, ok = [], 0
+    for _ in range(reps):
+        t, ok = smp.run()
+        ts.append(t)
+    t_all = statistics.median(ts)
+    t_leak = t_all if smp.full else smp.run(leak_only=True)[0]
+    t_full = smp.full_step_seconds(t_all, t_leak)
+    return {"value": 4096 * w.m / t_full, "unit": "correlations/s", "cores": 1, "kind": "oracle",
+            "sample": smp.describe, "sample_columns": len(smp.cols), "sample_traces": smp.n,
+            "seconds_sample": t_all, "seconds_leak_columns": t_leak, "repeats": reps,
+            "full_step_seconds": t_full, "extrapolated": not smp.full, "key_bytes_ranked_first": ok,
+            "rate_on_sample_columns": 4096 * len(smp.cols) / (t_all * w.n / smp.n)}
 
 
 def host_cpu_info():
@@ -196,85 +292,90 @@ def host_cpu_info():
     return info
 
 
-def cpu_baseline_all_cores(w, sample_traces=65536, cols_per_thread=2):
+def cpu_baseline_all_cores(w):
     """SURVEY 8d's all-cores CPU baseline (the paper's multi-threaded server
-    comparison [P:164]): the oracle's own functions, Phase 1 once, then its
-    Phase 2 loops (trace and cross sums, single-threaded C that releases the
-    GIL) over one column block per host thread, then Phases 3-4 over all
-    columns.  No other change to the oracle."""
+    comparison [P:164]): the oracle's own Phase 1-2 functions (single-threaded
+    C that releases the GIL) over one contiguous block of the sample's traces
+    per host thread -- every thread does a whole pass over its traces, like the
+    serial oracle -- the exact partial sums added, then Phases 3-4.  Same
+    sample and the same full-step extrapolation as cpu_baseline."""
     import concurrent.futures as cf
     import numpy as np
     from oracle import oracle as O
-    from synth import synth as S
+    smp = OracleSample(w)
     threads = max(1, min(len(os.sched_getaffinity(0)), 128))
-    n = min(sample_traces, w.n)
-    texts, lv = S.texts(w, 0, n)
-    lp = list(w.leak_positions())
-    extra = np.linspace(0, w.m - 1, threads * cols_per_thread, dtype=np.int64).tolist()
-    cols = np.array(sorted(set(lp + extra))[:threads * cols_per_thread], np.int32)
-    Ws = S.traces(w, lv, 0, cols)
-    is_f32 = Ws.dtype == np.float32
-    blocks = [np.arange(i, len(cols), threads) for i in range(threads)]
-    blocks = [c for c in blocks if len(c)]
-    Wb = [np.ascontiguousarray(Ws[:, c]) for c in blocks]
+    is_f32 = smp.W.dtype == np.float32
+    model = w.leak_model
 
-    def phase2(Wk):
-        if is_f32:
-            return O.sums_f32(w.leak_model, texts, Wk)
-        sw, sw2 = O.trace_sums_i8(Wk)
-        return O.cross_sums_i8(w.leak_model, texts, Wk), sw, sw2
+    def one_pass(W):
+        bl = [(smp.n * t // threads, smp.n * (t + 1) // threads) for t in range(threads)]
+        bl = [(i0, i1) for i0, i1 in bl if i1 > i0]
 
-    t0 = time.perf_counter()
-    sh, sh2 = O.model_sums(w.leak_model, texts)
-    with cf.ThreadPoolExecutor(max_workers=len(Wb)) as ex:
-        parts = list(ex.map(phase2, Wb))
-    shw = np.zeros((4096, len(cols)), parts[0][0].dtype)
-    sw = np.zeros(len(cols), parts[0][1].dtype)
-    sw2 = np.zeros(len(cols), parts[0][2].dtype)
-    for c, (a, b1, b2) in zip(blocks, parts):
-        shw[:, c], sw[c], sw2[c] = a, b1, b2
-    rho = (O.rho_eq1_f64_grid if is_f32 else O.rho_eq1_grid)(n, shw, sh, sh2, sw, sw2)
-    mx, _, _ = O.phase3(rho)
-    best, _ = O.phase4(mx)
-    t = time.perf_counter() - t0
-    t_full = t * (w.n / n)
-    return {"value": 4096 * len(cols) / t_full, "unit": "correlations/s", "cores": len(Wb),
-            "kind": "oracle, Phase 2 over one column block per host thread",
-            "sample": f"{len(cols)} sample columns x first {n} traces of {w.name}; time x{w.n / n:.2f} to N={w.n}",
-            "seconds": t, "host": host_cpu_info(),
-            "key_bytes_ranked_first": int(sum(np.asarray(best) == O.expand_key(w.key)[10]))}
+        def phase12(r):
+            i0, i1 = r
+            tx, Wb = smp.texts[i0:i1], np.ascontiguousarray(W[i0:i1])
+            sh, sh2 = O.model_sums(model, tx)
+            if is_f32:
+                shw, sw, sw2 = O.sums_f32(model, tx, Wb)
+            else:
+                sw, sw2 = O.trace_sums_i8(Wb)
+                shw = O.cross_sums_i8(model, tx, Wb)
+            return sh, sh2, shw, sw, sw2
+
+        t0 = time.perf_counter()
+        with cf.ThreadPoolExecutor(max_workers=len(bl)) as ex:
+            parts = list(ex.map(phase12, bl))
+        sh, sh2, shw, sw, sw2 = (sum(p[k] for p in parts) for k in range(5))
+        rho = (O.rho_eq1_f64_grid if is_f32 else O.rho_eq1_grid)(smp.n, shw, sh, sh2, sw, sw2)
+        mx, _, _ = O.phase3(rho)
+        best, _ = O.phase4(mx)
+        return time.perf_counter() - t0, int(sum(np.asarray(best) == O.expand_key(w.key)[10]))
+
+    t_all, ok = one_pass(smp.W)
+    t_leak = t_all if smp.full else one_pass(smp.W16)[0]
+    t_full = smp.full_step_seconds(t_all, t_leak)
+    return {"value": 4096 * w.m / t_full, "unit": "correlations/s", "cores": threads,
+            "kind": "oracle, Phases 1-2 over one trace block per host thread (exact partial sums added)",
+            "sample": smp.describe, "seconds_sample": t_all, "seconds_leak_columns": t_leak,
+            "full_step_seconds": t_full, "extrapolated": not smp.full, "host": host_cpu_info(),
+            "key_bytes_ranked_first": ok}
 
 
 def run_reference(args, w):
-    """--impl reference: the oracle on the host cores, one bounded sample of the
-    workload per step."""
+    """--impl reference: the oracle on the host cores (single thread), one
+    bounded sample of the workload per step (OracleSample).  ms_per_step is the
+    MEASURED time of the sample step; value is the metric at the workload's
+    full size, from the extrapolated full-step time (the 16-leak-column pass
+    that splits the cost is timed once, with the warm-up)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import numpy as np
-    from oracle import oracle as O
-    from synth import synth as S
-    n = min(65536, w.n)
-    texts, lv = S.texts(w, 0, n)
-    cols = np.array(sorted(w.leak_positions()[:2] + [w.m // 5, (3 * w.m) // 5]), np.int32)
-    Ws = S.traces(w, lv, 0, cols)
+    smp = OracleSample(w)
+    t_leak = None
     ts = []
+    ok = 0
     for s in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        oracle_attack(O, texts, Ws, w.leak_model)
-        dt = time.perf_counter() - t0
+        t, ok = smp.run()
         if s >= args.warmup:
-            ts.append(dt * (w.n / n))
-    t = sum(ts) / len(ts)
-    val = 4096 * len(cols) / t
-    sample = f"{len(cols)} sample columns x first {n} traces of {w.name}; time x{w.n / n:.2f} to N={w.n}"
+            ts.append(t)
+        elif s == 0 and not smp.full:
+            t_leak = smp.run(leak_only=True)[0]
+    t = statistics.mean(ts)
+    t_full = smp.full_step_seconds(t, t_leak if t_leak is not None else t)
+    val = 4096 * w.m / t_full
     line = {"metric": metric_name(w), "impl": "reference", "value": val,
             "unit": "correlations/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "int64", "data": "synthetic",
-            "config": {"workload": f"{w.name}: {w.n} traces x {w.m} samples int8, {MODEL_NAMES[w.leak_model]} model",
+            "dtype": "f64" if w.dtype == 2 else "int64", "data": "synthetic",
+            "config": {"workload": f"{w.name}: {w.n} traces x {w.m} samples "
+                                   f"{'float32' if w.dtype == 2 else 'int8'}, {MODEL_NAMES[w.leak_model]} model",
                        "n_traces": w.n, "n_samples": w.m},
-            "cpu_baseline": {"value": val, "unit": "correlations/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "step": f"one oracle pass (Phases 1-4) over the sample: {smp.describe}",
+            "extrapolation": {"full_step_ms": t_full * 1e3, "sample_step_ms": t * 1e3,
+                              "leak_columns_ms": (t_leak or t) * 1e3, "extrapolated": not smp.full},
+            "key_bytes_ranked_first_on_sample": ok,
+            "cpu_baseline": {"value": val, "unit": "correlations/s", "cores": 1, "kind": "oracle",
+                             "sample": smp.describe},
             "e2e": {"value": val, "unit": "correlations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -351,11 +452,31 @@ def main():
         MG.share_offsets(eng, dWv if rank == 0 else None)
     combine = ("columns" if shard == "samples" else args.combine) if world > 1 else "none"
     fused_note = None
-    if combine == "auto":
-        combine = "fused" if (not is_f32 and not class_sums and 16 % world == 0) else "rows"
+    if combine == "auto":   # north_star's NCCL combine: reduce-scatter of the rows (+ small-field all-reduce)
+        combine = "rows"
     owners = None
-    if combine == "fused":   # map the peers' accumulators (CUDA IPC), route the rows to their owners
-        owners, why = MG.FusedOwners.try_create(eng)
+    fused_ok = not is_f32 and not class_sums and 16 % world == 0
+
+    def use_owners(on: bool):
+        """Map the peers' accumulators (CUDA IPC) and route the rows to their
+        owners (on), or unmap (off).  Collective.  Returns why not, or None."""
+        nonlocal owners
+        if on and owners is None:
+            owners, why = MG.FusedOwners.try_create(eng)
+            return why if owners is None else None
+        if not on and owners is not None:
+            barrier()
+            owners.close()
+            owners = None
+        return None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    if combine == "fused":
+        why = use_owners(True) if fused_ok else "float or class-sum path, or G does not divide 16"
         if owners is None:      # no peer mapping on this box (every rank agrees): NCCL reduce-scatter
             fused_note, combine = f"fused combine unavailable ({why}); rows", "rows"
     h0, h1 = MG.row_range(rank, world) if combine in ("rows", "fused") else (0, 4096)
@@ -392,10 +513,22 @@ def main():
             eng.allreduce(check_offsets=False)   # float: checked once before the timed steps
         return P.cpa_finalize(eng.ctx, rho, maxabs, argmax, rank_t)
 
-    def barrier():
+    def timed_steps(k):
+        """k steps between a barrier + synchronize on both sides, CUDA events on
+        the library's stream; the max over ranks (ms)."""
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            r = step()
+        e1.record(stream)
+        barrier()
+        t = e0.elapsed_time(e1)
         if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+            tt = torch.tensor([t], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        return t, r
 
     for _ in range(args.warmup):
         res = step()
@@ -422,6 +555,36 @@ def main():
         t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
+    # N>1 trace shards: every other combine timed in the same invocation (the
+    # headline is `combine`), so one multi-GPU run compares them directly
+    combine_ms = None
+    if world > 1 and shard == "traces" and not args.no_combine_sweep:
+        head = (combine, h0, h1, rho)
+        combine_ms = {combine: ms_total / args.steps}
+        k2 = max(3, min(args.steps, 10))
+        for c in ("rows", "allreduce", "fused"):
+            if c == head[0]:
+                continue
+            if c == "fused":
+                why = use_owners(True) if fused_ok else "not applicable (float / class sums / G does not divide 16)"
+                if owners is None:
+                    combine_ms[c] = f"unavailable: {why}"
+                    continue
+            else:
+                use_owners(False)   # the NCCL combines: rows stay in this rank's accumulator
+            combine = c
+            h0, h1 = MG.row_range(rank, world) if c in ("rows", "fused") else (0, 4096)
+            rho = torch.empty((h1 - h0, m_local), dtype=torch.float64, device=dev)
+            for _ in range(2):
+                step()
+            t2, r2 = timed_steps(k2)
+            combine_ms[c] = t2 / k2
+            assert bytes(r2.master_key) == bytes(res.master_key), f"combine {c}: a different key"
+        combine, h0, h1, rho = head
+        if combine == "fused":
+            use_owners(True)
+        elif owners is not None:
+            use_owners(False)
     # a4 alone: the timed steps overlap it with a5 on a low-priority side stream,
     # which hides its own HBM rate; two untimed extra steps serialise it
     solo = None
@@ -477,6 +640,17 @@ def main():
         ceil = MMA_MACS_PER_CLK_SM[is_f32] * 2 * 148 * ncu_xt["sm_mhz"] * 1e6 / 1e12
         roofline["ncu"] = dict(ncu_xt, mma_ceiling_at_kernel_clock=ceil,
                                frac_of_ceiling_under_ncu=ops / (ncu_xt["duration_ms"] * 1e-3) / 1e12 / ceil)
+    roofline["frac_vs_datasheet"] = (F32_EXEC * achieved if is_f32 else achieved) / DATASHEET_TOPS[is_f32]
+    roofline["datasheet_tops"] = DATASHEET_TOPS[is_f32]
+    try:   # the library GEMM of the same precision class, measured now on this GPU
+        lib = cublaslt_peak_tops(dev, int8=not is_f32)
+        key = "cublaslt_bf16_tflops" if is_f32 else "cublaslt_int8_tops"
+        roofline[key] = lib
+        roofline["frac_vs_cublaslt"] = (F32_EXEC * achieved if is_f32 else achieved) / lib
+    except Exception as ex:  # noqa: BLE001
+        roofline["cublaslt_error"] = f"{type(ex).__name__}: {ex}"
+    roofline["mma_rate_source"] = ("tools/pair_bench.cu + tools/mma_bench.cu: kind::i8 8192, kind::f16 4096 "
+                                   "MAC/clk/SM reachable (profiles/mma_bench_r02.txt)")
     if class_sums:  # NEXT-4 path: HBM-bound by design (16 adds per trace byte), so report it as such
         gbs = n_local * m_local / (xt_ms * 1e-3) / 1e9
         roofline = {"kernel": "class sums (k_cs_sort + k_cs_sum + k_cs_contract)", "bound": "hbm",
@@ -565,6 +739,7 @@ def main():
             "phases_ms_per_step": step_phase_ms,
             "phase_share": {k: v / tot for k, v in step_phase_ms.items()},
             "roofline": roofline, "hbm": hbm, "e2e": e2e, "cpu_baseline": cpu,
+            "combine_ms_per_step": combine_ms,
             "cell_trace_macs_per_s": 4096 * w.m * w.n / (ms_step * 1e-3),
         }
         if not args.no_clocks:
@@ -615,7 +790,9 @@ def run_stream(args, w, dev, world, rank, local):
     torch.cuda.synchronize()
     rk10 = P.cpa_aes_expand_key(w.key)[10]   # the known round key (library host helper)
     key_idx = torch.tensor([256 * b + rk10[b] for b in range(16)], device=dev)
-    fused = world > 1 and args.combine in ("auto", "fused") and 16 % world == 0
+    # default (auto): reduce-scatter checkpoints (NCCL); the fused combine is
+    # timed after the headline in the same run (combine_ms_per_step)
+    fused = world > 1 and args.combine == "fused" and 16 % world == 0
     st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, local, fused=fused)
     if fused and st.owners is None:   # peers not mappable: NCCL reduce-scatter checkpoints
         print(f"fused combine unavailable ({st.fused_note}); reduce-scatter checkpoints", file=sys.stderr)
@@ -673,6 +850,35 @@ def run_stream(args, w, dev, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
+    # the other checkpoint combine, timed in the same invocation
+    combine_ms = None
+    if world > 1 and not args.no_combine_sweep:
+        name = "fused" if fused else "rows"
+        combine_ms = {name: ms_step}
+        other = not fused
+        if other and 16 % world:
+            combine_ms["fused"] = "not applicable: G does not divide 16"
+        else:
+            st_main = st
+            st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, local, fused=other)
+            if other and st.owners is None:
+                combine_ms["fused"] = f"unavailable: {st.fused_note}"
+            else:
+                k2 = max(2, min(args.steps, 5))
+                step()
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st.eng.stream)
+                for _ in range(k2):
+                    o2 = step()
+                e1.record(st.eng.stream)
+                barrier()
+                t = torch.tensor([e0.elapsed_time(e1) / k2], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                combine_ms["fused" if other else "rows"] = float(t.item())
+                assert bytes(o2["master_key"]) == bytes(out["master_key"])
+            st.close()
+            st = st_main
     peaks, src = load_peaks()
     xt_ms = phase_ms["xterm"] / max(1, phase_n["xterm"])
     ops = 2.0 * 4096 * n_local * w.m / max(1, phase_n["xterm"] // args.steps)  # per launch (one per chunk)
@@ -699,7 +905,7 @@ def run_stream(args, w, dev, world, rank, local):
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
                          "peak_source": f"{src} bf16_tflops (burst) x {INT8_PER_BF16:g}",
                          "ms_per_launch": xt_ms, "algorithmic_ops_per_launch": ops},
-            "e2e": None, "cpu_baseline": None,
+            "e2e": None, "cpu_baseline": None, "combine_ms_per_step": combine_ms,
         }
         if not args.no_clocks:
             line["clocks"] = clk.summary()

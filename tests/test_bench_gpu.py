@@ -45,6 +45,8 @@ def test_bench_two_ranks_one_gpu_gloo(combine, port):
     assert d["n_gpus"] == 2 and d["key_recovered"] is True
     assert KEYS <= set(d) and combine in d["config"]["parallelism"]
     assert "unavailable" not in d["config"]["parallelism"]   # fused: CUDA IPC between the ranks worked
+    cm = d["combine_ms_per_step"]   # every combine timed in the same invocation
+    assert set(cm) == {"rows", "allreduce", "fused"} and all(isinstance(v, float) for v in cm.values()), cm
 
 
 @pytest.mark.gpu
@@ -56,7 +58,9 @@ def test_bench_stream_two_ranks_one_gpu_gloo():
     assert d["n_gpus"] == 2 and d["key_recovered"] is True
     pts = d["rank_curve"]["points"]
     assert pts[-1][0] == 500 and d["config"]["checkpoints"] == len(pts)
-    assert "fused row combine" in d["config"]["parallelism"]   # rows routed to their owner by CUDA IPC
+    assert "reduce-scatter checkpoints" in d["config"]["parallelism"]   # the default (north_star's NCCL combine)
+    cm = d["combine_ms_per_step"]   # and the fused one (rows routed to their owner by CUDA IPC), same run
+    assert isinstance(cm["rows"], float) and isinstance(cm["fused"], float), cm
 
 
 @pytest.mark.gpu
