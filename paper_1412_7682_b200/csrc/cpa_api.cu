@@ -238,7 +238,7 @@ cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, 
     uint8_t vt[65536];
     cpa::build_vtable((int)model, vt);
     cudaError_t e = cudaMalloc(&c->d_vtab, 65536);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_sqrt_dw, sizeof(double) * M);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_sqrt_dw, 2 * sizeof(double) * M);  // sqrt(dw) | 1/sqrt(dw)
     if (e == cudaSuccess) e = cudaMalloc(&c->d_maxabs, sizeof(double) * 4096);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_peak, sizeof(double) * 4096);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_best_rho, sizeof(double) * 16);

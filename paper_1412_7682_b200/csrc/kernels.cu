@@ -188,7 +188,9 @@ __global__ void k_sqrt_dw_i8(const int64_t *__restrict__ sw, const int64_t *__re
     if (j >= M) return;
     const int64_t n = *count;
     const int64_t dw = n * sw2[j] - sw[j] * sw[j];
-    out[j] = __dsqrt_rn(__ll2double_rn(dw));
+    const double d = __dsqrt_rn(__ll2double_rn(dw));
+    out[j] = d;
+    out[M + j] = d != 0.0 ? __drcp_rn(d) : 0.0;  // for the no-rho filter of k_finalize_rows
 }
 
 struct Best {
@@ -214,10 +216,6 @@ __device__ __forceinline__ Best warp_best(Best x)
 }
 
 constexpr int FIN_THREADS = 256;
-#ifndef FIN_UNROLL_ROWS
-#define FIN_UNROLL_ROWS 4
-#endif
-constexpr int FIN_UNROLL = FIN_UNROLL_ROWS;
 
 __device__ __forceinline__ void block_best_store(Best best, int h, const FinalizeOut &o)
 {
@@ -236,69 +234,217 @@ __device__ __forceinline__ void block_best_store(Best best, int h, const Finaliz
     }
 }
 
+// ---------------------------------------------------------------------------
+// a8: one block = R hypothesis rows x all M samples (R = 1 by default, see
+// launch_fin).  Per column pair a thread loads the per-sample terms (sqrt(dw),
+// sum W: L2-resident, shared by all 4096 rows) once for its R rows; U column
+// pairs of 16-byte sum_hw loads are in flight per thread.  Every cell is the
+// fixed, FMA-free Eq. (1) sequence of DESIGN.md (fin_cell), so rho equals the
+// oracle's rho_B bit for bit.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double fin_cell(int64_t v, int64_t n, int64_t s_h, int64_t s_w, double den_w, double den_h)
+{
+    double r = 0.0;
+    if (den_w != 0.0 && den_h != 0.0) {
+        const int64_t num = n * v - s_h * s_w;
+        r = __ddiv_rn(__ll2double_rn(num), __dmul_rn(den_w, den_h));
+        r = fmin(1.0, fmax(-1.0, r));
+    }
+    return r;
+}
+__device__ __forceinline__ double fin_cell(double v, double n, double s_h, double s_w, double den_w, double den_h)
+{
+    double r = 0.0;
+    if (den_w != 0.0 && den_h != 0.0) {
+        const double num = __dsub_rn(__dmul_rn(n, v), __dmul_rn(s_h, s_w));
+        r = __ddiv_rn(num, __dmul_rn(den_w, den_h));
+        r = fmin(1.0, fmax(-1.0, r));
+    }
+    return r;
+}
+__device__ __forceinline__ double fin_den_h(int64_t n, int64_t s_h, int64_t s_h2)
+{
+    return __dsqrt_rn(__ll2double_rn(n * s_h2 - s_h * s_h));
+}
+__device__ __forceinline__ double fin_den_h(double n, double s_h, double s_h2)
+{
+    const double dh = __dsub_rn(__dmul_rn(n, s_h2), __dmul_rn(s_h, s_h));
+    return dh > 0.0 ? __dsqrt_rn(dh) : 0.0;
+}
+template <typename T> struct Pair2;
+template <> struct Pair2<int64_t> { using type = longlong2; };
+template <> struct Pair2<double> { using type = double2; };
+
+// Without rho output (streamed checkpoints, sharded maxima) only max|rho| and
+// its argmax are needed, so most cells skip the fp64 division (the kernel is
+// fp64-issue-bound, not HBM-bound, when it writes nothing): with
+// a_j = |num_j| * fl(1/den_w_j) (one DMUL; den_h is the same for the whole row)
+// and the exact value rho_j = fl(num_j / fl(den_w_j den_h)), rho_j den_h / a_j
+// lies in [1 - 4.01u, 1 + 4.01u] (u = 2^-53: two roundings on each side), so a
+// cell with a_j < a_best (1 - 2^-48) has |rho_j| < |rho_best| strictly (and the
+// clamp to 1 keeps <=); such a cell, at a larger j than the thread's best, can
+// neither beat nor tie-break it.  Every other cell is computed exactly as above,
+// so max|rho|, argmax and the signed peak are bit-identical to the full kernel.
+constexpr double kFinSkip = 1.0 - 3.552713678800501e-15;  // 1 - 2^-48
+
+template <int U, typename T>
 __global__ void __launch_bounds__(FIN_THREADS)
-k_finalize_i8(const int64_t *__restrict__ hw, const int64_t *__restrict__ sw,
-              const int64_t *__restrict__ sh, const int64_t *__restrict__ sh2,
-              const int64_t *__restrict__ count, const double *__restrict__ sqrt_dw, int32_t M,
-              FinalizeOut o)
+k_finalize_maxima(const T *__restrict__ hw, const T *__restrict__ sw, const T *__restrict__ sh,
+                  const T *__restrict__ sh2, const T *__restrict__ count, const double *__restrict__ sqrt_dw,
+                  int32_t M, FinalizeOut o)
 {
     const int h = o.h0 + blockIdx.x;
-    const int64_t n = *count;
-    const int64_t s_h = sh[h];
-    const int64_t dh = n * sh2[h] - s_h * s_h;
-    const double den_h = __dsqrt_rn(__ll2double_rn(dh));
-    const int64_t *row = hw + (int64_t)h * M;
-    double *rrow = o.rho ? o.rho + (int64_t)(h - o.h0) * M : nullptr;
+    const T n = *count;
+    const T s_h = sh[h];
+    const double den_h = fin_den_h(n, s_h, sh2[h]);
+    const T *row = hw + (int64_t)h * M;
+    const double *rcp_w = sqrt_dw + M;
     Best best{-1.0, 0.0, 0x7fffffff};
-    auto cell = [&](int64_t v, int j) {  // Eq. (1), fixed FMA-free sequence
-        const double den_w = sqrt_dw[j];
-        double r = 0.0;
-        if (den_w != 0.0 && den_h != 0.0) {
-            const int64_t num = n * v - s_h * sw[j];
-            r = __ddiv_rn(__ll2double_rn(num), __dmul_rn(den_w, den_h));
-            r = fmin(1.0, fmax(-1.0, r));
+    double abest = -1.0;  // a_j of the thread's best cell (-1: none yet)
+    auto visit = [&](T v, int j, double dw, double rw, T s_w) {
+        double num;
+        if constexpr (std::is_integral<T>::value) num = __ll2double_rn(n * v - s_h * s_w);
+        else num = __dsub_rn(__dmul_rn(n, v), __dmul_rn(s_h, s_w));
+        const double a = __dmul_rn(fabs(num), rw);
+        if (a < abest * kFinSkip) return;  // strictly below the best: skip the division
+        const double x = fin_cell(v, n, s_h, s_w, dw, den_h);
+        const double ax = fabs(x);
+        if (ax > best.v) {
+            best = Best{ax, x, j};
+            abest = a;
         }
-        const double a = fabs(r);
-        if (a > best.v) best = Best{a, r, j};
-        return r;
     };
-    // HBM-bound: FIN_UNROLL independent 16-byte row loads (2 samples each) in
-    // flight per thread before the long-latency fp64 division chains; j
-    // ascending per thread keeps the lowest-j tie rule with a strict '>'
-    constexpr int U = FIN_UNROLL;
     int j = 0;
-    if ((M & 1) == 0 && ((uintptr_t)o.rho & 15) == 0) {  // 16-byte aligned rows (M even)
-        const longlong2 *row2 = (const longlong2 *)row;
-        double2 *rrow2 = (double2 *)rrow;
+    if ((M & 1) == 0) {
+        using T2 = typename Pair2<T>::type;
         const int M2 = M >> 1;
         int p0 = threadIdx.x;
         for (; p0 + (U - 1) * FIN_THREADS < M2; p0 += U * FIN_THREADS) {
-            longlong2 v[U];
+            T2 v[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) v[u] = __ldcs(row2 + p0 + u * FIN_THREADS);
+            for (int u = 0; u < U; u++) v[u] = __ldcs((const T2 *)row + p0 + u * FIN_THREADS);
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const int jj = 2 * (p0 + u * FIN_THREADS);
-                double2 r;
-                r.x = cell(v[u].x, jj);
-                r.y = cell(v[u].y, jj + 1);
-                if (rrow2) __stcs(rrow2 + p0 + u * FIN_THREADS, r);
+                const int p = p0 + u * FIN_THREADS;
+                const double2 dw = ((const double2 *)sqrt_dw)[p];
+                const double2 rw = ((const double2 *)rcp_w)[p];
+                const T2 swp = ((const T2 *)sw)[p];
+                visit(v[u].x, 2 * p, dw.x, rw.x, swp.x);
+                visit(v[u].y, 2 * p + 1, dw.y, rw.y, swp.y);
             }
         }
         for (; p0 < M2; p0 += FIN_THREADS) {
-            const longlong2 v = __ldcs(row2 + p0);
-            double2 r;
-            r.x = cell(v.x, 2 * p0);
-            r.y = cell(v.y, 2 * p0 + 1);
-            if (rrow2) __stcs(rrow2 + p0, r);
+            const T2 v = __ldcs((const T2 *)row + p0);
+            const double2 dw = ((const double2 *)sqrt_dw)[p0];
+            const double2 rw = ((const double2 *)rcp_w)[p0];
+            const T2 swp = ((const T2 *)sw)[p0];
+            visit(v.x, 2 * p0, dw.x, rw.x, swp.x);
+            visit(v.y, 2 * p0 + 1, dw.y, rw.y, swp.y);
         }
-        j = M;  // done
+        j = M;
+    }
+    for (j += threadIdx.x; j < M; j += FIN_THREADS) visit(row[j], j, sqrt_dw[j], rcp_w[j], sw[j]);
+    block_best_store(best, h, o);
+}
+
+template <int R, int U, typename T>
+__global__ void __launch_bounds__(FIN_THREADS)
+k_finalize_rows(const T *__restrict__ hw, const T *__restrict__ sw, const T *__restrict__ sh,
+                const T *__restrict__ sh2, const T *__restrict__ count, const double *__restrict__ sqrt_dw, int32_t M,
+                FinalizeOut o)
+{
+    using T2 = typename Pair2<T>::type;
+    const int hb = o.h0 + blockIdx.x * R;
+    const int nr = min(R, o.h1 - hb);
+    const T n = *count;
+    T s_h[R];
+    double den_h[R];
+    Best best[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const int h = hb + (r < nr ? r : 0);
+        s_h[r] = sh[h];
+        den_h[r] = fin_den_h(n, s_h[r], sh2[h]);
+        best[r] = Best{-1.0, 0.0, 0x7fffffff};
+    }
+    const T *row0 = hw + (int64_t)hb * M;
+    double *rrow0 = o.rho ? o.rho + (int64_t)(hb - o.h0) * M : nullptr;
+    auto keep = [&](int r, double x, int j) {
+        const double a = fabs(x);
+        if (a > best[r].v) best[r] = Best{a, x, j};  // j ascending per thread: lowest-j ties
+    };
+    int j = 0;
+    if ((M & 1) == 0 && ((uintptr_t)o.rho & 15) == 0) {  // 16-byte aligned rows (M even)
+        const int M2 = M >> 1;
+        int p0 = threadIdx.x;
+        for (; p0 + (U - 1) * FIN_THREADS < M2; p0 += U * FIN_THREADS) {
+            T2 v[U][R];
+#pragma unroll
+            for (int u = 0; u < U; u++)
+#pragma unroll
+                for (int r = 0; r < R; r++)
+                    if (r < nr) v[u][r] = __ldcs((const T2 *)(row0 + (int64_t)r * M) + p0 + u * FIN_THREADS);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int p = p0 + u * FIN_THREADS;
+                const double2 dw = ((const double2 *)sqrt_dw)[p];
+                const T2 swp = ((const T2 *)sw)[p];
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    if (r >= nr) break;
+                    double2 x;
+                    x.x = fin_cell(v[u][r].x, n, s_h[r], swp.x, dw.x, den_h[r]);
+                    x.y = fin_cell(v[u][r].y, n, s_h[r], swp.y, dw.y, den_h[r]);
+                    keep(r, x.x, 2 * p);
+                    keep(r, x.y, 2 * p + 1);
+                    if (rrow0) __stcs((double2 *)(rrow0 + (int64_t)r * M) + p, x);
+                }
+            }
+        }
+        for (; p0 < M2; p0 += FIN_THREADS) {
+            const double2 dw = ((const double2 *)sqrt_dw)[p0];
+            const T2 swp = ((const T2 *)sw)[p0];
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                if (r >= nr) break;
+                const T2 v = __ldcs((const T2 *)(row0 + (int64_t)r * M) + p0);
+                double2 x;
+                x.x = fin_cell(v.x, n, s_h[r], swp.x, dw.x, den_h[r]);
+                x.y = fin_cell(v.y, n, s_h[r], swp.y, dw.y, den_h[r]);
+                keep(r, x.x, 2 * p0);
+                keep(r, x.y, 2 * p0 + 1);
+                if (rrow0) __stcs((double2 *)(rrow0 + (int64_t)r * M) + p0, x);
+            }
+        }
+        j = M;
     }
     for (j += threadIdx.x; j < M; j += FIN_THREADS) {
-        const double r = cell(row[j], j);
-        if (rrow) rrow[j] = r;
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            if (r >= nr) break;
+            const double x = fin_cell(row0[(int64_t)r * M + j], n, s_h[r], sw[j], sqrt_dw[j], den_h[r]);
+            keep(r, x, j);
+            if (rrow0) rrow0[(int64_t)r * M + j] = x;
+        }
     }
-    block_best_store(best, h, o);
+    // per-row block reductions (the shared staging array is reused: barrier between rows)
+    __shared__ Best red[R][FIN_THREADS / 32];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const Best b = warp_best(best[r]);
+        if ((threadIdx.x & 31) == 0) red[r][threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = warp; r < nr; r += FIN_THREADS / 32) {
+        Best x = lane < FIN_THREADS / 32 ? red[r][lane] : Best{-1.0, 0.0, 0x7fffffff};
+        x = warp_best(x);
+        if (lane == 0) {
+            o.maxabs[hb + r] = x.v;
+            o.argmax[hb + r] = x.j + o.col0;
+            o.peak[hb + r] = x.r;
+        }
+    }
 }
 
 // float path: all sums fp64 (same shape as the int accumulator)
@@ -317,36 +463,9 @@ __global__ void k_sqrt_dw_f64(const double *__restrict__ sw, const double *__res
     const double dw = __dsub_rn(__dmul_rn(n, sw2[j]), __dmul_rn(sw[j], sw[j]));
     const double o = offset ? (double)offset[j] : 0.0;
     const double raw2 = sw2[j] + o * (2.0 * sw[j] + n * o);
-    out[j] = (dw > 1e-12 * n * raw2) ? __dsqrt_rn(dw) : 0.0;
-}
-
-__global__ void __launch_bounds__(FIN_THREADS)
-k_finalize_f64(const double *__restrict__ hw, const double *__restrict__ sw,
-               const double *__restrict__ sh, const double *__restrict__ sh2,
-               const double *__restrict__ count, const double *__restrict__ sqrt_dw, int32_t M,
-               FinalizeOut o)
-{
-    const int h = o.h0 + blockIdx.x;
-    const double n = *count;
-    const double s_h = sh[h];
-    const double dh = __dsub_rn(__dmul_rn(n, sh2[h]), __dmul_rn(s_h, s_h));
-    const double den_h = dh > 0.0 ? __dsqrt_rn(dh) : 0.0;
-    const double *row = hw + (int64_t)h * M;
-    double *rrow = o.rho ? o.rho + (int64_t)(h - o.h0) * M : nullptr;
-    Best best{-1.0, 0.0, 0x7fffffff};
-    for (int j = threadIdx.x; j < M; j += FIN_THREADS) {
-        const double den_w = sqrt_dw[j];
-        double r = 0.0;
-        if (den_w != 0.0 && den_h != 0.0) {
-            const double num = __dsub_rn(__dmul_rn(n, row[j]), __dmul_rn(s_h, sw[j]));
-            r = __ddiv_rn(num, __dmul_rn(den_w, den_h));
-            r = fmin(1.0, fmax(-1.0, r));
-        }
-        if (rrow) rrow[j] = r;
-        const double a = fabs(r);
-        if (a > best.v) best = Best{a, r, j};
-    }
-    block_best_store(best, h, o);
+    const double d = (dw > 1e-12 * n * raw2) ? __dsqrt_rn(dw) : 0.0;
+    out[j] = d;
+    out[M + j] = d != 0.0 ? __drcp_rn(d) : 0.0;  // for the no-rho filter of k_finalize_rows
 }
 
 // ---------------------------------------------------------------------------
@@ -562,6 +681,24 @@ cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M,
     return cudaGetLastError();
 }
 
+// a8 launch: with rho, one row per block and 4 column pairs in flight per
+// thread (tools/fin_bench.py: 4.0 / 5.0 / 5.5 TB/s at M = 5000 / 20000 / 48000,
+// +9% over a plain one-row loop; R = 2..8 rows per block sharing the per-sample
+// loads were slower: more registers, fewer resident blocks); without rho, the
+// filtered maxima kernel from M = 8192 on (-13% / -23% at M = 20000 / 48000)
+constexpr int kFinFilterMinM = 8192;
+template <typename T>
+static cudaError_t launch_fin(const T *hw, const T *sw, const T *sh, const T *sh2, const T *cnt,
+                              const double *sqrt_dw, int32_t M, const FinalizeOut &o, cudaStream_t s)
+{
+    const int rows = o.h1 - o.h0;
+    if (o.rho == nullptr && M >= kFinFilterMinM)
+        k_finalize_maxima<4, T><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
+    else
+        k_finalize_rows<1, 4, T><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_finalize_i8(const int64_t *d_accum, int32_t M, double *d_sqrt_dw, const FinalizeOut &o,
                                cudaStream_t s, int *launches)
 {
@@ -572,7 +709,8 @@ cudaError_t launch_finalize_i8(const int64_t *d_accum, int32_t M, double *d_sqrt
     const int64_t *sh2 = sh + 4096;
     const int64_t *cnt = sh2 + 4096;
     k_sqrt_dw_i8<<<(M + 255) / 256, 256, 0, s>>>(sw, sw2, cnt, M, d_sqrt_dw);
-    k_finalize_i8<<<o.h1 - o.h0, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o);
+    cudaError_t e = launch_fin<int64_t>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o, s);
+    if (e != cudaSuccess) return e;
     if (launches) (*launches) += 2;
     return cudaGetLastError();
 }
@@ -587,7 +725,8 @@ cudaError_t launch_finalize_f64(const double *d_accum, int32_t M, const float *d
     const double *sh2 = sh + 4096;
     const double *cnt = sh2 + 4096;
     k_sqrt_dw_f64<<<(M + 255) / 256, 256, 0, s>>>(sw, sw2, cnt, d_offset, M, d_sqrt_dw);
-    k_finalize_f64<<<o.h1 - o.h0, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o);
+    cudaError_t e = launch_fin<double>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o, s);
+    if (e != cudaSuccess) return e;
     if (launches) (*launches) += 2;
     return cudaGetLastError();
 }

@@ -60,6 +60,30 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_
                  : "memory");
 }
 
+// bulk tensor reduce-add: the smem box at `src` is added element-wise into the
+// global tile at (x, y) of `map` (element type and swizzle from the map; int64
+// adds are two's-complement, so exact), by the TMA unit; out-of-bounds parts of
+// the box are dropped.  Completion via the bulk async-group of this thread.
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap *map, int32_t x, int32_t y, uint32_t src)
+{
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map),
+                 "r"(x), "r"(y), "r"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most N of this thread's bulk groups are still READING shared memory
+template <int N>
+__device__ __forceinline__ void bulk_wait_read()
+{
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// wait until at most N of this thread's bulk groups are incomplete (writes done)
+template <int N>
+__device__ __forceinline__ void bulk_wait()
+{
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // generic-proxy smem writes -> visible to the async proxy (tensor core / TMA)
 __device__ __forceinline__ void fence_proxy_async_smem()
 {
@@ -246,14 +270,6 @@ __host__ __device__ constexpr uint32_t idesc_e5m2_e4m3(uint32_t m, uint32_t n)
 {
     return (1u << 4)      // c_format = F32
            | (1u << 7)    // a_format = E5M2
-           | (0u << 10)   // b_format = E4M3
-           | (1u << 15) | (1u << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
-}
-// kind::f8f6f4 with e4m3 inputs (format code 0), fp32 accumulate, both operands MN-major
-__host__ __device__ constexpr uint32_t idesc_e4m3(uint32_t m, uint32_t n)
-{
-    return (1u << 4)      // c_format = F32
-           | (0u << 7)    // a_format = E4M3
            | (0u << 10)   // b_format = E4M3
            | (1u << 15) | (1u << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
