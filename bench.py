@@ -75,6 +75,9 @@ def parse():
     ap.add_argument("--xt-tiles", type=int, default=0, choices=[0, 1, 2],
                     help="CPA_OPT_XT_TILES: int8 cross-term variant (0 = the library's cost model, 1 = two "
                          "sample tiles per unit, 2 = one tile with the spill overlapped)")
+    ap.add_argument("--spill", type=int, default=0, choices=[0, 1, 2],
+                    help="CPA_OPT_SPILL: int8 cross-term spill, 0 = auto (default), 1 = red.add.u64 per "
+                         "element, 2 = bulk tensor reduce-add")
     ap.add_argument("--chunk", type=int, default=0,
                     help="stream the traces in chunks of this many, finalizing after every round "
                          "(key-rank curve); default for C5: 65536")
@@ -443,6 +446,7 @@ def main():
     eng.set_fuse_hist(args.fuse_hist == "1")
     if not is_f32:
         eng.set_xt_tiles(args.xt_tiles)
+        eng.set_spill(args.spill)
     eng.set_col0(j0)
     ovl_mode = 0 if args.no_overlap else (args.overlap_mode if args.overlap_mode is not None else OVERLAP_DEFAULT)
     eng.set_overlap(ovl_mode)

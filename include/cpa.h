@@ -285,9 +285,17 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *                   unit with double-buffered TMEM accumulators (the spill
  *                   overlaps the next unit's MMAs: short units, i.e. wide or
  *                   few traces; a4 then runs as a separate pass; measured
- *                   slower on B200).  Same exact sums either way.  */
+ *                   slower on B200).  Same exact sums either way.
+ *   CPA_OPT_SPILL:  how the int8 cross term adds each work unit's int32
+ *                   accumulators into the int64 sum_hw: 1 = one
+ *                   red.global.add.u64 per element; 2 = bulk tensor reduce-add
+ *                   (cp.reduce.async.bulk.tensor: the TMA unit adds 32 x 8
+ *                   int64 boxes; needs M even and no row owners, else 1);
+ *                   0 (default) = 2 for work units of >= 65536 traces, else 1
+ *                   (measured).  Exact either way.                 */
 enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2, CPA_OPT_OVERLAP = 3, CPA_OPT_STAGE_BYTES = 4,
-       CPA_OPT_COL0 = 5, CPA_OPT_CLASS_SUMS = 6, CPA_OPT_FUSE_HIST = 7, CPA_OPT_XT_TILES = 8 };
+       CPA_OPT_COL0 = 5, CPA_OPT_CLASS_SUMS = 6, CPA_OPT_FUSE_HIST = 7, CPA_OPT_XT_TILES = 8,
+       CPA_OPT_SPILL = 9 };
 CPA_API cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value);
 
 /* Per-phase device time (ms) and launch count since the last call, from the

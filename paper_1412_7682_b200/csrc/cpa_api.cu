@@ -72,6 +72,7 @@ PFN_addr_range get_addr_range()
 constexpr int64_t kMaxTraces = 1LL << 23;  // exact-int64 bound of Eq. (1), see DESIGN.md
 constexpr int32_t kMaxSamples = 1 << 22;
 constexpr int64_t kStageBytes = 256LL << 20;  // bytes per staging chunk (cpa_accumulate_host / unaligned input)
+constexpr int64_t kBulkSpillMinUnit = 65536;  // CPA_OPT_SPILL auto: bulk reduce from this unit length (traces) on
 
 }  // namespace
 
@@ -117,6 +118,7 @@ struct cpa_ctx {
     int class_sums = 0;
     int fuse_hist = 0;
     int xt_tiles = 0;  // CPA_OPT_XT_TILES: 0 model, 1 NT = 2, 2 NT = 1 overlapped
+    int spill = 0;  // CPA_OPT_SPILL: 0 auto, 1 red.add.u64 per element, 2 bulk tensor reduce-add
     // cpa_set_row_owners: fused multi-GPU combine (key byte b's sum_hw rows go to owners[b])
     int64_t *owners[16] = {};
     bool owners_set = false;
@@ -336,6 +338,11 @@ cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
     if (option == CPA_OPT_XT_TILES) {
         if (value < 0 || value > 2) return fail(CPA_E_INVALID_ARG, "XT_TILES=%lld outside [0, 2]", (long long)value);
         ctx->xt_tiles = (int)value;
+        return CPA_OK;
+    }
+    if (option == CPA_OPT_SPILL) {
+        if (value < 0 || value > 2) return fail(CPA_E_INVALID_ARG, "SPILL=%lld outside [0, 2]", (long long)value);
+        ctx->spill = (int)value;
         return CPA_OK;
     }
     if (option == CPA_OPT_FUSE_HIST) {
@@ -572,9 +579,30 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    // the epilogue's int64 spill by bulk tensor reduce-add into sum_hw [4096][M]
+    // (rows of M int64 must be 16-byte multiples: M even); the fused multi-GPU
+    // combine (row owners) keeps its system-scope red.add.  The map is typed
+    // UINT64: the TMA reduce-add rejects INT64 at run time (tools/reduce_probe.cu)
+    // and two's-complement addition is the same operation on the same bits.
+    // auto (CPA_OPT_SPILL 0): bulk for long units, where it measured 0.5% faster
+    // (C4); red.add for short ones, where it measured faster (C2 0.109 vs 0.122 ms,
+    // W48 1.18 vs 1.20): the spill is bound by the L2/HBM read-modify-write of
+    // sum_hw either way, not by the issuing SM
     const int64_t kc = c->kchunk ? c->kchunk : plan.kc_len;
+    CUtensorMap tmap_hw;
+    bool bulk = (M % 2 == 0) && !c->owners_set &&
+                (c->spill == 2 || (c->spill == 0 && kc >= kBulkSpillMinUnit));
+    if (bulk) {
+        cuuint64_t hdims[2] = {(cuuint64_t)M, 4096};
+        cuuint64_t hstr[1] = {(cuuint64_t)M * 8};
+        cuuint32_t hbox[2] = {8, 32};
+        bulk = get_encode()(&tmap_hw, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, acc, hdims, hstr, hbox, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
     CUDA_TRY(c->timed(2, [&] {
-                 return cpa::launch_xterm_i8(tmap, d_tx, c->d_vtab, acc, c->d_counter, M, n, kc, sgn, c->num_sms,
+                 return cpa::launch_xterm_i8(tmap, bulk ? &tmap_hw : nullptr, d_tx, c->d_vtab, acc, c->d_counter, M,
+                                             n, kc, sgn, c->num_sms,
                                              c->stream, &launches, fused ? acc + cpa_accum_offset(M, 1) : nullptr,
                                              fused ? acc + cpa_accum_offset(M, 2) : nullptr,
                                              fhist ? c->d_hist : nullptr, c->owners_set ? c->owners : nullptr,

@@ -115,7 +115,7 @@ constexpr int BN = 256;           // samples per accumulator (MMA N)
 #define XT_PREFETCH 0
 #endif
 constexpr int PREFETCH_STAGES = XT_PREFETCH;  // >0: W boxes prefetched into L2 this many stages ahead
-constexpr int TX_STAGES = 6;      // ciphertext ring, prefetched ahead of the stages
+constexpr int TX_STAGES = 4;      // ciphertext ring, prefetched ahead of the stages
 constexpr int SCHED_Q = 4;        // depth of the unit-id ring
 // V[y][x] = HW(InvS[x] ^ y) is 0..8: stored as nibbles, V[y][2i] | V[y][2i+1] << 4
 // (32 KB; the freed 32 KB deepens the W ring)
@@ -132,14 +132,20 @@ constexpr int GEN_WARPS = XT_GEN_WARPS;       // every generator warp works on e
 // peer = W producer + text producer + epilogue + generators
 constexpr int RING_CONSUMERS = 2 * (2 + EPI_WARPS + GEN_WARPS);
 constexpr int TB_LD = 9;                      // epilogue transpose row stride (words, odd)
-constexpr int TB_BYTES = EPI_WARPS * 32 * TB_LD * 4;
+// epilogue staging (union): the red.add path's transpose buffer, or the bulk
+// path's int64 boxes (per epilogue warp one 32 rows x 8 samples box, 64-byte
+// swizzled, 2 KB; the TMA reduce reads it while the warp loads the next columns)
+constexpr int RB_BYTES = 32 * 8 * 8;
+constexpr int TB_BYTES = (EPI_WARPS * RB_BYTES > EPI_WARPS * 32 * TB_LD * 4) ? EPI_WARPS * RB_BYTES
+                                                                             : EPI_WARPS * 32 * TB_LD * 4;
 constexpr int MAX_RING = 8;                   // barrier slots reserved per ring
 constexpr int SMEM_V = 0;
 constexpr int SMEM_A = SMEM_V + V_BYTES;      // A ring, then the B ring (per-config sizes)
 constexpr int RINGS_BYTES = 180224;           // A_STAGES*A_STAGE + B_STAGES*B_STAGE <= this
-constexpr int SMEM_TX = SMEM_A + RINGS_BYTES;
-constexpr int SMEM_TB = SMEM_TX + TX_STAGES * TX_BYTES;
-constexpr int SMEM_BAR = SMEM_TB + TB_BYTES;
+constexpr int SMEM_TB = SMEM_A + RINGS_BYTES;  // 1 KB aligned (64-byte-swizzled TMA boxes)
+constexpr int SMEM_TX = SMEM_TB + TB_BYTES;
+constexpr int SMEM_BAR = SMEM_TX + TX_STAGES * TX_BYTES;
+static_assert(SMEM_TB % 1024 == 0, "staging boxes: 1 KB alignment");
 constexpr int NUM_BARS = 4 * MAX_RING + 2 * TX_STAGES + 4 + 2 * SCHED_Q + 2 * MAX_RING;
 constexpr int SMEM_SCHED = SMEM_BAR + NUM_BARS * 8;
 constexpr int SMEM_TOTAL = SMEM_SCHED + SCHED_Q * 4 + 16;
@@ -186,6 +192,8 @@ struct Params {
     int64_t *sum_w;
     int64_t *sum_w2;
     int32_t w_signed;
+    // int8 spill by bulk tensor reduce-add (tmap_hw valid; else red.add.u64)
+    int32_t bulk_spill;
     // fused a3 histogram (null = off): the leader's generators of the units of
     // N tile group 0 count each trace's (c_b, c_SR(b)) pair of their key byte
     // (k_hist_contract turns the counts into sum H, sum H^2 afterwards)
@@ -296,7 +304,8 @@ __device__ __forceinline__ void moments_pass(const Params &p, uint32_t bring, ui
 
 template <int V>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
-k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUtensorMap tmap_b1, const Params p)
+k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUtensorMap tmap_b1,
+        const __grid_constant__ CUtensorMap tmap_hw, const Params p)
 {
     using C = Cfg<V>;
     constexpr bool F32 = C::F32;
@@ -580,12 +589,56 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             constexpr int NC = C::NACC * BN / 8;
             const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + acc * (C::NACC * BN);
             int64_t *const own = F32 ? nullptr : p.owners[b];  // KB == 1 for the owner routing
-            // 8 columns at a time through a small transpose buffer: each warp-wide
-            // atomic covers 4 rows x 8 consecutive samples = 8 full 32-byte sectors.
-            // The TMEM load of the next 8 columns is in flight during the atomics.
             uint32_t v[8];
             tmem_ld_32x32b_x8(tcol, v);
             tmem_ld_wait(v);
+            if (!F32 && p.bulk_spill && own == nullptr) {
+                // lane = accumulator row: its 8 samples as int64 into the warp's box (64 B
+                // per row, 16-byte chunks XOR-swizzled by (row >> 1) & 3 -- the TMA 64B
+                // swizzle, conflict-free STS.128), then ONE bulk tensor reduce-add of the
+                // 32 x 8 box into sum_hw by the TMA unit (exact int64 adds).  The box is
+                // rewritten only after the previous reduce has read it.
+                const uint32_t box = sbase + SMEM_TB + q * RB_BYTES;
+                const uint32_t rowb = box + lane * 64;
+                const uint32_t swz = ((uint32_t)lane >> 1) & 3;
+#pragma unroll 1
+                for (int c = 0; c < NC; c++) {
+                    const int kb = c / CPB, cc = c % CPB;
+                    const int hrow0 = (b + kb) * 256 + (int)rank * BMC + q * 32;
+                    uint32_t vn[8];
+                    if (c + 1 < NC) tmem_ld_32x32b_x8(tcol + (c + 1) * 8, vn);
+                    if (lane == 0) bulk_wait_read<0>();
+                    __syncwarp();
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const int64_t a0 = (int64_t)(int32_t)v[2 * k], a1 = (int64_t)(int32_t)v[2 * k + 1];
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowb + ((k ^ swz) << 4)),
+                                     "r"((uint32_t)a0), "r"((uint32_t)(a0 >> 32)), "r"((uint32_t)a1),
+                                     "r"((uint32_t)(a1 >> 32))
+                                     : "memory");
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    const int j = nt * (C::NT * BN) + cc * 8;
+                    if (lane == 0 && !(XT_EXP & 4) && j < p.M) {
+                        tma_reduce_add_2d(&tmap_hw, j, hrow0, box);
+                        bulk_commit();
+                    }
+                    if (c + 1 < NC) {
+                        tmem_ld_wait(vn);
+#pragma unroll
+                        for (int x = 0; x < 8; x++) v[x] = vn[x];
+                    }
+                }
+                if (lane == 0) bulk_wait_read<0>();  // box free; the adds complete asynchronously
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(to_leader(tempty_bar(acc)));
+                continue;
+            }
+            // 8 columns at a time through a small transpose buffer: each warp-wide
+            // atomic covers 4 rows x 8 consecutive samples = 8 full 32-byte sectors.
+            // The TMEM load of the next 8 columns is in flight during the atomics.
 #pragma unroll 1
             for (int c = 0; c < NC; c++) {
                 const int kb = c / CPB, cc = c % CPB;
@@ -734,6 +787,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
         }
     }
 
+    if (warp >= 4 && warp < 8 && lane == 0) bulk_wait<0>();  // every bulk reduce-add has landed
     tc_fence_before();
     __syncthreads();
     cluster_sync_all();  // the peer's MMAs / remote arrivals are done with our smem and TMEM
@@ -748,7 +802,8 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
 }
 
 template <int V>
-cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *d_texts, const uint8_t *d_vtab,
+cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorMap *mhw, const uint8_t *d_texts,
+                   const uint8_t *d_vtab,
                    void *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, uint32_t idesc, int num_sms,
                    cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr, int64_t *d_sum_w2 = nullptr,
                    bool w_signed = true, uint32_t *d_hist = nullptr, int64_t *const *owners = nullptr,
@@ -776,13 +831,14 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const uint8_t *
     p.hist = d_hist;
     for (int b = 0; b < 16; b++) p.owners[b] = owners ? owners[b] : nullptr;
     p.clk = d_clk;
+    p.bulk_spill = mhw != nullptr;
     static std::atomic<unsigned long long> attr_set{0};
     cudaError_t e = smem_attr_once((const void *)k_xterm<V>, SMEM_ALLOC, attr_set);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(d_counter, 0, sizeof(int), stream);
     if (e != cudaSuccess) return e;
     const int pairs = (p.units < num_sms / 2 ? p.units : num_sms / 2);
-    k_xterm<V><<<2 * pairs, THREADS, SMEM_ALLOC, stream>>>(m0, m1, p);
+    k_xterm<V><<<2 * pairs, THREADS, SMEM_ALLOC, stream>>>(m0, m1, mhw ? *mhw : m0, p);
     if (launches) (*launches)++;
     return cudaGetLastError();
 }
@@ -852,19 +908,20 @@ XtermI8Plan xterm_i8_plan(int32_t M, int64_t N, int num_sms, bool remote_epilogu
     return pl;
 }
 
-cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const uint8_t *d_texts, const uint8_t *d_vtab,
-                            int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, bool w_signed,
-                            int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w, int64_t *d_sum_w2,
-                            uint32_t *d_hist, int64_t *const *owners, unsigned long long *d_clk, bool overlapped)
+cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const CUtensorMap *tmap_hw, const uint8_t *d_texts,
+                            const uint8_t *d_vtab, int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len,
+                            bool w_signed, int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w,
+                            int64_t *d_sum_w2, uint32_t *d_hist, int64_t *const *owners, unsigned long long *d_clk,
+                            bool overlapped)
 {
     static_assert(Cfg<V_I8>::KB == 1 && Cfg<V_I8O>::KB == 1, "owner routing assumes one key byte per unit");
     if (overlapped) {
         if (d_sum_w != nullptr) return cudaErrorInvalidValue;  // a4 is fused into the NT = 2 variant only
-        return launch<V_I8O>(tmap_w, tmap_w, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
+        return launch<V_I8O>(tmap_w, tmap_w, tmap_hw, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                              idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, nullptr, nullptr, w_signed,
                              d_hist, owners, d_clk);
     }
-    return launch<V_I8>(tmap_w, tmap_w, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
+    return launch<V_I8>(tmap_w, tmap_w, tmap_hw, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                         idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, d_sum_w, d_sum_w2, w_signed,
                         d_hist, owners, d_clk);
 }
@@ -874,7 +931,8 @@ cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap
                              int64_t N, int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
                              uint32_t *d_hist, unsigned long long *d_clk)
 {
-    return launch<V_F32>(tmap_hi, tmap_lo, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len, idesc_f16(2 * BMC, BN),
+    return launch<V_F32>(tmap_hi, tmap_lo, nullptr, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
+                         idesc_f16(2 * BMC, BN),
                         num_sms, stream, launches, nullptr, nullptr, true, d_hist, nullptr, d_clk,
                         idesc_e5m2_e4m3(2 * BMC, BN), d_inv_scale);
 }

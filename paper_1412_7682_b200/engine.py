@@ -77,6 +77,10 @@ class Engine:
         """CPA_OPT_XT_TILES: int8 cross-term variant (0 model, 1 two sample tiles per unit, 2 one tile, overlapped spill)."""
         B.cpa_set_option(self.ctx, B.CPA_OPT_XT_TILES, v)
 
+    def set_spill(self, mode: int):
+        """CPA_OPT_SPILL: 0 auto (default), 1 red.add.u64 per element, 2 bulk tensor reduce-add."""
+        B.cpa_set_option(self.ctx, B.CPA_OPT_SPILL, mode)
+
     def set_row_owners(self, owners):
         """cpa_set_row_owners: 16 device addresses (0 = own accumulator) or None."""
         B.cpa_set_row_owners(self.ctx, owners)

@@ -24,11 +24,13 @@ MODEL = {O.HD_LAST: 0, O.HW_LAST: 1, O.HW_FIRST: 2}
 
 
 def run_gpu(P, texts, W, model=0, kchunk=0, chunks=None, want_rho=True, overlap=True, mode=None, fuse_hist=None,
-            xt=None):
+            xt=None, spill=None):
     dtype = {np.int8: P.CPA_S8, np.uint8: P.CPA_U8}[W.dtype.type]
     eng = P.Engine(W.shape[1], dtype, model, 0)
     if xt is not None:
         eng.set_xt_tiles(xt)
+    if spill is not None:
+        eng.set_spill(spill)
     if kchunk:
         eng.set_kchunk(kchunk)
     if not overlap:
@@ -97,28 +99,28 @@ def test_c1_noiseless_rho_one(P):
     assert out["master_key"] == w.key
 
 
-@pytest.mark.parametrize("xt", [1, 2])
+@pytest.mark.parametrize("xt,spill", [(1, 1), (1, 2), (2, 1), (2, 2)])
 @pytest.mark.parametrize("model", [O.HD_LAST, O.HW_LAST, O.HW_FIRST])
 @pytest.mark.parametrize("dtype", [np.int8, np.uint8])
-def test_models_dtypes_ragged(P, model, dtype, xt):
+def test_models_dtypes_ragged(P, model, dtype, xt, spill):
     rng = np.random.default_rng(100 + model)
     n, m = 333, 300                     # ragged: 333 = 5*64+13 traces, 300 = 256+44 samples
     texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
     lo, hi = (-128, 128) if dtype == np.int8 else (0, 256)
     W = rng.integers(lo, hi, (n, m)).astype(dtype)
     ref = O.attack_i8(model, texts, W)
-    sums, out = run_gpu(P, texts, W, model=MODEL[model], xt=xt)
+    sums, out = run_gpu(P, texts, W, model=MODEL[model], xt=xt, spill=spill)
     assert_parity(sums, out, ref)
 
 
-@pytest.mark.parametrize("xt", [1, 2])
-@pytest.mark.parametrize("n,m", [(2, 1), (3, 17), (64, 256), (65, 257), (130, 513), (1000, 16)])
-def test_edge_shapes(P, n, m, xt):
+@pytest.mark.parametrize("xt,spill", [(1, 1), (1, 2), (2, 1), (2, 2)])
+@pytest.mark.parametrize("n,m", [(2, 1), (3, 17), (64, 256), (65, 257), (65, 258), (130, 513), (130, 514), (1000, 16)])
+def test_edge_shapes(P, n, m, xt, spill):
     rng = np.random.default_rng(n * 1000 + m)
     texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
     W = rng.integers(-128, 128, (n, m)).astype(np.int8)
     ref = O.attack_i8(O.HD_LAST, texts, W)
-    sums, out = run_gpu(P, texts, W, xt=xt)
+    sums, out = run_gpu(P, texts, W, xt=xt, spill=spill)   # spill 2 needs M even (odd M falls back to red.add)
     assert_parity(sums, out, ref)
 
 
@@ -147,7 +149,8 @@ def test_split_k_chunks_and_permutation_bit_identical(P):
     for kw in (dict(kchunk=128), dict(kchunk=1024), dict(chunks=[0, 1, 700, 4097, 9000]),
                dict(overlap=False), dict(overlap=False, chunks=[0, 5000, 9000]),
                dict(xt=1), dict(xt=2), dict(xt=1, kchunk=256), dict(xt=2, kchunk=256),
-               dict(xt=2, chunks=[0, 1, 700, 4097, 9000])):
+               dict(xt=2, chunks=[0, 1, 700, 4097, 9000]), dict(spill=1), dict(spill=2, kchunk=128),
+               dict(spill=2, xt=2, kchunk=256)):
         s, o = run_gpu(P, texts, W, **kw)
         for k in base:
             assert np.array_equal(base[k], s[k]), (kw, k)
