@@ -241,6 +241,12 @@ CPA_API cpa_status cpa_get_offsets(cpa_ctx *ctx, float *d_out, int *is_set);
 
 CPA_API cpa_status cpa_reset(cpa_ctx *ctx);    /* zero the accumulator and the
                                                   non-finite flag (async) */
+/* After cpa_init / cpa_reset the library knows sum_hw is zero: the first
+ * int8 cpa_accumulate whose work units each cover all of its traces (one trace
+ * chunk) STORES its sums instead of adding them (half the HBM traffic of the
+ * spill).  So the caller must not write the sum_hw field between cpa_init /
+ * cpa_reset and the next cpa_accumulate (contexts with row owners -- which
+ * receive peer adds -- never store).                                        */
 CPA_API cpa_status cpa_sync(cpa_ctx *ctx);     /* wait for all queued work */
 CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum) */
 

@@ -91,6 +91,7 @@ struct cpa_ctx {
     int *d_counter = nullptr;  // work-unit counter of the cross-term scheduler
     int64_t kchunk = 0;
     int64_t n_since_reset = 0;  // traces accumulated through this context since init / cpa_reset
+    bool hw_zero = true;  // sum_hw holds the zeros of cpa_init / cpa_reset (no cross term since)
     int32_t col0 = 0;  // CPA_OPT_COL0: global index of sample 0 (sample-axis sharding)
     int64_t launches = 0;
     // cpa_accumulate_host staging
@@ -203,6 +204,7 @@ cpa_status cpa_reset(cpa_ctx *ctx)
     CUDA_TRY(cudaMemsetAsync(ctx->accum, 0, cpa_accum_bytes(ctx->M), ctx->stream), "reset accumulator");
     CUDA_TRY(cudaMemsetAsync(ctx->d_nonfinite, 0, sizeof(int), ctx->stream), "reset flag");
     ctx->n_since_reset = 0;
+    ctx->hw_zero = true;
     return CPA_OK;
 }
 
@@ -516,6 +518,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                                       fhist ? c->d_hist : nullptr, c->d_clk);
                      }),
                      "xterm_f32");
+            c->hw_zero = false;
         }
         if (fhist)
             CUDA_TRY(c->timed(0, [&] {
@@ -543,6 +546,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                  }),
                  "moments");
         cpa_status st = accumulate_class_sums(c, d_w, ld, d_tx, n, &launches);
+        c->hw_zero = false;
         c->launches += launches;
         return st;
     }
@@ -606,9 +610,10 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                              c->stream, &launches, fused ? acc + cpa_accum_offset(M, 1) : nullptr,
                                              fused ? acc + cpa_accum_offset(M, 2) : nullptr,
                                              fhist ? c->d_hist : nullptr, c->owners_set ? c->owners : nullptr,
-                                             c->d_clk, plan.overlapped);
+                                             c->d_clk, plan.overlapped, c->hw_zero);
              }),
              "xterm_i8");
+    c->hw_zero = false;
     if (!fused && mode == 1) CUDA_TRY(moments(), "moments");
     if (fhist)
         CUDA_TRY(c->timed(0, [&] {

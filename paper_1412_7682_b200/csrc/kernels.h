@@ -64,13 +64,15 @@ struct XtermI8Plan {
 };
 XtermI8Plan xterm_i8_plan(int32_t M, int64_t N, int num_sms, bool remote_epilogue, int force);
 // tmap_hw (may be null: red.add.u64 spill): sum_hw as int64 [4096][M], box 8 x 32,
-// 64-byte swizzle -- the epilogue spills by bulk tensor reduce-add (M even)
+// 64-byte swizzle -- the epilogue spills by bulk tensor reduce-add (M even).
+// hw_zero: sum_hw is all zero before the launch (the library zeroed it and
+// nothing was added since); with one trace chunk per unit the spill then stores.
 cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const CUtensorMap *tmap_hw, const uint8_t *d_texts,
                             const uint8_t *d_vtab, int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len,
                             bool w_signed, int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr,
                             int64_t *d_sum_w2 = nullptr, uint32_t *d_hist = nullptr,
                             int64_t *const *owners = nullptr, unsigned long long *d_clk = nullptr,
-                            bool overlapped = false);
+                            bool overlapped = false, bool hw_zero = false);
 
 // a6: float traces.  Split pre-pass: c = w - offset[j], hi = fp16(c s_j),
 // lo = e4m3(c s_j - hi) into [n][ldh] fp16 / [n][ldl] byte planes (s_j =

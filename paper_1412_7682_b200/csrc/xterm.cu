@@ -194,6 +194,10 @@ struct Params {
     int32_t w_signed;
     // int8 spill by bulk tensor reduce-add (tmap_hw valid; else red.add.u64)
     int32_t bulk_spill;
+    // first touch: sum_hw is known zero and every (row, sample) belongs to ONE
+    // work unit of this launch (one trace chunk), so the spill stores instead of
+    // adding: half the HBM traffic of a read-modify-write of sum_hw
+    int32_t store_hw;
     // fused a3 histogram (null = off): the leader's generators of the units of
     // N tile group 0 count each trace's (c_b, c_SR(b)) pair of their key byte
     // (k_hist_contract turns the counts into sum H, sum H^2 afterwards)
@@ -592,7 +596,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             uint32_t v[8];
             tmem_ld_32x32b_x8(tcol, v);
             tmem_ld_wait(v);
-            if (!F32 && p.bulk_spill && own == nullptr) {
+            if (!F32 && p.bulk_spill && own == nullptr && !p.store_hw) {
                 // lane = accumulator row: its 8 samples as int64 into the warp's box (64 B
                 // per row, 16-byte chunks XOR-swizzled by (row >> 1) & 3 -- the TMA 64B
                 // swizzle, conflict-free STS.128), then ONE bulk tensor reduce-add of the
@@ -660,6 +664,8 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                         } else if (own != nullptr) {  // peer (or own) accumulator of the row owner
                             atomicAdd_system((unsigned long long *)own + off + (int64_t)(4 * rr) * p.M,
                                              (unsigned long long)(long long)(int32_t)bits);
+                        } else if (p.store_hw) {      // first touch (store_hw): no read-modify-write
+                            ((long long *)p.hw)[off + (int64_t)(4 * rr) * p.M] = (long long)(int32_t)bits;
                         } else {
                             atomicAdd((unsigned long long *)p.hw + off + (int64_t)(4 * rr) * p.M,
                                       (unsigned long long)(long long)(int32_t)bits);
@@ -807,7 +813,8 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorM
                    void *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len, uint32_t idesc, int num_sms,
                    cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr, int64_t *d_sum_w2 = nullptr,
                    bool w_signed = true, uint32_t *d_hist = nullptr, int64_t *const *owners = nullptr,
-                   unsigned long long *d_clk = nullptr, uint32_t idesc8 = 0, const float *d_inv_scale = nullptr)
+                   unsigned long long *d_clk = nullptr, uint32_t idesc8 = 0, const float *d_inv_scale = nullptr,
+                   bool store_hw = false)
 {
     using Cf = Cfg<V>;
     Params p;
@@ -832,6 +839,7 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorM
     for (int b = 0; b < 16; b++) p.owners[b] = owners ? owners[b] : nullptr;
     p.clk = d_clk;
     p.bulk_spill = mhw != nullptr;
+    p.store_hw = store_hw && p.kc_count == 1 && owners == nullptr && V != V_F32;
     static std::atomic<unsigned long long> attr_set{0};
     cudaError_t e = smem_attr_once((const void *)k_xterm<V>, SMEM_ALLOC, attr_set);
     if (e != cudaSuccess) return e;
@@ -912,18 +920,18 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const CUtensorMap *tmap_h
                             const uint8_t *d_vtab, int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len,
                             bool w_signed, int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w,
                             int64_t *d_sum_w2, uint32_t *d_hist, int64_t *const *owners, unsigned long long *d_clk,
-                            bool overlapped)
+                            bool overlapped, bool hw_zero)
 {
     static_assert(Cfg<V_I8>::KB == 1 && Cfg<V_I8O>::KB == 1, "owner routing assumes one key byte per unit");
     if (overlapped) {
         if (d_sum_w != nullptr) return cudaErrorInvalidValue;  // a4 is fused into the NT = 2 variant only
         return launch<V_I8O>(tmap_w, tmap_w, tmap_hw, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                              idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, nullptr, nullptr, w_signed,
-                             d_hist, owners, d_clk);
+                             d_hist, owners, d_clk, 0, nullptr, hw_zero);
     }
     return launch<V_I8>(tmap_w, tmap_w, tmap_hw, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                         idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, d_sum_w, d_sum_w2, w_signed,
-                        d_hist, owners, d_clk);
+                        d_hist, owners, d_clk, 0, nullptr, hw_zero);
 }
 
 cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,

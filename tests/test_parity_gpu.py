@@ -415,3 +415,26 @@ def test_class_sums_chunked_sort_and_errors(P):
     with pytest.raises(Exception):
         eng.set_class_sums(True)
     eng.close()
+
+
+@pytest.mark.parametrize("spill", [1, 2])
+def test_first_touch_store_then_add(P, spill):
+    """After cpa_init / cpa_reset the first int8 accumulate with one trace chunk
+    per work unit stores its sums (include/cpa.h); later calls add.  The same
+    traces accumulated twice give exactly twice the sums, and a reset restarts."""
+    rng = np.random.default_rng(77)
+    n, m = 700, 600
+    texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    W = rng.integers(-128, 128, (n, m)).astype(np.int8)
+    ref = O.attack_i8(O.HD_LAST, texts, W)
+    eng = P.Engine(m, P.CPA_S8, P.CPA_HD_LAST, 0)
+    eng.set_spill(spill)
+    dW, dT = torch.from_numpy(W).cuda(), torch.from_numpy(texts).cuda()
+    for rounds in (1, 2, 3):
+        eng.reset()
+        for _ in range(rounds):
+            eng.accumulate(dW, dT)
+        eng.sync()
+        assert np.array_equal(eng.sum_hw.cpu().numpy(), rounds * ref["sum_hw"]), rounds
+        assert np.array_equal(eng.sum_w.cpu().numpy(), rounds * ref["sum_w"]), rounds
+    eng.close()
