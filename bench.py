@@ -75,6 +75,8 @@ def parse():
     ap.add_argument("--xt-tiles", type=int, default=0, choices=[0, 1, 2],
                     help="CPA_OPT_XT_TILES: int8 cross-term variant (0 = the library's cost model, 1 = two "
                          "sample tiles per unit, 2 = one tile with the spill overlapped)")
+    ap.add_argument("--kchunk", type=int, default=0,
+                    help="CPA_OPT_KCHUNK: traces per cross-term work unit (0 = the library's model)")
     ap.add_argument("--spill", type=int, default=0, choices=[0, 1, 2],
                     help="CPA_OPT_SPILL: int8 cross-term spill, 0 = auto (default), 1 = red.add.u64 per "
                          "element, 2 = bulk tensor reduce-add")
@@ -444,15 +446,17 @@ def main():
     if class_sums:
         eng.set_class_sums(True)
     eng.set_fuse_hist(args.fuse_hist == "1")
+    eng.set_xt_tiles(args.xt_tiles)
+    if args.kchunk:
+        eng.set_kchunk(args.kchunk)
     if not is_f32:
-        eng.set_xt_tiles(args.xt_tiles)
         eng.set_spill(args.spill)
     eng.set_col0(j0)
     ovl_mode = 0 if args.no_overlap else (args.overlap_mode if args.overlap_mode is not None else OVERLAP_DEFAULT)
     eng.set_overlap(ovl_mode)
     if is_f32 and world > 1:
         # float sums are centred per sample: every rank must use the same offsets
-        # (rank 0's first trace), or the combined sums mix differently-shifted data
+        # (rank 0's default ones), or the combined sums mix differently-shifted data
         MG.share_offsets(eng, dWv if rank == 0 else None)
     combine = ("columns" if shard == "samples" else args.combine) if world > 1 else "none"
     fused_note = None

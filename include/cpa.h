@@ -222,10 +222,10 @@ CPA_API cpa_status cpa_select(cpa_ctx *ctx, int32_t G, double *d_maxabs, int32_t
 /* CPA_F32 only: per-sample offsets o_j (device pointer, M floats; NULL = 0)
  * subtracted from every sample before the fp16 hi / e4m3 lo split.  rho is invariant
  * to per-sample offsets [S:285]; centring keeps the split and the fp32 tensor-
- * core accumulation accurate.  Default: the first trace of the first
- * cpa_accumulate call.  Multi-GPU: every rank must use the same offsets (the
+ * core accumulation accurate.  Default: the mean of the first <= 64 traces
+ * of the first cpa_accumulate call (cpa_default_offsets).  Multi-GPU: every rank must use the same offsets (the
  * accumulated sums are of the offset samples; a caller combining ranks sets
- * them explicitly, e.g. rank 0's first trace broadcast to every rank).  The
+ * them explicitly, e.g. rank 0's cpa_default_offsets broadcast to every rank).  The
  * finalize also reads them: SPEC's degenerate-column rule compares dw with the
  * RAW second moment [S:293], rebuilt from the centred sums and o_j.  Setting offsets also re-derives
  * the split's per-sample power-of-two scales (from the next accumulate's first
@@ -238,6 +238,13 @@ CPA_API cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets);
  * are centred on the same offsets before it adds them (paper_1412_7682_b200.
  * multigpu.check_same_offsets).  CPA_E_INVALID_ARG for an int context.       */
 CPA_API cpa_status cpa_get_offsets(cpa_ctx *ctx, float *d_out, int *is_set);
+/* CPA_F32 only: write the offsets the library would choose by default for the
+ * device traces d_traces (N rows, stride ld elements) -- the per-sample mean of
+ * the first min(N, 64) rows -- to d_out (device, M floats), asynchronously on
+ * the context's stream, without changing the context.  A multi-GPU caller runs
+ * it on one rank and broadcasts the result to every rank's cpa_set_offsets.  */
+CPA_API cpa_status cpa_default_offsets(cpa_ctx *ctx, const float *d_traces, int64_t ld, int64_t N,
+                                       float *d_out);
 
 CPA_API cpa_status cpa_reset(cpa_ctx *ctx);    /* zero the accumulator and the
                                                   non-finite flag (async) */
@@ -292,6 +299,11 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *                   overlaps the next unit's MMAs: short units, i.e. wide or
  *                   few traces; a4 then runs as a separate pass; measured
  *                   slower on B200).  Same exact sums either way.
+ *                   Float traces (CPA_F32): 0 (default) = 1 = two sample tiles
+ *                   per unit from one generated H tile, single-buffered fp32
+ *                   accumulators spilled every <= 16384 traces; 2 = one tile,
+ *                   double-buffered, every <= 4096 traces (measured slower,
+ *                   DESIGN.md).  Both within the float tolerance.
  *   CPA_OPT_SPILL:  how the int8 cross term adds each work unit's int32
  *                   accumulators into the int64 sum_hw: 1 = one
  *                   red.global.add.u64 per element; 2 = bulk tensor reduce-add

@@ -28,7 +28,7 @@ ABI_SYMBOLS = (
     "cpa_accum_words", "cpa_accum_bytes", "cpa_accum_offset", "cpa_init", "cpa_accumulate",
     "cpa_accumulate_host", "cpa_finalize", "cpa_finalize_async", "cpa_finalize_rows", "cpa_select",
     "cpa_set_row_owners", "cpa_ipc_export", "cpa_ipc_open", "cpa_ipc_close", "cpa_xterm_clock", "cpa_peer_atomics", "cpa_reset", "cpa_sync", "cpa_destroy",
-    "cpa_get_offsets",
+    "cpa_get_offsets", "cpa_default_offsets",
     "cpa_set_offsets", "cpa_set_option", "cpa_phase_times", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
     "cpa_aes_expand_key", "cpa_aes_invert_key_schedule",
 )
@@ -75,6 +75,7 @@ def _load():
         "cpa_destroy": (ST, [P]),
         "cpa_set_offsets": (ST, [P, P]),
         "cpa_get_offsets": (ST, [P, P, C.POINTER(C.c_int)]),
+        "cpa_default_offsets": (ST, [P, P, I64, I64, P]),
         "cpa_set_option": (ST, [P, C.c_int, I64]),
         "cpa_phase_times": (ST, [P, P, P]),
         "cpa_launch_count": (I64, [P]),
@@ -222,6 +223,12 @@ def cpa_get_offsets(ctx, d_out=None) -> bool:
     ok = C.c_int(0)
     _check(_lib.cpa_get_offsets(ctx, _ptr(d_out), C.byref(ok)), "cpa_get_offsets")
     return bool(ok.value)
+
+
+def cpa_default_offsets(ctx, d_traces, ld: int, N: int, d_out):
+    """The library's default offsets for these device traces (mean of the first
+    <= 64 rows) into d_out (device float32 [M]); asynchronous on the stream."""
+    _check(_lib.cpa_default_offsets(ctx, _ptr(d_traces), ld, N, _ptr(d_out)), "cpa_default_offsets")
 
 
 def cpa_set_option(ctx, option: int, value: int):

@@ -72,6 +72,12 @@ PFN_addr_range get_addr_range()
 constexpr int64_t kMaxTraces = 1LL << 23;  // exact-int64 bound of Eq. (1), see DESIGN.md
 constexpr int32_t kMaxSamples = 1 << 22;
 constexpr int64_t kStageBytes = 256LL << 20;  // bytes per staging chunk (cpa_accumulate_host / unaligned input)
+constexpr int64_t kOffsetRows = 64;            // float default offsets: mean of this many leading traces
+constexpr bool kF32DefaultNT2 = true;          // float cross term: NT = 2 variant by default
+#ifndef F32_MAX_UNIT_NT2
+#define F32_MAX_UNIT_NT2 16384
+#endif
+constexpr int64_t kF32MaxUnitNT2 = F32_MAX_UNIT_NT2;  // fp32 TMEM accumulation length bound (precision)
 constexpr int64_t kBulkSpillMinUnit = 65536;  // CPA_OPT_SPILL auto: bulk reduce from this unit length (traces) on
 
 }  // namespace
@@ -296,6 +302,20 @@ cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets)
     return CPA_OK;
 }
 
+cpa_status cpa_default_offsets(cpa_ctx *ctx, const float *d_traces, int64_t ld, int64_t N, float *d_out)
+{
+    if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
+    if (ctx->dtype != CPA_F32) return fail(CPA_E_INVALID_ARG, "offsets apply to CPA_F32 contexts only");
+    if (!d_traces || !d_out || N < 1 || ld < ctx->M) return fail(CPA_E_INVALID_ARG, "bad traces / N / ld / out");
+    CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+    int launches = 0;
+    CUDA_TRY(cpa::launch_mean_rows(d_traces, ld, N < kOffsetRows ? N : kOffsetRows, ctx->M, d_out, ctx->stream,
+                                   &launches),
+             "default offsets");
+    ctx->launches += launches;
+    return CPA_OK;
+}
+
 cpa_status cpa_get_offsets(cpa_ctx *ctx, float *d_out, int *is_set)
 {
     if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
@@ -457,9 +477,10 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                      "modelsums");
         // per-sample offsets (centring keeps the hi/lo split and the fp32
         // accumulation accurate; rho is invariant to them [S:285]): unless the
-        // caller set them, take the first trace of the first accumulate call
+        // caller set them, the mean of the first <= 64 traces of the first call
         if (!c->offset_set) {
-            CUDA_TRY(cudaMemcpyAsync(c->d_offset, d_w, sizeof(float) * M, cudaMemcpyDeviceToDevice, c->stream),
+            CUDA_TRY(cpa::launch_mean_rows((const float *)d_w, ld, n < kOffsetRows ? n : kOffsetRows, M, c->d_offset,
+                                           c->stream, &launches),
                      "offsets");
             c->offset_set = true;
         }
@@ -496,13 +517,15 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                                       &launches);
                      }),
                      "split_f32");
+            // float cross-term variant (CPA_OPT_XT_TILES): 1 = NT = 2, 2 = NT = 1, 0 = default
+            const bool nt2 = c->xt_tiles == 1 || (c->xt_tiles == 0 && kF32DefaultNT2);
             CUtensorMap mh, ml;
             cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)m};
             cuuint32_t estr[2] = {1, 1};
             for (int k = 0; k < 2; k++) {
                 // hi: 64 fp16 = the 128-byte swizzle span; lo: 128 e4m3 bytes; x one stage of traces
                 cuuint64_t strides[1] = {(cuuint64_t)(k ? ldl : ldh * 2)};
-                cuuint32_t box[2] = {k ? 128u : 64u, (cuuint32_t)cpa::xterm_f32_bk()};
+                cuuint32_t box[2] = {k ? 128u : 64u, (cuuint32_t)cpa::xterm_f32_bk(nt2)};
                 CUresult r = get_encode()(k ? &ml : &mh,
                                           k ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
                                           k ? (void *)c->d_lo : (void *)c->d_hi, dims, strides, box, estr,
@@ -510,12 +533,13 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
                 if (r != CUDA_SUCCESS) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled (hi/lo) failed (%d)", (int)r);
             }
-            const int64_t kc = c->kchunk ? (c->kchunk < 4096 ? c->kchunk : 4096)
-                                         : cpa::xterm_f32_auto_kchunk(M, m, c->num_sms);
+            const int64_t kmax = nt2 ? kF32MaxUnitNT2 : 4096;
+            const int64_t kc = c->kchunk ? (c->kchunk < kmax ? c->kchunk : kmax)
+                                         : cpa::xterm_f32_auto_kchunk(M, m, c->num_sms, nt2);
             CUDA_TRY(c->timed(2, [&] {
                          return cpa::launch_xterm_f32(mh, ml, d_tx + i0 * 16, c->d_vtab, acc, c->d_scale + M,
                                                       c->d_counter, M, m, kc, c->num_sms, c->stream, &launches,
-                                                      fhist ? c->d_hist : nullptr, c->d_clk);
+                                                      fhist ? c->d_hist : nullptr, c->d_clk, nt2);
                      }),
                      "xterm_f32");
             c->hw_zero = false;

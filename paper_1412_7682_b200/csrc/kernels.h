@@ -51,7 +51,7 @@ cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M,
 // a5: cross term (tcgen05 kind::i8, CTA pairs).  With d_sum_w / d_sum_w2 set,
 // the kernel also adds a4's sum W, sum W^2 (fused moments).
 int xterm_smem_bytes();
-int xterm_f32_bk();  // traces per stage of the float cross term (the TMA box height of its planes)
+int xterm_f32_bk(bool nt2);  // traces per stage of the float cross term variant (the TMA box height of its planes)
 int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms, bool remote_epilogue = false);
 // Variant choice: NT = 2 sample tiles per unit (A tile reused twice, a4 fused,
 // epilogue serialised with the unit's MMAs) or NT = 1 with double-buffered TMEM
@@ -82,17 +82,22 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const CUtensorMap *tmap_h
 // unit (A operands H 2^-16), spilled to fp64 times inv_scale[j] = 2^16 / s_j.  d_scale = [M] scale | [M] inv_scale;
 // a column whose |c s_j| reaches 2^15 in a chunk gets a smaller scale and its
 // planes rewritten before the cross term (d_scratch: 5 M + 16 bytes).
+// default float offsets: mean of the first n rows (the caller passes n <= 64)
+cudaError_t launch_mean_rows(const float *d_w, int64_t ld, int64_t n, int32_t M, float *d_out, cudaStream_t s,
+                             int *launches);
 cudaError_t launch_scale_f32(const float *d_w, int64_t ld, int64_t n, int32_t M, const float *d_offset,
                              float *d_scale, float *d_inv_scale, cudaStream_t s, int *launches);
 cudaError_t launch_split_f32(const float *d_w, int64_t ld, int64_t n, int32_t M, const float *d_offset,
                              const float *d_scale, uint16_t *d_hi, uint8_t *d_lo, int64_t ldh, int64_t ldl,
                              double *d_sum_w, double *d_sum_w2, int *d_nonfinite, uint8_t *d_scratch, cudaStream_t s,
                              int *launches);
-int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms);
+// nt2: the V_F32N variant (one H tile feeds two sample tiles, single-buffered
+// accumulators, units <= 16384 traces); else NT = 1 (double-buffered, <= 4096)
+int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms, bool nt2);
 cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
                              const uint8_t *d_vtab, double *d_hw, const float *d_inv_scale, int *d_counter, int32_t M,
                              int64_t N, int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
-                             uint32_t *d_hist = nullptr, unsigned long long *d_clk = nullptr);
+                             uint32_t *d_hist = nullptr, unsigned long long *d_clk = nullptr, bool nt2 = false);
 
 // a5 for the single-byte models (HW_LAST / HW_FIRST), class sums (classsum.cu):
 // counting sort of n traces by text byte per byte (perm: 16 x n int32, off: 16 x

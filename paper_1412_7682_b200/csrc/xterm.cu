@@ -82,17 +82,33 @@ namespace {
 // a4), V_F32 (a6), V_I8O (int8 with NT = 1 and double-buffered accumulators: the
 // epilogue overlaps the next unit's MMAs; for short units, where the spill of a
 // unit would otherwise stall the tensor pipe -- wide traces, few traces).
-constexpr int V_I8 = 0, V_F32 = 1, V_I8O = 2;
+// V_F32N (a6 with NT = 2): one generated H tile feeds two sample tiles (half the
+// generator stores and V reads per MMA, the smem port being what bounds V_F32),
+// single-buffered accumulators (the epilogue is exposed; units of <= 16384 traces,
+// 32 traces per stage, one ring: one commit frees a stage's H and W slots).
+constexpr int V_I8 = 0, V_F32 = 1, V_I8O = 2, V_F32N = 3;
+#ifndef XT_UNI_F32N
+#define XT_UNI_F32N 1
+#endif
+#ifndef XT_BK_F32N
+#define XT_BK_F32N 32
+#endif
+#ifndef XT_A_STAGES_F32N
+#define XT_A_STAGES_F32N 4
+#endif
+#ifndef XT_B_STAGES_F32N
+#define XT_B_STAGES_F32N 4
+#endif
 template <int V>
 struct Cfg {
-    static constexpr bool F32 = V == V_F32;
+    static constexpr bool F32 = V == V_F32 || V == V_F32N;
     static constexpr int ESZ = F32 ? 2 : 1;         // bytes per operand element
     static constexpr int KMMA = F32 ? 16 : 32;      // K per MMA instruction
     static constexpr int KB = F32 ? 1 : XT_KB_I8;   // key bytes per unit (A tiles sharing one W tile)
-    static constexpr int NT = V == V_I8 ? XT_NT_I8 : 1;  // N=256 sample tiles per unit (W tiles sharing one A tile)
-    static constexpr int NBUF = V == V_I8 ? 1 : 2;      // TMEM accumulator buffers
+    static constexpr int NT = V == V_I8 ? XT_NT_I8 : (V == V_F32N ? 2 : 1);  // N=256 sample tiles per unit
+    static constexpr int NBUF = (V == V_I8 || V == V_F32N) ? 1 : 2;           // TMEM accumulator buffers
     static constexpr int NACC = KB * NT;            // N=256 accumulators per unit
-    static constexpr int BK = F32 ? XT_BK_F32 : 128;  // traces per pipeline stage
+    static constexpr int BK = V == V_F32N ? XT_BK_F32N : (F32 ? XT_BK_F32 : 128);  // traces per pipeline stage
     static constexpr int BOX_X = 128 / ESZ;         // samples per TMA box (128-byte swizzle span)
     static constexpr int BH_BYTES = BK * 128 * ESZ; // one CTA's half (128 samples) of one N tile: W (I8) / hi (F32)
     static constexpr int BL_BYTES = F32 ? BK * 128 : 0;  // F32: the same half of the e4m3 lo plane
@@ -102,8 +118,11 @@ struct Cfg {
     static constexpr int A_STAGE = KB * A_BYTES + A8_BYTES;        // generated H tiles of one stage
     static constexpr int B_STAGE = NT * (BH_BYTES + BL_BYTES);     // TMA-loaded W tiles of one stage
     // separate rings: W (TMA, long latency) runs deeper than H (generated on chip)
-    static constexpr int A_STAGES = F32 ? XT_A_STAGES_F32 : XT_A_STAGES_I8;
-    static constexpr int B_STAGES = F32 ? XT_B_STAGES_F32 : XT_B_STAGES_I8;
+    static constexpr int A_STAGES = V == V_F32N ? XT_A_STAGES_F32N : (F32 ? XT_A_STAGES_F32 : XT_A_STAGES_I8);
+    static constexpr int B_STAGES = V == V_F32N ? XT_B_STAGES_F32N : (F32 ? XT_B_STAGES_F32 : XT_B_STAGES_I8);
+    // one ring (V_F32N): the H and W slots of a stage are freed by ONE commit (a
+    // tcgen05.commit costs tensor-pipe time; 6 MMAs per stage are too few to hide two)
+    static constexpr bool UNI = V == V_F32N && XT_UNI_F32N;
 };
 
 constexpr int BMC = 128;          // sub-keys per CTA (pair MMA M = 256)
@@ -159,9 +178,11 @@ constexpr bool cfg_ok()
 {
     using C = Cfg<V>;
     return C::A_STAGES * C::A_STAGE + C::B_STAGES * C::B_STAGE <= RINGS_BYTES && C::A_STAGES <= MAX_RING &&
+           (!C::UNI || C::A_STAGES == C::B_STAGES) &&
            C::B_STAGES <= MAX_RING && C::NACC * C::NBUF * BN == (int)TMEM_COLS;
 }
-static_assert(cfg_ok<V_I8>() && cfg_ok<V_F32>() && cfg_ok<V_I8O>(), "rings, barriers, TMEM columns");
+static_assert(cfg_ok<V_I8>() && cfg_ok<V_F32>() && cfg_ok<V_I8O>() && cfg_ok<V_F32N>(),
+              "rings, barriers, TMEM columns");
 static_assert(SMEM_ALLOC <= 232448, "shared memory");
 
 struct Params {
@@ -437,7 +458,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 const bool mom = !F32 && p.sum_w != nullptr;
                 for (int64_t tb = t0; tb < t1; tb += C::BK, it++) {
                     const int s = it % BS;
-                    mbar_wait(bempty_bar(s), ((it / BS) & 1) ^ 1);
+                    mbar_wait(C::UNI ? aempty_bar(s) : bempty_bar(s), ((it / BS) & 1) ^ 1);
                     if ((mpend >> s) & 1u) {  // the epilogue's moment pass over the old contents
                         mbar_wait(mdone_bar(s), (mph >> s) & 1u);
                         mph ^= 1u << s;
@@ -540,17 +561,21 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                         accum = 1;
                     }
                     if constexpr (F32) {
-                        // lo: (H 2^-16, e5m2) . (lo, e4m3), K = 32 rows of 128 bytes per MMA
-                        static_assert(C::KB == 1 && C::NT == 1, "F32 lo MMAs: one accumulator");
+                        // lo: (H 2^-16, e5m2) . (lo, e4m3), K = 32 rows of 128 bytes per MMA,
+                        // into the same accumulator as tile n's hi MMAs
+                        static_assert(C::KB == 1, "F32 lo MMAs: one key byte per unit");
                         const uint64_t a8 = ad + (uint64_t)(C::A_BYTES >> 4);
-                        const uint64_t b8 = bdd + (uint64_t)(C::BH_BYTES >> 4);
 #pragma unroll
-                        for (int k8 = 0; k8 < ((XT_EXP & 32) ? 0 : C::BK / 32); k8++)
-                            mma_f8_pair(dbase, a8 + (uint64_t)((k8 * 32 * 128) >> 4),
-                                        b8 + (uint64_t)((k8 * 32 * 128) >> 4), p.idesc8, 1u);
+                        for (int n = 0; n < C::NT; n++) {
+                            const uint64_t b8 = bdd + (uint64_t)((n * (C::BH_BYTES + C::BL_BYTES) + C::BH_BYTES) >> 4);
+#pragma unroll
+                            for (int k8 = 0; k8 < ((XT_EXP & 32) ? 0 : C::BK / 32); k8++)
+                                mma_f8_pair(dbase + n * BN, a8 + (uint64_t)((k8 * 32 * 128) >> 4),
+                                            b8 + (uint64_t)((k8 * 32 * 128) >> 4), p.idesc8, 1u);
+                        }
                     }
                     mma_commit_pair(aempty_bar(sa), 0x3);  // frees the slots in both CTAs when done
-                    mma_commit_pair(bempty_bar(sb), 0x3);
+                    if constexpr (!C::UNI) mma_commit_pair(bempty_bar(sb), 0x3);
                     if (++sa == AS) {
                         sa = 0;
                         pa ^= 1;
@@ -839,7 +864,7 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorM
     for (int b = 0; b < 16; b++) p.owners[b] = owners ? owners[b] : nullptr;
     p.clk = d_clk;
     p.bulk_spill = mhw != nullptr;
-    p.store_hw = store_hw && p.kc_count == 1 && owners == nullptr && V != V_F32;
+    p.store_hw = store_hw && p.kc_count == 1 && owners == nullptr && !Cf::F32;
     static std::atomic<unsigned long long> attr_set{0};
     cudaError_t e = smem_attr_once((const void *)k_xterm<V>, SMEM_ALLOC, attr_set);
     if (e != cudaSuccess) return e;
@@ -889,7 +914,7 @@ int64_t auto_kchunk(int32_t M, int64_t N, int num_sms, int kb, int nt, int bk, i
 }  // namespace
 
 int xterm_smem_bytes() { return SMEM_ALLOC; }
-int xterm_f32_bk() { return Cfg<V_F32>::BK; }
+int xterm_f32_bk(bool nt2) { return nt2 ? Cfg<V_F32N>::BK : Cfg<V_F32>::BK; }
 
 int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms, bool remote_epilogue)
 {
@@ -897,8 +922,16 @@ int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms, bool remote_epil
                        remote_epilogue ? 75000.0 : 25000.0);
 }
 
-int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms)
+int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms, bool nt2)
 {
+    // fp32 TMEM accumulation, spilled to fp64 per unit: <= 4096 traces (NT = 1,
+    // epilogue overlapped) or <= 16384 (NT = 2: the exposed epilogue amortised
+    // over 4x the traces; with mean-centred samples the fp32 partial sums stay
+    // small: max |drho| 2.4e-5 at full C3, tools/f32_unit_precision.py)
+#ifndef F32_MAX_UNIT_NT2
+#define F32_MAX_UNIT_NT2 16384
+#endif
+    if (nt2) return auto_kchunk(M, N, num_sms, 1, Cfg<V_F32N>::NT, Cfg<V_F32N>::BK, F32_MAX_UNIT_NT2, false);
     return auto_kchunk(M, N, num_sms, Cfg<V_F32>::KB, Cfg<V_F32>::NT, Cfg<V_F32>::BK, 4096, true);
 }
 
@@ -937,8 +970,12 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const CUtensorMap *tmap_h
 cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
                              const uint8_t *d_vtab, double *d_hw, const float *d_inv_scale, int *d_counter, int32_t M,
                              int64_t N, int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
-                             uint32_t *d_hist, unsigned long long *d_clk)
+                             uint32_t *d_hist, unsigned long long *d_clk, bool nt2)
 {
+    if (nt2)
+        return launch<V_F32N>(tmap_hi, tmap_lo, nullptr, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
+                              idesc_f16(2 * BMC, BN), num_sms, stream, launches, nullptr, nullptr, true, d_hist, nullptr,
+                              d_clk, idesc_e5m2_e4m3(2 * BMC, BN), d_inv_scale);
     return launch<V_F32>(tmap_hi, tmap_lo, nullptr, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                          idesc_f16(2 * BMC, BN),
                         num_sms, stream, launches, nullptr, nullptr, true, d_hist, nullptr, d_clk,

@@ -62,13 +62,13 @@ def allreduce_accumulator(acc, group=None):
 # ---- float traces: one set of per-sample offsets for every rank ---------------
 # The CPA_F32 sums are of centred samples w - o_j (include/cpa.h cpa_set_offsets);
 # partial sums of different ranks add up to the sums of ONE data set only if
-# every rank centred on the same o_j.  The library's default (each context's own
-# first trace) differs per rank, so a float multi-GPU run shares rank 0's.
+# every rank centred on the same o_j.  The library's default (from each context's
+# own first traces) differs per rank, so a float multi-GPU run shares rank 0's.
 
 def broadcast_offsets(first_trace, M: int, device, group=None, src: int = 0):
-    """Collective: rank `src` passes its first trace ([M] float32, any device),
-    the others anything (ignored); every rank returns the same [M] float32
-    tensor on `device`."""
+    """Collective: rank `src` passes its offsets ([M] float32, any device; e.g.
+    its first trace, or Engine.default_offsets), the others anything (ignored);
+    every rank returns the same [M] float32 tensor on `device`."""
     import torch
     import torch.distributed as dist
     world, rank = _world(group)
@@ -81,9 +81,12 @@ def broadcast_offsets(first_trace, M: int, device, group=None, src: int = 0):
 
 
 def share_offsets(engine, traces=None, group=None, src: int = 0):
-    """Set rank `src`'s first trace (traces[0], its shard's) as the offsets of
-    `engine` on every rank, before the first accumulate.  Returns them."""
-    t0 = traces[0] if traces is not None else None
+    """Set the offsets rank `src`'s engine would choose for its shard (the
+    library's default: the per-sample mean of its first <= 64 traces,
+    cpa_default_offsets) on every rank, before the first accumulate.  Returns
+    them."""
+    _, rank = _world(group)
+    t0 = engine.default_offsets(traces) if (rank == src and traces is not None) else None
     o = broadcast_offsets(t0, engine.M, engine.device, group, src)
     engine.set_offsets(o)
     return o

@@ -99,7 +99,7 @@ class StreamingAttack:
 
     def share_offsets(self, traces=None, src: int = 0):
         """Float traces, multi-GPU (collective, before the first add): centre
-        every rank's sums on rank `src`'s first trace (multigpu.share_offsets);
+        every rank's sums on rank `src`'s default offsets (multigpu.share_offsets);
         the checkpoint view finalizes with the same offsets."""
         from . import multigpu as MG
         o = MG.share_offsets(self.eng, traces, self.group, src)

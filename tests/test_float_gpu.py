@@ -194,7 +194,7 @@ def test_float_contexts_over_trace_shards_sum_exactly(P, parts):
     print(f"{parts} float shards: max |drho| = {err:.3g}")
     assert err <= TOL
     assert out["master_key"] == w.key
-    # the library default: each context's own first trace -> different offsets
+    # the library default: from each context's own first traces -> different offsets
     d = [P.Engine(w.m, P.CPA_F32, P.CPA_HD_LAST, 0) for _ in range(2)]
     for r, e in enumerate(d):
         i0, i1 = MG.shard_range(w.n, r, 2)
