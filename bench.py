@@ -449,8 +449,7 @@ def main():
     eng.set_xt_tiles(args.xt_tiles)
     if args.kchunk:
         eng.set_kchunk(args.kchunk)
-    if not is_f32:
-        eng.set_spill(args.spill)
+    eng.set_spill(args.spill)
     eng.set_col0(j0)
     ovl_mode = 0 if args.no_overlap else (args.overlap_mode if args.overlap_mode is not None else OVERLAP_DEFAULT)
     eng.set_overlap(ovl_mode)

@@ -222,7 +222,7 @@ CPA_API cpa_status cpa_select(cpa_ctx *ctx, int32_t G, double *d_maxabs, int32_t
 /* CPA_F32 only: per-sample offsets o_j (device pointer, M floats; NULL = 0)
  * subtracted from every sample before the fp16 hi / e4m3 lo split.  rho is invariant
  * to per-sample offsets [S:285]; centring keeps the split and the fp32 tensor-
- * core accumulation accurate.  Default: the mean of the first <= 64 traces
+ * core accumulation accurate.  Default: the mean of the first <= 1024 traces
  * of the first cpa_accumulate call (cpa_default_offsets).  Multi-GPU: every rank must use the same offsets (the
  * accumulated sums are of the offset samples; a caller combining ranks sets
  * them explicitly, e.g. rank 0's cpa_default_offsets broadcast to every rank).  The
@@ -240,7 +240,7 @@ CPA_API cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets);
 CPA_API cpa_status cpa_get_offsets(cpa_ctx *ctx, float *d_out, int *is_set);
 /* CPA_F32 only: write the offsets the library would choose by default for the
  * device traces d_traces (N rows, stride ld elements) -- the per-sample mean of
- * the first min(N, 64) rows -- to d_out (device, M floats), asynchronously on
+ * the first min(N, 1024) rows -- to d_out (device, M floats), asynchronously on
  * the context's stream, without changing the context.  A multi-GPU caller runs
  * it on one rank and broadcasts the result to every rank's cpa_set_offsets.  */
 CPA_API cpa_status cpa_default_offsets(cpa_ctx *ctx, const float *d_traces, int64_t ld, int64_t N,

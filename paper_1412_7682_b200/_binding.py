@@ -227,7 +227,7 @@ def cpa_get_offsets(ctx, d_out=None) -> bool:
 
 def cpa_default_offsets(ctx, d_traces, ld: int, N: int, d_out):
     """The library's default offsets for these device traces (mean of the first
-    <= 64 rows) into d_out (device float32 [M]); asynchronous on the stream."""
+    <= 1024 rows) into d_out (device float32 [M]); asynchronous on the stream."""
     _check(_lib.cpa_default_offsets(ctx, _ptr(d_traces), ld, N, _ptr(d_out)), "cpa_default_offsets")
 
 

@@ -72,7 +72,10 @@ PFN_addr_range get_addr_range()
 constexpr int64_t kMaxTraces = 1LL << 23;  // exact-int64 bound of Eq. (1), see DESIGN.md
 constexpr int32_t kMaxSamples = 1 << 22;
 constexpr int64_t kStageBytes = 256LL << 20;  // bytes per staging chunk (cpa_accumulate_host / unaligned input)
-constexpr int64_t kOffsetRows = 64;            // float default offsets: mean of this many leading traces
+#ifndef OFFSET_ROWS
+#define OFFSET_ROWS 1024
+#endif
+constexpr int64_t kOffsetRows = OFFSET_ROWS;   // float default offsets: mean of this many leading traces
 constexpr bool kF32DefaultNT2 = true;          // float cross term: NT = 2 variant by default
 #ifndef F32_MAX_UNIT_NT2
 #define F32_MAX_UNIT_NT2 16384
@@ -477,7 +480,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                      "modelsums");
         // per-sample offsets (centring keeps the hi/lo split and the fp32
         // accumulation accurate; rho is invariant to them [S:285]): unless the
-        // caller set them, the mean of the first <= 64 traces of the first call
+        // caller set them, the mean of the first <= 1024 traces of the first call
         if (!c->offset_set) {
             CUDA_TRY(cpa::launch_mean_rows((const float *)d_w, ld, n < kOffsetRows ? n : kOffsetRows, M, c->d_offset,
                                            c->stream, &launches),
@@ -536,8 +539,19 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
             const int64_t kmax = nt2 ? kF32MaxUnitNT2 : 4096;
             const int64_t kc = c->kchunk ? (c->kchunk < kmax ? c->kchunk : kmax)
                                          : cpa::xterm_f32_auto_kchunk(M, m, c->num_sms, nt2);
+            // fp64 spill by bulk tensor reduce-add (CPA_OPT_SPILL 0 / 2; M even)
+            CUtensorMap mhw;
+            bool bulk = (M % 2 == 0) && c->spill == 2;  // default: fp64 atomics (measured faster)
+            if (bulk) {
+                cuuint64_t hdims[2] = {(cuuint64_t)M, 4096};
+                cuuint64_t hstr[1] = {(cuuint64_t)M * 8};
+                cuuint32_t hbox[2] = {8, 32};
+                bulk = get_encode()(&mhw, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, acc, hdims, hstr, hbox, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            }
             CUDA_TRY(c->timed(2, [&] {
-                         return cpa::launch_xterm_f32(mh, ml, d_tx + i0 * 16, c->d_vtab, acc, c->d_scale + M,
+                         return cpa::launch_xterm_f32(mh, ml, bulk ? &mhw : nullptr, d_tx + i0 * 16, c->d_vtab, acc, c->d_scale + M,
                                                       c->d_counter, M, m, kc, c->num_sms, c->stream, &launches,
                                                       fhist ? c->d_hist : nullptr, c->d_clk, nt2);
                      }),

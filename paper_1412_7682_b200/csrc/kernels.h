@@ -82,7 +82,7 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const CUtensorMap *tmap_h
 // unit (A operands H 2^-16), spilled to fp64 times inv_scale[j] = 2^16 / s_j.  d_scale = [M] scale | [M] inv_scale;
 // a column whose |c s_j| reaches 2^15 in a chunk gets a smaller scale and its
 // planes rewritten before the cross term (d_scratch: 5 M + 16 bytes).
-// default float offsets: mean of the first n rows (the caller passes n <= 64)
+// default float offsets: mean of the first n rows (the caller passes n <= 1024)
 cudaError_t launch_mean_rows(const float *d_w, int64_t ld, int64_t n, int32_t M, float *d_out, cudaStream_t s,
                              int *launches);
 cudaError_t launch_scale_f32(const float *d_w, int64_t ld, int64_t n, int32_t M, const float *d_offset,
@@ -94,7 +94,10 @@ cudaError_t launch_split_f32(const float *d_w, int64_t ld, int64_t n, int32_t M,
 // nt2: the V_F32N variant (one H tile feeds two sample tiles, single-buffered
 // accumulators, units <= 16384 traces); else NT = 1 (double-buffered, <= 4096)
 int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms, bool nt2);
-cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
+// tmap_hw (may be null: fp64 atomics): sum_hw as fp64 [4096][M], box 8 x 32, 64B
+// swizzle -- the spill by bulk tensor reduce-add (M even)
+cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const CUtensorMap *tmap_hw,
+                             const uint8_t *d_texts,
                              const uint8_t *d_vtab, double *d_hw, const float *d_inv_scale, int *d_counter, int32_t M,
                              int64_t N, int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
                              uint32_t *d_hist = nullptr, unsigned long long *d_clk = nullptr, bool nt2 = false);

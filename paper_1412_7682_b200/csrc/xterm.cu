@@ -621,12 +621,13 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             uint32_t v[8];
             tmem_ld_32x32b_x8(tcol, v);
             tmem_ld_wait(v);
-            if (!F32 && p.bulk_spill && own == nullptr && !p.store_hw) {
-                // lane = accumulator row: its 8 samples as int64 into the warp's box (64 B
-                // per row, 16-byte chunks XOR-swizzled by (row >> 1) & 3 -- the TMA 64B
-                // swizzle, conflict-free STS.128), then ONE bulk tensor reduce-add of the
-                // 32 x 8 box into sum_hw by the TMA unit (exact int64 adds).  The box is
-                // rewritten only after the previous reduce has read it.
+            if (p.bulk_spill && own == nullptr && !p.store_hw) {
+                // lane = accumulator row: its 8 samples as int64 (I8) or as fp64 times
+                // 2^16 / s_j (F32) into the warp's box (64 B per row, 16-byte chunks
+                // XOR-swizzled by (row >> 1) & 3 -- the TMA 64B swizzle, conflict-free
+                // STS.128), then ONE bulk tensor reduce-add of the 32 x 8 box into sum_hw
+                // by the TMA unit (exact int64 adds / fp64 adds).  The box is rewritten
+                // only after the previous reduce has read it.
                 const uint32_t box = sbase + SMEM_TB + q * RB_BYTES;
                 const uint32_t rowb = box + lane * 64;
                 const uint32_t swz = ((uint32_t)lane >> 1) & 3;
@@ -638,9 +639,21 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     if (c + 1 < NC) tmem_ld_32x32b_x8(tcol + (c + 1) * 8, vn);
                     if (lane == 0) bulk_wait_read<0>();
                     __syncwarp();
+                    const int j = nt * (C::NT * BN) + cc * 8;
 #pragma unroll
                     for (int k = 0; k < 4; k++) {
-                        const int64_t a0 = (int64_t)(int32_t)v[2 * k], a1 = (int64_t)(int32_t)v[2 * k + 1];
+                        uint64_t a0, a1;
+                        if constexpr (F32) {  // same values as the atomic path: fp32 acc x 2^16 / s_j in fp64
+                            const int j0 = j + 2 * k < p.M ? j + 2 * k : p.M - 1;
+                            const int j1 = j + 2 * k + 1 < p.M ? j + 2 * k + 1 : p.M - 1;
+                            a0 = (uint64_t)__double_as_longlong((double)__uint_as_float(v[2 * k]) *
+                                                                (double)p.inv_scale[j0]);
+                            a1 = (uint64_t)__double_as_longlong((double)__uint_as_float(v[2 * k + 1]) *
+                                                                (double)p.inv_scale[j1]);
+                        } else {
+                            a0 = (uint64_t)(int64_t)(int32_t)v[2 * k];
+                            a1 = (uint64_t)(int64_t)(int32_t)v[2 * k + 1];
+                        }
                         asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowb + ((k ^ swz) << 4)),
                                      "r"((uint32_t)a0), "r"((uint32_t)(a0 >> 32)), "r"((uint32_t)a1),
                                      "r"((uint32_t)(a1 >> 32))
@@ -648,7 +661,6 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
-                    const int j = nt * (C::NT * BN) + cc * 8;
                     if (lane == 0 && !(XT_EXP & 4) && j < p.M) {
                         tma_reduce_add_2d(&tmap_hw, j, hrow0, box);
                         bulk_commit();
@@ -967,16 +979,17 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const CUtensorMap *tmap_h
                         d_hist, owners, d_clk, 0, nullptr, hw_zero);
 }
 
-cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const uint8_t *d_texts,
+cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const CUtensorMap *tmap_hw,
+                             const uint8_t *d_texts,
                              const uint8_t *d_vtab, double *d_hw, const float *d_inv_scale, int *d_counter, int32_t M,
                              int64_t N, int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
                              uint32_t *d_hist, unsigned long long *d_clk, bool nt2)
 {
     if (nt2)
-        return launch<V_F32N>(tmap_hi, tmap_lo, nullptr, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
+        return launch<V_F32N>(tmap_hi, tmap_lo, tmap_hw, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                               idesc_f16(2 * BMC, BN), num_sms, stream, launches, nullptr, nullptr, true, d_hist, nullptr,
                               d_clk, idesc_e5m2_e4m3(2 * BMC, BN), d_inv_scale);
-    return launch<V_F32>(tmap_hi, tmap_lo, nullptr, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
+    return launch<V_F32>(tmap_hi, tmap_lo, tmap_hw, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                          idesc_f16(2 * BMC, BN),
                         num_sms, stream, launches, nullptr, nullptr, true, d_hist, nullptr, d_clk,
                         idesc_e5m2_e4m3(2 * BMC, BN), d_inv_scale);

@@ -140,7 +140,7 @@ class Engine:
 
     def default_offsets(self, traces: torch.Tensor) -> torch.Tensor:
         """The offsets the library would choose for these device traces (the
-        per-sample mean of the first <= 64 rows), without setting them."""
+        per-sample mean of the first <= 1024 rows), without setting them."""
         assert traces.device == self.device and traces.dtype == torch.float32 and traces.stride(1) == 1
         out = torch.empty(self.M, dtype=torch.float32, device=self.device)
         B.cpa_default_offsets(self.ctx, traces, traces.stride(0), traces.shape[0], out)

@@ -82,7 +82,7 @@ def broadcast_offsets(first_trace, M: int, device, group=None, src: int = 0):
 
 def share_offsets(engine, traces=None, group=None, src: int = 0):
     """Set the offsets rank `src`'s engine would choose for its shard (the
-    library's default: the per-sample mean of its first <= 64 traces,
+    library's default: the per-sample mean of its first <= 1024 traces,
     cpa_default_offsets) on every rank, before the first accumulate.  Returns
     them."""
     _, rank = _world(group)
