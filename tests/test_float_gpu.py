@@ -20,8 +20,12 @@ def P():
     return P
 
 
-def gpu_rho(P, texts, W, offsets="default"):
+def gpu_rho(P, texts, W, offsets="default", xt=None, spill=None):
     eng = P.Engine(W.shape[1], P.CPA_F32, P.CPA_HD_LAST, 0)
+    if xt is not None:
+        eng.set_xt_tiles(xt)          # float cross-term variant: 1 = NT 2 (default), 2 = NT 1
+    if spill is not None:
+        eng.set_spill(spill)          # 2 = fp64 bulk tensor reduce-add
     if offsets is None:
         P.cpa_set_offsets(eng.ctx, None)
     eng.accumulate(torch.from_numpy(np.ascontiguousarray(W)).cuda(), torch.from_numpy(texts).cuda())
@@ -31,11 +35,12 @@ def gpu_rho(P, texts, W, offsets="default"):
     return out, n
 
 
+@pytest.mark.parametrize("xt,spill", [(None, None), (2, None), (1, 2), (2, 2)])
 @pytest.mark.parametrize("n,m", [(2000, 300), (65, 257), (130, 17)])
-def test_float_parity_all_cells(P, n, m):
+def test_float_parity_all_cells(P, n, m, xt, spill):
     w = S.CONFIGS["C3"].replace(n=n, m=m, a=0.02)
     texts, W = S.dataset(w)
-    out, cnt = gpu_rho(P, texts, W)
+    out, cnt = gpu_rho(P, texts, W, xt=xt, spill=spill)
     assert cnt == n
     shw, sw, sw2 = O.sums_f32(O.HD_LAST, texts, W)
     sh, sh2 = O.model_sums(O.HD_LAST, texts)
