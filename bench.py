@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-phase-times", action="store_true",
+                    help="no per-launch CUDA events inside the timed steps (the phase split and the "
+                         "roofline's kernel time are then unavailable)")
     ap.add_argument("--combine", choices=["auto", "fused", "rows", "allreduce"], default="auto",
                     help="N>1 trace shards: 'fused' = the cross-term kernel adds each key byte's rows "
                          "into the owner rank's accumulator over NVLink (cpa_set_row_owners), then "
@@ -541,7 +544,7 @@ def main():
         res = step()
     if is_f32 and world > 1 and shard == "traces":
         MG.check_same_offsets(eng)   # every rank's sums centred on the same offsets
-    eng.set_timing(True)
+    eng.set_timing(not args.no_phase_times)
     eng.phase_times()  # clear
     barrier()
     launches0 = eng.launches
@@ -612,7 +615,7 @@ def main():
 
     # ---- roofline of the dominant kernel (cross term, tensor-bound)
     peaks, src = load_peaks()
-    xt_ms = phase_ms["xterm"] / max(1, phase_n["xterm"])
+    xt_ms = phase_ms["xterm"] / max(1, phase_n["xterm"]) or float("nan")   # nan: --no-phase-times
     ops = 2.0 * 4096 * n_local * m_local   # algorithmic: one multiply-add per (h, i, j)
     achieved = ops / (xt_ms * 1e-3) / 1e12
     ratio = 1.0 if is_f32 else INT8_PER_BF16
@@ -836,7 +839,7 @@ def run_stream(args, w, dev, world, rank, local):
 
     for _ in range(args.warmup):
         step()
-    st.eng.set_timing(True)
+    st.eng.set_timing(not args.no_phase_times)
     st.eng.phase_times()
     barrier()
     launches0 = st.launches
@@ -887,7 +890,7 @@ def run_stream(args, w, dev, world, rank, local):
             st.close()
             st = st_main
     peaks, src = load_peaks()
-    xt_ms = phase_ms["xterm"] / max(1, phase_n["xterm"])
+    xt_ms = phase_ms["xterm"] / max(1, phase_n["xterm"]) or float("nan")   # nan: --no-phase-times
     ops = 2.0 * 4096 * n_local * w.m / max(1, phase_n["xterm"] // args.steps)  # per launch (one per chunk)
     achieved = ops / (xt_ms * 1e-3) / 1e12
     peak = peaks["bf16_tflops"] * INT8_PER_BF16
