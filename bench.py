@@ -813,7 +813,9 @@ def run_stream(args, w, dev, world, rank, local):
     # rank_buf and are read once per step; multi-GPU checkpoints block
     rank_buf = torch.empty((len(rounds), 4096), dtype=torch.int32, device=dev)
 
-    def step(curve=None):
+    def step():
+        """One streamed pass; returns (final result, the ranks of the blocking
+        checkpoints).  The non-blocking checkpoints' ranks stay in rank_buf."""
         st.reset()
         o = 0
         sync_ranks = {}
@@ -826,11 +828,15 @@ def run_stream(args, w, dev, world, rank, local):
             if last or not st.checkpoint_async(rank_buf[j]):
                 out = st.checkpoint(want_rho=last)
                 sync_ranks[j] = out["rank"]
-        if curve is not None:
-            for j, rnd in enumerate(rounds):
-                rk = sync_ranks.get(j, rank_buf[j])
-                curve.add(rnd[-1][2], rk[key_idx].tolist())
-        return out
+        return out, sync_ranks
+
+    def read_curve(sync_ranks):
+        """The key-rank curve of the last step (device reads: outside the timed region)."""
+        curve = Curve()
+        for j, rnd in enumerate(rounds):
+            rk = sync_ranks.get(j, rank_buf[j])
+            curve.add(rnd[-1][2], rk[key_idx].tolist())
+        return curve
 
     def barrier():
         if world > 1:
@@ -843,16 +849,16 @@ def run_stream(args, w, dev, world, rank, local):
     st.eng.phase_times()
     barrier()
     launches0 = st.launches
-    curve = Curve()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local, not args.no_clocks) as clk:
         ev0.record(stream)
         for s_ in range(args.steps):
-            out = step(curve if s_ == args.steps - 1 else None)
+            out, sync_ranks = step()
         ev1.record(stream)
         barrier()
     ms_total = ev0.elapsed_time(ev1)
+    curve = read_curve(sync_ranks)
     launches = st.launches - launches0
     phase_ms, phase_n = st.eng.phase_times()
     if world > 1:
@@ -880,7 +886,7 @@ def run_stream(args, w, dev, world, rank, local):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(st.eng.stream)
                 for _ in range(k2):
-                    o2 = step()
+                    o2, _ = step()
                 e1.record(st.eng.stream)
                 barrier()
                 t = torch.tensor([e0.elapsed_time(e1) / k2], dtype=torch.float64, device=dev)
