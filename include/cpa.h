@@ -301,7 +301,7 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *                   slower on B200).  Same exact sums either way.
  *                   Float traces (CPA_F32): 0 (default) = 1 = two sample tiles
  *                   per unit from one generated H tile, single-buffered fp32
- *                   accumulators spilled every <= 16384 traces; 2 = one tile,
+ *                   accumulators spilled every <= 24576 traces; 2 = one tile,
  *                   double-buffered, every <= 4096 traces (measured slower,
  *                   DESIGN.md).  Both within the float tolerance.
  *   CPA_OPT_SPILL:  how the int8 cross term adds each work unit's int32

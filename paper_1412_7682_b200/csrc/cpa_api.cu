@@ -78,7 +78,7 @@ constexpr int64_t kStageBytes = 256LL << 20;  // bytes per staging chunk (cpa_ac
 constexpr int64_t kOffsetRows = OFFSET_ROWS;   // float default offsets: mean of this many leading traces
 constexpr bool kF32DefaultNT2 = true;          // float cross term: NT = 2 variant by default
 #ifndef F32_MAX_UNIT_NT2
-#define F32_MAX_UNIT_NT2 16384
+#define F32_MAX_UNIT_NT2 24576
 #endif
 constexpr int64_t kF32MaxUnitNT2 = F32_MAX_UNIT_NT2;  // fp32 TMEM accumulation length bound (precision)
 constexpr int64_t kBulkSpillMinUnit = 65536;  // CPA_OPT_SPILL auto: bulk reduce from this unit length (traces) on

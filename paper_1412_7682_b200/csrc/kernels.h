@@ -92,7 +92,7 @@ cudaError_t launch_split_f32(const float *d_w, int64_t ld, int64_t n, int32_t M,
                              double *d_sum_w, double *d_sum_w2, int *d_nonfinite, uint8_t *d_scratch, cudaStream_t s,
                              int *launches);
 // nt2: the V_F32N variant (one H tile feeds two sample tiles, single-buffered
-// accumulators, units <= 16384 traces); else NT = 1 (double-buffered, <= 4096)
+// accumulators, units <= 24576 traces); else NT = 1 (double-buffered, <= 4096)
 int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms, bool nt2);
 // tmap_hw (may be null: fp64 atomics): sum_hw as fp64 [4096][M], box 8 x 32, 64B
 // swizzle -- the spill by bulk tensor reduce-add (M even)

@@ -84,7 +84,7 @@ namespace {
 // unit would otherwise stall the tensor pipe -- wide traces, few traces).
 // V_F32N (a6 with NT = 2): one generated H tile feeds two sample tiles (half the
 // generator stores and V reads per MMA, the smem port being what bounds V_F32),
-// single-buffered accumulators (the epilogue is exposed; units of <= 16384 traces,
+// single-buffered accumulators (the epilogue is exposed; units of <= 24576 traces,
 // 32 traces per stage, one ring: one commit frees a stage's H and W slots).
 constexpr int V_I8 = 0, V_F32 = 1, V_I8O = 2, V_F32N = 3;
 #ifndef XT_UNI_F32N
@@ -937,11 +937,11 @@ int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms, bool remote_epil
 int64_t xterm_f32_auto_kchunk(int32_t M, int64_t N, int num_sms, bool nt2)
 {
     // fp32 TMEM accumulation, spilled to fp64 per unit: <= 4096 traces (NT = 1,
-    // epilogue overlapped) or <= 16384 (NT = 2: the exposed epilogue amortised
+    // epilogue overlapped) or <= 24576 (NT = 2: the exposed epilogue amortised
     // over 4x the traces; with mean-centred samples the fp32 partial sums stay
     // small: max |drho| 2.4e-5 at full C3, tools/f32_unit_precision.py)
 #ifndef F32_MAX_UNIT_NT2
-#define F32_MAX_UNIT_NT2 16384
+#define F32_MAX_UNIT_NT2 24576
 #endif
     if (nt2) return auto_kchunk(M, N, num_sms, 1, Cfg<V_F32N>::NT, Cfg<V_F32N>::BK, F32_MAX_UNIT_NT2, false);
     return auto_kchunk(M, N, num_sms, Cfg<V_F32>::KB, Cfg<V_F32>::NT, Cfg<V_F32>::BK, 4096, true);
