@@ -13,8 +13,9 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-KERNELS = ["k_xterm", "k_moments_i8", "k_texthist", "k_hist_contract", "k_finalize_i8"]
-KERNELS_C3 = ["k_xterm_c3", "k_split_f32_c3"]  # float path (C3 bench step), tools/gpu_full.sh
+KERNELS = ["k_xterm", "k_moments_i8", "k_texthist", "k_hist_contract", "k_finalize_i8", "k_finalize_rows",
+           "k_finalize_maxima_c5"]
+KERNELS_C3 = ["k_xterm_c3", "k_split_f32_c3"]  # float path (C3 bench step), tools/ncu_r02.sh
 METRICS = {
     "duration_ms": ("gpu__time_duration.sum", 1e-3),  # reported in us by default -> ms below
     "dram_read_bytes": ("dram__bytes_read.sum", None),
