@@ -287,42 +287,31 @@ template <> struct Pair2<double> { using type = double2; };
 // so max|rho|, argmax and the signed peak are bit-identical to the full kernel.
 constexpr double kFinSkip = 1.0 - 3.552713678800501e-15;  // 1 - 2^-48
 
-// R rows per block: the per-sample terms (1/sqrt(dw), sum W) are loaded once per
-// column pair for all R rows (they are L2 reads of 16 B per cell otherwise, more
-// than the 8 B of sum_hw from HBM), and sqrt(dw) only for the rare candidates.
-template <int R, int U, typename T>
+template <int U, typename T>
 __global__ void __launch_bounds__(FIN_THREADS)
 k_finalize_maxima(const T *__restrict__ hw, const T *__restrict__ sw, const T *__restrict__ sh,
                   const T *__restrict__ sh2, const T *__restrict__ count, const double *__restrict__ sqrt_dw,
                   int32_t M, FinalizeOut o)
 {
-    const int hb = o.h0 + blockIdx.x * R;
-    const int nr = min(R, o.h1 - hb);
+    const int h = o.h0 + blockIdx.x;
     const T n = *count;
-    T s_h[R];
-    double den_h[R], abest[R];  // abest: a_j of the thread's best cell of row r (-1: none yet)
-    Best best[R];
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-        const int h = hb + (r < nr ? r : 0);
-        s_h[r] = sh[h];
-        den_h[r] = fin_den_h(n, s_h[r], sh2[h]);
-        best[r] = Best{-1.0, 0.0, 0x7fffffff};
-        abest[r] = -1.0;
-    }
-    const T *row0 = hw + (int64_t)hb * M;
+    const T s_h = sh[h];
+    const double den_h = fin_den_h(n, s_h, sh2[h]);
+    const T *row = hw + (int64_t)h * M;
     const double *rcp_w = sqrt_dw + M;
-    auto visit = [&](int r, T v, int j, double rw, T s_w) {
+    Best best{-1.0, 0.0, 0x7fffffff};
+    double abest = -1.0;  // a_j of the thread's best cell (-1: none yet)
+    auto visit = [&](T v, int j, double dw, double rw, T s_w) {
         double num;
-        if constexpr (std::is_integral<T>::value) num = __ll2double_rn(n * v - s_h[r] * s_w);
-        else num = __dsub_rn(__dmul_rn(n, v), __dmul_rn(s_h[r], s_w));
+        if constexpr (std::is_integral<T>::value) num = __ll2double_rn(n * v - s_h * s_w);
+        else num = __dsub_rn(__dmul_rn(n, v), __dmul_rn(s_h, s_w));
         const double a = __dmul_rn(fabs(num), rw);
-        if (a < abest[r] * kFinSkip) return;  // strictly below the best: skip the division
-        const double x = fin_cell(v, n, s_h[r], s_w, sqrt_dw[j], den_h[r]);
+        if (a < abest * kFinSkip) return;  // strictly below the best: skip the division
+        const double x = fin_cell(v, n, s_h, s_w, dw, den_h);
         const double ax = fabs(x);
-        if (ax > best[r].v) {
-            best[r] = Best{ax, x, j};
-            abest[r] = a;
+        if (ax > best.v) {
+            best = Best{ax, x, j};
+            abest = a;
         }
     };
     int j = 0;
@@ -331,61 +320,31 @@ k_finalize_maxima(const T *__restrict__ hw, const T *__restrict__ sw, const T *_
         const int M2 = M >> 1;
         int p0 = threadIdx.x;
         for (; p0 + (U - 1) * FIN_THREADS < M2; p0 += U * FIN_THREADS) {
-            T2 v[U][R];
+            T2 v[U];
 #pragma unroll
-            for (int u = 0; u < U; u++)
-#pragma unroll
-                for (int r = 0; r < R; r++)
-                    if (r < nr) v[u][r] = __ldcs((const T2 *)(row0 + (int64_t)r * M) + p0 + u * FIN_THREADS);
+            for (int u = 0; u < U; u++) v[u] = __ldcs((const T2 *)row + p0 + u * FIN_THREADS);
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const int p = p0 + u * FIN_THREADS;
+                const double2 dw = ((const double2 *)sqrt_dw)[p];
                 const double2 rw = ((const double2 *)rcp_w)[p];
                 const T2 swp = ((const T2 *)sw)[p];
-#pragma unroll
-                for (int r = 0; r < R; r++) {
-                    if (r >= nr) break;
-                    visit(r, v[u][r].x, 2 * p, rw.x, swp.x);
-                    visit(r, v[u][r].y, 2 * p + 1, rw.y, swp.y);
-                }
+                visit(v[u].x, 2 * p, dw.x, rw.x, swp.x);
+                visit(v[u].y, 2 * p + 1, dw.y, rw.y, swp.y);
             }
         }
         for (; p0 < M2; p0 += FIN_THREADS) {
+            const T2 v = __ldcs((const T2 *)row + p0);
+            const double2 dw = ((const double2 *)sqrt_dw)[p0];
             const double2 rw = ((const double2 *)rcp_w)[p0];
             const T2 swp = ((const T2 *)sw)[p0];
-#pragma unroll
-            for (int r = 0; r < R; r++) {
-                if (r >= nr) break;
-                const T2 v = __ldcs((const T2 *)(row0 + (int64_t)r * M) + p0);
-                visit(r, v.x, 2 * p0, rw.x, swp.x);
-                visit(r, v.y, 2 * p0 + 1, rw.y, swp.y);
-            }
+            visit(v.x, 2 * p0, dw.x, rw.x, swp.x);
+            visit(v.y, 2 * p0 + 1, dw.y, rw.y, swp.y);
         }
         j = M;
     }
-    for (j += threadIdx.x; j < M; j += FIN_THREADS) {
-#pragma unroll
-        for (int r = 0; r < R; r++)
-            if (r < nr) visit(r, row0[(int64_t)r * M + j], j, rcp_w[j], sw[j]);
-    }
-    // per-row block reductions (as k_finalize_rows)
-    __shared__ Best red[R][FIN_THREADS / 32];
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-        const Best b = warp_best(best[r]);
-        if ((threadIdx.x & 31) == 0) red[r][threadIdx.x >> 5] = b;
-    }
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int r = warp; r < nr; r += FIN_THREADS / 32) {
-        Best x = lane < FIN_THREADS / 32 ? red[r][lane] : Best{-1.0, 0.0, 0x7fffffff};
-        x = warp_best(x);
-        if (lane == 0) {
-            o.maxabs[hb + r] = x.v;
-            o.argmax[hb + r] = x.j + o.col0;
-            o.peak[hb + r] = x.r;
-        }
-    }
+    for (j += threadIdx.x; j < M; j += FIN_THREADS) visit(row[j], j, sqrt_dw[j], rcp_w[j], sw[j]);
+    block_best_store(best, h, o);
 }
 
 template <int R, int U, typename T>
@@ -734,17 +693,7 @@ static cudaError_t launch_fin(const T *hw, const T *sw, const T *sh, const T *sh
 {
     const int rows = o.h1 - o.h0;
     if (o.rho == nullptr && M >= kFinFilterMinM)
-    {
-#ifndef FIN_MAX_R
-#define FIN_MAX_R 2
-#endif
-#ifndef FIN_MAX_U
-#define FIN_MAX_U 2
-#endif
-        constexpr int R = FIN_MAX_R;
-        k_finalize_maxima<R, FIN_MAX_U, T><<<(rows + R - 1) / R, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw,
-                                                                                   M, o);
-    }
+        k_finalize_maxima<4, T><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
     else
         k_finalize_rows<1, 4, T><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
     return cudaGetLastError();
