@@ -588,8 +588,11 @@ def main():
             for _ in range(2):
                 step()
             t2, r2 = timed_steps(k2)
-            combine_ms[c] = t2 / k2
-            assert bytes(r2.master_key) == bytes(res.master_key), f"combine {c}: a different key"
+            # every rank holds the same result after the combine, so all take the same
+            # branch here: a mismatch is recorded, never raised (a raise on some ranks
+            # would leave the others waiting in a collective)
+            same = bytes(r2.master_key) == bytes(res.master_key)
+            combine_ms[c] = t2 / k2 if same else f"key mismatch ({t2 / k2:.3f} ms)"
         combine, h0, h1, rho = head
         if combine == "fused":
             use_owners(True)
@@ -892,7 +895,8 @@ def run_stream(args, w, dev, world, rank, local):
                 t = torch.tensor([e0.elapsed_time(e1) / k2], dtype=torch.float64, device=dev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 combine_ms["fused" if other else "rows"] = float(t.item())
-                assert bytes(o2["master_key"]) == bytes(out["master_key"])
+                if bytes(o2["master_key"]) != bytes(out["master_key"]):   # recorded, never raised (collectives)
+                    combine_ms["fused" if other else "rows"] = f"key mismatch ({float(t.item()):.3f} ms)"
             st.close()
             st = st_main
     peaks, src = load_peaks()
