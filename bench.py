@@ -80,9 +80,9 @@ def parse():
                          "sample tiles per unit, 2 = one tile with the spill overlapped)")
     ap.add_argument("--kchunk", type=int, default=0,
                     help="CPA_OPT_KCHUNK: traces per cross-term work unit (0 = the library's model)")
-    ap.add_argument("--spill", type=int, default=0, choices=[0, 1, 2],
-                    help="CPA_OPT_SPILL: int8 cross-term spill, 0 = auto (default), 1 = red.add.u64 per "
-                         "element, 2 = bulk tensor reduce-add")
+    ap.add_argument("--spill", type=int, default=0, choices=[0, 1, 2, 3],
+                    help="CPA_OPT_SPILL: cross-term spill, 0 = auto (default), 1 = red.add per "
+                         "element, 2 = bulk tensor reduce-add, 3 = per-chunk partial stores + one reduce pass")
     ap.add_argument("--chunk", type=int, default=0,
                     help="stream the traces in chunks of this many, finalizing after every round "
                          "(key-rank curve); default for C5: 65536")

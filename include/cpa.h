@@ -304,13 +304,19 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *                   accumulators spilled every <= 24576 traces; 2 = one tile,
  *                   double-buffered, every <= 4096 traces (measured slower,
  *                   DESIGN.md).  Both within the float tolerance.
- *   CPA_OPT_SPILL:  how the int8 cross term adds each work unit's int32
- *                   accumulators into the int64 sum_hw: 1 = one
- *                   red.global.add.u64 per element; 2 = bulk tensor reduce-add
+ *   CPA_OPT_SPILL:  how the cross term adds each work unit's 32-bit TMEM
+ *                   accumulators into sum_hw: 1 = one red.global.add per
+ *                   element; 2 = bulk tensor reduce-add
  *                   (cp.reduce.async.bulk.tensor: the TMA unit adds 32 x 8
- *                   int64 boxes; needs M even and no row owners, else 1);
- *                   0 (default) = 2 for work units of >= 65536 traces, else 1
- *                   (measured).  Exact either way.                 */
+ *                   int64 / fp64 boxes; needs M even and no row owners, else
+ *                   1); 3 = partial sums: each unit STORES its raw int32 /
+ *                   fp32 accumulators into its trace chunk's slice of a
+ *                   scratch buffer (4096 x 4 B per sample per chunk, <= 3 GiB,
+ *                   allocated on first use; else 1), then one pass adds the
+ *                   slices into sum_hw (no row owners).  0 (default): int8 =
+ *                   2 for work units of >= 65536 traces, else 1; float = 1
+ *                   (measured).  Exact (int8) / within the float
+ *                   tolerance (float) either way.                             */
 enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2, CPA_OPT_OVERLAP = 3, CPA_OPT_STAGE_BYTES = 4,
        CPA_OPT_COL0 = 5, CPA_OPT_CLASS_SUMS = 6, CPA_OPT_FUSE_HIST = 7, CPA_OPT_XT_TILES = 8,
        CPA_OPT_SPILL = 9 };
@@ -319,8 +325,9 @@ CPA_API cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value);
 /* Per-phase device time (ms) and launch count since the last call, from the
  * CPA_OPT_TIMING events; synchronises the stream.  Phases:
  *   0 model sums (a3)  1 trace moments (a4)  2 cross term (a5/a6)
- *   3 Eq. (1) finalize (a8)  4 phase-4 ranking (a9)                         */
-enum { CPA_NUM_PHASES = 5 };
+ *   3 Eq. (1) finalize (a8)  4 phase-4 ranking (a9)
+ *   5 partial-sum reduce of the cross term (CPA_OPT_SPILL 3)                */
+enum { CPA_NUM_PHASES = 6 };
 CPA_API cpa_status cpa_phase_times(cpa_ctx *ctx, double ms[CPA_NUM_PHASES],
                                    int64_t launches[CPA_NUM_PHASES]);
 

@@ -19,8 +19,8 @@ CPA_S8, CPA_U8, CPA_F32 = 0, 1, 2
 CPA_HD_LAST, CPA_HW_LAST, CPA_HW_FIRST = 0, 1, 2
 (CPA_OPT_KCHUNK, CPA_OPT_TIMING, CPA_OPT_OVERLAP, CPA_OPT_STAGE_BYTES, CPA_OPT_COL0, CPA_OPT_CLASS_SUMS,
  CPA_OPT_FUSE_HIST, CPA_OPT_XT_TILES, CPA_OPT_SPILL) = 1, 2, 3, 4, 5, 6, 7, 8, 9
-CPA_NUM_PHASES = 5
-PHASE_NAMES = ("modelsums", "moments", "xterm", "finalize", "phase4")
+CPA_NUM_PHASES = 6
+PHASE_NAMES = ("modelsums", "moments", "xterm", "finalize", "phase4", "spill_reduce")
 FIELD_HW, FIELD_W, FIELD_W2, FIELD_H, FIELD_H2, FIELD_N = range(6)
 
 # every symbol include/cpa.h declares (checked by tests/test_abi.py)

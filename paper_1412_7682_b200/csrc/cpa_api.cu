@@ -81,6 +81,11 @@ constexpr bool kF32DefaultNT2 = true;          // float cross term: NT = 2 varia
 #define F32_MAX_UNIT_NT2 24576
 #endif
 constexpr int64_t kF32MaxUnitNT2 = F32_MAX_UNIT_NT2;  // fp32 TMEM accumulation length bound (precision)
+// partial-sum spill (CPA_OPT_SPILL 3): bound on the 32-bit slice buffer.  Off
+// by default: at C3 the cross term ran 0.12 ms faster with plain stores, and the
+// reduce pass (5 slices + the sum_hw read-modify-write) cost it back
+constexpr int64_t kPartMaxBytes = 3LL << 30;
+constexpr bool kF32PartialSpill = false;
 constexpr int64_t kBulkSpillMinUnit = 65536;  // CPA_OPT_SPILL auto: bulk reduce from this unit length (traces) on
 
 }  // namespace
@@ -128,7 +133,27 @@ struct cpa_ctx {
     int class_sums = 0;
     int fuse_hist = 0;
     int xt_tiles = 0;  // CPA_OPT_XT_TILES: 0 model, 1 NT = 2, 2 NT = 1 overlapped
-    int spill = 0;  // CPA_OPT_SPILL: 0 auto, 1 red.add.u64 per element, 2 bulk tensor reduce-add
+    int spill = 0;  // CPA_OPT_SPILL: 0 auto, 1 red.add per element, 2 bulk tensor reduce-add, 3 partial stores
+    uint32_t *d_part = nullptr;  // partial-sum spill slices [kc][4096][ld] (32-bit), grown on demand
+    int64_t part_bytes = 0;
+    // the partial buffer for kc_count slices of part_ld samples (null: over the
+    // memory bound or the allocation failed -- the caller falls back to atomics)
+    uint32_t *part_buffer(int64_t kc_count, int64_t part_ld) {
+        const int64_t need = kc_count * 4096 * part_ld * 4;
+        if (need > kPartMaxBytes) return nullptr;
+        if (need > part_bytes) {
+            if (cudaStreamSynchronize(stream) != cudaSuccess) return nullptr;
+            cudaFree(d_part);
+            d_part = nullptr;
+            part_bytes = 0;
+            if (cudaMalloc(&d_part, need) != cudaSuccess) {
+                cudaGetLastError();
+                return nullptr;
+            }
+            part_bytes = need;
+        }
+        return d_part;
+    }
     // cpa_set_row_owners: fused multi-GPU combine (key byte b's sum_hw rows go to owners[b])
     int64_t *owners[16] = {};
     bool owners_set = false;
@@ -366,7 +391,7 @@ cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
         return CPA_OK;
     }
     if (option == CPA_OPT_SPILL) {
-        if (value < 0 || value > 2) return fail(CPA_E_INVALID_ARG, "SPILL=%lld outside [0, 2]", (long long)value);
+        if (value < 0 || value > 3) return fail(CPA_E_INVALID_ARG, "SPILL=%lld outside [0, 3]", (long long)value);
         ctx->spill = (int)value;
         return CPA_OK;
     }
@@ -513,6 +538,8 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
         for (int64_t i0 = 0; i0 < n; i0 += chunk) {
             const int64_t m = (n - i0) < chunk ? (n - i0) : chunk;
             const float *w = (const float *)d_w + i0 * ld;
+            // float cross-term variant (CPA_OPT_XT_TILES): 1 = NT = 2, 2 = NT = 1, 0 = default
+            const bool nt2 = c->xt_tiles == 1 || (c->xt_tiles == 0 && kF32DefaultNT2);
             CUDA_TRY(c->timed(1, [&] {
                          return cpa::launch_split_f32(w, ld, m, M, c->d_offset, c->d_scale, c->d_hi, c->d_lo, ldh,
                                                       ldl, acc + cpa_accum_offset(M, 1), acc + cpa_accum_offset(M, 2),
@@ -520,8 +547,6 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                                       &launches);
                      }),
                      "split_f32");
-            // float cross-term variant (CPA_OPT_XT_TILES): 1 = NT = 2, 2 = NT = 1, 0 = default
-            const bool nt2 = c->xt_tiles == 1 || (c->xt_tiles == 0 && kF32DefaultNT2);
             CUtensorMap mh, ml;
             cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)m};
             cuuint32_t estr[2] = {1, 1};
@@ -550,12 +575,25 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
             }
+            // partial-sum spill (CPA_OPT_SPILL 3): raw fp32 stores per trace
+            // chunk, then one reduce pass adds them (x 2^16 / s_j) into sum_hw
+            const int64_t part_ld = (M + 7) / 8 * 8;
+            const int64_t kcount = (m + kc - 1) / kc;
+            uint32_t *part = (!bulk && (c->spill == 3 || (c->spill == 0 && kF32PartialSpill)))
+                                 ? c->part_buffer(kcount, part_ld) : nullptr;
             CUDA_TRY(c->timed(2, [&] {
-                         return cpa::launch_xterm_f32(mh, ml, bulk ? &mhw : nullptr, d_tx + i0 * 16, c->d_vtab, acc, c->d_scale + M,
-                                                      c->d_counter, M, m, kc, c->num_sms, c->stream, &launches,
-                                                      fhist ? c->d_hist : nullptr, c->d_clk, nt2);
+                         return cpa::launch_xterm_f32(mh, ml, bulk ? &mhw : nullptr, d_tx + i0 * 16, c->d_vtab, acc,
+                                                      c->d_scale + M, c->d_counter, M, m, kc, c->num_sms, c->stream,
+                                                      &launches, fhist ? c->d_hist : nullptr, c->d_clk, nt2, part,
+                                                      part_ld);
                      }),
                      "xterm_f32");
+            if (part != nullptr)
+                CUDA_TRY(c->timed(5, [&] {
+                             return cpa::launch_part_reduce_f32(part, (int32_t)kcount, part_ld, M, c->d_scale + M, acc,
+                                                                c->stream, &launches);
+                         }),
+                         "spill reduce");
             c->hw_zero = false;
         }
         if (fhist)
@@ -642,15 +680,28 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
+    // partial-sum spill (CPA_OPT_SPILL 3; not with row owners): raw int32 stores
+    // per trace chunk, then one exact reduce pass into the int64 sum_hw
+    const int64_t part_ld = (M + 7) / 8 * 8;
+    const int64_t kcount = (n + kc - 1) / kc;
+    uint32_t *part = (!c->owners_set && c->spill == 3) ? c->part_buffer(kcount, part_ld) : nullptr;
+    if (part != nullptr) bulk = false;
     CUDA_TRY(c->timed(2, [&] {
-                 return cpa::launch_xterm_i8(tmap, bulk ? &tmap_hw : nullptr, d_tx, c->d_vtab, acc, c->d_counter, M,
-                                             n, kc, sgn, c->num_sms,
-                                             c->stream, &launches, fused ? acc + cpa_accum_offset(M, 1) : nullptr,
-                                             fused ? acc + cpa_accum_offset(M, 2) : nullptr,
-                                             fhist ? c->d_hist : nullptr, c->owners_set ? c->owners : nullptr,
-                                             c->d_clk, plan.overlapped, c->hw_zero);
+                 cudaError_t e = cpa::launch_xterm_i8(tmap, bulk ? &tmap_hw : nullptr, d_tx, c->d_vtab, acc,
+                                                      c->d_counter, M, n, kc, sgn, c->num_sms, c->stream, &launches,
+                                                      fused ? acc + cpa_accum_offset(M, 1) : nullptr,
+                                                      fused ? acc + cpa_accum_offset(M, 2) : nullptr,
+                                                      fhist ? c->d_hist : nullptr, c->owners_set ? c->owners : nullptr,
+                                                      c->d_clk, plan.overlapped, part ? false : c->hw_zero, part,
+                                                      part_ld);
+                 return e;
              }),
              "xterm_i8");
+    if (part != nullptr)
+        CUDA_TRY(c->timed(5, [&] {
+                     return cpa::launch_part_reduce_i32(part, (int32_t)kcount, part_ld, M, acc, c->stream, &launches);
+                 }),
+                 "spill reduce");
     c->hw_zero = false;
     if (!fused && mode == 1) CUDA_TRY(moments(), "moments");
     if (fhist)
@@ -1094,6 +1145,7 @@ cpa_status cpa_destroy(cpa_ctx *c)
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     cudaFree(c->d_offset);
     cudaFree(c->d_scale);
+    cudaFree(c->d_part);
     cudaFree(c->d_hi);
     cudaFree(c->d_lo);
     cudaFree(c->d_nonfinite);

@@ -299,20 +299,41 @@ k_finalize_maxima(const T *__restrict__ hw, const T *__restrict__ sw, const T *_
     const double den_h = fin_den_h(n, s_h, sh2[h]);
     const T *row = hw + (int64_t)h * M;
     const double *rcp_w = sqrt_dw + M;
+    // Skip threshold shared by the block (= the row): the largest a_best (1 - 2^-48)
+    // any thread has seen.  A cell below it is strictly below THAT thread's best
+    // cell, so it can be neither the row's maximum nor tie with it, whichever
+    // thread and sample it belongs to.  (A per-thread threshold let each lane's
+    // first few, still-rising maxima through: nearly every warp step ran some
+    // lane's fp64 division, and the kernel was issue-bound, ~3 TB/s.)  Positive
+    // doubles order as their bit patterns: the maximum is an integer atomicMax.
+    __shared__ unsigned long long s_thr;
+    if (threadIdx.x == 0) s_thr = 0ull;
+    __syncthreads();
     Best best{-1.0, 0.0, 0x7fffffff};
-    double abest = -1.0;  // a_j of the thread's best cell (-1: none yet)
-    auto visit = [&](T v, int j, double dw, double rw, T s_w) {
+    double thr = 0.0;  // this thread's copy of the block threshold (refreshed per group)
+    // sqrt(dw_j) is only needed by the (now rare) cells that pass the filter:
+    // loaded there (hoisting the group's per-sample loads ahead of its cells
+    // measured slower: 88 registers, half the resident blocks)
+    auto visit = [&](T v, int j, double rw, T s_w) {
         double num;
         if constexpr (std::is_integral<T>::value) num = __ll2double_rn(n * v - s_h * s_w);
         else num = __dsub_rn(__dmul_rn(n, v), __dmul_rn(s_h, s_w));
         const double a = __dmul_rn(fabs(num), rw);
-        if (a < abest * kFinSkip) return;  // strictly below the best: skip the division
-        const double x = fin_cell(v, n, s_h, s_w, dw, den_h);
+        if (a < thr) return;  // strictly below some thread's best: skip the division
+        const double x = fin_cell(v, n, s_h, s_w, sqrt_dw[j], den_h);
         const double ax = fabs(x);
         if (ax > best.v) {
             best = Best{ax, x, j};
-            abest = a;
+            const double t = __dmul_rn(a, kFinSkip);
+            if (t > thr) {
+                thr = t;
+                atomicMax(&s_thr, (unsigned long long)__double_as_longlong(t));
+            }
         }
+    };
+    auto refresh = [&] {
+        const double t = __longlong_as_double((long long)*(volatile unsigned long long *)&s_thr);
+        if (t > thr) thr = t;
     };
     int j = 0;
     if ((M & 1) == 0) {
@@ -323,27 +344,26 @@ k_finalize_maxima(const T *__restrict__ hw, const T *__restrict__ sw, const T *_
             T2 v[U];
 #pragma unroll
             for (int u = 0; u < U; u++) v[u] = __ldcs((const T2 *)row + p0 + u * FIN_THREADS);
+            refresh();
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const int p = p0 + u * FIN_THREADS;
-                const double2 dw = ((const double2 *)sqrt_dw)[p];
                 const double2 rw = ((const double2 *)rcp_w)[p];
                 const T2 swp = ((const T2 *)sw)[p];
-                visit(v[u].x, 2 * p, dw.x, rw.x, swp.x);
-                visit(v[u].y, 2 * p + 1, dw.y, rw.y, swp.y);
+                visit(v[u].x, 2 * p, rw.x, swp.x);
+                visit(v[u].y, 2 * p + 1, rw.y, swp.y);
             }
         }
         for (; p0 < M2; p0 += FIN_THREADS) {
             const T2 v = __ldcs((const T2 *)row + p0);
-            const double2 dw = ((const double2 *)sqrt_dw)[p0];
             const double2 rw = ((const double2 *)rcp_w)[p0];
             const T2 swp = ((const T2 *)sw)[p0];
-            visit(v.x, 2 * p0, dw.x, rw.x, swp.x);
-            visit(v.y, 2 * p0 + 1, dw.y, rw.y, swp.y);
+            visit(v.x, 2 * p0, rw.x, swp.x);
+            visit(v.y, 2 * p0 + 1, rw.y, swp.y);
         }
         j = M;
     }
-    for (j += threadIdx.x; j < M; j += FIN_THREADS) visit(row[j], j, sqrt_dw[j], rcp_w[j], sw[j]);
+    for (j += threadIdx.x; j < M; j += FIN_THREADS) visit(row[j], j, rcp_w[j], sw[j]);
     block_best_store(best, h, o);
 }
 
@@ -1033,6 +1053,98 @@ cudaError_t launch_split_f32(const float *d_w, int64_t ld, int64_t n, int32_t M,
     dim3 grid1((M + SP_THREADS - 1) / SP_THREADS, grid.y);
     k_resplit_f32<<<grid1, SP_THREADS, 0, s>>>(range, colflag, d_w, ld, n, M, d_offset, d_scale, d_hi, d_lo, ldh, ldl);
     if (launches) (*launches) += 3;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Partial-sum spill, second half: the cross term stored each work unit's raw
+// 32-bit accumulators into its trace chunk's slice part[kc][4096][part_ld]; add
+// the slices into sum_hw.  Thread = 4 consecutive samples of one row (16-byte
+// loads of every slice, all in flight before the adds).
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int PR_THREADS = 256;
+constexpr int PR_MAXKC = 8;  // slices loaded ahead per batch
+template <bool F32>
+__global__ void __launch_bounds__(PR_THREADS)
+k_part_reduce(const uint32_t *__restrict__ part, int32_t kc_count, int64_t part_ld, int32_t M,
+              const float *__restrict__ inv_scale, void *hw)
+{
+    const int64_t q4 = part_ld / 4;
+    const int64_t slice = 4096 * part_ld;
+    for (int64_t g = (int64_t)blockIdx.x * PR_THREADS + threadIdx.x; g < 4096 * q4; g += (int64_t)gridDim.x * PR_THREADS) {
+        const int64_t h = g / q4;
+        const int j0 = (int)(g - h * q4) * 4;
+        if (j0 >= M) continue;
+        const uint4 *src = (const uint4 *)(part + h * part_ld + j0);
+        if constexpr (F32) {
+            double a[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int k0 = 0; k0 < kc_count; k0 += PR_MAXKC) {
+                uint4 v[PR_MAXKC];
+#pragma unroll
+                for (int k = 0; k < PR_MAXKC; k++)
+                    if (k0 + k < kc_count) v[k] = __ldcs(src + (k0 + k) * (slice / 4));
+#pragma unroll
+                for (int k = 0; k < PR_MAXKC; k++)
+                    if (k0 + k < kc_count) {
+                        a[0] += (double)__uint_as_float(v[k].x);
+                        a[1] += (double)__uint_as_float(v[k].y);
+                        a[2] += (double)__uint_as_float(v[k].z);
+                        a[3] += (double)__uint_as_float(v[k].w);
+                    }
+            }
+            double *row = (double *)hw + h * M;
+#pragma unroll
+            for (int e = 0; e < 4; e++)
+                if (j0 + e < M) row[j0 + e] += a[e] * (double)inv_scale[j0 + e];  // power of two: exact
+        } else {
+            int64_t a[4] = {0, 0, 0, 0};
+            for (int k0 = 0; k0 < kc_count; k0 += PR_MAXKC) {
+                uint4 v[PR_MAXKC];
+#pragma unroll
+                for (int k = 0; k < PR_MAXKC; k++)
+                    if (k0 + k < kc_count) v[k] = __ldcs(src + (k0 + k) * (slice / 4));
+#pragma unroll
+                for (int k = 0; k < PR_MAXKC; k++)
+                    if (k0 + k < kc_count) {
+                        a[0] += (int32_t)v[k].x;
+                        a[1] += (int32_t)v[k].y;
+                        a[2] += (int32_t)v[k].z;
+                        a[3] += (int32_t)v[k].w;
+                    }
+            }
+            int64_t *row = (int64_t *)hw + h * M;
+#pragma unroll
+            for (int e = 0; e < 4; e++)
+                if (j0 + e < M) row[j0 + e] += a[e];
+        }
+    }
+}
+int part_reduce_grid(int64_t part_ld)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t need = (4096 * (part_ld / 4) + PR_THREADS - 1) / PR_THREADS;
+    const int64_t cap = (int64_t)sms * 8;  // 8 resident blocks per SM, grid-stride beyond
+    return (int)(need < cap ? need : cap);
+}
+}  // namespace
+
+cudaError_t launch_part_reduce_i32(const uint32_t *d_part, int32_t kc_count, int64_t part_ld, int32_t M,
+                                   int64_t *d_hw, cudaStream_t s, int *launches)
+{
+    k_part_reduce<false><<<part_reduce_grid(part_ld), PR_THREADS, 0, s>>>(d_part, kc_count, part_ld, M, nullptr, d_hw);
+    if (launches) (*launches)++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_part_reduce_f32(const uint32_t *d_part, int32_t kc_count, int64_t part_ld, int32_t M,
+                                   const float *d_inv_scale, double *d_hw, cudaStream_t s, int *launches)
+{
+    k_part_reduce<true><<<part_reduce_grid(part_ld), PR_THREADS, 0, s>>>(d_part, kc_count, part_ld, M, d_inv_scale,
+                                                                         d_hw);
+    if (launches) (*launches)++;
     return cudaGetLastError();
 }
 

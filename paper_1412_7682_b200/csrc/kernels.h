@@ -72,7 +72,18 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const CUtensorMap *tmap_h
                             bool w_signed, int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr,
                             int64_t *d_sum_w2 = nullptr, uint32_t *d_hist = nullptr,
                             int64_t *const *owners = nullptr, unsigned long long *d_clk = nullptr,
-                            bool overlapped = false, bool hw_zero = false);
+                            bool overlapped = false, bool hw_zero = false, uint32_t *d_part = nullptr,
+                            int64_t part_ld = 0);
+// Partial-sum spill (d_part non-null, part_ld >= M a multiple of 8): every work
+// unit stores its raw 32-bit accumulators into part[kc][4096][part_ld] (kc = its
+// trace chunk) instead of adding them into sum_hw; then launch_part_reduce adds
+//   I8:  sum_hw[h][j] += sum_kc (int64) part[kc][h][j]                (exact)
+//   F32: sum_hw[h][j] += (sum_kc (double) part[kc][h][j]) * inv_scale[j]
+// (inv_scale a power of two: the product is exact, as in the atomic spill).
+cudaError_t launch_part_reduce_i32(const uint32_t *d_part, int32_t kc_count, int64_t part_ld, int32_t M,
+                                   int64_t *d_hw, cudaStream_t s, int *launches);
+cudaError_t launch_part_reduce_f32(const uint32_t *d_part, int32_t kc_count, int64_t part_ld, int32_t M,
+                                   const float *d_inv_scale, double *d_hw, cudaStream_t s, int *launches);
 
 // a6: float traces.  Split pre-pass: c = w - offset[j], hi = fp16(c s_j),
 // lo = e4m3(c s_j - hi) into [n][ldh] fp16 / [n][ldl] byte planes (s_j =
@@ -100,7 +111,8 @@ cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap
                              const uint8_t *d_texts,
                              const uint8_t *d_vtab, double *d_hw, const float *d_inv_scale, int *d_counter, int32_t M,
                              int64_t N, int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
-                             uint32_t *d_hist = nullptr, unsigned long long *d_clk = nullptr, bool nt2 = false);
+                             uint32_t *d_hist = nullptr, unsigned long long *d_clk = nullptr, bool nt2 = false,
+                             uint32_t *d_part = nullptr, int64_t part_ld = 0);
 
 // a5 for the single-byte models (HW_LAST / HW_FIRST), class sums (classsum.cu):
 // counting sort of n traces by text byte per byte (perm: 16 x n int32, off: 16 x

@@ -223,6 +223,12 @@ struct Params {
     // N tile group 0 count each trace's (c_b, c_SR(b)) pair of their key byte
     // (k_hist_contract turns the counts into sum H, sum H^2 afterwards)
     uint32_t *hist;
+    // partial-sum spill (null = off): each unit STORES its raw 32-bit
+    // accumulators (int32 / fp32 bits) into its trace chunk's slice
+    // part[kc][4096][part_ld] -- plain stores, no read-modify-write of sum_hw in
+    // the exposed epilogue; launch_part_reduce adds the slices into sum_hw after
+    uint32_t *part;
+    int64_t part_ld;
 };
 
 template <int V>
@@ -621,6 +627,36 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
             uint32_t v[8];
             tmem_ld_32x32b_x8(tcol, v);
             tmem_ld_wait(v);
+            if (p.part != nullptr) {
+                // lane = accumulator row: its 8 samples (32 bytes, one sector) per
+                // column group straight to the unit's chunk slice; the TMEM load of
+                // the next group is in flight during the stores
+                static_assert(C::KB == 1, "partial spill: one key byte per unit");
+                const int kc = (u / p.groups) % p.kc_count;
+                uint32_t *prow = p.part + ((int64_t)kc * 4096 + b * 256 + (int)rank * BMC + q * 32 + lane) * p.part_ld;
+#pragma unroll 1
+                for (int c = 0; c < NC; c++) {
+                    uint32_t vn[8];
+                    if (c + 1 < NC) tmem_ld_32x32b_x8(tcol + (c + 1) * 8, vn);
+                    const int j = nt * (C::NT * BN) + c * 8;
+                    if (!(XT_EXP & 4) && j < p.part_ld) {
+                        uint32_t *dst = prow + j;
+                        asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(v[0]), "r"(v[1]),
+                                     "r"(v[2]), "r"(v[3]) : "memory");
+                        asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4), "r"(v[4]), "r"(v[5]),
+                                     "r"(v[6]), "r"(v[7]) : "memory");
+                    }
+                    if (c + 1 < NC) {
+                        tmem_ld_wait(vn);
+#pragma unroll
+                        for (int x = 0; x < 8; x++) v[x] = vn[x];
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(to_leader(tempty_bar(acc)));
+                continue;
+            }
             if (p.bulk_spill && own == nullptr && !p.store_hw) {
                 // lane = accumulator row: its 8 samples as int64 (I8) or as fp64 times
                 // 2^16 / s_j (F32) into the warp's box (64 B per row, 16-byte chunks
@@ -851,7 +887,7 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorM
                    cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr, int64_t *d_sum_w2 = nullptr,
                    bool w_signed = true, uint32_t *d_hist = nullptr, int64_t *const *owners = nullptr,
                    unsigned long long *d_clk = nullptr, uint32_t idesc8 = 0, const float *d_inv_scale = nullptr,
-                   bool store_hw = false)
+                   bool store_hw = false, uint32_t *d_part = nullptr, int64_t part_ld = 0)
 {
     using Cf = Cfg<V>;
     Params p;
@@ -875,6 +911,10 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorM
     p.hist = d_hist;
     for (int b = 0; b < 16; b++) p.owners[b] = owners ? owners[b] : nullptr;
     p.clk = d_clk;
+    p.part = d_part;
+    p.part_ld = part_ld;
+    if (d_part != nullptr && (part_ld % 8 != 0 || part_ld < M || Cf::KB != 1 || owners != nullptr))
+        return cudaErrorInvalidValue;
     p.bulk_spill = mhw != nullptr;
     p.store_hw = store_hw && p.kc_count == 1 && owners == nullptr && !Cf::F32;
     static std::atomic<unsigned long long> attr_set{0};
@@ -965,34 +1005,35 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const CUtensorMap *tmap_h
                             const uint8_t *d_vtab, int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len,
                             bool w_signed, int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w,
                             int64_t *d_sum_w2, uint32_t *d_hist, int64_t *const *owners, unsigned long long *d_clk,
-                            bool overlapped, bool hw_zero)
+                            bool overlapped, bool hw_zero, uint32_t *d_part, int64_t part_ld)
 {
     static_assert(Cfg<V_I8>::KB == 1 && Cfg<V_I8O>::KB == 1, "owner routing assumes one key byte per unit");
     if (overlapped) {
         if (d_sum_w != nullptr) return cudaErrorInvalidValue;  // a4 is fused into the NT = 2 variant only
         return launch<V_I8O>(tmap_w, tmap_w, tmap_hw, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                              idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, nullptr, nullptr, w_signed,
-                             d_hist, owners, d_clk, 0, nullptr, hw_zero);
+                             d_hist, owners, d_clk, 0, nullptr, hw_zero, d_part, part_ld);
     }
     return launch<V_I8>(tmap_w, tmap_w, tmap_hw, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                         idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, d_sum_w, d_sum_w2, w_signed,
-                        d_hist, owners, d_clk, 0, nullptr, hw_zero);
+                        d_hist, owners, d_clk, 0, nullptr, hw_zero, d_part, part_ld);
 }
 
 cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const CUtensorMap *tmap_hw,
                              const uint8_t *d_texts,
                              const uint8_t *d_vtab, double *d_hw, const float *d_inv_scale, int *d_counter, int32_t M,
                              int64_t N, int64_t kc_len, int num_sms, cudaStream_t stream, int *launches,
-                             uint32_t *d_hist, unsigned long long *d_clk, bool nt2)
+                             uint32_t *d_hist, unsigned long long *d_clk, bool nt2, uint32_t *d_part,
+                             int64_t part_ld)
 {
     if (nt2)
         return launch<V_F32N>(tmap_hi, tmap_lo, tmap_hw, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                               idesc_f16(2 * BMC, BN), num_sms, stream, launches, nullptr, nullptr, true, d_hist, nullptr,
-                              d_clk, idesc_e5m2_e4m3(2 * BMC, BN), d_inv_scale);
+                              d_clk, idesc_e5m2_e4m3(2 * BMC, BN), d_inv_scale, false, d_part, part_ld);
     return launch<V_F32>(tmap_hi, tmap_lo, tmap_hw, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                          idesc_f16(2 * BMC, BN),
                         num_sms, stream, launches, nullptr, nullptr, true, d_hist, nullptr, d_clk,
-                        idesc_e5m2_e4m3(2 * BMC, BN), d_inv_scale);
+                        idesc_e5m2_e4m3(2 * BMC, BN), d_inv_scale, false, d_part, part_ld);
 }
 
 }  // namespace cpa

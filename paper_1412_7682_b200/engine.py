@@ -78,7 +78,8 @@ class Engine:
         B.cpa_set_option(self.ctx, B.CPA_OPT_XT_TILES, v)
 
     def set_spill(self, mode: int):
-        """CPA_OPT_SPILL: 0 auto (default), 1 red.add.u64 per element, 2 bulk tensor reduce-add."""
+        """CPA_OPT_SPILL: 0 auto (default), 1 red.add per element, 2 bulk tensor reduce-add,
+        3 per-chunk partial stores + one reduce pass (include/cpa.h)."""
         B.cpa_set_option(self.ctx, B.CPA_OPT_SPILL, mode)
 
     def set_row_owners(self, owners):

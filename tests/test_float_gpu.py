@@ -25,7 +25,7 @@ def gpu_rho(P, texts, W, offsets="default", xt=None, spill=None):
     if xt is not None:
         eng.set_xt_tiles(xt)          # float cross-term variant: 1 = NT 2 (default), 2 = NT 1
     if spill is not None:
-        eng.set_spill(spill)          # 2 = fp64 bulk tensor reduce-add
+        eng.set_spill(spill)          # 1 = fp64 atomics, 2 = bulk tensor reduce-add, 3 = partial stores
     if offsets is None:
         P.cpa_set_offsets(eng.ctx, None)
     eng.accumulate(torch.from_numpy(np.ascontiguousarray(W)).cuda(), torch.from_numpy(texts).cuda())
@@ -35,9 +35,10 @@ def gpu_rho(P, texts, W, offsets="default", xt=None, spill=None):
     return out, n
 
 
-@pytest.mark.parametrize("xt,spill", [(None, None), (2, None), (1, 2), (2, 2)])
-@pytest.mark.parametrize("n,m", [(2000, 300), (65, 257), (130, 17)])
+@pytest.mark.parametrize("xt,spill", [(None, None), (2, None), (1, 1), (1, 2), (1, 3), (2, 2), (2, 3)])
+@pytest.mark.parametrize("n,m", [(2000, 300), (65, 257), (130, 17), (1500, 1032)])
 def test_float_parity_all_cells(P, n, m, xt, spill):
+    """Every cell within the bar, for every cross-term variant and spill mode."""
     w = S.CONFIGS["C3"].replace(n=n, m=m, a=0.02)
     texts, W = S.dataset(w)
     out, cnt = gpu_rho(P, texts, W, xt=xt, spill=spill)
@@ -234,3 +235,23 @@ def test_float_degenerate_columns_match_oracle(P):
                 if offsets is not None:
                     assert np.max(np.abs(rho[:, j] - ref[:, j])) <= TOL, (offsets, j)
                 assert np.any(rho[:, j] != 0.0)
+
+
+@pytest.mark.parametrize("pitch,col", [(264, 0), (264, 1), (260, 3)])
+def test_float_strided_rows(P, pitch, col):
+    """Traces as a [N][257] view of wider rows (pitch samples, first sample at
+    `col`, so rows 16-byte aligned or not): the split reads them in place, within
+    the bar against the oracle."""
+    w = S.CONFIGS["C3"].replace(n=2100, m=257, a=0.02)
+    texts, W = S.dataset(w)
+    buf = np.full((w.n, pitch), np.float32(1e30), np.float32)
+    buf[:, col:col + w.m] = W
+    d = torch.from_numpy(buf).cuda()[:, col:col + w.m]
+    eng = P.Engine(w.m, P.CPA_F32, P.CPA_HD_LAST, 0)
+    eng.accumulate(d, torch.from_numpy(texts).cuda())
+    out = eng.finalize(want_rho=True)
+    eng.close()
+    err = float(np.max(np.abs(out["rho"].cpu().numpy() - _oracle_rho_f32(texts, W))))
+    print(f"pitch {pitch} col {col}: max |drho| = {err:.3g}")
+    assert err <= TIGHT
+    assert out["master_key"] == w.key

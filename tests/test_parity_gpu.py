@@ -99,7 +99,7 @@ def test_c1_noiseless_rho_one(P):
     assert out["master_key"] == w.key
 
 
-@pytest.mark.parametrize("xt,spill", [(1, 1), (1, 2), (2, 1), (2, 2)])
+@pytest.mark.parametrize("xt,spill", [(1, 1), (1, 2), (1, 3), (2, 1), (2, 2), (2, 3)])
 @pytest.mark.parametrize("model", [O.HD_LAST, O.HW_LAST, O.HW_FIRST])
 @pytest.mark.parametrize("dtype", [np.int8, np.uint8])
 def test_models_dtypes_ragged(P, model, dtype, xt, spill):
@@ -113,7 +113,7 @@ def test_models_dtypes_ragged(P, model, dtype, xt, spill):
     assert_parity(sums, out, ref)
 
 
-@pytest.mark.parametrize("xt,spill", [(1, 1), (1, 2), (2, 1), (2, 2)])
+@pytest.mark.parametrize("xt,spill", [(1, 1), (1, 2), (1, 3), (2, 1), (2, 2), (2, 3)])
 @pytest.mark.parametrize("n,m", [(2, 1), (3, 17), (64, 256), (65, 257), (65, 258), (130, 513), (130, 514), (1000, 16)])
 def test_edge_shapes(P, n, m, xt, spill):
     rng = np.random.default_rng(n * 1000 + m)
@@ -150,7 +150,8 @@ def test_split_k_chunks_and_permutation_bit_identical(P):
                dict(overlap=False), dict(overlap=False, chunks=[0, 5000, 9000]),
                dict(xt=1), dict(xt=2), dict(xt=1, kchunk=256), dict(xt=2, kchunk=256),
                dict(xt=2, chunks=[0, 1, 700, 4097, 9000]), dict(spill=1), dict(spill=2, kchunk=128),
-               dict(spill=2, xt=2, kchunk=256)):
+               dict(spill=2, xt=2, kchunk=256), dict(spill=3), dict(spill=3, kchunk=128),
+               dict(spill=3, xt=2, kchunk=256), dict(spill=3, chunks=[0, 1, 700, 4097, 9000])):
         s, o = run_gpu(P, texts, W, **kw)
         for k in base:
             assert np.array_equal(base[k], s[k]), (kw, k)
@@ -417,7 +418,7 @@ def test_class_sums_chunked_sort_and_errors(P):
     eng.close()
 
 
-@pytest.mark.parametrize("spill", [1, 2])
+@pytest.mark.parametrize("spill", [1, 2, 3])
 def test_first_touch_store_then_add(P, spill):
     """After cpa_init / cpa_reset the first int8 accumulate with one trace chunk
     per work unit stores its sums (include/cpa.h); later calls add.  The same
@@ -437,4 +438,45 @@ def test_first_touch_store_then_add(P, spill):
         eng.sync()
         assert np.array_equal(eng.sum_hw.cpu().numpy(), rounds * ref["sum_hw"]), rounds
         assert np.array_equal(eng.sum_w.cpu().numpy(), rounds * ref["sum_w"]), rounds
+    eng.close()
+
+
+@pytest.mark.parametrize("dtype", ["s8", "f32"])
+@pytest.mark.parametrize("m,dup", [(8192, False), (9002, True), (20000, False), (8193, False)])
+def test_maxima_only_finalize_equals_rho_maxima(P, dtype, m, dup):
+    """Without rho (checkpoints, M >= 8192) the finalize runs the filtered maxima
+    kernel (most cells skip the division against a row-wide threshold): its max
+    |rho|, argmax, signed peak and ranks equal those of the rho-writing kernel
+    (bit-exact against the oracle elsewhere) bit for bit, ties to the lowest
+    sample [S:298] (dup, int8: the second half of the columns repeats the first,
+    so every maximum ties exactly), also for a partial row range."""
+    rng = np.random.default_rng(m + (7 if dup else 0))
+    n = 300
+    texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    half = m // 2 if dup else m
+    W = rng.integers(-128, 128, (n, half)).astype(np.int8)
+    if dtype == "f32":
+        W = W.astype(np.float32) + 0.01 * rng.standard_normal(W.shape).astype(np.float32)
+    if dup:
+        W = np.concatenate([W, W], axis=1)
+    eng = P.Engine(m, P.CPA_S8 if dtype == "s8" else P.CPA_F32, P.CPA_HD_LAST, 0)
+    eng.accumulate(torch.from_numpy(np.ascontiguousarray(W)).cuda(), torch.from_numpy(texts).cuda())
+    full = eng.finalize(want_rho=True)
+    fast = eng.finalize(want_rho=False)
+    rho = full["rho"].cpu().numpy()
+    a = np.abs(rho)
+    assert np.array_equal(full["maxabs"].cpu().numpy(), a.max(axis=1))
+    assert np.array_equal(full["argmax"].cpu().numpy(), a.argmax(axis=1))   # first maximum
+    for k in ("maxabs", "argmax", "rank"):
+        assert np.array_equal(fast[k].cpu().numpy(), full[k].cpu().numpy()), k
+    assert fast["peak_rho"] == full["peak_rho"] and fast["peak_sample"] == full["peak_sample"]
+    if dup and dtype == "s8":                       # exact sums: the copies tie exactly
+        assert np.all(full["argmax"].cpu().numpy() < half)
+    mx, am, pk = (t[0] for t in eng.maxima_buffers(1))
+    h0, h1 = 5, 1003                                   # a partial last row group
+    eng.finalize_rows(h0, h1, mx, am, pk)
+    assert np.array_equal(mx[h0:h1].cpu().numpy(), a.max(axis=1)[h0:h1])
+    assert np.array_equal(am[h0:h1].cpu().numpy(), a.argmax(axis=1)[h0:h1])
+    assert np.array_equal(pk[h0:h1].cpu().numpy(), rho[np.arange(h0, h1), a.argmax(axis=1)[h0:h1]])
+    assert not mx[:h0].any() and not mx[h1:].any()
     eng.close()
