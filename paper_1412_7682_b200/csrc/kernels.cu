@@ -707,13 +707,16 @@ cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M,
 // loads were slower: more registers, fewer resident blocks); without rho, the
 // filtered maxima kernel from M = 8192 on (-13% / -23% at M = 20000 / 48000)
 constexpr int kFinFilterMinM = 8192;
+#ifndef FIN_MAXIMA_U
+#define FIN_MAXIMA_U 4  // column pairs of row loads in flight per thread (maxima kernel)
+#endif
 template <typename T>
 static cudaError_t launch_fin(const T *hw, const T *sw, const T *sh, const T *sh2, const T *cnt,
                               const double *sqrt_dw, int32_t M, const FinalizeOut &o, cudaStream_t s)
 {
     const int rows = o.h1 - o.h0;
     if (o.rho == nullptr && M >= kFinFilterMinM)
-        k_finalize_maxima<4, T><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
+        k_finalize_maxima<FIN_MAXIMA_U, T><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
     else
         k_finalize_rows<1, 4, T><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
     return cudaGetLastError();
