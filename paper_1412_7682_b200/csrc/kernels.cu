@@ -340,26 +340,24 @@ k_finalize_maxima(const T *__restrict__ hw, const T *__restrict__ sw, const T *_
         using T2 = typename Pair2<T>::type;
         const int M2 = M >> 1;
         int p0 = threadIdx.x;
-        for (; p0 + (U - 1) * FIN_THREADS < M2; p0 += U * FIN_THREADS) {
+        // the ragged last group is predicated, not a loop of single pairs: each of
+        // its iterations would wait out a full load latency (per block: ~6 us at
+        // any M, 25% of the kernel at M = 20000)
+        for (; p0 < M2; p0 += U * FIN_THREADS) {
             T2 v[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) v[u] = __ldcs((const T2 *)row + p0 + u * FIN_THREADS);
+            for (int u = 0; u < U; u++)
+                if (p0 + u * FIN_THREADS < M2) v[u] = __ldcs((const T2 *)row + p0 + u * FIN_THREADS);
             refresh();
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const int p = p0 + u * FIN_THREADS;
+                if (p >= M2) break;
                 const double2 rw = ((const double2 *)rcp_w)[p];
                 const T2 swp = ((const T2 *)sw)[p];
                 visit(v[u].x, 2 * p, rw.x, swp.x);
                 visit(v[u].y, 2 * p + 1, rw.y, swp.y);
             }
-        }
-        for (; p0 < M2; p0 += FIN_THREADS) {
-            const T2 v = __ldcs((const T2 *)row + p0);
-            const double2 rw = ((const double2 *)rcp_w)[p0];
-            const T2 swp = ((const T2 *)sw)[p0];
-            visit(v.x, 2 * p0, rw.x, swp.x);
-            visit(v.y, 2 * p0 + 1, rw.y, swp.y);
         }
         j = M;
     }
@@ -397,16 +395,18 @@ k_finalize_rows(const T *__restrict__ hw, const T *__restrict__ sw, const T *__r
     if ((M & 1) == 0 && ((uintptr_t)o.rho & 15) == 0) {  // 16-byte aligned rows (M even)
         const int M2 = M >> 1;
         int p0 = threadIdx.x;
-        for (; p0 + (U - 1) * FIN_THREADS < M2; p0 += U * FIN_THREADS) {
+        for (; p0 < M2; p0 += U * FIN_THREADS) {  // ragged last group predicated (see k_finalize_maxima)
             T2 v[U][R];
 #pragma unroll
             for (int u = 0; u < U; u++)
 #pragma unroll
                 for (int r = 0; r < R; r++)
-                    if (r < nr) v[u][r] = __ldcs((const T2 *)(row0 + (int64_t)r * M) + p0 + u * FIN_THREADS);
+                    if (r < nr && p0 + u * FIN_THREADS < M2)
+                        v[u][r] = __ldcs((const T2 *)(row0 + (int64_t)r * M) + p0 + u * FIN_THREADS);
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const int p = p0 + u * FIN_THREADS;
+                if (p >= M2) break;
                 const double2 dw = ((const double2 *)sqrt_dw)[p];
                 const T2 swp = ((const T2 *)sw)[p];
 #pragma unroll
@@ -419,21 +419,6 @@ k_finalize_rows(const T *__restrict__ hw, const T *__restrict__ sw, const T *__r
                     keep(r, x.y, 2 * p + 1);
                     if (rrow0) __stcs((double2 *)(rrow0 + (int64_t)r * M) + p, x);
                 }
-            }
-        }
-        for (; p0 < M2; p0 += FIN_THREADS) {
-            const double2 dw = ((const double2 *)sqrt_dw)[p0];
-            const T2 swp = ((const T2 *)sw)[p0];
-#pragma unroll
-            for (int r = 0; r < R; r++) {
-                if (r >= nr) break;
-                const T2 v = __ldcs((const T2 *)(row0 + (int64_t)r * M) + p0);
-                double2 x;
-                x.x = fin_cell(v.x, n, s_h[r], swp.x, dw.x, den_h[r]);
-                x.y = fin_cell(v.y, n, s_h[r], swp.y, dw.y, den_h[r]);
-                keep(r, x.x, 2 * p0);
-                keep(r, x.y, 2 * p0 + 1);
-                if (rrow0) __stcs((double2 *)(rrow0 + (int64_t)r * M) + p0, x);
             }
         }
         j = M;

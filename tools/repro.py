@@ -1,5 +1,6 @@
 """Run one accumulate+finalize on a synthetic config (debug / sanitizer aid).
-usage: python tools/repro.py C2 [n] [kchunk] [a]   (C3 runs the float path; a = leak amplitude)
+usage: python tools/repro.py C2 [n] [kchunk] [a] [m]   (C3 runs the float path; a = leak amplitude;
+m >= 8192 also takes the maxima-only finalize kernel in the finalize_rows call below)
 REPRO_CLASS_SUMS=1 with an HW workload (C2-HW) takes the class-sum cross term."""
 import os
 import sys
@@ -13,8 +14,10 @@ name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 w = S.CONFIGS[name]
 if len(sys.argv) > 2:
     w = w.replace(n=int(sys.argv[2]))
-if len(sys.argv) > 4:
+if len(sys.argv) > 4 and float(sys.argv[4]) > 0:
     w = w.replace(a=float(sys.argv[4]))
+if len(sys.argv) > 5:
+    w = w.replace(m=int(sys.argv[5]))
 texts, W = S.dataset(w)
 f32 = w.dtype == S.F32
 ld = (w.m + 3) // 4 * 4 if f32 else (w.m + 15) // 16 * 16
