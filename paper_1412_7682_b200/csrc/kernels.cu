@@ -544,39 +544,67 @@ __global__ void k_texthist(const uint8_t *__restrict__ texts, int64_t n, uint32_
 }
 
 constexpr int HC_X = 8;  // histogram rows (x = c_b) per block
+// Thread z owns column z of V (one byte of V[y][z] per y, reused for the HC_X
+// rows of the block) and accumulates, for each row x, the key k = x ^ z; the
+// counts are staged transposed, [y][x], so one 16-byte broadcast load gives 4
+// rows' counts.  3 shared loads per 2 x HC_X multiply-adds (the per-(x, k)
+// layout needed 2 per 2: the contraction was shared-load-bound).  For a fixed
+// row x, z -> x ^ z is a bijection, so the per-key sums go through shared
+// memory without atomics (one row at a time), then one int64 atomic per key.
 template <typename Acc>
 __global__ void __launch_bounds__(256)
 k_hist_contract(const uint32_t *__restrict__ hist, const uint8_t *__restrict__ vtab, Acc *sum_h, Acc *sum_h2,
                 Acc *count, int64_t n)
 {
-    extern __shared__ uint8_t sm[];
+    extern __shared__ __align__(16) uint8_t sm[];
     uint8_t *vs = sm;                                // 64 KB: V[y][z]
-    uint32_t *hs = (uint32_t *)(sm + 65536);         // HC_X x 256 counts
-    const int b = blockIdx.y, x0 = blockIdx.x * HC_X, k = threadIdx.x;
+    uint32_t *ct = (uint32_t *)(sm + 65536);         // 256 x HC_X counts, [y][x]
+    __shared__ uint32_t sk1[256], sk2[256];
+    const int b = blockIdx.y, x0 = blockIdx.x * HC_X, z = threadIdx.x;
     for (int i = threadIdx.x; i < 4096; i += 256) ((uint4 *)vs)[i] = ((const uint4 *)vtab)[i];
-    for (int i = threadIdx.x; i < HC_X * 256; i += 256) hs[i] = hist[(b << 16) | (x0 << 8) | i];
+    for (int i = threadIdx.x; i < HC_X * 256; i += 256) {
+        const int xx = i >> 8, y = i & 255;  // coalesced read of row x0 + xx
+        ct[y * HC_X + xx] = hist[(b << 16) | ((x0 + xx) << 8) | y];
+    }
+    sk1[z] = 0;
+    sk2[z] = 0;
     __syncthreads();
-    uint32_t a1 = 0, a2 = 0;  // exact: <= 8 N and 64 N for N <= 2^23
-    for (int xx = 0; xx < HC_X; xx++) {
-        const uint32_t z = (uint32_t)(x0 + xx) ^ (uint32_t)k;
-        const uint32_t *hr = hs + xx * 256;
-#pragma unroll 4
-        for (int y = 0; y < 256; y++) {
-            const uint32_t c = hr[y];
-            const uint32_t v = vs[y * 256 + z];
-            a1 += c * v;
-            a2 += c * v * v;
+    uint32_t a1[HC_X], a2[HC_X];  // exact: <= 8 N and 64 N for N <= 2^23
+#pragma unroll
+    for (int xx = 0; xx < HC_X; xx++) a1[xx] = a2[xx] = 0;
+#pragma unroll 2
+    for (int y = 0; y < 256; y++) {
+        const uint32_t v = vs[y * 256 + z], v2 = v * v;
+        const uint4 *c4 = (const uint4 *)(ct + y * HC_X);
+#pragma unroll
+        for (int q = 0; q < HC_X / 4; q++) {
+            const uint4 c = c4[q];
+            a1[4 * q] += c.x * v;
+            a2[4 * q] += c.x * v2;
+            a1[4 * q + 1] += c.y * v;
+            a2[4 * q + 1] += c.y * v2;
+            a1[4 * q + 2] += c.z * v;
+            a2[4 * q + 2] += c.z * v2;
+            a1[4 * q + 3] += c.w * v;
+            a2[4 * q + 3] += c.w * v2;
         }
     }
-    const int h = b * 256 + k;
+#pragma unroll
+    for (int xx = 0; xx < HC_X; xx++) {
+        const int k = (x0 + xx) ^ z;  // distinct over the block's threads for this row
+        sk1[k] += a1[xx];
+        sk2[k] += a2[xx];
+        __syncthreads();
+    }
+    const int h = b * 256 + z;
     if constexpr (std::is_integral<Acc>::value) {
-        atomicAdd((unsigned long long *)&sum_h[h], (unsigned long long)a1);
-        atomicAdd((unsigned long long *)&sum_h2[h], (unsigned long long)a2);
-        if (blockIdx.x == 0 && blockIdx.y == 0 && k == 0) atomicAdd((unsigned long long *)count, (unsigned long long)n);
+        atomicAdd((unsigned long long *)&sum_h[h], (unsigned long long)sk1[z]);
+        atomicAdd((unsigned long long *)&sum_h2[h], (unsigned long long)sk2[z]);
+        if (blockIdx.x == 0 && blockIdx.y == 0 && z == 0) atomicAdd((unsigned long long *)count, (unsigned long long)n);
     } else {
-        atomicAdd(&sum_h[h], (Acc)a1);
-        atomicAdd(&sum_h2[h], (Acc)a2);
-        if (blockIdx.x == 0 && blockIdx.y == 0 && k == 0) atomicAdd(count, (Acc)n);
+        atomicAdd(&sum_h[h], (Acc)sk1[z]);
+        atomicAdd(&sum_h2[h], (Acc)sk2[z]);
+        if (blockIdx.x == 0 && blockIdx.y == 0 && z == 0) atomicAdd(count, (Acc)n);
     }
 }
 
