@@ -86,6 +86,13 @@ constexpr int64_t kF32MaxUnitNT2 = F32_MAX_UNIT_NT2;  // fp32 TMEM accumulation 
 // reduce pass (5 slices + the sum_hw read-modify-write) cost it back
 constexpr int64_t kPartMaxBytes = 3LL << 30;
 constexpr bool kF32PartialSpill = false;
+// int8 W tensor map: no L2 promotion.  With 256-byte promotion every 128-byte
+// box row pulled its neighbour (the peer CTA's half or the next tile group) into
+// L2 early, and part of it was evicted again before use: ncu DRAM reads per C4
+// launch 12.63 GB (256B) vs 11.51 (128B) vs 11.51 (none), time within noise
+#ifndef XT_W_PROMOTION
+#define XT_W_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_NONE
+#endif
 constexpr int64_t kBulkSpillMinUnit = 65536;  // CPA_OPT_SPILL auto: bulk reduce from this unit length (traces) on
 
 }  // namespace
@@ -657,7 +664,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     cuuint32_t estr[2] = {1, 1};
     CUresult r = get_encode()(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(d_w), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                              XT_W_PROMOTION, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     // the epilogue's int64 spill by bulk tensor reduce-add into sum_hw [4096][M]
     // (rows of M int64 must be 16-byte multiples: M even); the fused multi-GPU
