@@ -90,6 +90,9 @@ constexpr bool kF32PartialSpill = false;
 // box row pulled its neighbour (the peer CTA's half or the next tile group) into
 // L2 early, and part of it was evicted again before use: ncu DRAM reads per C4
 // launch 12.63 GB (256B) vs 11.51 (128B) vs 11.51 (none), time within noise
+#ifndef XT_P_PROMOTION
+#define XT_P_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_NONE  // float hi / lo plane maps: C3 2.54 -> 2.40 GB, same time
+#endif
 #ifndef XT_W_PROMOTION
 #define XT_W_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_NONE
 #endif
@@ -565,7 +568,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                                           k ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
                                           k ? (void *)c->d_lo : (void *)c->d_hi, dims, strides, box, estr,
                                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                          XT_P_PROMOTION, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
                 if (r != CUDA_SUCCESS) return fail(CPA_E_CUDA, "cuTensorMapEncodeTiled (hi/lo) failed (%d)", (int)r);
             }
             const int64_t kmax = nt2 ? kF32MaxUnitNT2 : 4096;
