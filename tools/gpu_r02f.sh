@@ -1,5 +1,5 @@
-# Round-2 evidence on HEAD (under gpurun): smoke, all GPU tests, bench lines, ncu launch lists + captures
-TAG=${TAG:-r02e}
+# Round-2 evidence on HEAD (final kernels; + sanitizers) (under gpurun): smoke, all GPU tests, bench lines, ncu launch lists + captures
+TAG=${TAG:-r02f}
 mkdir -p gpurun_out/$TAG
 O=gpurun_out/$TAG
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $O/smi.txt
@@ -16,3 +16,5 @@ timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --
     --log-file $O/launches_c5_$TAG.csv python bench.py --config C5 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-clocks > /dev/null 2>&1
 TAG=$TAG bash tools/ncu_r02.sh > /dev/null 2>&1
 ls gpurun_out/*$TAG* | head -30
+rm -f gpurun_out/sanitize.log
+timeout -s KILL 2400 bash tools/sanitize.sh > /dev/null 2>&1; cp gpurun_out/sanitize.log $O/sanitize_$TAG.txt; grep -c "exit 0" $O/sanitize_$TAG.txt
