@@ -139,7 +139,6 @@ constexpr int SCHED_Q = 4;        // depth of the unit-id ring
 // V[y][x] = HW(InvS[x] ^ y) is 0..8: stored as nibbles, V[y][2i] | V[y][2i+1] << 4
 // (32 KB; the freed 32 KB deepens the W ring)
 constexpr int V_BYTES = 32768;
-constexpr int TX_BYTES = 128 * 16;            // ciphertext rows of one stage (max BK)
 constexpr int EPI_WARPS = 4;
 #ifndef XT_GEN_WARPS
 #define XT_GEN_WARPS 8
@@ -160,30 +159,33 @@ constexpr int TB_BYTES = (EPI_WARPS * RB_BYTES > EPI_WARPS * 32 * TB_LD * 4) ? E
 constexpr int MAX_RING = 8;                   // barrier slots reserved per ring
 constexpr int SMEM_V = 0;
 constexpr int SMEM_A = SMEM_V + V_BYTES;      // A ring, then the B ring (per-config sizes)
-constexpr int RINGS_BYTES = 180224;           // A_STAGES*A_STAGE + B_STAGES*B_STAGE <= this
-constexpr int SMEM_TB = SMEM_A + RINGS_BYTES;  // 1 KB aligned (64-byte-swizzled TMA boxes)
-constexpr int SMEM_TX = SMEM_TB + TB_BYTES;
-constexpr int SMEM_BAR = SMEM_TX + TX_STAGES * TX_BYTES;
-static_assert(SMEM_TB % 1024 == 0, "staging boxes: 1 KB alignment");
 constexpr int NUM_BARS = 4 * MAX_RING + 2 * TX_STAGES + 4 + 2 * SCHED_Q + 2 * MAX_RING;
-constexpr int SMEM_SCHED = SMEM_BAR + NUM_BARS * 8;
-constexpr int SMEM_TOTAL = SMEM_SCHED + SCHED_Q * 4 + 16;
-constexpr int SMEM_ALLOC = SMEM_TOTAL;
 constexpr int THREADS = 32 * (8 + GEN_WARPS);
 constexpr uint32_t TMEM_COLS = 512;
 template <int V>
 __host__ __device__ constexpr int smem_b() { return SMEM_A + Cfg<V>::A_STAGES * Cfg<V>::A_STAGE; }
+// per-variant shared-memory layout: [V table | A ring, B ring | epilogue staging |
+// ciphertext ring | barriers | unit-id ring, TMEM slot]
+template <int V>
+struct Lay {
+    using C = Cfg<V>;
+    static constexpr int RINGS = (C::A_STAGES * C::A_STAGE + C::B_STAGES * C::B_STAGE + 1023) / 1024 * 1024;
+    static constexpr int TXB = C::BK * 16;         // ciphertext rows of one stage
+    static constexpr int TB = SMEM_A + RINGS;      // 1 KB aligned (64-byte-swizzled TMA boxes)
+    static constexpr int TX = TB + TB_BYTES;
+    static constexpr int BAR = TX + TX_STAGES * TXB;
+    static constexpr int SCHED = BAR + NUM_BARS * 8;
+    static constexpr int ALLOC = SCHED + SCHED_Q * 4 + 16;
+};
 template <int V>
 constexpr bool cfg_ok()
 {
     using C = Cfg<V>;
-    return C::A_STAGES * C::A_STAGE + C::B_STAGES * C::B_STAGE <= RINGS_BYTES && C::A_STAGES <= MAX_RING &&
-           (!C::UNI || C::A_STAGES == C::B_STAGES) &&
-           C::B_STAGES <= MAX_RING && C::NACC * C::NBUF * BN == (int)TMEM_COLS;
+    return C::A_STAGES <= MAX_RING && (!C::UNI || C::A_STAGES == C::B_STAGES) && C::B_STAGES <= MAX_RING &&
+           C::NACC * C::NBUF * BN == (int)TMEM_COLS && Lay<V>::TB % 1024 == 0 && Lay<V>::ALLOC <= 232448;
 }
 static_assert(cfg_ok<V_I8>() && cfg_ok<V_F32>() && cfg_ok<V_I8O>() && cfg_ok<V_F32N>(),
-              "rings, barriers, TMEM columns");
-static_assert(SMEM_ALLOC <= 232448, "shared memory");
+              "rings, barriers, TMEM columns, shared memory");
 
 struct Params {
     const uint8_t *texts;    // N x 16
@@ -349,24 +351,24 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
     const bool leader = rank == 0;
 
     constexpr int AS = C::A_STAGES, BS = C::B_STAGES;
-    auto afull_bar = [&](int s) { return sbase + SMEM_BAR + 8 * s; };                  // leader's is used
-    auto aempty_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (MAX_RING + s); };    // both CTAs
-    auto bfull_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (2 * MAX_RING + s); }; // leader's is used
-    auto bempty_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (3 * MAX_RING + s); };// both CTAs
-    auto txfull_bar = [&](int x) { return sbase + SMEM_BAR + 8 * (4 * MAX_RING + x); };
-    auto txempty_bar = [&](int x) { return sbase + SMEM_BAR + 8 * (4 * MAX_RING + TX_STAGES + x); };
+    auto afull_bar = [&](int s) { return sbase + Lay<V>::BAR + 8 * s; };                  // leader's is used
+    auto aempty_bar = [&](int s) { return sbase + Lay<V>::BAR + 8 * (MAX_RING + s); };    // both CTAs
+    auto bfull_bar = [&](int s) { return sbase + Lay<V>::BAR + 8 * (2 * MAX_RING + s); }; // leader's is used
+    auto bempty_bar = [&](int s) { return sbase + Lay<V>::BAR + 8 * (3 * MAX_RING + s); };// both CTAs
+    auto txfull_bar = [&](int x) { return sbase + Lay<V>::BAR + 8 * (4 * MAX_RING + x); };
+    auto txempty_bar = [&](int x) { return sbase + Lay<V>::BAR + 8 * (4 * MAX_RING + TX_STAGES + x); };
     constexpr int BAR_T = 4 * MAX_RING + 2 * TX_STAGES, BAR_S = BAR_T + 4;
-    auto tfull_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + a); };      // both (multicast)
-    auto tempty_bar = [&](int a) { return sbase + SMEM_BAR + 8 * (BAR_T + 2 + a); }; // leader's
-    auto sfull_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + q); };        // both CTAs
-    auto sempty_bar = [&](int q) { return sbase + SMEM_BAR + 8 * (BAR_S + SCHED_Q + q); };  // leader's
+    auto tfull_bar = [&](int a) { return sbase + Lay<V>::BAR + 8 * (BAR_T + a); };      // both (multicast)
+    auto tempty_bar = [&](int a) { return sbase + Lay<V>::BAR + 8 * (BAR_T + 2 + a); }; // leader's
+    auto sfull_bar = [&](int q) { return sbase + Lay<V>::BAR + 8 * (BAR_S + q); };        // both CTAs
+    auto sempty_bar = [&](int q) { return sbase + Lay<V>::BAR + 8 * (BAR_S + SCHED_Q + q); };  // leader's
     constexpr int BAR_M = BAR_S + 2 * SCHED_Q;
     // fused moments: W slot s landed (peer: relayed by the leader's epilogue), and
     // this CTA's epilogue warps are done reading it (gates the W producer's refill)
-    auto mready_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (BAR_M + s); };             // peer's
-    auto mdone_bar = [&](int s) { return sbase + SMEM_BAR + 8 * (BAR_M + MAX_RING + s); };   // both CTAs
-    volatile int *sched = (volatile int *)(smem + SMEM_SCHED);
-    uint32_t *tmem_slot = (uint32_t *)(smem + SMEM_SCHED + SCHED_Q * 4);
+    auto mready_bar = [&](int s) { return sbase + Lay<V>::BAR + 8 * (BAR_M + s); };             // peer's
+    auto mdone_bar = [&](int s) { return sbase + Lay<V>::BAR + 8 * (BAR_M + MAX_RING + s); };   // both CTAs
+    volatile int *sched = (volatile int *)(smem + Lay<V>::SCHED);
+    uint32_t *tmem_slot = (uint32_t *)(smem + Lay<V>::SCHED + SCHED_Q * 4);
     auto to_leader = [&](uint32_t a) { return mapa_shared(a, 0); };
 
     // consumers: the t-th unit of this pair (-1 = done).  Called either by a
@@ -517,7 +519,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     mbar_wait(txempty_bar(x), ((it / TX_STAGES) & 1) ^ 1);
                     const int rows = (int)((t1 - tb) < C::BK ? (t1 - tb) : C::BK);
                     mbar_arrive_expect_tx(txfull_bar(x), rows * 16);
-                    bulk_load(sbase + SMEM_TX + x * TX_BYTES, p.texts + tb * 16, rows * 16, txfull_bar(x));
+                    bulk_load(sbase + Lay<V>::TX + x * Lay<V>::TXB, p.texts + tb * 16, rows * 16, txfull_bar(x));
                 }
             }
         }
@@ -597,7 +599,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
     } else if (warp >= 4 && warp < 8) {
         // ================= epilogue: TMEM -> int64 / fp64 global (atomic add) =================
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        uint32_t *tbuf = (uint32_t *)(smem + SMEM_TB) + q * 32 * TB_LD;
+        uint32_t *tbuf = (uint32_t *)(smem + Lay<V>::TB) + q * 32 * TB_LD;
         const int rsub = lane >> 3, csub = lane & 7;
         uint32_t eit = 0;     // W ring stage counter (same sequence as the producer's)
         for (uint32_t t = 0;; t++) {
@@ -664,7 +666,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 // STS.128), then ONE bulk tensor reduce-add of the 32 x 8 box into sum_hw
                 // by the TMA unit (exact int64 adds / fp64 adds).  The box is rewritten
                 // only after the previous reduce has read it.
-                const uint32_t box = sbase + SMEM_TB + q * RB_BYTES;
+                const uint32_t box = sbase + Lay<V>::TB + q * RB_BYTES;
                 const uint32_t rowb = box + lane * 64;
                 const uint32_t swz = ((uint32_t)lane >> 1) & 3;
 #pragma unroll 1
@@ -790,7 +792,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 const uint32_t ph = (it / AS) & 1;
                 const int x = it % TX_STAGES;
                 mbar_wait(txfull_bar(x), (it / TX_STAGES) & 1);
-                const uint8_t *tx = smem + SMEM_TX + x * TX_BYTES;
+                const uint8_t *tx = smem + Lay<V>::TX + x * Lay<V>::TXB;
                 uint32_t desc = 0;
                 if (lane < ROWS * C::KB) {
                     const uint32_t cb = tx[drow * 16 + b + dkb], cs = tx[drow * 16 + dsrc];
@@ -918,12 +920,12 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorM
     p.bulk_spill = mhw != nullptr;
     p.store_hw = store_hw && p.kc_count == 1 && owners == nullptr && !Cf::F32;
     static std::atomic<unsigned long long> attr_set{0};
-    cudaError_t e = smem_attr_once((const void *)k_xterm<V>, SMEM_ALLOC, attr_set);
+    cudaError_t e = smem_attr_once((const void *)k_xterm<V>, Lay<V>::ALLOC, attr_set);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(d_counter, 0, sizeof(int), stream);
     if (e != cudaSuccess) return e;
     const int pairs = (p.units < num_sms / 2 ? p.units : num_sms / 2);
-    k_xterm<V><<<2 * pairs, THREADS, SMEM_ALLOC, stream>>>(m0, m1, mhw ? *mhw : m0, p);
+    k_xterm<V><<<2 * pairs, THREADS, Lay<V>::ALLOC, stream>>>(m0, m1, mhw ? *mhw : m0, p);
     if (launches) (*launches)++;
     return cudaGetLastError();
 }
@@ -965,7 +967,7 @@ int64_t auto_kchunk(int32_t M, int64_t N, int num_sms, int kb, int nt, int bk, i
 
 }  // namespace
 
-int xterm_smem_bytes() { return SMEM_ALLOC; }
+int xterm_smem_bytes() { return Lay<V_I8>::ALLOC; }
 int xterm_f32_bk(bool nt2) { return nt2 ? Cfg<V_F32N>::BK : Cfg<V_F32>::BK; }
 
 int64_t xterm_i8_auto_kchunk(int32_t M, int64_t N, int num_sms, bool remote_epilogue)

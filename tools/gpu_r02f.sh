@@ -16,5 +16,3 @@ timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --
     --log-file $O/launches_c5_$TAG.csv python bench.py --config C5 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-clocks > /dev/null 2>&1
 TAG=$TAG bash tools/ncu_r02.sh > /dev/null 2>&1
 ls gpurun_out/*$TAG* | head -30
-rm -f gpurun_out/sanitize.log
-timeout -s KILL 2400 bash tools/sanitize.sh > /dev/null 2>&1; cp gpurun_out/sanitize.log $O/sanitize_$TAG.txt; grep -c "exit 0" $O/sanitize_$TAG.txt
