@@ -131,7 +131,10 @@ typedef struct {
  *   d_argmax  [4096]    int32    lowest j attaining it [S:298]
  *   d_rank    [4096]    int32    rank of k within byte b (1 = best; ties to
  *                                lower k [S:261, S:298])
- * res (host, may be NULL) receives the recovered key.                        */
+ * res (host, may be NULL) receives the recovered key.  The checks on N (and
+ * the float non-finite flag) are made after the kernels, from the one readback
+ * the call does: on CPA_E_TOO_FEW_TRACES / CPA_E_OVERFLOW / CPA_E_NONFINITE the
+ * device outputs are unspecified and res is not written.                     */
 CPA_API cpa_status cpa_finalize(cpa_ctx *ctx, double *d_rho, double *d_maxabs,
                         int32_t *d_argmax, int32_t *d_rank, cpa_result *res);
 

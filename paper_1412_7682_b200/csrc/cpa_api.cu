@@ -137,6 +137,15 @@ struct cpa_ctx {
     uint8_t *d_lo = nullptr;
     int64_t plane_rows = 0;
     int *d_nonfinite = nullptr;
+    // pinned host block for the one readback a blocking finalize does (N, the
+    // non-finite flag, the key) -- see readback()
+    struct HostStatus {
+        int64_t n_i;
+        double n_f;
+        int32_t nonfinite, pad;
+        int32_t best[32];
+        double best_rho[16];
+    } *h_status = nullptr;
     uint32_t *d_hist = nullptr;  // a3 byte-pair histogram scratch (16 x 65536)
     // CPA_OPT_CLASS_SUMS (HW_LAST / HW_FIRST, int8 traces): class-sum cross term
     // (classsum.cu); scratch allocated on first use
@@ -295,6 +304,7 @@ cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, 
     if (e == cudaSuccess) e = cudaMalloc(&c->d_best, sizeof(int32_t) * 32);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_counter, 256);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_nonfinite, 256);
+    if (e == cudaSuccess) e = cudaHostAlloc((void **)&c->h_status, sizeof(cpa_ctx::HostStatus), cudaHostAllocDefault);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_hist, sizeof(uint32_t) * 16 * 65536);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_clk, 4 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemsetAsync(c->d_clk, 0, 4 * sizeof(unsigned long long), c->stream);
@@ -851,34 +861,36 @@ cpa_status cpa_accumulate_host(cpa_ctx *c, const void *h_traces, int64_t ld, con
 }
 
 // N from the accumulator, with the preconditions of Eq. (1) [P:69]
-static cpa_status read_n(cpa_ctx *c, int64_t *n_out)
+// One round trip per blocking call, after its kernels are queued: N (and the
+// float path's non-finite flag, and with_key: the Phase-4 key) into pinned host
+// memory, one synchronisation, then the checks (Eq. (1) needs N >= 2; the int
+// path's int64 intermediates need N <= 2^23 [DESIGN.md]).  The kernels read N on
+// the device, so nothing waits for the host before they run; on an error return
+// the device outputs are unspecified.  (Checking first cost the step one or two
+// extra host round trips with the GPU idle.)
+static cpa_status readback(cpa_ctx *c, bool with_key, bool check, int64_t *n_out)
 {
+    cpa_ctx::HostStatus *h = c->h_status;
     const size_t off = cpa_accum_offset(c->M, 5);
-    if (c->dtype == CPA_F32) {
-        double dn = 0;
-        CUDA_TRY(cudaMemcpyAsync(&dn, (double *)c->accum + off, 8, cudaMemcpyDeviceToHost, c->stream), "read N");
-        CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
-        *n_out = (int64_t)dn;
-    } else {
-        CUDA_TRY(cudaMemcpyAsync(n_out, (int64_t *)c->accum + off, 8, cudaMemcpyDeviceToHost, c->stream), "read N");
-        CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+    const bool f32 = c->dtype == CPA_F32;
+    CUDA_TRY(cudaMemcpyAsync(f32 ? (void *)&h->n_f : (void *)&h->n_i,
+                             f32 ? (const void *)((const double *)c->accum + off) : (const void *)((const int64_t *)c->accum + off),
+                             8, cudaMemcpyDeviceToHost, c->stream), "read N");
+    if (f32) CUDA_TRY(cudaMemcpyAsync(&h->nonfinite, c->d_nonfinite, sizeof(int), cudaMemcpyDeviceToHost, c->stream),
+                      "read flag");
+    if (with_key) {
+        CUDA_TRY(cudaMemcpyAsync(h->best, c->d_best, sizeof h->best, cudaMemcpyDeviceToHost, c->stream), "D2H best");
+        CUDA_TRY(cudaMemcpyAsync(h->best_rho, c->d_best_rho, sizeof h->best_rho, cudaMemcpyDeviceToHost, c->stream),
+                 "D2H best rho");
     }
-    return CPA_OK;
-}
-
-static cpa_status finalize_checks(cpa_ctx *c, int64_t *n_out)
-{
-    int64_t n = 0;
-    cpa_status st = read_n(c, &n);
-    if (st != CPA_OK) return st;
-    if (n < 2) return fail(CPA_E_TOO_FEW_TRACES, "N=%lld < 2: Eq. (1) undefined", (long long)n);
-    if (c->dtype == CPA_F32) {
-        int bad = 0;
-        CUDA_TRY(cudaMemcpy(&bad, c->d_nonfinite, sizeof(int), cudaMemcpyDeviceToHost), "read flag");
-        if (bad) return fail(CPA_E_NONFINITE, "a float trace sample was NaN or Inf");
+    CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+    const int64_t n = f32 ? (int64_t)h->n_f : h->n_i;
+    if (check) {
+        if (n < 2) return fail(CPA_E_TOO_FEW_TRACES, "N=%lld < 2: Eq. (1) undefined", (long long)n);
+        if (f32 && h->nonfinite) return fail(CPA_E_NONFINITE, "a float trace sample was NaN or Inf");
+        if (!f32 && n > kMaxTraces)
+            return fail(CPA_E_OVERFLOW, "N=%lld > 2^23: Eq. (1) intermediates may overflow int64", (long long)n);
     }
-    if (c->dtype != CPA_F32 && n > kMaxTraces)
-        return fail(CPA_E_OVERFLOW, "N=%lld > 2^23: Eq. (1) intermediates may overflow int64", (long long)n);
     *n_out = n;
     return CPA_OK;
 }
@@ -899,27 +911,26 @@ static cpa_status phase3(cpa_ctx *c, const cpa::FinalizeOut &o, int *launches)
 }
 
 // a9 on o.maxabs/argmax/peak, then the key D2H
-static cpa_status phase4(cpa_ctx *c, const cpa::FinalizeOut &o, int64_t n, int *launches, cpa_result *res)
+static cpa_status phase4(cpa_ctx *c, const cpa::FinalizeOut &o, int *launches)
 {
     CUDA_TRY(c->timed(4, [&] { return cpa::launch_phase4(o, c->stream, launches); }), "phase4");
-    int32_t best[32];
-    double brho[16];
-    CUDA_TRY(cudaMemcpyAsync(best, c->d_best, sizeof best, cudaMemcpyDeviceToHost, c->stream), "D2H best");
-    CUDA_TRY(cudaMemcpyAsync(brho, c->d_best_rho, sizeof brho, cudaMemcpyDeviceToHost, c->stream), "D2H best rho");
-    CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
-    if (res) {
-        for (int b = 0; b < 16; b++) {
-            res->round_key[b] = (uint8_t)best[b];
-            res->peak_sample[b] = best[16 + b];
-            res->peak_rho[b] = brho[b];
-        }
-        if (c->model == CPA_HW_FIRST)
-            std::memcpy(res->master_key, res->round_key, 16);
-        else
-            cpa::aes_invert_key_schedule(res->round_key, 10, res->master_key);
-        res->n_traces = n;
-    }
     return CPA_OK;
+}
+// the key of the last readback(with_key)
+static void fill_result(cpa_ctx *c, int64_t n, cpa_result *res)
+{
+    if (!res) return;
+    const cpa_ctx::HostStatus *h = c->h_status;
+    for (int b = 0; b < 16; b++) {
+        res->round_key[b] = (uint8_t)h->best[b];
+        res->peak_sample[b] = h->best[16 + b];
+        res->peak_rho[b] = h->best_rho[b];
+    }
+    if (c->model == CPA_HW_FIRST)
+        std::memcpy(res->master_key, res->round_key, 16);
+    else
+        cpa::aes_invert_key_schedule(res->round_key, 10, res->master_key);
+    res->n_traces = n;
 }
 
 static cpa::FinalizeOut outputs(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_argmax, double *d_peak,
@@ -942,14 +953,14 @@ cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_
 {
     if (!c) return fail(CPA_E_INVALID_ARG, "null context");
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
-    int64_t n = 0;
-    cpa_status st = finalize_checks(c, &n);
-    if (st != CPA_OK) return st;
     cpa::FinalizeOut o = outputs(c, d_rho, d_maxabs, d_argmax, nullptr, d_rank);
     int launches = 0;
-    st = phase3(c, o, &launches);
-    if (st == CPA_OK) st = phase4(c, o, n, &launches, res);
+    cpa_status st = phase3(c, o, &launches);
+    if (st == CPA_OK) st = phase4(c, o, &launches);
     c->launches += launches;
+    int64_t n = 0;
+    if (st == CPA_OK) st = readback(c, true, true, &n);
+    if (st == CPA_OK) fill_result(c, n, res);
     return st;
 }
 
@@ -1059,16 +1070,14 @@ cpa_status cpa_finalize_rows(cpa_ctx *c, int32_t h0, int32_t h1, double *d_rho, 
     if (h0 < 0 || h1 > 4096 || h0 > h1) return fail(CPA_E_INVALID_ARG, "rows [%d, %d) outside [0, 4096]", h0, h1);
     if (!d_maxabs || !d_argmax || !d_peak) return fail(CPA_E_INVALID_ARG, "d_maxabs, d_argmax and d_peak are required");
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
-    int64_t n = 0;
-    cpa_status st = finalize_checks(c, &n);
-    if (st != CPA_OK) return st;
     cpa::FinalizeOut o = outputs(c, d_rho, d_maxabs, d_argmax, d_peak, nullptr);
     o.h0 = h0;
     o.h1 = h1;
     int launches = 0;
-    st = phase3(c, o, &launches);
+    cpa_status st = phase3(c, o, &launches);
     c->launches += launches;
-    if (st == CPA_OK) CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+    int64_t n = 0;
+    if (st == CPA_OK) st = readback(c, false, true, &n);
     return st;
 }
 
@@ -1079,17 +1088,17 @@ cpa_status cpa_select(cpa_ctx *c, int32_t G, double *d_maxabs, int32_t *d_argmax
     if (G < 1 || G > 65536) return fail(CPA_E_INVALID_ARG, "G=%d outside [1, 65536]", G);
     if (!d_maxabs || !d_argmax || !d_peak) return fail(CPA_E_INVALID_ARG, "d_maxabs, d_argmax and d_peak are required");
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
-    int64_t n = 0;
-    cpa_status st = read_n(c, &n);
-    if (st != CPA_OK) return st;
     cpa::FinalizeOut o = outputs(c, nullptr, d_maxabs, d_argmax, d_peak, d_rank);
     int launches = 0;
     if (G > 1)
         CUDA_TRY(c->timed(4, [&] { return cpa::launch_merge_shards(G, d_maxabs, d_argmax, d_peak, c->stream,
                                                                    &launches); }),
                  "merge shards");
-    st = phase4(c, o, n, &launches, res);
+    cpa_status st = phase4(c, o, &launches);
     c->launches += launches;
+    int64_t n = 0;
+    if (st == CPA_OK) st = readback(c, true, false, &n);
+    if (st == CPA_OK) fill_result(c, n, res);
     return st;
 }
 
@@ -1159,6 +1168,7 @@ cpa_status cpa_destroy(cpa_ctx *c)
     cudaFree(c->d_hi);
     cudaFree(c->d_lo);
     cudaFree(c->d_nonfinite);
+    cudaFreeHost(c->h_status);
     cudaFree(c->d_hist);
     cudaFree(c->d_clk);
     cudaFree(c->d_cs_cnt);

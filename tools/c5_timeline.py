@@ -14,7 +14,8 @@ sys.path.insert(0, ROOT)
 def main():
     import bench
     cfg = sys.argv[1] if len(sys.argv) > 1 else "C5"
-    sys.argv = ["bench.py", "--config", cfg, "--steps", "2", "--warmup", "2", "--no-clocks", "--no-phase-times"]
+    sys.argv = ["bench.py", "--config", cfg, "--steps", "2", "--warmup", "2", "--no-clocks", "--no-phase-times",
+                "--no-e2e", "--no-cpu-baseline"]
     from torch.profiler import ProfilerActivity, profile
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         bench.main()
