@@ -40,6 +40,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -205,6 +206,12 @@ struct Params {
     int32_t groups;          // key-byte groups (16 / KB)
     int32_t kc_count;
     int32_t units;
+    // tail split (one trace chunk per tile): units [0, full_units) are whole
+    // tiles; the remaining tiles are cut into tail_parts pieces of tail_len
+    // traces, ordered piece-major, so the last wave is filled by short units
+    // instead of leaving pairs idle (full_units == units: no tail split)
+    int32_t full_units;
+    int64_t tail_len;
     int64_t N;
     int64_t kc_len;
     uint32_t idesc;
@@ -236,6 +243,16 @@ struct Params {
 template <int V>
 __device__ __forceinline__ void unit_coords(const Params &p, int u, int &b, int &n_tile, int64_t &t0, int64_t &t1)
 {
+    if (u >= p.full_units) {  // tail piece: (tile, piece), tiles fastest within a piece
+        const int tail_tiles = p.groups * p.n_tiles - p.full_units;
+        const int v = u - p.full_units, tile = p.full_units + v % tail_tiles;
+        b = (tile % p.groups) * Cfg<V>::KB;
+        n_tile = tile / p.groups;
+        t0 = (int64_t)(v / tail_tiles) * p.tail_len;
+        t1 = t0 + p.tail_len;
+        if (t1 > p.N) t1 = p.N;
+        return;
+    }
     // b = first key byte of the unit's group (bytes b .. b+KB-1)
     b = (u % p.groups) * Cfg<V>::KB;
     const int r = u / p.groups;
@@ -659,7 +676,9 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 if (lane == 0) mbar_arrive_cluster(to_leader(tempty_bar(acc)));
                 continue;
             }
-            if (p.bulk_spill && own == nullptr && !p.store_hw) {
+            // first touch: the unit is the only writer of its cells (a whole tile)
+            const bool store_u = p.store_hw && u < p.full_units;
+            if (p.bulk_spill && own == nullptr && !store_u) {
                 // lane = accumulator row: its 8 samples as int64 (I8) or as fp64 times
                 // 2^16 / s_j (F32) into the warp's box (64 B per row, 16-byte chunks
                 // XOR-swizzled by (row >> 1) & 3 -- the TMA 64B swizzle, conflict-free
@@ -739,7 +758,7 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                         } else if (own != nullptr) {  // peer (or own) accumulator of the row owner
                             atomicAdd_system((unsigned long long *)own + off + (int64_t)(4 * rr) * p.M,
                                              (unsigned long long)(long long)(int32_t)bits);
-                        } else if (p.store_hw) {      // first touch (store_hw): no read-modify-write
+                        } else if (store_u) {         // first touch (store_hw): no read-modify-write
                             ((long long *)p.hw)[off + (int64_t)(4 * rr) * p.M] = (long long)(int32_t)bits;
                         } else {
                             atomicAdd((unsigned long long *)p.hw + off + (int64_t)(4 * rr) * p.M,
@@ -882,6 +901,66 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
     }
 }
 
+// Tail split (one trace chunk per tile, more tiles than CTA pairs, not a whole
+// number of waves): the last, partial wave of whole tiles leaves pairs idle (C5:
+// 640 tiles on 74 pairs = 8.65 waves, run as 9).  Keep whole tiles for the full
+// waves (rounded down to whole tile groups, so a W tile stays shared by its 16
+// key bytes) and cut the remaining tiles into S pieces; S is chosen by simulating
+// the in-order, earliest-free-pair schedule with each unit paying its epilogue
+// (modelled as ~25k clk against 1024 clk per stage).
+#ifndef XT_TAIL_SPLIT
+#define XT_TAIL_SPLIT 1
+#endif
+void tail_split(Params &p, int pairs, int bk)
+{
+    const int T = p.units;
+    if (pairs < 1 || T <= pairs || T % pairs == 0) return;
+    // short units (W48: 63 stages, C2: 16) measured SLOWER split (W48 cross term
+    // 1.155 vs 1.103 ms, C2 0.101 vs 0.081): their pieces lose the first-touch
+    // stores and pay a whole epilogue for a few stages.  Long units only.
+    if (p.store_hw || (p.N + bk - 1) / bk < 256) return;
+    const int F = (T / pairs) * pairs / p.groups * p.groups;
+    const int R = T - F;
+    const int64_t stages = (p.N + bk - 1) / bk;
+    const double epi = 25000.0 / (1024.0 * (double)stages);  // per unit, in whole-tile lengths
+    auto makespan = [&](int S, int64_t len) {
+        const int pieces = (int)((p.N + len - 1) / len);
+        std::vector<double> busy((size_t)pairs, 0.0);
+        auto take = [&](double w) {
+            size_t k = 0;
+            for (size_t i = 1; i < busy.size(); i++)
+                if (busy[i] < busy[k]) k = i;
+            busy[k] += w + epi;
+        };
+        for (int u = 0; u < F; u++) take(1.0);
+        for (int q = 0; q < pieces; q++) {
+            const double w = (double)std::min(len, p.N - (int64_t)q * len) / (double)p.N;
+            for (int t = 0; t < R; t++) take(w);
+        }
+        (void)S;
+        double m = 0.0;
+        for (double x : busy) m = x > m ? x : m;
+        return m;
+    };
+    double best = makespan(1, p.N);
+    int best_s = 1;
+    int64_t best_len = p.N;
+    for (int S = 2; S <= 4; S++) {
+        const int64_t len = (stages + S - 1) / S * bk;
+        if (len >= p.N) break;
+        const double m = makespan(S, len);
+        if (m < best * 0.995) {
+            best = m;
+            best_s = S;
+            best_len = len;
+        }
+    }
+    if (best_s == 1) return;
+    p.full_units = F;
+    p.tail_len = best_len;
+    p.units = F + R * (int)((p.N + best_len - 1) / best_len);
+}
+
 template <int V>
 cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorMap *mhw, const uint8_t *d_texts,
                    const uint8_t *d_vtab,
@@ -919,6 +998,9 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorM
         return cudaErrorInvalidValue;
     p.bulk_spill = mhw != nullptr;
     p.store_hw = store_hw && p.kc_count == 1 && owners == nullptr && !Cf::F32;
+    p.full_units = p.units;
+    p.tail_len = 0;
+    if (XT_TAIL_SPLIT && p.kc_count == 1 && d_part == nullptr) tail_split(p, num_sms / 2, Cf::BK);
     static std::atomic<unsigned long long> attr_set{0};
     cudaError_t e = smem_attr_once((const void *)k_xterm<V>, Lay<V>::ALLOC, attr_set);
     if (e != cudaSuccess) return e;

@@ -480,3 +480,27 @@ def test_maxima_only_finalize_equals_rho_maxima(P, dtype, m, dup):
     assert np.array_equal(pk[h0:h1].cpu().numpy(), rho[np.arange(h0, h1), a.argmax(axis=1)[h0:h1]])
     assert not mx[:h0].any() and not mx[h1:].any()
     eng.close()
+
+
+@pytest.mark.parametrize("n,m", [(40000, 2600), (34000, 5000)])
+def test_tail_split_bit_identical(P, n, m):
+    """One trace chunk per tile, long units, more tiles than CTA pairs and not a
+    whole number of waves: the last wave's tiles are cut into pieces
+    (xterm.cu tail_split).  Every sum equals a two-chunk run (no tail split) bit
+    for bit, and sampled columns of the split tiles (the last tile groups) equal
+    the oracle."""
+    rng = np.random.default_rng(n + m)
+    texts = rng.integers(0, 256, (n, 16), dtype=np.uint8)
+    W = rng.integers(-128, 128, (n, m)).astype(np.int8)
+    # one trace chunk per tile (kchunk >= n); a first 1-trace call, so the second
+    # adds (long units and no first touch: the tail split applies)
+    split, out0 = run_gpu(P, texts, W, chunks=[0, 1, n], kchunk=(n + 127) // 128 * 128)
+    kc = ((n + 1) // 2 + 127) // 128 * 128
+    two, out1 = run_gpu(P, texts, W, kchunk=kc)
+    for k in split:
+        assert np.array_equal(split[k], two[k]), k
+    assert np.array_equal(out0["rho"].cpu().numpy(), out1["rho"].cpu().numpy())
+    cols = np.array(sorted({0, 511, m - 512, m - 300, m - 1}), np.int32)
+    assert np.array_equal(split["sum_hw"][:, cols], O.cross_sums_i8(O.HD_LAST, texts, W, cols))
+    sw, sw2 = O.trace_sums_i8(W)
+    assert np.array_equal(split["sum_w"], sw) and np.array_equal(split["sum_w2"], sw2)
