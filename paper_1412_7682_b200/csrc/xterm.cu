@@ -207,9 +207,9 @@ struct Params {
     int32_t kc_count;
     int32_t units;
     // tail split (one trace chunk per tile): units [0, full_units) are whole
-    // tiles; the remaining tiles are cut into tail_parts pieces of tail_len
-    // traces, ordered piece-major, so the last wave is filled by short units
-    // instead of leaving pairs idle (full_units == units: no tail split)
+    // tiles; the remaining tiles are cut into pieces of tail_len traces, ordered
+    // piece-major, so the last wave is filled by short units instead of leaving
+    // pairs idle (full_units == units: no tail split; see tail_split)
     int32_t full_units;
     int64_t tail_len;
     int64_t N;
