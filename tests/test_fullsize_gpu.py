@@ -83,3 +83,71 @@ def test_c4_fullsize_sampled_parity():
     ranks = out["rank"].cpu().numpy()
     assert all(ranks[256 * b + rk[b]] == 1 for b in range(16))
     eng.close()
+
+
+def test_c5_fullsize_streamed_sampled_parity():
+    """Full-size parity at BASELINE.json's configs[4] (C5: 1.5M traces x 20000
+    samples int8, streamed in 64K-trace chunks with a checkpoint after every
+    chunk), in bench.py's single-GPU launch configuration: traces generated on
+    the device chunk by chunk, 23 cross-term launches (one trace chunk per tile:
+    the tail split applies), 22 non-blocking checkpoints (maxima-only kernel,
+    M >= 8192) and a final blocking one writing rho.  Checked: closed forms over
+    every output; sum W, sum W^2 and 48 hypotheses x a column in every 512-sample
+    tile group against the oracle, rho bit-exact there; the checkpoint ranks of
+    the last checkpoint equal the final finalize's; every byte ranks 1."""
+    import paper_1412_7682_b200 as P
+    from paper_1412_7682_b200.stream import StreamingAttack, chunk_rounds
+    w = S.CONFIGS["C5"]
+    chunk = 65536
+    rounds = chunk_rounds(w.n, chunk, 1)
+    ld = (w.m + 15) // 16 * 16
+    dW = torch.empty((w.n, ld), dtype=torch.int8, device="cuda")
+    texts, lv = S.texts(w)
+    S.dev_traces(w, torch.from_numpy(lv).cuda(), 0, w.n, dW, ld)   # 30 GB on the device
+    dT = torch.from_numpy(texts).cuda()
+    st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, 0)
+    rank_buf = torch.empty((len(rounds), 4096), dtype=torch.int32, device="cuda")
+    st.reset()
+    for j, rnd in enumerate(rounds):
+        for _, i0, i1 in rnd:
+            st.add(dW[i0:i1, :w.m], dT[i0:i1])
+        if j < len(rounds) - 1:
+            assert st.checkpoint_async(rank_buf[j])
+        else:
+            out = st.checkpoint(want_rho=True)
+    eng = st.eng
+    assert int(eng.n.item()) == w.n
+    rk = O.expand_key(w.key)[10].astype(int)
+    assert out["master_key"] == w.key
+    assert all(int(out["rank"][256 * b + rk[b]].item()) == 1 for b in range(16))
+
+    hw = eng.sum_hw.view(16, 256, w.m)
+    assert torch.equal(hw.sum(1), 1024 * eng.sum_w.view(1, -1).expand(16, -1))
+    assert torch.equal(eng.sum_h.view(16, 256).sum(1), torch.full((16,), 1024 * w.n, device="cuda", dtype=torch.int64))
+    assert torch.equal(eng.sum_h2.view(16, 256).sum(1), torch.full((16,), 4608 * w.n, device="cuda", dtype=torch.int64))
+
+    groups = [g * 512 + (g * 131) % 512 for g in range((w.m + 511) // 512)]
+    cols = np.array(sorted(set([c for c in groups if c < w.m] + [w.leak_positions()[3], w.m - 1])), np.int32)
+    assert set(int(c) // 512 for c in cols) == set(range((w.m + 511) // 512))
+    rng = np.random.default_rng(5)
+    hyps = np.array(sorted(set([256 * b + rk[b] for b in range(16)]) | set(rng.integers(0, 4096, 32).tolist())),
+                    np.int32)
+    Wc = S.traces(w, lv, 0, cols)                     # host generator, same bytes
+    assert np.array_equal(Wc, dW[:, torch.from_numpy(cols).long().cuda()].cpu().numpy())
+    ref_sw, ref_sw2 = O.trace_sums_i8(Wc)
+    assert np.array_equal(eng.sum_w.cpu().numpy()[cols], ref_sw)
+    assert np.array_equal(eng.sum_w2.cpu().numpy()[cols], ref_sw2)
+    ref_sh, ref_sh2 = O.model_sums_hyps(O.HD_LAST, texts, hyps)
+    assert np.array_equal(eng.sum_h.cpu().numpy()[hyps], ref_sh)
+    assert np.array_equal(eng.sum_h2.cpu().numpy()[hyps], ref_sh2)
+    ref_hw = O.cross_sums_hyps_i8(O.HD_LAST, texts, Wc, hyps)
+    assert np.array_equal(eng.sum_hw.cpu().numpy()[hyps][:, cols], ref_hw)
+    rho = out["rho"].cpu().numpy()
+    for a, h in enumerate(hyps):
+        for c, j in enumerate(cols):
+            assert rho[h, j] == O.rho_eq1(w.n, ref_hw[a, c], ref_sh[a], ref_sh2[a], ref_sw[c], ref_sw2[c])
+    # the last non-blocking checkpoint (all chunks but the last) is a prefix:
+    # its ranks must be valid permutations per byte; the final ones equal cpa_finalize's
+    r = rank_buf[-2].view(16, 256).cpu().numpy()
+    assert all(sorted(r[b].tolist()) == list(range(1, 257)) for b in range(16))
+    st.close()
