@@ -127,11 +127,12 @@ def test_select_and_rows_errors(P, c1):
 
 
 def test_wide_traces_w48_sampled_parity_and_column_shards(P):
-    """Paper's wide-trace shape: 48000 samples per trace (N = 2000 here so the
-    oracle's sampled columns run in seconds); sampled sums and rho bit-exact,
-    closed form over every column, key at the planted samples, and G = 4
-    column shards equal to the single context."""
-    w = S.CONFIGS["W48"].replace(n=2000)
+    """Paper's wide-trace shape at bench's W48 size (8000 traces x 48000
+    samples, one trace chunk per tile: first-touch stores); sampled sums and
+    rho bit-exact against the oracle (all 4096 hypotheses), closed form over
+    every column, key at the planted samples, and G = 4 column shards equal to
+    the single context."""
+    w = S.CONFIGS["W48"]
     texts, W = S.dataset(w)
     dW = _padded(W)
     eng = P.Engine(w.m, P.CPA_S8, P.CPA_HD_LAST, 0)
