@@ -1,8 +1,8 @@
 """Phase-3 finalize (a8) timing: for each M, sums from N synthetic traces,
 then cpa_finalize_rows(0, 4096) with and without rho, timed by the library's
-CUDA events (phase 3), interleaved rounds.  (During development it compared
-kernel variants through a CPA_FIN_VARIANT hook, since removed; DESIGN.md
-records the results.)  One JSON line per (M, rho)."""
+CUDA events (phase 3) over FIN_ROUNDS rounds.  Kernel variants are compared by
+running it against differently built libraries (CPA_LIB_PATH, tools/ab.sh);
+DESIGN.md records the results.  One JSON line per (M, rho)."""
 import json
 import os
 import sys
@@ -14,21 +14,7 @@ sys.path.insert(0, ROOT)
 import paper_1412_7682_b200 as P  # noqa: E402
 from synth import synth as S  # noqa: E402
 
-VARIANTS = os.environ.get("FIN_VARIANTS", "default").split(",")
-
-
-def set_variant(v):
-    """'0' one-row kernels; 'RU' rows x unroll; suffix 'nf' = no-rho filter off;
-    'RUuK' = the filtered kernel with unroll K."""
-    os.environ.pop("CPA_FIN_FILTER_U", None)
-    os.environ.pop("CPA_FIN_NOFILTER", None)
-    base = v.replace("nf", "")
-    if "u" in base:
-        base, fu = base.split("u")
-        os.environ["CPA_FIN_FILTER_U"] = fu
-    os.environ["CPA_FIN_VARIANT"] = base
-    if v.endswith("nf"):
-        os.environ["CPA_FIN_NOFILTER"] = "1"
+VARIANTS = ["default"]
 
 
 def main():
@@ -52,7 +38,6 @@ def main():
             mx, am, pk = (t[0] for t in eng.maxima_buffers(1))
             for rnd in range(int(os.environ.get("FIN_ROUNDS", "5"))):   # interleaved: clock drift hits all alike
                 for v in VARIANTS:
-                    set_variant(v)
                     if rnd == 0:
                         rho = eng.finalize_rows(0, 4096, mx, am, pk, want_rho)
                         out = (rho, mx.clone(), am.clone(), pk.clone())
