@@ -255,3 +255,26 @@ def test_float_strided_rows(P, pitch, col):
     print(f"pitch {pitch} col {col}: max |drho| = {err:.3g}")
     assert err <= TIGHT
     assert out["master_key"] == w.key
+
+
+def test_float_tail_split(P):
+    """Float traces with one trace chunk per tile, long units and more tiles
+    than CTA pairs (the tail split of the last wave, xterm.cu tail_split): rho
+    within the bar against the oracle on columns of the split tiles, and every
+    cell within 1e-5 of a two-chunk run."""
+    w = S.CONFIGS["C3"].replace(n=20000, m=2600, a=0.02)
+    texts, W = S.dataset(w)
+    cols = np.array([0, 700, 2047, 2048, 2300, 2599], np.int32)   # the split tiles: columns >= 2048
+    shw, sw, sw2 = O.sums_f32(O.HD_LAST, texts, W, cols)
+    sh, sh2 = O.model_sums(O.HD_LAST, texts)
+    ref = O.rho_eq1_f64_grid(w.n, shw, sh, sh2, sw, sw2)
+    outs = []
+    for kc in (20096, 10112):                       # one chunk (tail split) / two chunks
+        eng = P.Engine(w.m, P.CPA_F32, P.CPA_HD_LAST, 0)
+        eng.set_kchunk(kc)
+        eng.accumulate(torch.from_numpy(W).cuda(), torch.from_numpy(texts).cuda())
+        outs.append(eng.finalize(want_rho=True)["rho"].cpu().numpy())
+        eng.close()
+    for rho in outs:
+        assert np.max(np.abs(rho[:, cols] - ref)) <= TOL
+    assert np.max(np.abs(outs[0] - outs[1])) <= TIGHT
