@@ -157,6 +157,27 @@ CPA_API cpa_status cpa_finalize(cpa_ctx *ctx, double *d_rho, double *d_maxabs,
 CPA_API cpa_status cpa_finalize_async(cpa_ctx *ctx, double *d_rho, double *d_maxabs, int32_t *d_argmax,
                                       int32_t *d_rank, int32_t *d_best);
 
+/* ---- CUDA-graph replay of a fixed-shape step ------------------------------
+ * cpa_graph_begin starts capturing the context's stream (stream capture, thread-
+ * local mode; the context's stream must not be the legacy default stream):
+ * the calls made until cpa_graph_end are recorded instead of run, and
+ * cpa_graph_launch then replays them on the context's stream as ONE graph
+ * launch, asynchronously (no per-kernel launch cost, no host work between the
+ * kernels of a step).  Capturable: cpa_reset, cpa_accumulate on 16-byte aligned
+ * device buffers (not with class sums), cpa_finalize_async; a captured
+ * cpa_accumulate needs a captured cpa_reset before it (a replay starts from
+ * zeroed sums), and the buffers it allocates on first use (float planes) must
+ * already exist -- run the step once outside the capture first.  Calls that
+ * synchronise, read back or allocate (cpa_finalize, cpa_finalize_rows,
+ * cpa_select, cpa_accumulate_host, cpa_sync, cpa_phase_times, the offset calls)
+ * return CPA_E_INVALID_ARG while capturing.  Replays update no host-side state
+ * (the running-total N check, launch count, phase times: CPA_OPT_TIMING events
+ * are not captured); the pointers and sizes are those of the capture.
+ * cpa_graph_end replaces a previous graph; cpa_destroy frees it.            */
+CPA_API cpa_status cpa_graph_begin(cpa_ctx *ctx);
+CPA_API cpa_status cpa_graph_end(cpa_ctx *ctx);
+CPA_API cpa_status cpa_graph_launch(cpa_ctx *ctx);
+
 /* ---- fused multi-GPU combine ([P:230]) -----------------------
  * cpa_set_row_owners: the cross-term kernel adds its int64 partial sum_hw of key
  * byte b (hypothesis rows [256 b, 256 b + 256)) straight into the packed

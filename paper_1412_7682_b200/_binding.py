@@ -30,7 +30,7 @@ ABI_SYMBOLS = (
     "cpa_set_row_owners", "cpa_ipc_export", "cpa_ipc_open", "cpa_ipc_close", "cpa_xterm_clock", "cpa_peer_atomics", "cpa_reset", "cpa_sync", "cpa_destroy",
     "cpa_get_offsets", "cpa_default_offsets",
     "cpa_set_offsets", "cpa_set_option", "cpa_phase_times", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
-    "cpa_aes_expand_key", "cpa_aes_invert_key_schedule",
+    "cpa_aes_expand_key", "cpa_aes_invert_key_schedule", "cpa_graph_begin", "cpa_graph_end", "cpa_graph_launch",
 )
 
 
@@ -63,6 +63,9 @@ def _load():
         "cpa_finalize": (ST, [P, P, P, P, P, C.POINTER(cpa_result)]),
         "cpa_finalize_rows": (ST, [P, I32, I32, P, P, P, P]),
         "cpa_finalize_async": (ST, [P, P, P, P, P, P]),
+        "cpa_graph_begin": (ST, [P]),
+        "cpa_graph_end": (ST, [P]),
+        "cpa_graph_launch": (ST, [P]),
         "cpa_select": (ST, [P, I32, P, P, P, P, C.POINTER(cpa_result)]),
         "cpa_set_row_owners": (ST, [P, P]),
         "cpa_ipc_export": (ST, [P, P, C.POINTER(C.c_uint64)]),
@@ -207,6 +210,18 @@ def cpa_reset(ctx):
 
 def cpa_sync(ctx):
     _check(_lib.cpa_sync(ctx), "cpa_sync")
+
+
+def cpa_graph_begin(ctx):
+    _check(_lib.cpa_graph_begin(ctx), "cpa_graph_begin")
+
+
+def cpa_graph_end(ctx):
+    _check(_lib.cpa_graph_end(ctx), "cpa_graph_end")
+
+
+def cpa_graph_launch(ctx):
+    _check(_lib.cpa_graph_launch(ctx), "cpa_graph_launch")
 
 
 def cpa_destroy(ctx):

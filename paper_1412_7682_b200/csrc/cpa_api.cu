@@ -41,6 +41,12 @@ cpa_status cuda_fail(cudaError_t e, const char *where)
         cudaError_t e_ = (expr);                     \
         if (e_ != cudaSuccess) return cuda_fail(e_, where); \
     } while (0)
+// calls that synchronise, read back or allocate cannot be part of a captured graph
+#define NO_CAPTURE(c)                                                                              \
+    do {                                                                                           \
+        if ((c)->capturing)                                                                        \
+            return fail(CPA_E_INVALID_ARG, "%s: not allowed while capturing a graph", __func__);   \
+    } while (0)
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode()
 {
@@ -153,6 +159,10 @@ struct cpa_ctx {
     int fuse_hist = 0;
     int xt_tiles = 0;  // CPA_OPT_XT_TILES: 0 model, 1 NT = 2, 2 NT = 1 overlapped
     int spill = 0;  // CPA_OPT_SPILL: 0 auto, 1 red.add per element, 2 bulk tensor reduce-add, 3 partial stores
+    // CUDA-graph capture of the context's stream (cpa_graph_begin / _end / _launch)
+    bool capturing = false;
+    bool captured_reset = false;  // a cpa_reset was captured before any accumulate
+    cudaGraphExec_t graph_exec = nullptr;
     uint32_t *d_part = nullptr;  // partial-sum spill slices [kc][4096][ld] (32-bit), grown on demand
     int64_t part_bytes = 0;
     // the partial buffer for kc_count slices of part_ld samples (null: over the
@@ -161,6 +171,7 @@ struct cpa_ctx {
         const int64_t need = kc_count * 4096 * part_ld * 4;
         if (need > kPartMaxBytes) return nullptr;
         if (need > part_bytes) {
+            if (capturing) return nullptr;  // no allocation inside a capture: the atomic spill
             if (cudaStreamSynchronize(stream) != cudaSuccess) return nullptr;
             cudaFree(d_part);
             d_part = nullptr;
@@ -191,7 +202,7 @@ struct cpa_ctx {
     // time the launches `fn` issues on the stream as phase `ph`
     template <typename F> cudaError_t timed(int ph, F &&fn) { return timed_on(ph, stream, fn); }
     template <typename F> cudaError_t timed_on(int ph, cudaStream_t st, F &&fn) {
-        if (!timing) return fn();
+        if (!timing || capturing) return fn();  // replays of a captured graph are not phase-timed
         Rec r{ph, ev(), ev()};
         cudaEventRecord(r.a, st);
         cudaError_t e = fn();
@@ -258,6 +269,7 @@ cpa_status cpa_reset(cpa_ctx *ctx)
     CUDA_TRY(cudaMemsetAsync(ctx->d_nonfinite, 0, sizeof(int), ctx->stream), "reset flag");
     ctx->n_since_reset = 0;
     ctx->hw_zero = true;
+    if (ctx->capturing) ctx->captured_reset = true;
     return CPA_OK;
 }
 
@@ -338,6 +350,7 @@ cpa_status cpa_init(cpa_ctx **out, int32_t M, cpa_dtype dtype, cpa_model model, 
 cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets)
 {
     if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
+    NO_CAPTURE(ctx);
     if (ctx->dtype != CPA_F32) return fail(CPA_E_INVALID_ARG, "offsets apply to CPA_F32 contexts only");
     CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
     if (d_offsets)
@@ -353,6 +366,7 @@ cpa_status cpa_set_offsets(cpa_ctx *ctx, const float *d_offsets)
 cpa_status cpa_default_offsets(cpa_ctx *ctx, const float *d_traces, int64_t ld, int64_t N, float *d_out)
 {
     if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
+    NO_CAPTURE(ctx);
     if (ctx->dtype != CPA_F32) return fail(CPA_E_INVALID_ARG, "offsets apply to CPA_F32 contexts only");
     if (!d_traces || !d_out || N < 1 || ld < ctx->M) return fail(CPA_E_INVALID_ARG, "bad traces / N / ld / out");
     CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
@@ -367,6 +381,7 @@ cpa_status cpa_default_offsets(cpa_ctx *ctx, const float *d_traces, int64_t ld, 
 cpa_status cpa_get_offsets(cpa_ctx *ctx, float *d_out, int *is_set)
 {
     if (!ctx) return fail(CPA_E_INVALID_ARG, "null context");
+    NO_CAPTURE(ctx);
     if (ctx->dtype != CPA_F32) return fail(CPA_E_INVALID_ARG, "offsets apply to CPA_F32 contexts only");
     CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
     if (d_out)
@@ -545,6 +560,9 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
         const int64_t max_rows = (1LL << 30) / (ldh * 2);  // <= 1 GiB per fp16 plane
         const int64_t chunk = n < max_rows ? n : max_rows;
         if (c->plane_rows < chunk) {
+            if (c->capturing)
+                return fail(CPA_E_INVALID_ARG, "the float planes must be allocated before a capture: run the "
+                                               "call once outside it");
             CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
             cudaFree(c->d_hi);
             cudaFree(c->d_lo);
@@ -761,7 +779,16 @@ cpa_status cpa_accumulate(cpa_ctx *c, const void *d_traces, int64_t ld, const ui
     if (st != CPA_OK || N == 0) return st;
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
     const int64_t esz = c->dtype == CPA_F32 ? 4 : 1;
-    if (((uintptr_t)d_traces & 15) || ((ld * esz) & 15) || ((uintptr_t)d_texts & 15))
+    const bool staged = ((uintptr_t)d_traces & 15) || ((ld * esz) & 15) || ((uintptr_t)d_texts & 15);
+    if (c->capturing) {
+        // a replay must start from the sums the capture assumed (first-touch
+        // stores, the N bookkeeping): the graph begins with cpa_reset
+        if (!c->captured_reset)
+            return fail(CPA_E_INVALID_ARG, "cpa_accumulate in a graph capture needs a captured cpa_reset first");
+        if (staged) return fail(CPA_E_INVALID_ARG, "unaligned traces go through staging buffers: not capturable");
+        if (c->class_sums) return fail(CPA_E_INVALID_ARG, "the class-sum cross term is not capturable");
+    }
+    if (staged)
         st = accumulate_staged(c, d_traces, ld, d_texts, N);  // TMA needs 16-byte strides
     else
         st = accumulate_device(c, d_traces, ld, d_texts, N);
@@ -850,6 +877,7 @@ static cpa_status accumulate_staged(cpa_ctx *c, const void *src, int64_t ld, con
 
 cpa_status cpa_accumulate_host(cpa_ctx *c, const void *h_traces, int64_t ld, const uint8_t *h_texts, int64_t N)
 {
+    if (c && c->capturing) NO_CAPTURE(c);
     cpa_status st = check_accumulate_args(c, h_traces, ld, h_texts, N);
     if (st != CPA_OK || N == 0) return st;
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
@@ -952,6 +980,7 @@ cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_
                         cpa_result *res)
 {
     if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    NO_CAPTURE(c);
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
     cpa::FinalizeOut o = outputs(c, d_rho, d_maxabs, d_argmax, nullptr, d_rank);
     int launches = 0;
@@ -967,6 +996,7 @@ cpa_status cpa_finalize(cpa_ctx *c, double *d_rho, double *d_maxabs, int32_t *d_
 cpa_status cpa_xterm_clock(cpa_ctx *c, double *mhz)
 {
     if (!c || !mhz) return fail(CPA_E_INVALID_ARG, "null argument");
+    NO_CAPTURE(c);
     unsigned long long v[4];
     CUDA_TRY(cudaMemcpyAsync(v, c->d_clk, sizeof v, cudaMemcpyDeviceToHost, c->stream), "D2H clock probe");
     CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
@@ -1067,6 +1097,7 @@ cpa_status cpa_finalize_rows(cpa_ctx *c, int32_t h0, int32_t h1, double *d_rho, 
                              int32_t *d_argmax, double *d_peak)
 {
     if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    NO_CAPTURE(c);
     if (h0 < 0 || h1 > 4096 || h0 > h1) return fail(CPA_E_INVALID_ARG, "rows [%d, %d) outside [0, 4096]", h0, h1);
     if (!d_maxabs || !d_argmax || !d_peak) return fail(CPA_E_INVALID_ARG, "d_maxabs, d_argmax and d_peak are required");
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
@@ -1085,6 +1116,7 @@ cpa_status cpa_select(cpa_ctx *c, int32_t G, double *d_maxabs, int32_t *d_argmax
                       cpa_result *res)
 {
     if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    NO_CAPTURE(c);
     if (G < 1 || G > 65536) return fail(CPA_E_INVALID_ARG, "G=%d outside [1, 65536]", G);
     if (!d_maxabs || !d_argmax || !d_peak) return fail(CPA_E_INVALID_ARG, "d_maxabs, d_argmax and d_peak are required");
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
@@ -1105,6 +1137,7 @@ cpa_status cpa_select(cpa_ctx *c, int32_t G, double *d_maxabs, int32_t *d_argmax
 cpa_status cpa_phase_times(cpa_ctx *c, double ms[CPA_NUM_PHASES], int64_t launches[CPA_NUM_PHASES])
 {
     if (!c || !ms) return fail(CPA_E_INVALID_ARG, "null argument");
+    NO_CAPTURE(c);
     CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
     for (int p = 0; p < CPA_NUM_PHASES; p++) {
         ms[p] = 0.0;
@@ -1125,7 +1158,57 @@ cpa_status cpa_phase_times(cpa_ctx *c, double ms[CPA_NUM_PHASES], int64_t launch
 cpa_status cpa_sync(cpa_ctx *c)
 {
     if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    NO_CAPTURE(c);
     CUDA_TRY(cudaStreamSynchronize(c->stream), "sync");
+    return CPA_OK;
+}
+
+// CUDA-graph capture of the context's stream: the calls made between
+// cpa_graph_begin and cpa_graph_end (cpa_reset, cpa_accumulate on aligned device
+// buffers, cpa_finalize_async) are recorded instead of run, and cpa_graph_launch
+// replays them as one graph launch -- no per-kernel host launch cost, no host
+// work between the steps of a repeated attack of a fixed shape.
+cpa_status cpa_graph_begin(cpa_ctx *c)
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    if (c->capturing) return fail(CPA_E_INVALID_ARG, "already capturing");
+    if (c->stream == nullptr)
+        return fail(CPA_E_INVALID_ARG, "graph capture needs a context stream other than the legacy default stream");
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    c->capturing = true;
+    c->captured_reset = false;
+    return CPA_OK;
+}
+
+cpa_status cpa_graph_end(cpa_ctx *c)
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    if (!c->capturing) return fail(CPA_E_INVALID_ARG, "not capturing");
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    c->capturing = false;
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    if (c->graph_exec) {
+        cudaGraphExecDestroy(c->graph_exec);
+        c->graph_exec = nullptr;
+    }
+    e = cudaGraphInstantiate(&c->graph_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        c->graph_exec = nullptr;
+        return cuda_fail(e, "cudaGraphInstantiate");
+    }
+    return CPA_OK;
+}
+
+cpa_status cpa_graph_launch(cpa_ctx *c)
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    if (c->capturing || !c->graph_exec) return fail(CPA_E_INVALID_ARG, "no captured graph");
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    CUDA_TRY(cudaGraphLaunch(c->graph_exec, c->stream), "cudaGraphLaunch");
     return CPA_OK;
 }
 
@@ -1133,6 +1216,12 @@ cpa_status cpa_destroy(cpa_ctx *c)
 {
     if (!c) return fail(CPA_E_INVALID_ARG, "null context");
     cudaSetDevice(c->device);
+    if (c->capturing) {  // abandon an unfinished capture
+        cudaGraph_t g = nullptr;
+        if (cudaStreamEndCapture(c->stream, &g) == cudaSuccess && g) cudaGraphDestroy(g);
+        cudaGetLastError();
+    }
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     cudaFree(c->d_vtab);

@@ -183,6 +183,19 @@ class Engine:
         int32 (and the optional maxabs/argmax/best[32]/rho) fill in stream order."""
         B.cpa_finalize_async(self.ctx, rho, maxabs, argmax, rank, best)
 
+    # ---- CUDA-graph replay of a fixed-shape step (include/cpa.h cpa_graph_*) ----
+    def graph_begin(self):
+        """Start capturing this context's stream (needs a non-default stream):
+        reset / accumulate / finalize_async are recorded until graph_end."""
+        B.cpa_graph_begin(self.ctx)
+
+    def graph_end(self):
+        B.cpa_graph_end(self.ctx)
+
+    def graph_launch(self):
+        """Replay the captured calls as one graph launch (asynchronous)."""
+        B.cpa_graph_launch(self.ctx)
+
     def maxima_buffers(self, G: int = 1):
         """Zeroed per-hypothesis maxima (maxabs, argmax, peak) for G stacked shards."""
         dev = self.device
