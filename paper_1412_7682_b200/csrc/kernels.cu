@@ -803,7 +803,10 @@ cudaError_t launch_phase4(const FinalizeOut &o, cudaStream_t s, int *launches)
 namespace cpa {
 namespace {
 constexpr int SP_THREADS = 256;
-constexpr int SP_ROWS = 512;
+#ifndef SP_ROWS_N
+#define SP_ROWS_N 128  // C3: 3920 blocks, 6.6 waves (512: 1.66 waves, the second one two-thirds empty)
+#endif
+constexpr int SP_ROWS = SP_ROWS_N;  // rows per block of the split pre-pass
 #ifndef SP_U_ROWS
 #define SP_U_ROWS 4
 #endif
