@@ -83,6 +83,9 @@ def parse():
     ap.add_argument("--spill", type=int, default=0, choices=[0, 1, 2, 3],
                     help="CPA_OPT_SPILL: cross-term spill, 0 = auto (default), 1 = red.add per "
                          "element, 2 = bulk tensor reduce-add, 3 = per-chunk partial stores + one reduce pass")
+    ap.add_argument("--narrow", choices=["auto", "0", "1"], default="auto",
+                    help="CPA_OPT_NARROW: int8 cross-term sums in an int32 shadow while exact (half the "
+                         "sum_hw bytes); auto = on for one rank / sample shards (no accumulator combine)")
     ap.add_argument("--chunk", type=int, default=0,
                     help="stream the traces in chunks of this many, finalizing after every round "
                          "(key-rank curve); default for C5: 65536")
@@ -454,6 +457,11 @@ def main():
         eng.set_kchunk(args.kchunk)
     eng.set_spill(args.spill)
     eng.set_col0(j0)
+    combine0 = ("columns" if shard == "samples" else args.combine) if world > 1 else "none"
+    narrow = not is_f32 and not class_sums and (args.narrow == "1" or (args.narrow == "auto" and
+                                                                     combine0 in ("none", "columns")))
+    if narrow:
+        eng.set_narrow(True)
     ovl_mode = 0 if args.no_overlap else (args.overlap_mode if args.overlap_mode is not None else OVERLAP_DEFAULT)
     eng.set_overlap(ovl_mode)
     if is_f32 and world > 1:
@@ -506,6 +514,8 @@ def main():
             eng.accumulate(dWv, dT)
         else:
             eng.accumulate_host(*host)
+        if narrow and combine in ("fused", "rows"):
+            eng.flush()         # the int32 shadow into the accumulator the combine reads
         if combine == "fused":  # rows already with their owners; small fields + ordering point
             MG.allreduce_small_fields(eng.accum, w.m)
             P.cpa_finalize_rows(eng.ctx, h0, h1, rho, maxabs, argmax, peak)
@@ -688,7 +698,8 @@ def main():
                                "measured in two extra serialised steps)") if fused else
                               ("k_split_f32 pre-pass (centring, fp16 hi + e4m3 lo planes, fp64 sums)" if is_f32
                                else "separate k_moments_i8 pass"),
-           "finalize_GBps": ((h1 - h0) * m_local * 16) / (step_phase_ms["finalize"] * 1e-3) / 1e9 if step_phase_ms["finalize"] else None,
+           # bytes per cell: the sum_hw read (4 B narrow / 8 B) + the rho write (8 B)
+           "finalize_GBps": ((h1 - h0) * m_local * (12 if narrow else 16)) / (step_phase_ms["finalize"] * 1e-3) / 1e9 if step_phase_ms["finalize"] else None,
            "hbm_peak_GBps": peaks["hbm_gbs"]}
 
     # ---- end to end through the public API: host (pinned) buffers -> key on host
@@ -747,7 +758,8 @@ def main():
                                        + (f" [{fused_note}]" if fused_note else "")),
                        "l2": f"inputs {n_local * m_local * dW.element_size() / 1e9:.2f} GB per rank > 126 MB L2, "
                              "no flush needed",
-                       "rho_written": True},
+                       "rho_written": True,
+                       "sum_hw": "int32 shadow (CPA_OPT_NARROW, exact)" if narrow else ("fp64" if is_f32 else "int64")},
             "key_recovered": key_ok, "gpu_launches": launches,
             "phases_ms_per_step": step_phase_ms,
             "phase_share": {k: v / tot for k, v in step_phase_ms.items()},
@@ -806,7 +818,8 @@ def run_stream(args, w, dev, world, rank, local):
     # default (auto): reduce-scatter checkpoints (NCCL); the fused combine is
     # timed after the headline in the same run (combine_ms_per_step)
     fused = world > 1 and args.combine == "fused" and 16 % world == 0
-    st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, local, fused=fused)
+    narrow = args.narrow == "1" or (args.narrow == "auto" and world == 1)
+    st = StreamingAttack(w.m, P.CPA_S8, P.CPA_HD_LAST, local, fused=fused, narrow=narrow)
     if fused and st.owners is None:   # peers not mappable: NCCL reduce-scatter checkpoints
         print(f"fused combine unavailable ({st.fused_note}); reduce-scatter checkpoints", file=sys.stderr)
         fused = False
@@ -915,7 +928,8 @@ def run_stream(args, w, dev, world, rank, local):
                        "n_traces": w.n, "n_samples": w.m, "chunk": chunk, "checkpoints": len(rounds),
                        "parallelism": f"trace-chunk round-robin x{world}"
                                       + (", fused row combine" if fused else (", reduce-scatter checkpoints" if world > 1 else "")),
-                       "l2": f"inputs {w.n * w.m / 1e9:.0f} GB > 126 MB L2, no flush needed"},
+                       "l2": f"inputs {w.n * w.m / 1e9:.0f} GB > 126 MB L2, no flush needed",
+                       "sum_hw": "int32 shadow (CPA_OPT_NARROW, exact)" if narrow else "int64"},
             "key_recovered": bytes(out["master_key"]) == w.key,
             "traces_to_key": curve.traces_to_key(),
             "rank_curve": {"columns": ["traces", "worst_rank", "bytes_at_rank_1"], "points": curve.summary()},

@@ -170,9 +170,12 @@ CPA_API cpa_status cpa_finalize_async(cpa_ctx *ctx, double *d_rho, double *d_max
  * already exist -- run the step once outside the capture first.  Calls that
  * synchronise, read back or allocate (cpa_finalize, cpa_finalize_rows,
  * cpa_select, cpa_accumulate_host, cpa_sync, cpa_phase_times, the offset calls)
- * return CPA_E_INVALID_ARG while capturing.  Replays update no host-side state
- * (the running-total N check, launch count, phase times: CPA_OPT_TIMING events
- * are not captured); the pointers and sizes are those of the capture.
+ * return CPA_E_INVALID_ARG while capturing.  The host's record of the sums
+ * (traces since reset, first-touch and CPA_OPT_NARROW shadow state) is left as
+ * before the capture by cpa_graph_end and set to the graph's end state by each
+ * replay of a graph that begins with cpa_reset; replays update nothing else on
+ * the host (launch count, phase times: CPA_OPT_TIMING events are not
+ * captured); the pointers and sizes are those of the capture.
  * cpa_graph_end replaces a previous graph; cpa_destroy frees it.            */
 CPA_API cpa_status cpa_graph_begin(cpa_ctx *ctx);
 CPA_API cpa_status cpa_graph_end(cpa_ctx *ctx);
@@ -340,10 +343,31 @@ CPA_API cpa_status cpa_destroy(cpa_ctx *ctx);  /* frees the context (not d_accum
  *                   slices into sum_hw (no row owners).  0 (default): int8 =
  *                   2 for work units of >= 65536 traces, else 1; float = 1
  *                   (measured).  Exact (int8) / within the float
- *                   tolerance (float) either way.                             */
+ *                   tolerance (float) either way.
+ *   CPA_OPT_NARROW: int8 traces. 1 = keep the cross-term field sum_hw in a
+ *                   context-owned int32 shadow (4096 x M x 4 bytes, allocated
+ *                   by this call; not capturable) while it is exact: while the
+ *                   traces in it satisfy N * 8 * max|W| < 2^31 (max|W| = 128
+ *                   s8 / 255 u8: N <= 2097151 / 1052688; max|H| = 8 for every
+ *                   model).  The cross term then stores / adds 32-bit words
+ *                   and cpa_finalize* read the shadow: half the sum_hw bytes in
+ *                   both.  The ACCUMULATOR's HW field is stale while the shadow
+ *                   is live: cpa_flush adds the shadow into it (call it before
+ *                   reading, combining or exporting the accumulator); an
+ *                   accumulate that would pass the bound, or uses class sums,
+ *                   row owners or CPA_OPT_SPILL 2 / 3, flushes first and goes on
+ *                   in int64; cpa_reset drops the shadow.  A value > 1 also
+ *                   caps the shadow at that many traces (tests).  0 (default):
+ *                   off (flushes a live shadow).  Ignored for float traces.
+ *                   Results are bit-identical either way.                     */
 enum { CPA_OPT_KCHUNK = 1, CPA_OPT_TIMING = 2, CPA_OPT_OVERLAP = 3, CPA_OPT_STAGE_BYTES = 4,
        CPA_OPT_COL0 = 5, CPA_OPT_CLASS_SUMS = 6, CPA_OPT_FUSE_HIST = 7, CPA_OPT_XT_TILES = 8,
-       CPA_OPT_SPILL = 9 };
+       CPA_OPT_SPILL = 9, CPA_OPT_NARROW = 10 };
+
+/* CPA_OPT_NARROW: add a live int32 shadow of sum_hw into the accumulator's HW
+ * field (one kernel on the context's stream, asynchronous; capturable) so the
+ * accumulator holds every sum.  No-op without a live shadow.                 */
+CPA_API cpa_status cpa_flush(cpa_ctx *ctx);
 CPA_API cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value);
 
 /* Per-phase device time (ms) and launch count since the last call, from the

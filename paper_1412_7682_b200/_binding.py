@@ -18,7 +18,7 @@ CPA_E_TOO_FEW_TRACES, CPA_E_OVERFLOW, CPA_E_UNSUPPORTED_DEVICE, CPA_E_NONFINITE 
 CPA_S8, CPA_U8, CPA_F32 = 0, 1, 2
 CPA_HD_LAST, CPA_HW_LAST, CPA_HW_FIRST = 0, 1, 2
 (CPA_OPT_KCHUNK, CPA_OPT_TIMING, CPA_OPT_OVERLAP, CPA_OPT_STAGE_BYTES, CPA_OPT_COL0, CPA_OPT_CLASS_SUMS,
- CPA_OPT_FUSE_HIST, CPA_OPT_XT_TILES, CPA_OPT_SPILL) = 1, 2, 3, 4, 5, 6, 7, 8, 9
+ CPA_OPT_FUSE_HIST, CPA_OPT_XT_TILES, CPA_OPT_SPILL, CPA_OPT_NARROW) = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
 CPA_NUM_PHASES = 6
 PHASE_NAMES = ("modelsums", "moments", "xterm", "finalize", "phase4", "spill_reduce")
 FIELD_HW, FIELD_W, FIELD_W2, FIELD_H, FIELD_H2, FIELD_N = range(6)
@@ -27,7 +27,7 @@ FIELD_HW, FIELD_W, FIELD_W2, FIELD_H, FIELD_H2, FIELD_N = range(6)
 ABI_SYMBOLS = (
     "cpa_accum_words", "cpa_accum_bytes", "cpa_accum_offset", "cpa_init", "cpa_accumulate",
     "cpa_accumulate_host", "cpa_finalize", "cpa_finalize_async", "cpa_finalize_rows", "cpa_select",
-    "cpa_set_row_owners", "cpa_ipc_export", "cpa_ipc_open", "cpa_ipc_close", "cpa_xterm_clock", "cpa_peer_atomics", "cpa_reset", "cpa_sync", "cpa_destroy",
+    "cpa_set_row_owners", "cpa_ipc_export", "cpa_ipc_open", "cpa_ipc_close", "cpa_xterm_clock", "cpa_peer_atomics", "cpa_reset", "cpa_sync", "cpa_flush", "cpa_destroy",
     "cpa_get_offsets", "cpa_default_offsets",
     "cpa_set_offsets", "cpa_set_option", "cpa_phase_times", "cpa_launch_count", "cpa_status_str", "cpa_last_error",
     "cpa_aes_expand_key", "cpa_aes_invert_key_schedule", "cpa_graph_begin", "cpa_graph_end", "cpa_graph_launch",
@@ -75,6 +75,7 @@ def _load():
         "cpa_peer_atomics": (ST, [C.c_int, C.c_int, C.POINTER(C.c_int)]),
         "cpa_reset": (ST, [P]),
         "cpa_sync": (ST, [P]),
+        "cpa_flush": (ST, [P]),
         "cpa_destroy": (ST, [P]),
         "cpa_set_offsets": (ST, [P, P]),
         "cpa_get_offsets": (ST, [P, P, C.POINTER(C.c_int)]),
@@ -210,6 +211,10 @@ def cpa_reset(ctx):
 
 def cpa_sync(ctx):
     _check(_lib.cpa_sync(ctx), "cpa_sync")
+
+
+def cpa_flush(ctx):
+    _check(_lib.cpa_flush(ctx), "cpa_flush")
 
 
 def cpa_graph_begin(ctx):

@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -163,6 +164,41 @@ struct cpa_ctx {
     bool capturing = false;
     bool captured_reset = false;  // a cpa_reset was captured before any accumulate
     cudaGraphExec_t graph_exec = nullptr;
+    // host bookkeeping of the sums (what the next calls assume about them): a
+    // capture changes it without running anything, so cpa_graph_end restores the
+    // state from before the capture and keeps the captured end state, which each
+    // replay of a graph that begins with a reset then installs
+    struct SumState {
+        int64_t n_since_reset;
+        bool hw_zero, hw32_live;
+        int64_t hw32_n;
+    };
+    SumState sum_state() const { return SumState{n_since_reset, hw_zero, hw32_live, hw32_n}; }
+    void set_sum_state(const SumState &x) {
+        n_since_reset = x.n_since_reset;
+        hw_zero = x.hw_zero;
+        hw32_live = x.hw32_live;
+        hw32_n = x.hw32_n;
+    }
+    SumState pre_capture{}, graph_end_state{};
+    bool graph_sets_state = false;
+    // CPA_OPT_NARROW: the HW field kept in an int32 shadow [4096][M] while it is
+    // exact (hw32_n traces in it, N max|H| max|W| < 2^31); hw32_live: the shadow
+    // holds HW contributions not yet in the accumulator (flush() adds them)
+    int64_t narrow = 0;
+    int32_t *d_hw32 = nullptr;
+    bool hw32_live = false;
+    int64_t hw32_n = 0;
+    cudaError_t flush() {
+        if (!hw32_live) return cudaSuccess;
+        int l = 0;
+        cudaError_t e = cpa::launch_widen_hw(d_hw32, (int64_t *)accum, 4096LL * M, num_sms, stream, &l);
+        launches += l;
+        hw32_live = false;
+        hw32_n = 0;
+        hw_zero = false;
+        return e;
+    }
     uint32_t *d_part = nullptr;  // partial-sum spill slices [kc][4096][ld] (32-bit), grown on demand
     int64_t part_bytes = 0;
     // the partial buffer for kc_count slices of part_ld samples (null: over the
@@ -269,6 +305,8 @@ cpa_status cpa_reset(cpa_ctx *ctx)
     CUDA_TRY(cudaMemsetAsync(ctx->d_nonfinite, 0, sizeof(int), ctx->stream), "reset flag");
     ctx->n_since_reset = 0;
     ctx->hw_zero = true;
+    ctx->hw32_live = false;  // the shadow's contents are dropped with the sums
+    ctx->hw32_n = 0;
     if (ctx->capturing) ctx->captured_reset = true;
     return CPA_OK;
 }
@@ -423,6 +461,22 @@ cpa_status cpa_set_option(cpa_ctx *ctx, int option, int64_t value)
     if (option == CPA_OPT_XT_TILES) {
         if (value < 0 || value > 2) return fail(CPA_E_INVALID_ARG, "XT_TILES=%lld outside [0, 2]", (long long)value);
         ctx->xt_tiles = (int)value;
+        return CPA_OK;
+    }
+    if (option == CPA_OPT_NARROW) {
+        if (value < 0) return fail(CPA_E_INVALID_ARG, "NARROW=%lld < 0", (long long)value);
+        if (ctx->dtype == CPA_F32) {  // fp64 sums: nothing to narrow
+            ctx->narrow = 0;
+            return CPA_OK;
+        }
+        NO_CAPTURE(ctx);
+        CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (value == 0) {
+            CUDA_TRY(ctx->flush(), "flush narrow sums");
+        } else if (ctx->d_hw32 == nullptr) {
+            CUDA_TRY(cudaMalloc(&ctx->d_hw32, 4096LL * ctx->M * sizeof(int32_t)), "cudaMalloc narrow sums");
+        }
+        ctx->narrow = value;
         return CPA_OK;
     }
     if (option == CPA_OPT_SPILL) {
@@ -646,6 +700,14 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     }
     int64_t *acc = (int64_t *)c->accum;
     const bool sgn = c->dtype == CPA_S8;
+    // CPA_OPT_NARROW: int32 cross-term sums while exact -- N max|H| max|W| < 2^31
+    // with max|H| = 8 (every model's V is a Hamming weight / distance of a byte)
+    // and max|W| = 128 (s8) / 255 (u8); NARROW > 1 lowers the trace bound (tests)
+    const int64_t n32_max = std::min<int64_t>(((1LL << 31) - 1) / (8 * (sgn ? 128 : 255)),
+                                              c->narrow > 1 ? c->narrow : INT64_MAX);
+    const bool use32 = c->narrow && c->d_hw32 && !c->class_sums && !c->owners_set && c->spill <= 1 &&
+                       (c->hw32_live ? c->hw32_n : 0) + n <= n32_max;
+    if (c->hw32_live && !use32) CUDA_TRY(c->flush(), "flush narrow sums");
     if (!fhist)
         CUDA_TRY(c->timed(0, [&] {
                      return cpa::launch_modelsums(d_tx, n, c->d_vtab, c->d_hist, acc + cpa_accum_offset(M, 3),
@@ -708,7 +770,7 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     // sum_hw either way, not by the issuing SM
     const int64_t kc = c->kchunk ? c->kchunk : plan.kc_len;
     CUtensorMap tmap_hw;
-    bool bulk = (M % 2 == 0) && !c->owners_set &&
+    bool bulk = !use32 && (M % 2 == 0) && !c->owners_set &&
                 (c->spill == 2 || (c->spill == 0 && kc >= kBulkSpillMinUnit));
     if (bulk) {
         cuuint64_t hdims[2] = {(cuuint64_t)M, 4096};
@@ -724,14 +786,22 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
     const int64_t kcount = (n + kc - 1) / kc;
     uint32_t *part = (!c->owners_set && c->spill == 3) ? c->part_buffer(kcount, part_ld) : nullptr;
     if (part != nullptr) bulk = false;
+    // narrow sums: a fresh shadow is first-touch stored by a one-chunk launch,
+    // else zeroed first; a live one is added to
+    bool first32 = false;
+    if (use32 && !c->hw32_live) {
+        if (kcount == 1) first32 = true;
+        else CUDA_TRY(cudaMemsetAsync(c->d_hw32, 0, 4096LL * M * sizeof(int32_t), c->stream), "zero narrow sums");
+    }
     CUDA_TRY(c->timed(2, [&] {
                  cudaError_t e = cpa::launch_xterm_i8(tmap, bulk ? &tmap_hw : nullptr, d_tx, c->d_vtab, acc,
                                                       c->d_counter, M, n, kc, sgn, c->num_sms, c->stream, &launches,
                                                       fused ? acc + cpa_accum_offset(M, 1) : nullptr,
                                                       fused ? acc + cpa_accum_offset(M, 2) : nullptr,
                                                       fhist ? c->d_hist : nullptr, c->owners_set ? c->owners : nullptr,
-                                                      c->d_clk, plan.overlapped, part ? false : c->hw_zero, part,
-                                                      part_ld);
+                                                      c->d_clk, plan.overlapped,
+                                                      use32 ? first32 : (part ? false : c->hw_zero), part, part_ld,
+                                                      use32 ? c->d_hw32 : nullptr);
                  return e;
              }),
              "xterm_i8");
@@ -740,7 +810,12 @@ static cpa_status accumulate_device(cpa_ctx *c, const void *d_w, int64_t ld, con
                      return cpa::launch_part_reduce_i32(part, (int32_t)kcount, part_ld, M, acc, c->stream, &launches);
                  }),
                  "spill reduce");
-    c->hw_zero = false;
+    if (use32) {
+        c->hw32_live = true;
+        c->hw32_n += n;
+    } else {
+        c->hw_zero = false;
+    }
     if (!fused && mode == 1) CUDA_TRY(moments(), "moments");
     if (fhist)
         CUDA_TRY(c->timed(0, [&] {
@@ -932,7 +1007,7 @@ static cpa_status phase3(cpa_ctx *c, const cpa::FinalizeOut &o, int *launches)
                             ? cpa::launch_finalize_f64((const double *)c->accum, c->M, c->d_offset, c->d_sqrt_dw, o,
                                                        c->stream, launches)
                             : cpa::launch_finalize_i8((const int64_t *)c->accum, c->M, c->d_sqrt_dw, o, c->stream,
-                                                      launches);
+                                                      launches, c->hw32_live ? c->d_hw32 : nullptr);
              }),
              "finalize");
     return CPA_OK;
@@ -1155,6 +1230,14 @@ cpa_status cpa_phase_times(cpa_ctx *c, double ms[CPA_NUM_PHASES], int64_t launch
     return CPA_OK;
 }
 
+cpa_status cpa_flush(cpa_ctx *c)
+{
+    if (!c) return fail(CPA_E_INVALID_ARG, "null context");
+    CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    CUDA_TRY(c->flush(), "flush narrow sums");
+    return CPA_OK;
+}
+
 cpa_status cpa_sync(cpa_ctx *c)
 {
     if (!c) return fail(CPA_E_INVALID_ARG, "null context");
@@ -1178,6 +1261,7 @@ cpa_status cpa_graph_begin(cpa_ctx *c)
     CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
     c->capturing = true;
     c->captured_reset = false;
+    c->pre_capture = c->sum_state();
     return CPA_OK;
 }
 
@@ -1189,6 +1273,9 @@ cpa_status cpa_graph_end(cpa_ctx *c)
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(c->stream, &g);
     c->capturing = false;
+    c->graph_end_state = c->sum_state();
+    c->graph_sets_state = c->captured_reset;
+    c->set_sum_state(c->pre_capture);  // nothing has run yet
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
     if (c->graph_exec) {
         cudaGraphExecDestroy(c->graph_exec);
@@ -1209,6 +1296,7 @@ cpa_status cpa_graph_launch(cpa_ctx *c)
     if (c->capturing || !c->graph_exec) return fail(CPA_E_INVALID_ARG, "no captured graph");
     CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
     CUDA_TRY(cudaGraphLaunch(c->graph_exec, c->stream), "cudaGraphLaunch");
+    if (c->graph_sets_state) c->set_sum_state(c->graph_end_state);
     return CPA_OK;
 }
 
@@ -1254,6 +1342,7 @@ cpa_status cpa_destroy(cpa_ctx *c)
     cudaFree(c->d_offset);
     cudaFree(c->d_scale);
     cudaFree(c->d_part);
+    cudaFree(c->d_hw32);
     cudaFree(c->d_hi);
     cudaFree(c->d_lo);
     cudaFree(c->d_nonfinite);

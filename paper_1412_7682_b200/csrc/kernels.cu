@@ -273,6 +273,21 @@ __device__ __forceinline__ double fin_den_h(double n, double s_h, double s_h2)
 }
 template <typename T> struct Pair2;
 template <> struct Pair2<int64_t> { using type = longlong2; };
+template <> struct Pair2<int32_t> { using type = int2; };
+// VV consecutive sum_hw elements loaded with ONE evict-first vector load (8 or 16 bytes)
+template <int BYTES> struct LdT;
+template <> struct LdT<8> { using type = int2; };
+template <> struct LdT<16> { using type = int4; };
+template <typename TH, int VV> struct alignas(VV * sizeof(TH)) RowV { TH e[VV]; };
+template <typename TH, int VV>
+__device__ __forceinline__ RowV<TH, VV> ldcs_row(const TH *p)
+{
+    using L = typename LdT<VV * sizeof(TH)>::type;
+    const L q = __ldcs((const L *)p);
+    RowV<TH, VV> r;
+    memcpy(&r, &q, sizeof(q));
+    return r;
+}
 template <> struct Pair2<double> { using type = double2; };
 
 // Without rho output (streamed checkpoints, sharded maxima) only max|rho| and
@@ -287,9 +302,13 @@ template <> struct Pair2<double> { using type = double2; };
 // so max|rho|, argmax and the signed peak are bit-identical to the full kernel.
 constexpr double kFinSkip = 1.0 - 3.552713678800501e-15;  // 1 - 2^-48
 
-template <int U, typename T>
-__global__ void __launch_bounds__(FIN_THREADS)
-k_finalize_maxima(const T *__restrict__ hw, const T *__restrict__ sw, const T *__restrict__ sh,
+// TH: element type of the sum_hw rows (T, or int32 for narrow sums, widened on load)
+#ifndef FIN_MAXIMA_MINB
+#define FIN_MAXIMA_MINB 4  // 64 registers: 4 resident blocks (C5 finalize 4.5 vs 5.8 ms with 1)
+#endif
+template <int U, typename T, typename TH = T>
+__global__ void __launch_bounds__(FIN_THREADS, FIN_MAXIMA_MINB)
+k_finalize_maxima(const TH *__restrict__ hw, const T *__restrict__ sw, const T *__restrict__ sh,
                   const T *__restrict__ sh2, const T *__restrict__ count, const double *__restrict__ sqrt_dw,
                   int32_t M, FinalizeOut o)
 {
@@ -297,7 +316,7 @@ k_finalize_maxima(const T *__restrict__ hw, const T *__restrict__ sw, const T *_
     const T n = *count;
     const T s_h = sh[h];
     const double den_h = fin_den_h(n, s_h, sh2[h]);
-    const T *row = hw + (int64_t)h * M;
+    const TH *row = hw + (int64_t)h * M;
     const double *rcp_w = sqrt_dw + M;
     // Skip threshold shared by the block (= the row): the largest a_best (1 - 2^-48)
     // any thread has seen.  A cell below it is strictly below THAT thread's best
@@ -336,38 +355,46 @@ k_finalize_maxima(const T *__restrict__ hw, const T *__restrict__ sw, const T *_
         if (t > thr) thr = t;
     };
     int j = 0;
-    if ((M & 1) == 0) {
+    // VV samples per row load: 16 bytes (2 int64 / fp64, 4 int32), else 8 bytes
+    // (int32 rows with M % 4 == 2); the ragged last group is predicated, not a
+    // loop of single samples: each of its iterations would wait out a full load
+    // latency (per block: ~6 us at any M, 25% of the kernel at M = 20000)
+    auto vec_path = [&](auto vc) {
+        constexpr int VV = decltype(vc)::value;
         using T2 = typename Pair2<T>::type;
-        const int M2 = M >> 1;
-        int p0 = threadIdx.x;
-        // the ragged last group is predicated, not a loop of single pairs: each of
-        // its iterations would wait out a full load latency (per block: ~6 us at
-        // any M, 25% of the kernel at M = 20000)
-        for (; p0 < M2; p0 += U * FIN_THREADS) {
-            T2 v[U];
+        const int MV = M / VV;
+        for (int p0 = threadIdx.x; p0 < MV; p0 += U * FIN_THREADS) {
+            RowV<TH, VV> v[U];
 #pragma unroll
             for (int u = 0; u < U; u++)
-                if (p0 + u * FIN_THREADS < M2) v[u] = __ldcs((const T2 *)row + p0 + u * FIN_THREADS);
+                if (p0 + u * FIN_THREADS < MV) v[u] = ldcs_row<TH, VV>(row + (int64_t)(p0 + u * FIN_THREADS) * VV);
             refresh();
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const int p = p0 + u * FIN_THREADS;
-                if (p >= M2) break;
-                const double2 rw = ((const double2 *)rcp_w)[p];
-                const T2 swp = ((const T2 *)sw)[p];
-                visit(v[u].x, 2 * p, rw.x, swp.x);
-                visit(v[u].y, 2 * p + 1, rw.y, swp.y);
+                if (p >= MV) break;
+#pragma unroll
+                for (int e = 0; e < VV; e += 2) {
+                    const int jj = VV * p + e;
+                    const double2 rw = *(const double2 *)(rcp_w + jj);
+                    const T2 swp = *(const T2 *)(sw + jj);
+                    visit((T)v[u].e[e], jj, rw.x, swp.x);
+                    visit((T)v[u].e[e + 1], jj + 1, rw.y, swp.y);
+                }
             }
         }
         j = M;
-    }
-    for (j += threadIdx.x; j < M; j += FIN_THREADS) visit(row[j], j, rcp_w[j], sw[j]);
+    };
+    constexpr int V16 = 16 / (int)sizeof(TH);
+    if (M % V16 == 0) vec_path(std::integral_constant<int, V16>{});
+    else if (V16 > 2 && (M & 1) == 0) vec_path(std::integral_constant<int, 2>{});
+    for (j += threadIdx.x; j < M; j += FIN_THREADS) visit((T)row[j], j, rcp_w[j], sw[j]);
     block_best_store(best, h, o);
 }
 
-template <int R, int U, typename T>
+template <int R, int U, typename T, typename TH = T>
 __global__ void __launch_bounds__(FIN_THREADS)
-k_finalize_rows(const T *__restrict__ hw, const T *__restrict__ sw, const T *__restrict__ sh,
+k_finalize_rows(const TH *__restrict__ hw, const T *__restrict__ sw, const T *__restrict__ sh,
                 const T *__restrict__ sh2, const T *__restrict__ count, const double *__restrict__ sqrt_dw, int32_t M,
                 FinalizeOut o)
 {
@@ -385,49 +412,59 @@ k_finalize_rows(const T *__restrict__ hw, const T *__restrict__ sw, const T *__r
         den_h[r] = fin_den_h(n, s_h[r], sh2[h]);
         best[r] = Best{-1.0, 0.0, 0x7fffffff};
     }
-    const T *row0 = hw + (int64_t)hb * M;
+    const TH *row0 = hw + (int64_t)hb * M;
     double *rrow0 = o.rho ? o.rho + (int64_t)(hb - o.h0) * M : nullptr;
     auto keep = [&](int r, double x, int j) {
         const double a = fabs(x);
         if (a > best[r].v) best[r] = Best{a, x, j};  // j ascending per thread: lowest-j ties
     };
     int j = 0;
-    if ((M & 1) == 0 && ((uintptr_t)o.rho & 15) == 0) {  // 16-byte aligned rows (M even)
-        const int M2 = M >> 1;
-        int p0 = threadIdx.x;
-        for (; p0 < M2; p0 += U * FIN_THREADS) {  // ragged last group predicated (see k_finalize_maxima)
-            T2 v[U][R];
+    // VV samples per row load, as in k_finalize_maxima; rho rows 16-byte aligned
+    auto vec_path = [&](auto vc) {
+        constexpr int VV = decltype(vc)::value;
+        const int MV = M / VV;
+        for (int p0 = threadIdx.x; p0 < MV; p0 += U * FIN_THREADS) {  // ragged last group predicated
+            RowV<TH, VV> v[U][R];
 #pragma unroll
             for (int u = 0; u < U; u++)
 #pragma unroll
                 for (int r = 0; r < R; r++)
-                    if (r < nr && p0 + u * FIN_THREADS < M2)
-                        v[u][r] = __ldcs((const T2 *)(row0 + (int64_t)r * M) + p0 + u * FIN_THREADS);
+                    if (r < nr && p0 + u * FIN_THREADS < MV)
+                        v[u][r] = ldcs_row<TH, VV>(row0 + (int64_t)r * M + (int64_t)(p0 + u * FIN_THREADS) * VV);
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const int p = p0 + u * FIN_THREADS;
-                if (p >= M2) break;
-                const double2 dw = ((const double2 *)sqrt_dw)[p];
-                const T2 swp = ((const T2 *)sw)[p];
+                if (p >= MV) break;
 #pragma unroll
-                for (int r = 0; r < R; r++) {
-                    if (r >= nr) break;
-                    double2 x;
-                    x.x = fin_cell(v[u][r].x, n, s_h[r], swp.x, dw.x, den_h[r]);
-                    x.y = fin_cell(v[u][r].y, n, s_h[r], swp.y, dw.y, den_h[r]);
-                    keep(r, x.x, 2 * p);
-                    keep(r, x.y, 2 * p + 1);
-                    if (rrow0) __stcs((double2 *)(rrow0 + (int64_t)r * M) + p, x);
+                for (int e = 0; e < VV; e += 2) {
+                    const int jj = VV * p + e;
+                    const double2 dw = *(const double2 *)(sqrt_dw + jj);
+                    const T2 swp = *(const T2 *)(sw + jj);
+#pragma unroll
+                    for (int r = 0; r < R; r++) {
+                        if (r >= nr) break;
+                        double2 x;
+                        x.x = fin_cell((T)v[u][r].e[e], n, s_h[r], swp.x, dw.x, den_h[r]);
+                        x.y = fin_cell((T)v[u][r].e[e + 1], n, s_h[r], swp.y, dw.y, den_h[r]);
+                        keep(r, x.x, jj);
+                        keep(r, x.y, jj + 1);
+                        if (rrow0) __stcs((double2 *)(rrow0 + (int64_t)r * M + jj), x);
+                    }
                 }
             }
         }
         j = M;
+    };
+    if (((uintptr_t)o.rho & 15) == 0) {
+        constexpr int V16 = 16 / (int)sizeof(TH);
+        if (M % V16 == 0) vec_path(std::integral_constant<int, V16>{});
+        else if (V16 > 2 && (M & 1) == 0) vec_path(std::integral_constant<int, 2>{});
     }
     for (j += threadIdx.x; j < M; j += FIN_THREADS) {
 #pragma unroll
         for (int r = 0; r < R; r++) {
             if (r >= nr) break;
-            const double x = fin_cell(row0[(int64_t)r * M + j], n, s_h[r], sw[j], sqrt_dw[j], den_h[r]);
+            const double x = fin_cell((T)row0[(int64_t)r * M + j], n, s_h[r], sw[j], sqrt_dw[j], den_h[r]);
             keep(r, x, j);
             if (rrow0) rrow0[(int64_t)r * M + j] = x;
         }
@@ -723,20 +760,26 @@ constexpr int kFinFilterMinM = 8192;
 #ifndef FIN_MAXIMA_U
 #define FIN_MAXIMA_U 4  // column pairs of row loads in flight per thread (maxima kernel)
 #endif
-template <typename T>
-static cudaError_t launch_fin(const T *hw, const T *sw, const T *sh, const T *sh2, const T *cnt,
+// narrow (int32) sum_hw rows: FIN_NARROW_UX times the row loads in flight per
+// thread (each load is 16 bytes either way; 1 measured best)
+#ifndef FIN_NARROW_UX
+#define FIN_NARROW_UX 1
+#endif
+template <typename T, typename TH = T>
+static cudaError_t launch_fin(const TH *hw, const T *sw, const T *sh, const T *sh2, const T *cnt,
                               const double *sqrt_dw, int32_t M, const FinalizeOut &o, cudaStream_t s)
 {
+    constexpr int X = sizeof(TH) < sizeof(T) ? FIN_NARROW_UX : 1;
     const int rows = o.h1 - o.h0;
     if (o.rho == nullptr && M >= kFinFilterMinM)
-        k_finalize_maxima<FIN_MAXIMA_U, T><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
+        k_finalize_maxima<FIN_MAXIMA_U * X, T, TH><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
     else
-        k_finalize_rows<1, 4, T><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
+        k_finalize_rows<1, 4 * X, T, TH><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
     return cudaGetLastError();
 }
 
 cudaError_t launch_finalize_i8(const int64_t *d_accum, int32_t M, double *d_sqrt_dw, const FinalizeOut &o,
-                               cudaStream_t s, int *launches)
+                               cudaStream_t s, int *launches, const int32_t *d_hw32)
 {
     const int64_t *hw = d_accum;
     const int64_t *sw = d_accum + 4096LL * M;
@@ -745,9 +788,34 @@ cudaError_t launch_finalize_i8(const int64_t *d_accum, int32_t M, double *d_sqrt
     const int64_t *sh2 = sh + 4096;
     const int64_t *cnt = sh2 + 4096;
     k_sqrt_dw_i8<<<(M + 255) / 256, 256, 0, s>>>(sw, sw2, cnt, M, d_sqrt_dw);
-    cudaError_t e = launch_fin<int64_t>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o, s);
+    cudaError_t e = d_hw32 ? launch_fin<int64_t, int32_t>(d_hw32, sw, sh, sh2, cnt, d_sqrt_dw, M, o, s)
+                           : launch_fin<int64_t>(hw, sw, sh, sh2, cnt, d_sqrt_dw, M, o, s);
     if (e != cudaSuccess) return e;
     if (launches) (*launches) += 2;
+    return cudaGetLastError();
+}
+
+// CPA_OPT_NARROW flush: sum_hw (int64) += hw32 (int32), n elements, then the
+// shadow is dead (the caller drops it)
+__global__ void k_widen_hw(const int4 *__restrict__ src, longlong2 *__restrict__ dst, int64_t n4)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        const int4 v = __ldcs(src + i);
+        longlong2 a = dst[2 * i], b = dst[2 * i + 1];
+        a.x += v.x;
+        a.y += v.y;
+        b.x += v.z;
+        b.y += v.w;
+        dst[2 * i] = a;
+        dst[2 * i + 1] = b;
+    }
+}
+cudaError_t launch_widen_hw(const int32_t *d_hw32, int64_t *d_hw, int64_t n, int num_sms, cudaStream_t s,
+                            int *launches)
+{
+    if (n % 4 != 0) return cudaErrorInvalidValue;  // 4096 M: always a multiple of 4
+    k_widen_hw<<<num_sms * 8, 256, 0, s>>>((const int4 *)d_hw32, (longlong2 *)d_hw, n / 4);
+    if (launches) (*launches)++;
     return cudaGetLastError();
 }
 

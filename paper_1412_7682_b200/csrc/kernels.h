@@ -73,7 +73,10 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const CUtensorMap *tmap_h
                             int64_t *d_sum_w2 = nullptr, uint32_t *d_hist = nullptr,
                             int64_t *const *owners = nullptr, unsigned long long *d_clk = nullptr,
                             bool overlapped = false, bool hw_zero = false, uint32_t *d_part = nullptr,
-                            int64_t part_ld = 0);
+                            int64_t part_ld = 0, int32_t *d_hw32 = nullptr);
+// d_hw32 non-null (CPA_OPT_NARROW): the cross term goes to that int32 [4096][M]
+// array instead of d_hw (the caller guarantees N max|H| max|W| < 2^31); not with
+// tmap_hw, d_part or owners
 // Partial-sum spill (d_part non-null, part_ld >= M a multiple of 8): every work
 // unit stores its raw 32-bit accumulators into part[kc][4096][part_ld] (kc = its
 // trace chunk) instead of adding them into sum_hw; then launch_part_reduce adds
@@ -147,7 +150,11 @@ struct FinalizeOut {
     double *best_rho;  // [16]
 };
 cudaError_t launch_finalize_i8(const int64_t *d_accum, int32_t M, double *d_sqrt_dw,
-                               const FinalizeOut &o, cudaStream_t s, int *launches);
+                               const FinalizeOut &o, cudaStream_t s, int *launches,
+                               const int32_t *d_hw32 = nullptr);  // non-null: sum_hw rows from this int32 shadow
+// CPA_OPT_NARROW flush: d_hw[i] += d_hw32[i], i < n (n a multiple of 4)
+cudaError_t launch_widen_hw(const int32_t *d_hw32, int64_t *d_hw, int64_t n, int num_sms, cudaStream_t s,
+                            int *launches);
 // float path: d_offset = the context's per-sample offsets (the sums are centred
 // on them; the degenerate-column rule needs the raw second moment)
 cudaError_t launch_finalize_f64(const double *d_accum, int32_t M, const float *d_offset, double *d_sqrt_dw,

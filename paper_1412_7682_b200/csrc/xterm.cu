@@ -238,6 +238,10 @@ struct Params {
     // the exposed epilogue; launch_part_reduce adds the slices into sum_hw after
     uint32_t *part;
     int64_t part_ld;
+    // narrow sums (CPA_OPT_NARROW): hw is an int32 [4096][M] array (the host
+    // guarantees N max|H| max|W| < 2^31, so the int32 sums are exact); first
+    // touch stores / red.add.u32 of half the bytes
+    int32_t hw32;
 };
 
 template <int V>
@@ -750,20 +754,29 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                 if (!(XT_EXP & 4) && j < p.M) {
                     const int64_t off = (int64_t)(hrow0 + rsub) * p.M + j;
                     const double inv = F32 ? (double)p.inv_scale[j] : 1.0;
+                    // one unswitched loop per output kind (the kind is uniform per unit)
+                    auto put = [&](auto op) {
 #pragma unroll
-                    for (int rr = 0; rr < 8; rr++) {
-                        const uint32_t bits = tbuf[(4 * rr + rsub) * TB_LD + csub];
-                        if (F32) {
-                            atomicAdd((double *)p.hw + off + (int64_t)(4 * rr) * p.M, (double)__uint_as_float(bits) * inv);
-                        } else if (own != nullptr) {  // peer (or own) accumulator of the row owner
-                            atomicAdd_system((unsigned long long *)own + off + (int64_t)(4 * rr) * p.M,
-                                             (unsigned long long)(long long)(int32_t)bits);
-                        } else if (store_u) {         // first touch (store_hw): no read-modify-write
-                            ((long long *)p.hw)[off + (int64_t)(4 * rr) * p.M] = (long long)(int32_t)bits;
-                        } else {
-                            atomicAdd((unsigned long long *)p.hw + off + (int64_t)(4 * rr) * p.M,
-                                      (unsigned long long)(long long)(int32_t)bits);
-                        }
+                        for (int rr = 0; rr < 8; rr++)
+                            op(off + (int64_t)(4 * rr) * p.M, tbuf[(4 * rr + rsub) * TB_LD + csub]);
+                    };
+                    if (F32) {
+                        put([&](int64_t o, uint32_t bits) {
+                            atomicAdd((double *)p.hw + o, (double)__uint_as_float(bits) * inv);
+                        });
+                    } else if (own != nullptr) {  // peer (or own) accumulator of the row owner
+                        put([&](int64_t o, uint32_t bits) {
+                            atomicAdd_system((unsigned long long *)own + o, (unsigned long long)(long long)(int32_t)bits);
+                        });
+                    } else if (p.hw32) {          // narrow sums: 32-bit words
+                        if (store_u) put([&](int64_t o, uint32_t bits) { ((uint32_t *)p.hw)[o] = bits; });
+                        else put([&](int64_t o, uint32_t bits) { atomicAdd((unsigned int *)p.hw + o, bits); });
+                    } else if (store_u) {         // first touch (store_hw): no read-modify-write
+                        put([&](int64_t o, uint32_t bits) { ((long long *)p.hw)[o] = (long long)(int32_t)bits; });
+                    } else {
+                        put([&](int64_t o, uint32_t bits) {
+                            atomicAdd((unsigned long long *)p.hw + o, (unsigned long long)(long long)(int32_t)bits);
+                        });
                     }
                 }
                 __syncwarp();
@@ -968,7 +981,8 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorM
                    cudaStream_t stream, int *launches, int64_t *d_sum_w = nullptr, int64_t *d_sum_w2 = nullptr,
                    bool w_signed = true, uint32_t *d_hist = nullptr, int64_t *const *owners = nullptr,
                    unsigned long long *d_clk = nullptr, uint32_t idesc8 = 0, const float *d_inv_scale = nullptr,
-                   bool store_hw = false, uint32_t *d_part = nullptr, int64_t part_ld = 0)
+                   bool store_hw = false, uint32_t *d_part = nullptr, int64_t part_ld = 0,
+                   int32_t *d_hw32 = nullptr)
 {
     using Cf = Cfg<V>;
     Params p;
@@ -996,6 +1010,11 @@ cudaError_t launch(const CUtensorMap &m0, const CUtensorMap &m1, const CUtensorM
     p.part_ld = part_ld;
     if (d_part != nullptr && (part_ld % 8 != 0 || part_ld < M || Cf::KB != 1 || owners != nullptr))
         return cudaErrorInvalidValue;
+    p.hw32 = d_hw32 != nullptr;
+    if (p.hw32) {
+        if (Cf::F32 || mhw != nullptr || d_part != nullptr || owners != nullptr) return cudaErrorInvalidValue;
+        p.hw = d_hw32;
+    }
     p.bulk_spill = mhw != nullptr;
     p.store_hw = store_hw && p.kc_count == 1 && owners == nullptr && !Cf::F32;
     p.full_units = p.units;
@@ -1089,18 +1108,18 @@ cudaError_t launch_xterm_i8(const CUtensorMap &tmap_w, const CUtensorMap *tmap_h
                             const uint8_t *d_vtab, int64_t *d_hw, int *d_counter, int32_t M, int64_t N, int64_t kc_len,
                             bool w_signed, int num_sms, cudaStream_t stream, int *launches, int64_t *d_sum_w,
                             int64_t *d_sum_w2, uint32_t *d_hist, int64_t *const *owners, unsigned long long *d_clk,
-                            bool overlapped, bool hw_zero, uint32_t *d_part, int64_t part_ld)
+                            bool overlapped, bool hw_zero, uint32_t *d_part, int64_t part_ld, int32_t *d_hw32)
 {
     static_assert(Cfg<V_I8>::KB == 1 && Cfg<V_I8O>::KB == 1, "owner routing assumes one key byte per unit");
     if (overlapped) {
         if (d_sum_w != nullptr) return cudaErrorInvalidValue;  // a4 is fused into the NT = 2 variant only
         return launch<V_I8O>(tmap_w, tmap_w, tmap_hw, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                              idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, nullptr, nullptr, w_signed,
-                             d_hist, owners, d_clk, 0, nullptr, hw_zero, d_part, part_ld);
+                             d_hist, owners, d_clk, 0, nullptr, hw_zero, d_part, part_ld, d_hw32);
     }
     return launch<V_I8>(tmap_w, tmap_w, tmap_hw, d_texts, d_vtab, d_hw, d_counter, M, N, kc_len,
                         idesc_i8(2 * BMC, BN, w_signed), num_sms, stream, launches, d_sum_w, d_sum_w2, w_signed,
-                        d_hist, owners, d_clk, 0, nullptr, hw_zero, d_part, part_ld);
+                        d_hist, owners, d_clk, 0, nullptr, hw_zero, d_part, part_ld, d_hw32);
 }
 
 cudaError_t launch_xterm_f32(const CUtensorMap &tmap_hi, const CUtensorMap &tmap_lo, const CUtensorMap *tmap_hw,

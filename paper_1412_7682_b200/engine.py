@@ -33,6 +33,7 @@ class Engine:
 
     @property
     def sum_hw(self):
+        self.flush()  # CPA_OPT_NARROW: the int32 shadow into the accumulator first
         return self._field(B.FIELD_HW, 4096 * self.M).view(4096, self.M)
 
     @property
@@ -81,6 +82,19 @@ class Engine:
         """CPA_OPT_SPILL: 0 auto (default), 1 red.add per element, 2 bulk tensor reduce-add,
         3 per-chunk partial stores + one reduce pass (include/cpa.h)."""
         B.cpa_set_option(self.ctx, B.CPA_OPT_SPILL, mode)
+
+    def set_narrow(self, on: bool | int = True):
+        """CPA_OPT_NARROW: int32 cross-term sums while exact (half the sum_hw bytes);
+        the accumulator's HW field is stale until flush() (include/cpa.h).  An int
+        > 1 also caps the shadow at that many traces (tests)."""
+        B.cpa_set_option(self.ctx, B.CPA_OPT_NARROW, int(on))
+
+    def flush(self):
+        """cpa_flush: add a live int32 shadow (CPA_OPT_NARROW) into the accumulator
+        (on the context's stream; torch's current stream then waits for it, so a
+        read of the accumulator in torch sees the flushed sums)."""
+        B.cpa_flush(self.ctx)
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
 
     def set_row_owners(self, owners):
         """cpa_set_row_owners: 16 device addresses (0 = own accumulator) or None."""
@@ -163,6 +177,7 @@ class Engine:
         from .multigpu import allreduce_accumulator, check_same_offsets
         if self.dtype == B.CPA_F32 and check_offsets:
             check_same_offsets(self, group)
+        self.flush()
         with torch.cuda.stream(self.stream):
             allreduce_accumulator(self.accum, group)
 

@@ -223,6 +223,8 @@ def finalize_rows_sharded(engine, group=None, want_rho: bool = False) -> dict:
     from . import _binding as B
     if getattr(engine, "dtype", None) == B.CPA_F32:
         check_same_offsets(engine, group)
+    if hasattr(engine, "flush"):
+        engine.flush()  # CPA_OPT_NARROW: the int32 shadow into the accumulator
     h0, h1 = reduce_scatter_rows(engine.accum, engine.M, group)
     mx, am, pk = (t[0] for t in engine.maxima_buffers(1))
     rho = engine.finalize_rows(h0, h1, mx, am, pk, want_rho)

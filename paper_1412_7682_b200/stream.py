@@ -78,7 +78,8 @@ class StreamingAttack:
     multi-GPU) run.  `group` is a torch.distributed group (None = default when
     initialized; single process otherwise)."""
 
-    def __init__(self, M: int, dtype: int, model: int, device: int = 0, group=None, fused: bool = False):
+    def __init__(self, M: int, dtype: int, model: int, device: int = 0, group=None, fused: bool = False,
+                 narrow: bool | None = None):
         import torch
         import torch.distributed as dist
 
@@ -87,6 +88,12 @@ class StreamingAttack:
         self.group = group
         self.world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
         self.eng = Engine(M, dtype, model, device)
+        # CPA_OPT_NARROW (int8): the cross term in int32 while exact -- half the
+        # sum_hw bytes in every chunk's spill and every checkpoint's finalize.
+        # Default: one rank (a multi-GPU checkpoint combines the int64 accumulator)
+        from . import _binding as B
+        if (self.world == 1 if narrow is None else narrow) and dtype != B.CPA_F32:
+            self.eng.set_narrow(True)
         # multi-GPU checkpoints finalize from an all-reduced copy of the partials
         self.view = Engine(M, dtype, model, device, stream=self.eng.stream) if self.world > 1 else None
         self.n_local = 0
@@ -121,6 +128,7 @@ class StreamingAttack:
         import torch
 
         from . import multigpu as MG
+        self.eng.flush()  # CPA_OPT_NARROW: the int32 shadow into the accumulator
         with torch.cuda.stream(self.eng.stream):
             if self.owners is not None:
                 # small fields: all-reduced copy (also the point after which every

@@ -13,7 +13,8 @@ from synth import synth as S  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-def test_c4_fullsize_sampled_parity():
+@pytest.mark.parametrize("narrow", [False, True])   # CPA_OPT_NARROW: bench.py's default at one GPU
+def test_c4_fullsize_sampled_parity(narrow):
     import paper_1412_7682_b200 as P
     w = S.CONFIGS["C4"]
     texts, lv = S.texts(w)
@@ -21,6 +22,7 @@ def test_c4_fullsize_sampled_parity():
     dW = torch.empty((w.n, ld), dtype=torch.int8, device="cuda")
     S.dev_traces(w, torch.from_numpy(lv).cuda(), 0, w.n, dW, ld)
     eng = P.Engine(w.m, P.CPA_S8, P.CPA_HD_LAST, 0)
+    eng.set_narrow(narrow)
     eng.accumulate(dW[:, :w.m], torch.from_numpy(texts).cuda())
     out = eng.finalize(want_rho=True)
     rk = O.expand_key(w.key)[10].astype(int)

@@ -24,9 +24,11 @@ MODEL = {O.HD_LAST: 0, O.HW_LAST: 1, O.HW_FIRST: 2}
 
 
 def run_gpu(P, texts, W, model=0, kchunk=0, chunks=None, want_rho=True, overlap=True, mode=None, fuse_hist=None,
-            xt=None, spill=None):
+            xt=None, spill=None, narrow=None):
     dtype = {np.int8: P.CPA_S8, np.uint8: P.CPA_U8}[W.dtype.type]
     eng = P.Engine(W.shape[1], dtype, model, 0)
+    if narrow is not None:
+        eng.set_narrow(narrow)
     if xt is not None:
         eng.set_xt_tiles(xt)
     if spill is not None:
