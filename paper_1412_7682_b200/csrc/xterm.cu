@@ -150,6 +150,9 @@ constexpr int GEN_WARPS = XT_GEN_WARPS;       // every generator warp works on e
 // readers of the unit-id ring: leader = MMA + text producer + epilogue + generators,
 // peer = W producer + text producer + epilogue + generators
 constexpr int RING_CONSUMERS = 2 * (2 + EPI_WARPS + GEN_WARPS);
+#ifndef XT_ST32_ROWS2
+#define XT_ST32_ROWS2 1  // narrow first-touch spill: 2 rows x 64 B per warp-wide store
+#endif
 constexpr int TB_LD = 9;                      // epilogue transpose row stride (words, odd)
 // epilogue staging (union): the red.add path's transpose buffer, or the bulk
 // path's int64 boxes (per epilogue warp one 32 rows x 8 samples box, 64-byte
@@ -733,6 +736,56 @@ k_xterm(const __grid_constant__ CUtensorMap tmap_b0, const __grid_constant__ CUt
                     }
                 }
                 if (lane == 0) bulk_wait_read<0>();  // box free; the adds complete asynchronously
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(to_leader(tempty_bar(acc)));
+                continue;
+            }
+            if (!F32 && own == nullptr && p.hw32 && store_u && XT_ST32_ROWS2) {
+                // narrow first touch, two column groups at a time: 32 rows x 16 samples
+                // staged in the warp's bulk box (word (r, c) at r*16 + (c ^ ((r >> 1) & 15)):
+                // conflict-free both ways), then each warp-wide store covers 2 rows x 64 B
+                static_assert(NC % 2 == 0 && CPB % 2 == 0, "column groups in pairs");
+                uint32_t *sb = (uint32_t *)(smem + Lay<V>::TB + q * RB_BYTES);
+                const int rl = lane >> 4, cl = lane & 15;
+                uint32_t v2[8];
+                tmem_ld_32x32b_x8(tcol + 8, v2);
+                tmem_ld_wait(v2);
+#pragma unroll 1
+                for (int c = 0; c < NC; c += 2) {
+                    const int cc = c % CPB;
+                    const int hrow0 = (b + c / CPB) * 256 + (int)rank * BMC + q * 32;
+                    uint32_t vn[8], vn2[8];
+                    if (c + 2 < NC) {
+                        tmem_ld_32x32b_x8(tcol + (c + 2) * 8, vn);
+                        tmem_ld_32x32b_x8(tcol + (c + 3) * 8, vn2);
+                    }
+                    const int sw = (lane >> 1) & 15;
+#pragma unroll
+                    for (int x = 0; x < 8; x++) {
+                        sb[lane * 16 + (x ^ sw)] = v[x];
+                        sb[lane * 16 + ((x + 8) ^ sw)] = v2[x];
+                    }
+                    __syncwarp();
+                    const int jc = nt * (C::NT * BN) + cc * 8 + cl;
+                    if (!(XT_EXP & 4) && jc < p.M) {
+#pragma unroll
+                        for (int i = 0; i < 16; i++) {
+                            const int row = 2 * i + rl;
+                            ((uint32_t *)p.hw)[(int64_t)(hrow0 + row) * p.M + jc] = sb[row * 16 + (cl ^ i)];
+                        }
+                    }
+                    __syncwarp();
+                    if (c + 2 < NC) {
+                        tmem_ld_wait(vn);
+                        tmem_ld_wait(vn2);
+#pragma unroll
+                        for (int x = 0; x < 8; x++) {
+                            v[x] = vn[x];
+                            v2[x] = vn2[x];
+                        }
+                    }
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(to_leader(tempty_bar(acc)));
