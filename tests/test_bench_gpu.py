@@ -86,3 +86,29 @@ def test_bench_float_two_ranks_one_gpu_gloo(combine, port):
              env={"CPA_BENCH_SAME_DEVICE": "1", "CPA_BENCH_BACKEND": "gloo"})
     assert d["n_gpus"] == 2 and d["key_recovered"] is True
     assert combine in d["config"]["parallelism"] and "float32" in d["config"]["workload"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("combine,port", [("rows", 29543), ("allreduce", 29544)])
+def test_bench_two_ranks_narrow_flush_before_combine(combine, port):
+    """--narrow 1 with an accumulator combine: every rank flushes its int32
+    shadow (CPA_OPT_NARROW) into the int64 accumulator before the NCCL / gloo
+    combine reads it; the key and the line are as without the option."""
+    d = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+              "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--config", "C2",
+              "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--combine", combine,
+              "--narrow", "1", "--no-combine-sweep"],
+             env={"CPA_BENCH_SAME_DEVICE": "1", "CPA_BENCH_BACKEND": "gloo"})
+    assert d["n_gpus"] == 2 and d["key_recovered"] is True
+    assert d["config"]["sum_hw"].startswith("int32 shadow")
+
+
+@pytest.mark.gpu
+def test_bench_stream_two_ranks_narrow():
+    d = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+              "--master-addr", "127.0.0.1", "--master-port", "29545", "bench.py", "--gpus", "2", "--config", "C1",
+              "--chunk", "64", "--steps", "3", "--warmup", "3", "--no-clocks", "--narrow", "1", "--no-combine-sweep"],
+             env={"CPA_BENCH_SAME_DEVICE": "1", "CPA_BENCH_BACKEND": "gloo"})
+    assert d["n_gpus"] == 2 and d["key_recovered"] is True
+    assert d["config"]["sum_hw"].startswith("int32 shadow")
+    assert d["rank_curve"]["points"][-1][0] == 500

@@ -179,3 +179,26 @@ def test_narrow_graph_replay(P):
     cols = np.arange(0, w.m, 97, dtype=np.int32)
     assert np.array_equal(ref_hw.cpu().numpy()[:, cols], O.cross_sums_i8(O.HD_LAST, texts, W, cols))
     eng.close()
+
+
+def test_narrow_contexts_over_trace_shards_flush_and_sum(P):
+    """Two contexts on trace halves, each with a live shadow: after cpa_flush the
+    int64 accumulators add up to the whole run's (the multi-GPU combine's
+    precondition), and the summed accumulator finalizes to the oracle's rho."""
+    texts, W = _data(11, 900, 640)
+    ref = O.attack_i8(O.HD_LAST, texts, W)
+    engs = [P.Engine(640, P.CPA_S8, P.CPA_HD_LAST, 0) for _ in range(2)]
+    for e, (a, b) in zip(engs, [(0, 450), (450, 900)]):
+        e.set_narrow(True)
+        e.accumulate(torch.from_numpy(W[a:b]).cuda(), torch.from_numpy(texts[a:b]).cuda())
+        e.flush()
+        e.sync()
+    engs[0].accum += engs[1].accum
+    torch.cuda.synchronize()
+    engs[0].set_narrow(False)      # no live shadow left: finalize reads the summed accumulator
+    out = engs[0].finalize(want_rho=True)
+    assert np.array_equal(engs[0].sum_hw.cpu().numpy(), ref["sum_hw"])
+    assert np.array_equal(out["rho"].cpu().numpy(), ref["rho"])
+    assert np.array_equal(out["rank"].cpu().numpy(), ref["rank"])
+    for e in engs:
+        e.close()
