@@ -30,6 +30,8 @@ def main():
         dW = torch.empty((n, ld), dtype=torch.float32 if f32 else torch.int8, device="cuda")
         S.dev_traces(w, torch.from_numpy(lv).cuda(), 0, n, dW, ld)
         eng = P.Engine(M, P.CPA_F32 if f32 else P.CPA_S8, P.CPA_HD_LAST, 0)
+        if os.environ.get("FIN_NARROW") == "1":   # int32 sum_hw rows (CPA_OPT_NARROW)
+            eng.set_narrow(True)
         eng.accumulate(dW[:, :M], torch.from_numpy(texts).cuda())
         eng.sync()
         for want_rho in rhos:
