@@ -48,6 +48,8 @@ def run_attack(traces: np.ndarray, texts: np.ndarray, model: int = 0, device: in
         raise TypeError(f"unsupported trace dtype {traces.dtype} (int8, uint8, float32 or float64)")
     dt = kind.get(traces.dtype, B.CPA_F32)
     eng = Engine(m, dt, model, device)
+    if dt != B.CPA_F32:
+        eng.set_narrow(True)   # int32 cross-term sums while exact (one GPU, no combine)
     rows = max(1, chunk_bytes // (m * traces.dtype.itemsize))
     texts = np.ascontiguousarray(texts, np.uint8)
     for i0 in range(0, n, rows):
