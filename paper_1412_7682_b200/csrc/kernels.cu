@@ -306,8 +306,8 @@ constexpr double kFinSkip = 1.0 - 3.552713678800501e-15;  // 1 - 2^-48
 #ifndef FIN_MAXIMA_MINB
 #define FIN_MAXIMA_MINB 4  // 64 registers: 4 resident blocks (C5 finalize 4.5 vs 5.8 ms with 1)
 #endif
-template <int U, typename T, typename TH = T>
-__global__ void __launch_bounds__(FIN_THREADS, FIN_MAXIMA_MINB)
+template <int U, typename T, typename TH = T, int MINB = FIN_MAXIMA_MINB>
+__global__ void __launch_bounds__(FIN_THREADS, MINB)
 k_finalize_maxima(const TH *__restrict__ hw, const T *__restrict__ sw, const T *__restrict__ sh,
                   const T *__restrict__ sh2, const T *__restrict__ count, const double *__restrict__ sqrt_dw,
                   int32_t M, FinalizeOut o)
@@ -759,6 +759,15 @@ cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M,
 constexpr int kFinFilterMinM = 8192;
 #ifndef FIN_MAXIMA_U
 #define FIN_MAXIMA_U 4  // column pairs of row loads in flight per thread (maxima kernel)
+// int32 rows: 2 16-byte loads (8 samples) in flight per thread, 5 resident blocks
+// (tools/fin_bench.py, M = 20000: 0.133 ms vs 0.156 for 4 loads / 4 blocks; 3
+// loads 0.147; C5 checkpoint maxima 3.89 vs 4.45 ms per step)
+#ifndef FIN_NARROW_MAXIMA_U
+#define FIN_NARROW_MAXIMA_U 2
+#endif
+#ifndef FIN_NARROW_MAXIMA_MINB
+#define FIN_NARROW_MAXIMA_MINB 5
+#endif
 #endif
 // narrow (int32) sum_hw rows: FIN_NARROW_UX times the row loads in flight per
 // thread (each load is 16 bytes either way; 1 measured best)
@@ -772,7 +781,9 @@ static cudaError_t launch_fin(const TH *hw, const T *sw, const T *sh, const T *s
     constexpr int X = sizeof(TH) < sizeof(T) ? FIN_NARROW_UX : 1;
     const int rows = o.h1 - o.h0;
     if (o.rho == nullptr && M >= kFinFilterMinM)
-        k_finalize_maxima<FIN_MAXIMA_U * X, T, TH><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
+        k_finalize_maxima<(X > 1 || sizeof(TH) == sizeof(T)) ? FIN_MAXIMA_U * X : FIN_NARROW_MAXIMA_U, T, TH,
+                          sizeof(TH) == sizeof(T) ? FIN_MAXIMA_MINB : FIN_NARROW_MAXIMA_MINB>
+            <<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
     else
         k_finalize_rows<1, 4 * X, T, TH><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
     return cudaGetLastError();

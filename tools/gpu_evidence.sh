@@ -1,5 +1,5 @@
 # Round-2 evidence on HEAD (final kernels; + sanitizers) (under gpurun): smoke, all GPU tests, bench lines, ncu launch lists + captures
-TAG=${TAG:-r02k}
+TAG=${TAG:-r02l}
 mkdir -p gpurun_out/$TAG
 O=gpurun_out/$TAG
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $O/smi.txt
