@@ -759,6 +759,7 @@ cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M,
 constexpr int kFinFilterMinM = 8192;
 #ifndef FIN_MAXIMA_U
 #define FIN_MAXIMA_U 4  // column pairs of row loads in flight per thread (maxima kernel)
+#endif
 // int32 rows: 2 16-byte loads (8 samples) in flight per thread, 5 resident blocks
 // (tools/fin_bench.py, M = 20000: 0.133 ms vs 0.156 for 4 loads / 4 blocks; 3
 // loads 0.147; C5 checkpoint maxima 3.89 vs 4.45 ms per step)
@@ -767,7 +768,6 @@ constexpr int kFinFilterMinM = 8192;
 #endif
 #ifndef FIN_NARROW_MAXIMA_MINB
 #define FIN_NARROW_MAXIMA_MINB 5
-#endif
 #endif
 // narrow (int32) sum_hw rows: FIN_NARROW_UX times the row loads in flight per
 // thread (each load is 16 bytes either way; 1 measured best)
