@@ -304,7 +304,7 @@ constexpr double kFinSkip = 1.0 - 3.552713678800501e-15;  // 1 - 2^-48
 
 // TH: element type of the sum_hw rows (T, or int32 for narrow sums, widened on load)
 #ifndef FIN_MAXIMA_MINB
-#define FIN_MAXIMA_MINB 4  // 64 registers: 4 resident blocks (C5 finalize 4.5 vs 5.8 ms with 1)
+#define FIN_MAXIMA_MINB 5  // 5 resident blocks with 2 row loads in flight (tools/gpu_ab_w.sh)
 #endif
 template <int U, typename T, typename TH = T, int MINB = FIN_MAXIMA_MINB>
 __global__ void __launch_bounds__(FIN_THREADS, MINB)
@@ -758,7 +758,7 @@ cudaError_t launch_moments_i8(const void *d_w, int64_t ld, int64_t n, int32_t M,
 // filtered maxima kernel from M = 8192 on (-13% / -23% at M = 20000 / 48000)
 constexpr int kFinFilterMinM = 8192;
 #ifndef FIN_MAXIMA_U
-#define FIN_MAXIMA_U 4  // column pairs of row loads in flight per thread (maxima kernel)
+#define FIN_MAXIMA_U 2  // 16-byte row loads in flight per thread (maxima kernel; 4 with 4 blocks: slower)
 #endif
 // int32 rows: 2 16-byte loads (8 samples) in flight per thread, 5 resident blocks
 // (tools/fin_bench.py, M = 20000: 0.133 ms vs 0.156 for 4 loads / 4 blocks; 3
