@@ -766,6 +766,9 @@ constexpr int kFinFilterMinM = 8192;
 #ifndef FIN_NARROW_MAXIMA_U
 #define FIN_NARROW_MAXIMA_U 2
 #endif
+#ifndef FIN_NARROW_ROWS_U
+#define FIN_NARROW_ROWS_U 4  // rho-writing kernel, int32 rows: 16-byte row loads in flight per thread
+#endif
 #ifndef FIN_NARROW_MAXIMA_MINB
 #define FIN_NARROW_MAXIMA_MINB 5
 #endif
@@ -785,7 +788,8 @@ static cudaError_t launch_fin(const TH *hw, const T *sw, const T *sh, const T *s
                           sizeof(TH) == sizeof(T) ? FIN_MAXIMA_MINB : FIN_NARROW_MAXIMA_MINB>
             <<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
     else
-        k_finalize_rows<1, 4 * X, T, TH><<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
+        k_finalize_rows<1, (sizeof(TH) == sizeof(T) || X > 1) ? 4 * X : FIN_NARROW_ROWS_U, T, TH>
+            <<<rows, FIN_THREADS, 0, s>>>(hw, sw, sh, sh2, cnt, sqrt_dw, M, o);
     return cudaGetLastError();
 }
 
